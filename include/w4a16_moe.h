@@ -1,0 +1,115 @@
+/*
+ * w4a16_moe.h -- C ABI of the B200 (sm_100a) W4A16 mixture-of-experts path.
+ *
+ * The reference (Hexcute's `tilesynth`, /root/reference/pkg) has no C/C++/CUDA code and no FFI: its
+ * boundary is the Python API (pkg/src/tilesynth/__init__.py:16-58) and it stops at the synthesized
+ * layout plan for the fp16 x int4 tile (pkg/fixtures/mixed_int4.prog:1-18). The paper's MoE operator
+ * is the kernel that plan feeds. These entry points are that operator, split
+ * the way the Python host (paper_2504_16214_b200/moe) and a vLLM-style caller
+ * (vllm fused_experts(hidden_states, w1, w2, topk_weights, topk_ids, ...)) bind it:
+ *
+ *   route:    w4a16_route_topk                         top-k of softmax/sigmoid router scores
+ *   permute:  w4a16_moe_permute                        stable counting sort of (token, slot) by expert
+ *   gather:   w4a16_moe_gather                         X_perm[p] = x[token(p)]   (128-bit vectors)
+ *   GEMM:     w4a16_grouped_gemm                       per-expert X_e * W_e^T, optional fused SiLU*up
+ *   combine:  w4a16_moe_combine                        y[t] = sum_j w[t,j] * Y_perm[pos(t,j)]
+ *   EP:       w4a16_ep_pack_counts / w4a16_moe_permute over received rows (NCCL all-to-all is
+ *             driven by the host through torch.distributed)
+ *   weights:  w4a16_repack_awq, w4a16_dequant (test/oracle aid), w4a16_packed_bytes
+ *   driver:   w4a16_moe_forward                        the whole layer, one call, caller workspace
+ *
+ * Conventions: raw device pointers, int64_t extents, cudaStream_t (pass 0 for the legacy stream);
+ * every function is stream-ordered, returns an int status (0 ok, < 0 error, never throws), performs
+ * no hidden host synchronisation and allocates nothing: the caller owns every buffer including
+ * workspace (query sizes with the *_workspace_bytes functions). Activations are fp16 or bf16
+ * (W4_DTYPE_*); scales use the activation dtype; int4 codes/zeros are AWQ (uint4, group 128).
+ */
+#ifndef W4A16_MOE_H_
+#define W4A16_MOE_H_
+
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  W4_OK = 0,
+  W4_ERR_ARG = -1,    /* null pointer / bad enum */
+  W4_ERR_SHAPE = -2,  /* extent not a multiple of the tile (N % 128, K % 128) or too large */
+  W4_ERR_DTYPE = -3,  /* unsupported activation dtype */
+  W4_ERR_GROUP = -4,  /* unsupported quantisation group size (only 128) */
+  W4_ERR_CUDA = -5,   /* launch / driver failure (cudaGetLastError() has details) */
+  W4_ERR_WORKSPACE = -6
+};
+
+enum { W4_DTYPE_F16 = 0, W4_DTYPE_BF16 = 1 };
+enum { W4_SCORE_SOFTMAX = 0, W4_SCORE_SIGMOID = 1 };
+
+/* ---- weights --------------------------------------------------------------------------------- */
+/* Bytes of the packed block format for [num_experts][n_rows][K] (== AWQ bytes; -1 if misaligned). */
+int64_t w4a16_packed_bytes(int64_t num_experts, int64_t n_rows, int64_t K);
+int w4a16_tile_rows(void); /* 128 */
+int w4a16_tile_k(void);    /* 128 */
+int w4a16_part_bytes(void);
+
+/* AWQ -> packed blocks. qweight [E][K][n_rows/8] int32, scales [E][K/G][n_rows] (act dtype),
+ * qzeros [E][K/G][n_rows/8] int32 (AWQ nibble order 0,2,4,6,1,3,5,7). parts = 2 interleaves the
+ * first and second halves of n_rows (gate | up) block-wise for the fused gate/up GEMM.
+ * Replaces vLLM's AWQ->Marlin repack for this path (vllm .../awq_marlin.py:70-74). */
+int w4a16_repack_awq(const int32_t* qweight, const void* scales, const int32_t* qzeros, int64_t num_experts,
+                     int64_t K, int64_t n_rows, int parts, int group_size, uint8_t* wblocks, cudaStream_t stream);
+
+/* packed blocks -> dense W [E][n_rows][K] (act dtype), bit-exact fp16((q - z) * s). */
+int w4a16_dequant(const uint8_t* wblocks, int64_t num_experts, int64_t n_rows, int64_t K, int parts, int dtype,
+                  void* out, cudaStream_t stream);
+
+/* ---- routing ---------------------------------------------------------------------------------- */
+/* logits [T][E] fp32 -> topk_ids [T][k] int32 (descending score, ties -> lower expert id),
+ * topk_weights [T][k] fp32 (softmax or sigmoid of the selected logits, optionally renormalised). */
+int w4a16_route_topk(const float* logits, int64_t T, int64_t E, int64_t k, int scoring, int renormalize,
+                     int32_t* topk_ids, float* topk_weights, cudaStream_t stream);
+
+/* Stable counting sort of the P = T*k flattened (token, slot) pairs by expert id.
+ * ids outside [0, E) are dropped (pair_pos = -1). Outputs: expert_counts [E], expert_offsets [E+1],
+ * sorted_pairs [P] (flat pair index at each permuted row; rows >= offsets[E] untouched),
+ * pair_pos [P] (permuted row of each pair or -1). */
+int w4a16_moe_permute(const int32_t* topk_ids, int64_t P, int64_t E, int32_t* expert_counts,
+                      int32_t* expert_offsets, int32_t* sorted_pairs, int32_t* pair_pos, cudaStream_t stream);
+
+/* X_perm[p][:] = x[sorted_pairs[p] / topk][:] for p < rows, and p < *row_limit when row_limit (a
+ * device pointer, e.g. expert_offsets + E) is non-null -- rows past it are left untouched. */
+int w4a16_moe_gather(const void* x, int64_t H, int64_t topk, const int32_t* sorted_pairs, int64_t rows,
+                     const int32_t* row_limit, void* x_perm, cudaStream_t stream);
+
+/* y[t][:] = act(sum_j topk_weights[t][j] * Y_perm[pair_pos[t*k+j]][:]), fp32 accumulate in slot
+ * order; pairs with pair_pos < 0 contribute nothing. */
+int w4a16_moe_combine(const void* y_perm, int64_t T, int64_t H, int64_t topk, const int32_t* pair_pos,
+                      const float* topk_weights, int dtype, void* y, cudaStream_t stream);
+
+/* ---- grouped GEMM ----------------------------------------------------------------------------- */
+/* For each expert e: out[off_e + m][n] = act( sum_k X[off_e + m][k] * W_e[n][k] ), m < counts[e].
+ * x [rows][K]; wblocks packed (parts = gated ? 2 : 1, n_rows = gated ? 2*n_out : n_out);
+ * gated: out[.., n] = silu(X W_gate^T)[n] * (X W_up^T)[n] (fused SwiGLU). ntok = token tile
+ * (16/32/64/128; 0 = pick from rows/num_experts). */
+int w4a16_grouped_gemm(const void* x, int64_t rows, int64_t K, const uint8_t* wblocks, int64_t num_experts,
+                       int64_t n_out, int gated, const int32_t* expert_counts, const int32_t* expert_offsets,
+                       void* out, int dtype, int ntok, cudaStream_t stream);
+int w4a16_pick_ntok(int64_t rows, int64_t num_experts);
+
+/* ---- whole layer ------------------------------------------------------------------------------- */
+/* Workspace for w4a16_moe_forward with T tokens, top-k, E experts, hidden H, intermediate I. */
+int64_t w4a16_moe_workspace_bytes(int64_t T, int64_t topk, int64_t E, int64_t H, int64_t I);
+
+/* y = MoE(x) for precomputed routing: permute -> gather -> gate/up GEMM (+SiLU*up) -> down GEMM ->
+ * combine. w13 packed with parts=2 (n_rows = 2I, K = H), w2 packed with parts=1 (n_rows = H, K = I). */
+int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, int64_t topk,
+                      const int32_t* topk_ids, const float* topk_weights, const uint8_t* w13,
+                      const uint8_t* w2, int dtype, void* y, void* workspace, int64_t workspace_bytes,
+                      cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* W4A16_MOE_H_ */

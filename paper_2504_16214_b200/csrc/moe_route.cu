@@ -1,0 +1,325 @@
+// Routing, permutation, gather and combine kernels for the W4A16 MoE layer (sm_100a), and the
+// one-call layer driver. All index outputs are deterministic (no atomics on the output order):
+//   * top-k selects on the raw logits (softmax / sigmoid are monotone), ties -> lower expert id;
+//   * the permutation is a stable counting sort of flat pair index i = t*k + j by expert id,
+//     i.e. rows of one expert appear in (token, slot) order.
+#include <cuda_runtime.h>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include "ptx.cuh"
+#include "w4a16_moe.h"
+
+namespace w4 {
+
+// ---------------------------------------------------------------------------------------- top-k
+// One warp per token; lane l holds logits l, l+32, ... (E <= 1024, k <= 32).
+__global__ void route_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int scoring, int renorm,
+                                  int32_t* __restrict__ ids, float* __restrict__ wts) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= T) return;
+  const float* row = logits + static_cast<int64_t>(warp) * E;
+  constexpr int kMaxPer = 32;
+  float v[kMaxPer];
+  const int per = (E + 31) / 32;
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < kMaxPer; ++i) {
+    if (i < per) {
+      const int e = lane + 32 * i;
+      v[i] = e < E ? row[e] : -INFINITY;
+      mx = fmaxf(mx, v[i]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float denom = 0.f;
+  if (scoring == W4_SCORE_SOFTMAX) {
+#pragma unroll
+    for (int i = 0; i < kMaxPer; ++i)
+      if (i < per && lane + 32 * i < E) denom += expf(v[i] - mx);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) denom += __shfl_xor_sync(0xffffffffu, denom, o);
+  }
+  uint32_t taken = 0;  // bit i: v[i] already selected
+  float sel_sum = 0.f;
+  float my_w = 0.f;
+  int my_id = 0;
+  for (int j = 0; j < k; ++j) {
+    float best = -INFINITY;
+    int bidx = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < kMaxPer; ++i) {
+      const int e = lane + 32 * i;
+      if (i < per && e < E && !((taken >> i) & 1u)) {
+        if (v[i] > best || (v[i] == best && e < bidx) || bidx == 0x7fffffff) { best = v[i]; bidx = e; }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+      if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+    }
+    if ((bidx & 31) == lane) taken |= 1u << (bidx >> 5);
+    const float w = scoring == W4_SCORE_SOFTMAX ? expf(best - mx) / denom : 1.0f / (1.0f + expf(-best));
+    sel_sum += w;
+    if (lane == j) { my_w = w; my_id = bidx; }
+  }
+  if (lane < k) {
+    ids[static_cast<int64_t>(warp) * k + lane] = my_id;
+    wts[static_cast<int64_t>(warp) * k + lane] = renorm ? my_w / sel_sum : my_w;
+  }
+}
+
+// ---------------------------------------------------------------------------------------- permute
+// Single CTA of 1024 threads. Pass 1: histogram (smem atomics; counts are order-independent).
+// Pass 2: exclusive scan. Pass 3: walk the pairs in 1024-wide chunks; within a chunk a pair's rank
+// among same-expert pairs = (#same in earlier warps) + (#same in lower lanes), so the output order is
+// exactly ascending flat index within each expert.
+constexpr int kPermThreads = 1024;
+constexpr int kPermWarps = kPermThreads / 32;
+
+__global__ void __launch_bounds__(kPermThreads, 1)
+    moe_permute_kernel(const int32_t* __restrict__ ids, int P, int E, int32_t* __restrict__ counts,
+                       int32_t* __restrict__ offsets, int32_t* __restrict__ sorted_pairs,
+                       int32_t* __restrict__ pair_pos) {
+  extern __shared__ int sm[];
+  int* cnt = sm;                     // [E]
+  int* base = cnt + E;               // [E]
+  int* wcnt = base + E;              // [kPermWarps][E]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < E; e += kPermThreads) cnt[e] = 0;
+  __syncthreads();
+  for (int i = tid; i < P; i += kPermThreads) {
+    const int e = ids[i];
+    if (e >= 0 && e < E) atomicAdd(&cnt[e], 1);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int per = (E + 31) / 32;
+    const int beg = min(E, lane * per), end = min(E, beg + per);
+    int s = 0;
+    for (int e = beg; e < end; ++e) s += cnt[e];
+    int incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int run = incl - s;
+    for (int e = beg; e < end; ++e) {
+      base[e] = run;
+      offsets[e] = run;
+      counts[e] = cnt[e];
+      run += cnt[e];
+    }
+    if (lane == 31) offsets[E] = incl;
+  }
+  __syncthreads();
+  const unsigned lt_mask = (1u << lane) - 1u;
+  for (int start = 0; start < P; start += kPermThreads) {
+    for (int x = tid; x < kPermWarps * E; x += kPermThreads) wcnt[x] = 0;
+    __syncthreads();
+    const int i = start + tid;
+    int e = i < P ? ids[i] : -1;
+    if (e >= E) e = -1;
+    const unsigned same = __match_any_sync(0xffffffffu, e);
+    const int lrank = __popc(same & lt_mask);
+    if (e >= 0 && lrank == 0) wcnt[warp * E + e] = __popc(same);
+    __syncthreads();
+    if (i < P) {
+      if (e >= 0) {
+        int pre = 0;
+        for (int w = 0; w < warp; ++w) pre += wcnt[w * E + e];
+        const int pos = base[e] + pre + lrank;
+        sorted_pairs[pos] = i;
+        pair_pos[i] = pos;
+      } else {
+        pair_pos[i] = -1;
+      }
+    }
+    __syncthreads();
+    for (int x = tid; x < E; x += kPermThreads) {
+      int s = 0;
+      for (int w = 0; w < kPermWarps; ++w) s += wcnt[w * E + x];
+      base[x] += s;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------- gather
+// One CTA per permuted row, 128-bit vectors (H % 8 == 0).
+__global__ void moe_gather_kernel(const uint4* __restrict__ x, int64_t hv, int topk,
+                                  const int32_t* __restrict__ sorted_pairs, const int32_t* __restrict__ row_limit,
+                                  uint4* __restrict__ xp) {
+  const int64_t p = blockIdx.x;
+  if (row_limit && p >= __ldg(row_limit)) return;
+  const int64_t t = __ldg(sorted_pairs + p) / topk;
+  const uint4* src = x + t * hv;
+  uint4* dst = xp + p * hv;
+  for (int64_t i = threadIdx.x; i < hv; i += blockDim.x) dst[i] = __ldg(src + i);
+}
+
+// ---------------------------------------------------------------------------------------- combine
+template <bool kBF16>
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if constexpr (kBF16) {
+      const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+      const float2 ff = __bfloat1622float2(h);
+      f[2 * i] = ff.x, f[2 * i + 1] = ff.y;
+    } else {
+      const __half2 h = *reinterpret_cast<const __half2*>(&w[i]);
+      const float2 ff = __half22float2(h);
+      f[2 * i] = ff.x, f[2 * i + 1] = ff.y;
+    }
+  }
+}
+
+template <bool kBF16>
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if constexpr (kBF16) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
+    } else {
+      __half2 h = __floats2half2_rn(f[2 * i], f[2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// One CTA per token; accumulate the k expert rows in slot order in fp32.
+template <bool kBF16>
+__global__ void moe_combine_kernel(const uint4* __restrict__ yp, int64_t hv, int topk,
+                                   const int32_t* __restrict__ pair_pos, const float* __restrict__ wts,
+                                   uint4* __restrict__ y) {
+  const int64_t t = blockIdx.x;
+  constexpr int kMaxK = 32;
+  __shared__ int pos[kMaxK];
+  __shared__ float wt[kMaxK];
+  if (threadIdx.x < topk) {
+    pos[threadIdx.x] = pair_pos[t * topk + threadIdx.x];
+    wt[threadIdx.x] = wts[t * topk + threadIdx.x];
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < hv; i += blockDim.x) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int j = 0; j < topk; ++j) {
+      if (pos[j] < 0) continue;
+      float f[8];
+      unpack8<kBF16>(__ldg(yp + static_cast<int64_t>(pos[j]) * hv + i), f);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = fmaf(wt[j], f[q], acc[q]);
+    }
+    y[t * hv + i] = pack8<kBF16>(acc);
+  }
+}
+
+}  // namespace w4
+
+using namespace w4;
+
+namespace {
+inline int64_t align256(int64_t b) { return (b + 255) & ~int64_t(255); }
+}  // namespace
+
+extern "C" {
+
+int w4a16_route_topk(const float* logits, int64_t T, int64_t E, int64_t k, int scoring, int renormalize,
+                     int32_t* topk_ids, float* topk_weights, cudaStream_t stream) {
+  if (!logits || !topk_ids || !topk_weights) return W4_ERR_ARG;
+  if (E <= 0 || E > 1024 || k <= 0 || k > 32 || k > E) return W4_ERR_SHAPE;
+  if (scoring != W4_SCORE_SOFTMAX && scoring != W4_SCORE_SIGMOID) return W4_ERR_ARG;
+  if (T <= 0) return W4_OK;
+  const int thr = 256;
+  const int64_t blocks = (T * 32 + thr - 1) / thr;
+  route_topk_kernel<<<blocks, thr, 0, stream>>>(logits, (int)T, (int)E, (int)k, scoring, renormalize, topk_ids,
+                                                topk_weights);
+  return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
+}
+
+int w4a16_moe_permute(const int32_t* topk_ids, int64_t P, int64_t E, int32_t* expert_counts,
+                      int32_t* expert_offsets, int32_t* sorted_pairs, int32_t* pair_pos, cudaStream_t stream) {
+  if (!topk_ids || !expert_counts || !expert_offsets || !sorted_pairs || !pair_pos) return W4_ERR_ARG;
+  if (E <= 0 || E > 1024 || P < 0 || P > (int64_t(1) << 30)) return W4_ERR_SHAPE;
+  const size_t smem = sizeof(int) * (2 * E + kPermWarps * E);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(moe_permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             sizeof(int) * (2 * 1024 + kPermWarps * 1024)) != cudaSuccess)
+      return W4_ERR_CUDA;
+    attr = true;
+  }
+  moe_permute_kernel<<<1, kPermThreads, smem, stream>>>(topk_ids, (int)P, (int)E, expert_counts, expert_offsets,
+                                                         sorted_pairs, pair_pos);
+  return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
+}
+
+int w4a16_moe_gather(const void* x, int64_t H, int64_t topk, const int32_t* sorted_pairs, int64_t rows,
+                     const int32_t* row_limit, void* x_perm, cudaStream_t stream) {
+  if (!x || !sorted_pairs || !x_perm) return W4_ERR_ARG;
+  if (H <= 0 || H % 8 || topk <= 0) return W4_ERR_SHAPE;
+  if (rows <= 0) return W4_OK;
+  moe_gather_kernel<<<rows, 128, 0, stream>>>(static_cast<const uint4*>(x), H / 8, (int)topk, sorted_pairs,
+                                               row_limit, static_cast<uint4*>(x_perm));
+  return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
+}
+
+int w4a16_moe_combine(const void* y_perm, int64_t T, int64_t H, int64_t topk, const int32_t* pair_pos,
+                      const float* topk_weights, int dtype, void* y, cudaStream_t stream) {
+  if (!y_perm || !pair_pos || !topk_weights || !y) return W4_ERR_ARG;
+  if (H <= 0 || H % 8 || topk <= 0 || topk > 32) return W4_ERR_SHAPE;
+  if (T <= 0) return W4_OK;
+  const int thr = 128;
+  if (dtype == W4_DTYPE_BF16)
+    moe_combine_kernel<true><<<T, thr, 0, stream>>>(static_cast<const uint4*>(y_perm), H / 8, (int)topk, pair_pos,
+                                                    topk_weights, static_cast<uint4*>(y));
+  else if (dtype == W4_DTYPE_F16)
+    moe_combine_kernel<false><<<T, thr, 0, stream>>>(static_cast<const uint4*>(y_perm), H / 8, (int)topk, pair_pos,
+                                                     topk_weights, static_cast<uint4*>(y));
+  else
+    return W4_ERR_DTYPE;
+  return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
+}
+
+int64_t w4a16_moe_workspace_bytes(int64_t T, int64_t topk, int64_t E, int64_t H, int64_t I) {
+  const int64_t P = T * topk;
+  return align256(4 * E) + align256(4 * (E + 1)) + 2 * align256(4 * P) + align256(2 * P * H) +
+         align256(2 * P * I) + align256(2 * P * H);
+}
+
+int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, int64_t topk,
+                      const int32_t* topk_ids, const float* topk_weights, const uint8_t* w13,
+                      const uint8_t* w2, int dtype, void* y, void* workspace, int64_t workspace_bytes,
+                      cudaStream_t stream) {
+  if (!x || !topk_ids || !topk_weights || !w13 || !w2 || !y || !workspace) return W4_ERR_ARG;
+  if (workspace_bytes < w4a16_moe_workspace_bytes(T, topk, E, H, I)) return W4_ERR_WORKSPACE;
+  if (T <= 0) return W4_OK;
+  const int64_t P = T * topk;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  int32_t* counts = reinterpret_cast<int32_t*>(ws); ws += align256(4 * E);
+  int32_t* offsets = reinterpret_cast<int32_t*>(ws); ws += align256(4 * (E + 1));
+  int32_t* sorted = reinterpret_cast<int32_t*>(ws); ws += align256(4 * P);
+  int32_t* pos = reinterpret_cast<int32_t*>(ws); ws += align256(4 * P);
+  void* xp = ws; ws += align256(2 * P * H);
+  void* hp = ws; ws += align256(2 * P * I);
+  void* yp = ws;
+  int rc;
+  if ((rc = w4a16_moe_permute(topk_ids, P, E, counts, offsets, sorted, pos, stream))) return rc;
+  if ((rc = w4a16_moe_gather(x, H, topk, sorted, P, offsets + E, xp, stream))) return rc;
+  const int nt = w4a16_pick_ntok(P, E);
+  if ((rc = w4a16_grouped_gemm(xp, P, H, w13, E, I, 1, counts, offsets, hp, dtype, nt, stream))) return rc;
+  if ((rc = w4a16_grouped_gemm(hp, P, I, w2, E, H, 0, counts, offsets, yp, dtype, nt, stream))) return rc;
+  return w4a16_moe_combine(yp, T, H, topk, pos, topk_weights, dtype, y, stream);
+}
+
+}  // extern "C"

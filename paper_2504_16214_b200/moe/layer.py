@@ -1,0 +1,97 @@
+"""MoE operator entry points (Python host side).
+
+The reference exposes no MoE operator (``/root/reference/pkg/src/tilesynth/__init__.py:16-58`` is
+layout synthesis only). The entry points mirror the call the paper's kernel is
+dropped into -- vLLM's ``fused_experts(hidden_states, w1, w2, topk_weights, topk_ids, ...)``
+(``vllm/model_executor/layers/fused_moe/fused_moe.py:1587-1597``) -- with AWQ int4 weights packed
+once by :mod:`.weights`:
+
+* :func:`moe_w4a16` -- routed experts for precomputed ``topk_weights`` / ``topk_ids``;
+* :func:`fused_moe_w4a16` -- router logits in, top-k routing on the device, then :func:`moe_w4a16`;
+* :func:`select_experts` -- the routing step alone.
+
+Pipeline (all on the current stream, no host synchronisation): permute -> gather -> gate/up
+grouped GEMM with fused SiLU*up -> down grouped GEMM -> weighted combine. With ``ep_group`` set
+the experts are sharded across ranks and tokens travel by all-to-all (:mod:`.ep`).
+"""
+from __future__ import annotations
+
+import torch
+
+from . import ops
+from .weights import MoEWeights
+
+
+def select_experts(router_logits: torch.Tensor, top_k: int, scoring: str = "softmax",
+                   renormalize: bool = False):
+    """-> (topk_weights fp32 [T, k], topk_ids int32 [T, k]); ties go to the lower expert id."""
+    ids, wts = ops.route_topk(router_logits.float().contiguous(), top_k, scoring, renormalize)
+    return wts, ids
+
+
+class _Workspace:
+    """Grow-only per-device scratch so steady-state calls allocate nothing."""
+
+    def __init__(self):
+        self.buf: dict[tuple, torch.Tensor] = {}
+
+    def get(self, name: str, shape, dtype, device) -> torch.Tensor:
+        n = 1
+        for s in shape:
+            n *= s
+        key = (name, dtype, str(device))
+        t = self.buf.get(key)
+        if t is None or t.numel() < n:
+            t = torch.empty(max(n, 1), dtype=dtype, device=device)
+            self.buf[key] = t
+        return t[:n].view(*shape)
+
+
+_ws = _Workspace()
+
+
+def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, topk_ids: torch.Tensor,
+              ep_group=None, ntok: int = 0) -> torch.Tensor:
+    """y[t] = sum_j topk_weights[t, j] * Expert_{topk_ids[t, j]}(x[t]) for the W4A16 SwiGLU experts.
+
+    ``x`` [T, H] fp16/bf16 on CUDA; ``topk_ids`` int32 [T, k]; ``topk_weights`` fp32 [T, k]."""
+    if ep_group is not None:
+        from .ep import moe_w4a16_ep
+        return moe_w4a16_ep(x, weights, topk_weights, topk_ids, ep_group, ntok=ntok)
+    T, H = x.shape
+    if H != weights.hidden:
+        raise ValueError(f"hidden size {H} != packed weights' {weights.hidden}")
+    if x.dtype != weights.w13.dtype:
+        raise ValueError(f"activation dtype {x.dtype} != weight scale dtype {weights.w13.dtype}")
+    x = x.contiguous()
+    topk_ids = topk_ids.to(torch.int32).contiguous()
+    topk_weights = topk_weights.to(torch.float32).contiguous()
+    k = topk_ids.shape[1]
+    E, I = weights.num_experts, weights.inter
+    P = T * k
+    dev = x.device
+    counts, offsets, sorted_pairs, pair_pos = ops.moe_permute(topk_ids, E)
+    xp = ops.moe_gather(x, sorted_pairs, k, P, offsets[E:], out=_ws.get("xp", (P, H), x.dtype, dev))
+    nt = ntok or ops.pick_ntok(P, E)
+    h = ops.grouped_gemm(xp, weights.w13.blocks, E, I, True, counts, offsets, nt,
+                         out=_ws.get("h", (P, I), x.dtype, dev))
+    yp = ops.grouped_gemm(h, weights.w2.blocks, E, H, False, counts, offsets, nt,
+                          out=_ws.get("yp", (P, H), x.dtype, dev))
+    return ops.moe_combine(yp, pair_pos, topk_weights)
+
+
+def fused_moe_w4a16(x: torch.Tensor, router_logits: torch.Tensor, weights: MoEWeights, top_k: int,
+                    scoring: str = "softmax", renormalize: bool = False, ep_group=None) -> torch.Tensor:
+    topk_weights, topk_ids = select_experts(router_logits, top_k, scoring, renormalize)
+    return moe_w4a16(x, weights, topk_weights, topk_ids, ep_group=ep_group)
+
+
+def w4a16_linear(x: torch.Tensor, w, ntok: int = 0) -> torch.Tensor:
+    """Dense W4A16 linear y = x @ W^T (one "expert"; BASELINE config 2). ``w`` is a PackedW4 with
+    num_experts == 1 and parts == 1."""
+    M, K = x.shape
+    dev = x.device
+    counts = torch.tensor([M], dtype=torch.int32, device=dev)
+    offsets = torch.tensor([0, M], dtype=torch.int32, device=dev)
+    return ops.grouped_gemm(x.contiguous(), w.blocks, 1, w.n_rows, False, counts, offsets,
+                            ntok or ops.pick_ntok(M, 1))

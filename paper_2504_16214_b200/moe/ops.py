@@ -1,0 +1,137 @@
+"""torch-tensor wrappers over the C ABI: each op validates, allocates outputs and launches on the
+current CUDA stream. Inputs must already be CUDA tensors; nothing here runs on the CPU."""
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+_ACT = {torch.float16: _lib.DTYPE_F16, torch.bfloat16: _lib.DTYPE_BF16}
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _need_cuda(*ts: torch.Tensor) -> None:
+    for t in ts:
+        if not t.is_cuda:
+            raise _lib.W4A16Error("W4A16 ops take CUDA tensors (no CPU fallback)")
+        if not t.is_contiguous():
+            raise _lib.W4A16Error("W4A16 ops take contiguous tensors")
+
+
+def act_code(dtype: torch.dtype) -> int:
+    try:
+        return _ACT[dtype]
+    except KeyError:
+        raise _lib.W4A16Error(f"activation dtype must be float16 or bfloat16, got {dtype}") from None
+
+
+# ------------------------------------------------------------------------------------------ weights
+def packed_bytes(num_experts: int, n_rows: int, K: int) -> int:
+    n = _lib.load().w4a16_packed_bytes(num_experts, n_rows, K)
+    if n < 0:
+        raise _lib.W4A16Error(f"n_rows={n_rows} and K={K} must be multiples of 128")
+    return n
+
+
+def repack_awq(qweight: torch.Tensor, scales: torch.Tensor, qzeros: torch.Tensor, parts: int,
+               group_size: int = 128) -> torch.Tensor:
+    """AWQ [E][K][N/8] int32 / [E][K/G][N] / [E][K/G][N/8] -> packed uint8 blocks."""
+    _need_cuda(qweight, scales, qzeros)
+    E, K, N8 = qweight.shape
+    N = N8 * 8
+    if scales.shape != (E, K // group_size, N) or qzeros.shape != (E, K // group_size, N8):
+        raise _lib.W4A16Error("AWQ scales/qzeros shapes do not match qweight")
+    out = torch.empty(packed_bytes(E, N, K), dtype=torch.uint8, device=qweight.device)
+    _lib.call("w4a16_repack_awq", qweight.data_ptr(), scales.data_ptr(), qzeros.data_ptr(), E, K, N, parts,
+              group_size, out.data_ptr(), _stream())
+    return out
+
+
+def dequant(blocks: torch.Tensor, num_experts: int, n_rows: int, K: int, parts: int,
+            dtype: torch.dtype) -> torch.Tensor:
+    _need_cuda(blocks)
+    out = torch.empty((num_experts, n_rows, K), dtype=dtype, device=blocks.device)
+    _lib.call("w4a16_dequant", blocks.data_ptr(), num_experts, n_rows, K, parts, act_code(dtype), out.data_ptr(),
+              _stream())
+    return out
+
+
+# ------------------------------------------------------------------------------------------ routing
+def route_topk(logits: torch.Tensor, k: int, scoring: str = "softmax", renormalize: bool = False):
+    _need_cuda(logits)
+    if logits.dtype != torch.float32:
+        raise _lib.W4A16Error("router logits must be float32")
+    T, E = logits.shape
+    ids = torch.empty((T, k), dtype=torch.int32, device=logits.device)
+    wts = torch.empty((T, k), dtype=torch.float32, device=logits.device)
+    sc = {"softmax": _lib.SCORE_SOFTMAX, "sigmoid": _lib.SCORE_SIGMOID}[scoring]
+    _lib.call("w4a16_route_topk", logits.data_ptr(), T, E, k, sc, int(renormalize), ids.data_ptr(), wts.data_ptr(),
+              _stream())
+    return ids, wts
+
+
+def moe_permute(topk_ids: torch.Tensor, num_experts: int):
+    """-> (expert_counts [E], expert_offsets [E+1], sorted_pairs [P], pair_pos [P]) int32."""
+    _need_cuda(topk_ids)
+    if topk_ids.dtype != torch.int32:
+        raise _lib.W4A16Error("topk_ids must be int32")
+    P = topk_ids.numel()
+    dev = topk_ids.device
+    counts = torch.empty(num_experts, dtype=torch.int32, device=dev)
+    offsets = torch.empty(num_experts + 1, dtype=torch.int32, device=dev)
+    sorted_pairs = torch.empty(max(P, 1), dtype=torch.int32, device=dev)
+    pair_pos = torch.empty(max(P, 1), dtype=torch.int32, device=dev)
+    _lib.call("w4a16_moe_permute", topk_ids.data_ptr(), P, num_experts, counts.data_ptr(), offsets.data_ptr(),
+              sorted_pairs.data_ptr(), pair_pos.data_ptr(), _stream())
+    return counts, offsets, sorted_pairs[:P], pair_pos[:P]
+
+
+def moe_gather(x: torch.Tensor, sorted_pairs: torch.Tensor, topk: int, rows: int | None = None,
+               row_limit: torch.Tensor | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+    _need_cuda(x, sorted_pairs)
+    act_code(x.dtype)
+    rows = sorted_pairs.numel() if rows is None else rows
+    H = x.shape[1]
+    if out is None:
+        out = torch.empty((rows, H), dtype=x.dtype, device=x.device)
+    _lib.call("w4a16_moe_gather", x.data_ptr(), H, topk, sorted_pairs.data_ptr(), rows, _ptr(row_limit),
+              out.data_ptr(), _stream())
+    return out
+
+
+def moe_combine(y_perm: torch.Tensor, pair_pos: torch.Tensor, topk_weights: torch.Tensor,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    _need_cuda(y_perm, pair_pos, topk_weights)
+    T, k = topk_weights.shape
+    H = y_perm.shape[1]
+    if out is None:
+        out = torch.empty((T, H), dtype=y_perm.dtype, device=y_perm.device)
+    _lib.call("w4a16_moe_combine", y_perm.data_ptr(), T, H, k, pair_pos.data_ptr(), topk_weights.data_ptr(),
+              act_code(y_perm.dtype), out.data_ptr(), _stream())
+    return out
+
+
+# ------------------------------------------------------------------------------------------ GEMM
+def grouped_gemm(x: torch.Tensor, blocks: torch.Tensor, num_experts: int, n_out: int, gated: bool,
+                 expert_counts: torch.Tensor, expert_offsets: torch.Tensor, ntok: int = 0,
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+    """out[off_e + m] = act(x[off_e + m] @ W_e^T) (gated: silu(gate) * up), per expert."""
+    _need_cuda(x, blocks, expert_counts, expert_offsets)
+    rows, K = x.shape
+    if out is None:
+        out = torch.empty((rows, n_out), dtype=x.dtype, device=x.device)
+    _lib.call("w4a16_grouped_gemm", x.data_ptr(), rows, K, blocks.data_ptr(), num_experts, n_out, int(gated),
+              expert_counts.data_ptr(), expert_offsets.data_ptr(), out.data_ptr(), act_code(x.dtype), ntok,
+              _stream())
+    return out
+
+
+def pick_ntok(rows: int, num_experts: int) -> int:
+    return _lib.load().w4a16_pick_ntok(rows, num_experts)

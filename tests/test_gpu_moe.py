@@ -1,0 +1,167 @@
+"""GPU parity tests: every CUDA kernel of the W4A16 MoE path against the CPU oracle
+(``oracle/moe_oracle.py``), called through the C ABI (ctypes) via the host wrappers.
+
+Bars (north star): bit-exact for dequantised weights, routing ids and permutation indices;
+rtol 1e-2 / atol 1e-2 for GEMM / layer outputs (fp32 accumulate)."""
+import numpy as np
+import pytest
+import torch
+
+import moe_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-2
+ATOL = 1e-2
+TDT = {"f16": torch.float16, "bf16": torch.bfloat16}
+
+
+def _ops():
+    from paper_2504_16214_b200.moe import ops
+    return ops
+
+
+def _to_dev_act(a: np.ndarray, dt: str) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(O.act_bits(a, dt))).view(TDT[dt]).cuda()
+
+
+def _from_dev_act(t: torch.Tensor, dt: str) -> np.ndarray:
+    return O.bits_to_f32(t.view(torch.int16).cpu().numpy().view(np.uint16), dt)
+
+
+def _packed(q, z, s, dt, gated):
+    from paper_2504_16214_b200.moe.weights import pack_awq
+    qw, sc, qz = O.to_awq(q, z, s)
+    return pack_awq(torch.from_numpy(qw).cuda(), _to_dev_act(sc, dt), torch.from_numpy(qz).cuda(), gated=gated)
+
+
+# ------------------------------------------------------------------------------------------- dequant
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+@pytest.mark.parametrize("gated", [False, True])
+def test_repack_dequant_bit_exact(dt, gated):
+    rng = np.random.default_rng(1)
+    E, N, K = 3, 256, 384
+    q, z, s = O.synth_awq_expert_weights(rng, E, N, K, dt)
+    s[0, 0, 0] = O.round_act(np.array([-0.75], np.float32), dt)[0]  # a negative scale and extreme codes too
+    q[0, 0, :8] = [0, 15, 0, 15, 7, 8, 15, 0]
+    w = _packed(q, z, s, dt, gated)
+    got = w.dense()
+    torch.cuda.synchronize()
+    want = O.dequant(q, z, s, dt)
+    got_bits = got.view(torch.int16).cpu().numpy().view(np.uint16)
+    want_bits = O.act_bits(want, dt)
+    assert got_bits.shape == want_bits.shape
+    assert np.array_equal(got_bits, want_bits)
+
+
+# ------------------------------------------------------------------------------------------- routing
+@pytest.mark.parametrize("scoring", ["softmax", "sigmoid"])
+@pytest.mark.parametrize("renorm", [False, True])
+@pytest.mark.parametrize("E,k", [(8, 2), (64, 6), (256, 8), (128, 8), (1000, 3)])
+def test_route_topk(scoring, renorm, E, k):
+    rng = np.random.default_rng(E * 7 + k)
+    T = 67
+    lg = rng.standard_normal((T, E)).astype(np.float32)
+    lg[3, :] = 0.25                                  # all tied -> ids 0..k-1
+    lg[5, E // 2] = lg[5, E // 3] = lg[5].max() + 1  # tie at the top
+    ids, w = _ops().route_topk(torch.from_numpy(lg).cuda(), k, scoring, renorm)
+    rid, rw = O.route_topk(lg, k, scoring, renorm)
+    assert np.array_equal(ids.cpu().numpy(), rid)
+    np.testing.assert_allclose(w.cpu().numpy(), rw, rtol=1e-5, atol=1e-6)
+
+
+# ------------------------------------------------------------------------------------------- permute
+@pytest.mark.parametrize("P,E", [(1, 4), (64 * 8, 256), (3000, 256), (5000, 7), (65536, 256), (2048, 1024)])
+def test_permute_bit_exact(P, E):
+    rng = np.random.default_rng(P + E)
+    ids = rng.integers(0, E, size=P).astype(np.int32)
+    if P > 10:
+        ids[::11] = -1        # dropped pairs (non-local experts)
+        ids[5::13] = E + 3    # out of range -> dropped
+    c, o, sp, pp = _ops().moe_permute(torch.from_numpy(ids).cuda(), E)
+    rc, ro, rsp, rpp = O.moe_permute(ids, E)
+    assert np.array_equal(c.cpu().numpy(), rc)
+    assert np.array_equal(o.cpu().numpy(), ro)
+    n = int(ro[-1])
+    assert np.array_equal(sp.cpu().numpy()[:n], rsp)
+    assert np.array_equal(pp.cpu().numpy(), rpp)
+
+
+# ------------------------------------------------------------------------------------------- gather / combine
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+def test_gather_combine(dt):
+    rng = np.random.default_rng(5)
+    T, k, E, H = 33, 4, 16, 7168
+    ids = np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
+    x = O.round_act(rng.standard_normal((T, H)).astype(np.float32) * 0.5, dt)
+    ops = _ops()
+    c, o, sp, pp = ops.moe_permute(torch.from_numpy(ids).cuda(), E)
+    xp = ops.moe_gather(_to_dev_act(x, dt), sp, k)
+    _, _, rsp, rpp = O.moe_permute(ids, E)
+    assert np.array_equal(_from_dev_act(xp, dt), x[rsp // k])
+    yp = O.round_act(rng.standard_normal((T * k, H)).astype(np.float32), dt)
+    w = rng.uniform(0, 1, (T, k)).astype(np.float32)
+    y = ops.moe_combine(_to_dev_act(yp, dt), pp, torch.from_numpy(w).cuda())
+    want = np.zeros((T, H), np.float32)
+    for j in range(k):
+        want += w[:, j:j + 1] * yp[rpp.reshape(T, k)[:, j]]
+    np.testing.assert_allclose(_from_dev_act(y, dt), O.round_act(want, dt), rtol=RTOL, atol=ATOL)
+
+
+# ------------------------------------------------------------------------------------------- grouped GEMM
+def _gemm_case(dt, gated, counts, K, N, ntok, seed=0):
+    rng = np.random.default_rng(seed)
+    E = len(counts)
+    rows = int(sum(counts))
+    q, z, s = O.synth_awq_expert_weights(rng, E, 2 * N if gated else N, K, dt)
+    w = _packed(q, z, s, dt, gated)
+    x = O.round_act(rng.standard_normal((rows, K)).astype(np.float32) * 0.5, dt)
+    cnt = np.asarray(counts, np.int32)
+    off = np.zeros(E + 1, np.int32)
+    np.cumsum(cnt, out=off[1:])
+    out = _ops().grouped_gemm(_to_dev_act(x, dt), w.blocks, E, N, gated, torch.from_numpy(cnt).cuda(),
+                              torch.from_numpy(off).cuda(), ntok)
+    torch.cuda.synchronize()
+    want = O.grouped_gemm(x, O.dequant(q, z, s, dt), cnt, off, dt, gated)
+    return _from_dev_act(out, dt), want
+
+
+@pytest.mark.parametrize("ntok", [16, 32, 64, 128])
+@pytest.mark.parametrize("gated", [False, True])
+def test_grouped_gemm_f16(ntok, gated):
+    got, want = _gemm_case("f16", gated, [5, 0, 17, 1, 40, 130], K=512, N=256, ntok=ntok)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("gated", [False, True])
+def test_grouped_gemm_bf16(gated):
+    got, want = _gemm_case("bf16", gated, [3, 16, 0, 33], K=384, N=384, ntok=16)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=2 * ATOL)
+
+
+def test_dense_w4a16_linear():
+    """Config 1 shape: M=16, N=K=1024, one expert."""
+    got, want = _gemm_case("f16", False, [16], K=1024, N=1024, ntok=16, seed=3)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+# ------------------------------------------------------------------------------------------- layer
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+@pytest.mark.parametrize("T,E,k,H,I", [(1, 8, 2, 256, 384), (24, 16, 4, 512, 256), (130, 8, 2, 256, 256),
+                                       (64, 32, 8, 256, 128)])
+def test_moe_layer(dt, T, E, k, H, I):
+    from paper_2504_16214_b200.moe import moe_w4a16, select_experts
+    from paper_2504_16214_b200.moe.weights import MoEWeights
+    rng = np.random.default_rng(T + E)
+    q13, z13, s13 = O.synth_awq_expert_weights(rng, E, 2 * I, H, dt)
+    q2, z2, s2 = O.synth_awq_expert_weights(rng, E, H, I, dt)
+    weights = MoEWeights(_packed(q13, z13, s13, dt, True), _packed(q2, z2, s2, dt, False))
+    x = O.round_act(rng.standard_normal((T, H)).astype(np.float32) * 0.5, dt)
+    lg = rng.standard_normal((T, E)).astype(np.float32)
+    wts, ids = select_experts(torch.from_numpy(lg).cuda(), k, "softmax", True)
+    y = moe_w4a16(_to_dev_act(x, dt), weights, wts, ids)
+    torch.cuda.synchronize()
+    rid, rw = O.route_topk(lg, k, "softmax", True)
+    assert np.array_equal(ids.cpu().numpy(), rid)
+    want = O.moe_forward(x, O.dequant(q13, z13, s13, dt), O.dequant(q2, z2, s2, dt), rid, rw, dt)
+    np.testing.assert_allclose(_from_dev_act(y, dt), want, rtol=RTOL, atol=ATOL)
