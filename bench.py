@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Benchmark: W4A16 MoE layer at DeepSeek-R1 shapes on 1..8 B200 (BASELINE.json ``metric``).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--tokens T] [--impl ours|reference]
+
+One *step* = one forward of the MoE layer (router logits -> top-8 routing -> permute -> gather ->
+gate/up grouped GEMM with fused SiLU*up -> down grouped GEMM -> weighted combine) over T tokens per
+rank, everything resident in HBM. N > 1 runs expert-parallel (torchrun, one rank per GPU, NCCL
+all-to-all dispatch/combine, 256/N experts per rank, T tokens per rank: weak scaling).
+
+Printed (rank 0, one JSON line): value = algorithmic HBM bytes of the whole job / max-over-ranks
+device time (GB/s) -- the decode regime is weight-bandwidth bound -- plus TFLOP/s, the per-kernel
+roofline of the dominant kernel (gate/up grouped GEMM), the end-to-end number through the public
+API with host buffers (``e2e``), the CPU oracle baseline (``cpu_baseline``), clocks and a small
+regime sweep (decode .. prefill). ``--impl reference`` times the CPU oracle port alone (the
+reference has no MoE kernel) on the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+# DeepSeek-R1 MoE layer (BASELINE.json configs[3])
+E_DS, K_DS, H_DS, I_DS = 256, 8, 7168, 2048
+METRIC = "W4A16 MoE layer TFLOP/s & HBM GB/s (% roofline), DeepSeek-R1 shapes, 1–8 B200"
+
+
+def w_bytes(n: int, k: int) -> int:
+    """AWQ weight-block bytes: int4 codes + fp16 scales + int4 zeros, group 128."""
+    return n * k // 2 + (k // 128) * n * 2 + (k // 128) * n // 2
+
+
+def layer_bytes(e_touched: int, T: int, H: int, I: int, k: int) -> int:
+    return e_touched * (w_bytes(2 * I, H) + w_bytes(H, I)) + 4 * T * H + 8 * T * k
+
+
+def layer_flops(T: int, k: int, H: int, I: int) -> int:
+    return 6 * T * k * H * I
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained"), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) >= 6:
+                try:
+                    rows.append((float(f[0]), float(f[1]), f[2:6]))
+                except ValueError:
+                    pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------------------------- CPU
+def cpu_oracle_sample(T: int, dtype: str = "f16", budget_s: float = 12.0, seed: int = 0):
+    """Time the numpy oracle (oracle/moe_oracle.py) on a bounded sample of the DS-R1 layer: the
+    first routed experts of a T-token batch, processed one expert at a time until ``budget_s`` of
+    CPU work; returns the algorithmic bytes/s of the processed experts."""
+    import numpy as np
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import moe_oracle as O
+    rng = np.random.default_rng(seed)
+    x = O.round_act(rng.standard_normal((T, H_DS)).astype(np.float32) * 0.5, dtype)
+    lg = rng.standard_normal((T, E_DS)).astype(np.float32)
+    ids, wts = O.route_topk(lg, K_DS, "softmax", True)
+    counts, offsets, sorted_pairs, _ = O.moe_permute(ids, E_DS)
+    xp = x[sorted_pairs // K_DS]
+    touched = [e for e in range(E_DS) if counts[e] > 0]
+    done_bytes, done_flops, n_exp, elapsed = 0, 0, 0, 0.0
+    for e in touched:
+        q13, z13, s13 = O.synth_awq_expert_weights(rng, 1, 2 * I_DS, H_DS, dtype)
+        q2, z2, s2 = O.synth_awq_expert_weights(rng, 1, H_DS, I_DS, dtype)
+        a, b = int(offsets[e]), int(offsets[e] + counts[e])
+        t0 = time.perf_counter()
+        w13 = O.dequant(q13[0], z13[0], s13[0], dtype)
+        acc = xp[a:b] @ w13.T
+        h = O.round_act(O.silu(acc[:, :I_DS]) * acc[:, I_DS:], dtype)
+        w2 = O.dequant(q2[0], z2[0], s2[0], dtype)
+        O.round_act(h @ w2.T, dtype)
+        elapsed += time.perf_counter() - t0
+        n_exp += 1
+        done_bytes += w_bytes(2 * I_DS, H_DS) + w_bytes(H_DS, I_DS) + 4 * (b - a) * H_DS
+        done_flops += 6 * (b - a) * H_DS * I_DS
+        if elapsed >= budget_s:
+            break
+    try:
+        import numpy.__config__ as npc  # noqa: F401
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    return {
+        "value": round(done_bytes / elapsed / 1e9, 3),
+        "unit": "GB/s",
+        "cores": cores,
+        "kind": "port",
+        "sample": (f"numpy oracle (oracle/moe_oracle.py, expert-at-a-time dequant + fp32 GEMM), "
+                   f"{n_exp} of {len(touched)} routed experts of the DeepSeek-R1 layer at T={T}, "
+                   f"{elapsed:.1f} s of CPU work; threads = BLAS default over {cores} host cores"),
+        "tflops": round(done_flops / elapsed / 1e12, 6),
+    }
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    vals = []
+    cb = None
+    for _ in range(args.warmup):
+        cpu_oracle_sample(args.tokens, budget_s=2.0)
+    for _ in range(args.steps):
+        cb = cpu_oracle_sample(args.tokens, budget_s=max(2.0, 20.0 / max(1, args.steps)))
+        vals.append(cb["value"])
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+        "config": {"workload": f"deepseek_r1_moe_layer_T{args.tokens}", "E": E_DS, "topk": K_DS, "hidden": H_DS,
+                   "moe_inter": I_DS, "tokens_per_rank": args.tokens, "group_size": 128},
+        "cpu_baseline": {**cb, "value": v},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": ("the reference (tilesynth) has no MoE kernel: this arm is the CPU oracle port of the "
+                 "numeric path (DESIGN.md §Oracle)"),
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# --------------------------------------------------------------------------------------------- GPU
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--tokens", type=int, default=64, help="tokens per rank (decode batch)")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--dtype", choices=["f16", "bf16"], default="f16")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2504_16214_b200.moe import fused_moe_w4a16, random_moe_weights
+    from paper_2504_16214_b200.moe.layer import KernelTimer
+    from paper_2504_16214_b200.moe.ep import shard_bounds
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    tdt = torch.float16 if args.dtype == "f16" else torch.bfloat16
+    T = args.tokens
+    lo, hi = shard_bounds(E_DS, world, rank)
+    weights = random_moe_weights(hi - lo, H_DS, I_DS, tdt, device=dev, seed=1234 + rank)
+    g = torch.Generator(device="cpu")
+    g.manual_seed(rank)
+    x_host = (torch.randn((T, H_DS), generator=g) * 0.5).to(tdt).pin_memory()
+    lg_host = torch.randn((T, E_DS), generator=g).pin_memory()
+    x = x_host.to(dev)
+    lg = lg_host.to(dev)
+
+    def step(timer=None, xx=x, ll=lg):
+        return fused_moe_w4a16(xx, ll, weights, K_DS, "softmax", True, ep_group=group, timer=timer)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v: int) -> int:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.int64)
+        dist.all_reduce(t)
+        return int(t.item())
+
+    # experts touched (whole job): union over ranks of routed experts
+    from paper_2504_16214_b200.moe import select_experts
+    _, ids = select_experts(lg, K_DS, "softmax", True)
+    touched = torch.zeros(E_DS, dtype=torch.int32, device=dev)
+    touched[ids.long().flatten()] = 1
+    if world > 1:
+        dist.all_reduce(touched, op=dist.ReduceOp.MAX)
+    e_touched = int(touched.sum().item())
+    T_job = T * world
+    job_bytes = layer_bytes(e_touched, T_job, H_DS, I_DS, K_DS)
+    job_flops = layer_flops(T_job, K_DS, H_DS, I_DS)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    timer = KernelTimer()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record()
+        for _ in range(args.steps):
+            step(timer)
+        ev1.record()
+        barrier()
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    ms = ms_total / args.steps
+    value = job_bytes / (ms * 1e-3) / 1e9
+    tflops = job_flops / (ms * 1e-3) / 1e12
+    hbm_peak, tc_peak, tc_sus, peak_src = peaks()
+
+    # dominant kernel: gate/up grouped GEMM (2/3 of the weight bytes). Algorithmic bytes per launch
+    # = this rank's touched W13 blocks + X_perm read + H write.
+    per_rank_touched = int(touched[lo:hi].sum().item()) if world > 1 else e_touched
+    k_bytes = per_rank_touched * w_bytes(2 * I_DS, H_DS) + T_job * K_DS // world * (H_DS + I_DS) * 2
+    k_ms = timer.mean_ms("gemm_gate_up")
+    k_gbs = k_bytes / (k_ms * 1e-3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "traffic.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get(f"gemm_gate_up_T{T}")
+    launches_per_step = timer.count() // args.steps
+
+    # ---- end to end through the public API with host buffers (H2D inputs, D2H output)
+    y_host = torch.empty((T, H_DS), dtype=tdt).pin_memory()
+    for _ in range(2):
+        xx = x_host.to(dev, non_blocking=True)
+        ll = lg_host.to(dev, non_blocking=True)
+        y_host.copy_(step(None, xx, ll), non_blocking=True)
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        xx = x_host.to(dev, non_blocking=True)
+        ll = lg_host.to(dev, non_blocking=True)
+        y_host.copy_(step(None, xx, ll), non_blocking=True)
+    e1.record()
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    e2e = {"value": round(job_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+           "h2d_bytes_per_step": x_host.numel() * x_host.element_size() + lg_host.numel() * 4,
+           "d2h_bytes_per_step": y_host.numel() * y_host.element_size(), "ms_per_step": round(e2e_ms, 4),
+           "api": "paper_2504_16214_b200.moe.fused_moe_w4a16"}
+
+    # ---- regime sweep (1 GPU only): decode .. prefill, same weights
+    sweep = []
+    if world == 1 and not args.no_sweep:
+        for Ts in (1, 16, 256, 1024, 4096, 8192):
+            xs = (torch.randn((Ts, H_DS), generator=g) * 0.5).to(tdt).to(dev)
+            ls = torch.randn((Ts, E_DS), generator=g).to(dev)
+            _, sid = select_experts(ls, K_DS, "softmax", True)
+            et = int(torch.unique(sid).numel())
+            for _ in range(2):
+                fused_moe_w4a16(xs, ls, weights, K_DS, "softmax", True)
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            reps = 5
+            a.record()
+            for _ in range(reps):
+                fused_moe_w4a16(xs, ls, weights, K_DS, "softmax", True)
+            b.record()
+            torch.cuda.synchronize()
+            sm = a.elapsed_time(b) / reps
+            by, fl = layer_bytes(et, Ts, H_DS, I_DS, K_DS), layer_flops(Ts, K_DS, H_DS, I_DS)
+            sweep.append({"tokens": Ts, "experts_touched": et, "ms": round(sm, 4),
+                          "GB/s": round(by / sm / 1e6, 1), "TFLOP/s": round(fl / sm / 1e9, 2),
+                          "hbm_frac": round(by / sm / 1e6 / hbm_peak, 4),
+                          "tc_frac": round(fl / sm / 1e9 / tc_peak, 4)})
+            del xs, ls
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_oracle_sample(T, args.dtype)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": f"deepseek_r1_moe_layer_T{T}", "E": E_DS, "topk": K_DS, "hidden": H_DS,
+                       "moe_inter": I_DS, "tokens_per_rank": T, "tokens_job": T_job, "group_size": 128,
+                       "parallelism": f"ep{world}", "experts_touched": e_touched,
+                       "l2": "no flush: 5.9 GB of packed weights per step >> 126 MB L2",
+                       "bytes_per_step": job_bytes, "flops_per_step": job_flops},
+            "tflops": round(tflops, 3),
+            "hbm_frac": round(value / hbm_peak, 4),
+            "roofline": {"bound": "hbm", "kernel": "w4a16_moe_gemm_kernel (gate/up, fused SiLU*up)",
+                         "achieved": round(k_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
+                         "frac": round(k_gbs / hbm_peak, 4), "traffic": traffic,
+                         "algorithmic_bytes_per_launch": k_bytes, "ms_per_launch": round(k_ms, 4),
+                         "peak_source": peak_src},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": launches_per_step * args.steps,
+            "kernel_ms": {n: round(timer.mean_ms(n), 4) for n in timer.events},
+            "sweep": sweep,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

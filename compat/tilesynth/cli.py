@@ -1,0 +1,10 @@
+"""Compat alias: reference module ``tilesynth.cli`` -> ``paper_2504_16214_b200.tilesynth.cli``
+(also runnable as ``python -m tilesynth.cli``)."""
+import sys as _sys
+
+from paper_2504_16214_b200.tilesynth import cli as _m
+
+if __name__ == "__main__":
+    _sys.exit(_m.main())
+else:
+    _sys.modules[__name__] = _m

@@ -1,0 +1,6 @@
+"""Compat alias: reference module ``tilesynth.ir`` -> ``paper_2504_16214_b200.tilesynth.program``."""
+import sys as _sys
+
+from paper_2504_16214_b200.tilesynth import program as _m
+
+_sys.modules[__name__] = _m

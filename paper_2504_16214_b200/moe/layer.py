@@ -50,14 +50,62 @@ class _Workspace:
 _ws = _Workspace()
 
 
+class KernelTimer:
+    """Optional per-kernel CUDA-event recorder (used by bench.py to time the dominant kernel live
+    on the launching stream). ``timer.mark(name)`` brackets the next launch."""
+
+    def __init__(self):
+        self.events: dict[str, list] = {}
+
+    def span(self, name: str):
+        timer = self
+
+        class _Span:
+            def __enter__(self):
+                self.a = torch.cuda.Event(enable_timing=True)
+                self.b = torch.cuda.Event(enable_timing=True)
+                self.a.record()
+
+            def __exit__(self, *exc):
+                self.b.record()
+                timer.events.setdefault(name, []).append((self.a, self.b))
+
+        return _Span()
+
+    def mean_ms(self, name: str) -> float:
+        ev = self.events.get(name, [])
+        return sum(a.elapsed_time(b) for a, b in ev) / max(1, len(ev))
+
+    def count(self) -> int:
+        return sum(len(v) for v in self.events.values())
+
+
+class _NoTimer:
+    class _Null:
+        def __enter__(self):
+            return None
+
+        def __exit__(self, *exc):
+            return False
+
+    _null = _Null()
+
+    def span(self, name):
+        return self._null
+
+
+_NOTIMER = _NoTimer()
+
+
 def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, topk_ids: torch.Tensor,
-              ep_group=None, ntok: int = 0) -> torch.Tensor:
+              ep_group=None, ntok: int = 0, timer: KernelTimer | None = None) -> torch.Tensor:
     """y[t] = sum_j topk_weights[t, j] * Expert_{topk_ids[t, j]}(x[t]) for the W4A16 SwiGLU experts.
 
     ``x`` [T, H] fp16/bf16 on CUDA; ``topk_ids`` int32 [T, k]; ``topk_weights`` fp32 [T, k]."""
     if ep_group is not None:
         from .ep import moe_w4a16_ep
-        return moe_w4a16_ep(x, weights, topk_weights, topk_ids, ep_group, ntok=ntok)
+        return moe_w4a16_ep(x, weights, topk_weights, topk_ids, ep_group, ntok=ntok, timer=timer)
+    tm = timer or _NOTIMER
     T, H = x.shape
     if H != weights.hidden:
         raise ValueError(f"hidden size {H} != packed weights' {weights.hidden}")
@@ -70,20 +118,27 @@ def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, 
     E, I = weights.num_experts, weights.inter
     P = T * k
     dev = x.device
-    counts, offsets, sorted_pairs, pair_pos = ops.moe_permute(topk_ids, E)
-    xp = ops.moe_gather(x, sorted_pairs, k, P, offsets[E:], out=_ws.get("xp", (P, H), x.dtype, dev))
+    with tm.span("permute"):
+        counts, offsets, sorted_pairs, pair_pos = ops.moe_permute(topk_ids, E)
+    with tm.span("gather"):
+        xp = ops.moe_gather(x, sorted_pairs, k, P, offsets[E:], out=_ws.get("xp", (P, H), x.dtype, dev))
     nt = ntok or ops.pick_ntok(P, E)
-    h = ops.grouped_gemm(xp, weights.w13.blocks, E, I, True, counts, offsets, nt,
-                         out=_ws.get("h", (P, I), x.dtype, dev))
-    yp = ops.grouped_gemm(h, weights.w2.blocks, E, H, False, counts, offsets, nt,
-                          out=_ws.get("yp", (P, H), x.dtype, dev))
-    return ops.moe_combine(yp, pair_pos, topk_weights)
+    with tm.span("gemm_gate_up"):
+        h = ops.grouped_gemm(xp, weights.w13.blocks, E, I, True, counts, offsets, nt,
+                             out=_ws.get("h", (P, I), x.dtype, dev))
+    with tm.span("gemm_down"):
+        yp = ops.grouped_gemm(h, weights.w2.blocks, E, H, False, counts, offsets, nt,
+                              out=_ws.get("yp", (P, H), x.dtype, dev))
+    with tm.span("combine"):
+        return ops.moe_combine(yp, pair_pos, topk_weights)
 
 
 def fused_moe_w4a16(x: torch.Tensor, router_logits: torch.Tensor, weights: MoEWeights, top_k: int,
-                    scoring: str = "softmax", renormalize: bool = False, ep_group=None) -> torch.Tensor:
-    topk_weights, topk_ids = select_experts(router_logits, top_k, scoring, renormalize)
-    return moe_w4a16(x, weights, topk_weights, topk_ids, ep_group=ep_group)
+                    scoring: str = "softmax", renormalize: bool = False, ep_group=None,
+                    timer: KernelTimer | None = None) -> torch.Tensor:
+    with (timer or _NOTIMER).span("route"):
+        topk_weights, topk_ids = select_experts(router_logits, top_k, scoring, renormalize)
+    return moe_w4a16(x, weights, topk_weights, topk_ids, ep_group=ep_group, timer=timer)
 
 
 def w4a16_linear(x: torch.Tensor, w, ntok: int = 0) -> torch.Tensor:

@@ -81,23 +81,31 @@ def pack_moe_awq(w13_qweight, w13_scales, w13_qzeros, w2_qweight, w2_scales, w2_
                       pack_awq(w2_qweight, w2_scales, w2_qzeros, False, group_size))
 
 
+def random_packed(E: int, N: int, K: int, gated: bool, dtype: torch.dtype, generator: torch.Generator,
+                  device="cuda", chunk: int = 16) -> PackedW4:
+    """Synthetic AWQ weights generated on the device in expert chunks (q, z ~ U{0..15} from random
+    bytes; scales ~ U(0.5, 1.5) * 2^-7) and packed straight into one buffer."""
+    parts = 2 if gated else 1
+    per = ops.packed_bytes(1, N, K)
+    blocks = torch.empty(E * per, dtype=torch.uint8, device=device)
+    for e0 in range(0, E, chunk):
+        n = min(chunk, E - e0)
+        qw = torch.randint(0, 256, (n, K, N // 2), generator=generator, device=device,
+                           dtype=torch.uint8).view(torch.int32)
+        qz = torch.randint(0, 256, (n, K // 128, N // 2), generator=generator, device=device,
+                           dtype=torch.uint8).view(torch.int32)
+        sc = ((torch.rand((n, K // 128, N), generator=generator, device=device) + 0.5) * (2.0 ** -7)).to(dtype)
+        out = blocks[e0 * per:(e0 + n) * per]
+        from . import _lib
+        _lib.call("w4a16_repack_awq", qw.data_ptr(), sc.data_ptr(), qz.data_ptr(), n, K, N, parts, 128,
+                  out.data_ptr(), ops._stream())
+        del qw, qz, sc
+    return PackedW4(blocks, E, N, K, parts, dtype)
+
+
 def random_moe_weights(E: int, H: int, I: int, dtype: torch.dtype, device="cuda", seed: int = 0) -> MoEWeights:
-    """Synthetic AWQ weights of the named shapes generated on the device (q, z ~ U{0..15};
-    scales ~ U(0.5, 1.5) * 2^-7), then packed. Used for benchmarks at full size."""
+    """Synthetic packed MoE weights of the named shapes (benchmarks at full size)."""
     g = torch.Generator(device=device)
     g.manual_seed(seed)
-
-    def one(N, K):
-        qw = torch.randint(-2**31, 2**31 - 1, (E, K, N // 8), generator=g, device=device, dtype=torch.int64)
-        qw = qw.to(torch.int32)
-        qz = torch.randint(-2**31, 2**31 - 1, (E, K // 128, N // 8), generator=g, device=device,
-                           dtype=torch.int64).to(torch.int32)
-        sc = (torch.rand((E, K // 128, N), generator=g, device=device) + 0.5) * (2.0 ** -7)
-        return qw, sc.to(dtype), qz
-
-    a = one(2 * I, H)
-    w13 = pack_awq(*a, gated=True)
-    del a
-    b = one(H, I)
-    w2 = pack_awq(*b, gated=False)
-    return MoEWeights(w13, w2)
+    return MoEWeights(random_packed(E, 2 * I, H, True, dtype, g, device),
+                      random_packed(E, H, I, False, dtype, g, device))
