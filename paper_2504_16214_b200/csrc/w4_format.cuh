@@ -51,13 +51,35 @@ struct Dq<false> {
   struct Ctx {
     __half2 zz, zz16, sixteenth, s2;
   };
+  // all constants are built from integer bit patterns: 1024 + z = 0x6400 | z,
+  // -(64 + z) = 0xD400 | (z << 4), 1/16 = 0x2C00 (no int->float->half conversions)
   static __device__ __forceinline__ Ctx make(uint32_t z, uint16_t sbits) {
     Ctx c;
-    c.zz = __half2half2(__ushort_as_half(static_cast<unsigned short>(0x6400u | z)));
-    c.zz16 = __half2half2(__float2half_rn(-(64.0f + static_cast<float>(z))));
-    c.sixteenth = __half2half2(__ushort_as_half(static_cast<unsigned short>(0x2C00u)));  // 1/16
-    c.s2 = __half2half2(__ushort_as_half(sbits));
+    const uint32_t zz = (0x6400u | z) * 0x10001u, zz16 = (0xD400u | (z << 4)) * 0x10001u;
+    const uint32_t sx = 0x2C002C00u, s2 = static_cast<uint32_t>(sbits) * 0x10001u;
+    c.zz = *reinterpret_cast<const __half2*>(&zz);
+    c.zz16 = *reinterpret_cast<const __half2*>(&zz16);
+    c.sixteenth = *reinterpret_cast<const __half2*>(&sx);
+    c.s2 = *reinterpret_cast<const __half2*>(&s2);
     return c;
+  }
+  // exact (q - z) pairs only (the scale is applied to the fp32 group partial by the epilogue)
+  static __device__ __forceinline__ void word_qz(uint32_t w, const Ctx& c, uint32_t* o) {
+    const uint32_t kMagic = 0x64006400u;
+    uint32_t a, b, d, e;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(a) : "r"(w), "r"(0x000F000Fu), "r"(kMagic));
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(b) : "r"(w), "r"(0x00F000F0u), "r"(kMagic));
+    const uint32_t w8 = w >> 8;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(w8), "r"(0x000F000Fu), "r"(kMagic));
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(e) : "r"(w8), "r"(0x00F000F0u), "r"(kMagic));
+    __half2 q01 = __hsub2(*reinterpret_cast<__half2*>(&a), c.zz);
+    __half2 q23 = __hfma2(*reinterpret_cast<__half2*>(&b), c.sixteenth, c.zz16);
+    __half2 q45 = __hsub2(*reinterpret_cast<__half2*>(&d), c.zz);
+    __half2 q67 = __hfma2(*reinterpret_cast<__half2*>(&e), c.sixteenth, c.zz16);
+    o[0] = *reinterpret_cast<uint32_t*>(&q01);
+    o[1] = *reinterpret_cast<uint32_t*>(&q23);
+    o[2] = *reinterpret_cast<uint32_t*>(&q45);
+    o[3] = *reinterpret_cast<uint32_t*>(&q67);
   }
   static __device__ __forceinline__ void word(uint32_t w, const Ctx& c, uint32_t* o) {
     const uint32_t kMagic = 0x64006400u;
@@ -90,9 +112,20 @@ struct Dq<true> {
   };
   static __device__ __forceinline__ Ctx make(uint32_t z, uint16_t sbits) {
     Ctx c;
-    c.zz = __bfloat162bfloat162(__ushort_as_bfloat16(static_cast<unsigned short>(0x4300u | z)));
-    c.s2 = __bfloat162bfloat162(__ushort_as_bfloat16(sbits));
+    const uint32_t zz = (0x4300u | z) * 0x10001u, s2 = static_cast<uint32_t>(sbits) * 0x10001u;
+    c.zz = *reinterpret_cast<const __nv_bfloat162*>(&zz);
+    c.s2 = *reinterpret_cast<const __nv_bfloat162*>(&s2);
     return c;
+  }
+  static __device__ __forceinline__ void word_qz(uint32_t w, const Ctx& c, uint32_t* o) {
+    const uint32_t kMagic = 0x43004300u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint32_t x;
+      asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(x) : "r"(w >> (4 * i)), "r"(0x000F000Fu), "r"(kMagic));
+      __nv_bfloat162 q = __hsub2(*reinterpret_cast<__nv_bfloat162*>(&x), c.zz);
+      o[i] = *reinterpret_cast<uint32_t*>(&q);
+    }
   }
   static __device__ __forceinline__ void word(uint32_t w, const Ctx& c, uint32_t* o) {
     const uint32_t kMagic = 0x43004300u;
@@ -107,13 +140,37 @@ struct Dq<true> {
   }
 };
 
-// Dequantise one 16 B chunk (32 consecutive k of one row) into 16 packed pairs, k order.
-template <bool kBF16>
+// Dequantise one 16 B chunk (32 consecutive k of one row) into 16 packed pairs, k order:
+// kScaled -> act((q - z) * s) (bit-exact dequant); otherwise the exact integers (q - z).
+template <bool kBF16, bool kScaled = true>
 __device__ __forceinline__ void dequant_chunk(const uint4& v, const typename Dq<kBF16>::Ctx& c, uint32_t (&o)[16]) {
-  Dq<kBF16>::word(v.x, c, o + 0);
-  Dq<kBF16>::word(v.y, c, o + 4);
-  Dq<kBF16>::word(v.z, c, o + 8);
-  Dq<kBF16>::word(v.w, c, o + 12);
+  if constexpr (kScaled) {
+    Dq<kBF16>::word(v.x, c, o + 0);
+    Dq<kBF16>::word(v.y, c, o + 4);
+    Dq<kBF16>::word(v.z, c, o + 8);
+    Dq<kBF16>::word(v.w, c, o + 12);
+  } else {
+    Dq<kBF16>::word_qz(v.x, c, o + 0);
+    Dq<kBF16>::word_qz(v.y, c, o + 4);
+    Dq<kBF16>::word_qz(v.z, c, o + 8);
+    Dq<kBF16>::word_qz(v.w, c, o + 12);
+  }
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
 }
 
 }  // namespace w4

@@ -39,25 +39,33 @@ struct GemmArgs {
   int num_experts, nt, kt;
 };
 
-template <int kNTok, bool kGated>
+// kScaleEpi (decode, small token tiles): the dequant warps produce the exact integers (q - z) and
+// the MMA writes one fp32 partial per k-tile (= per quantisation group) into a TMEM ring; the
+// epilogue warps fold acc += s[row, g] * partial in registers. This removes the per-weight HMUL2
+// from the dequant (the scale is applied once per group per output instead of once per weight)
+// and is numerically at least as accurate as dequantise-then-MMA. Otherwise (prefill, large token
+// tiles) the dequant applies the scale and the MMA accumulates across k-tiles in TMEM.
+template <int kNTok, bool kGated, bool kScaleEpi>
 struct Cfg {
   static constexpr int kParts = kGated ? 2 : 1;
   static constexpr int kBlk = kParts * kPartBytes;
   static constexpr int kXBytes = kNTok * kTileK * 2;  // bf16/fp16 X tile, two 64-wide swizzle atoms
-  static constexpr int kAccCols = kGated ? 2 * kNTok : kNTok;
+  static constexpr int kAccCols = kParts * kNTok;       // one accumulator / partial stage
   static constexpr int kACols = kParts * (kTileK / 2);  // fp16 pairs per 32-bit column
-  static constexpr int kNumAcc = (2 * kAccCols + 2 * kACols <= 512) ? 2 : 1;
+  static constexpr int kNumAcc = kScaleEpi ? 4 : ((2 * kAccCols + 2 * kACols <= 512) ? 2 : 1);
   static constexpr int kNumA0 = (512 - kNumAcc * kAccCols) / kACols;
   static constexpr int kNumA = kNumA0 > 4 ? 4 : kNumA0;
   static constexpr int kStageBytes = kBlk + kXBytes;
   static constexpr int kFixed = 2048 + 4 * (kMaxExperts + 1);  // barriers + tile table
   static constexpr int kNS0 = (kSmemBudget - kFixed - 1024) / kStageBytes;
   static constexpr int kNS = kNS0 > 12 ? 12 : kNS0;
+  static constexpr int kEmptyArrivals = kNumDequantWarps + 1 + (kScaleEpi ? 4 : 0);
   // X ring first (needs 1024 B alignment for the 128B swizzle atoms), then weights.
   static constexpr int kSmemBytes = 1024 + kNS * kStageBytes + kFixed;
   static_assert(kNumA >= 2, "TMEM budget");
   static_assert(kNS >= 2, "smem budget");
   static_assert(kXBytes % 1024 == 0, "X tile alignment");
+  static_assert(!kScaleEpi || kNTok <= 32, "register accumulators");
 };
 
 struct TileInfo {
@@ -94,10 +102,24 @@ __device__ __forceinline__ uint16_t to_act_bits(float v) {
   else return __half_as_ushort(__float2half_rn(v));
 }
 
-template <int kNTok, bool kGated, bool kBF16>
+template <bool kBF16>
+__device__ __forceinline__ float act_bits_to_float(uint32_t b) {
+  if constexpr (kBF16) return __uint_as_float(b << 16);
+  else return __half2float(__ushort_as_half(static_cast<unsigned short>(b)));
+}
+
+struct Ring {  // (stage, phase) iterator of an mbarrier ring
+  int i = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++i == n) { i = 0; ph ^= 1; }
+  }
+};
+
+template <int kNTok, bool kGated, bool kBF16, bool kScaleEpi>
 __global__ void __launch_bounds__(kNumThreads, 1)
     w4a16_moe_gemm_kernel(const GemmArgs args, const __grid_constant__ CUtensorMap xmap) {
-  using C = Cfg<kNTok, kGated>;
+  using C = Cfg<kNTok, kGated, kScaleEpi>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_x = smem;                                  // [NS][kXBytes]
@@ -118,7 +140,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   if (warp == 0) {
     tmem_alloc<512>(tmem_holder);
   } else if (warp == 1 && lane == 0) {
-    for (int i = 0; i < C::kNS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], kNumDequantWarps + 1); }
+    for (int i = 0; i < C::kNS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], C::kEmptyArrivals); }
     for (int i = 0; i < C::kNumA; ++i) { mbar_init(&afull[i], kNumDequantWarps); mbar_init(&aempty[i], 1); }
     for (int i = 0; i < C::kNumAcc; ++i) { mbar_init(&accfull[i], 1); mbar_init(&accempty[i], 4); }
     fence_mbar_init();
@@ -149,25 +171,26 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
   constexpr uint32_t kAcol0 = C::kNumAcc * C::kAccCols;  // first column of the TMEM A ring
+  const uint32_t w_u32 = smem_u32(smem_w);
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       const uint64_t pol_w = policy_evict_first();
-      int s = 0;
-      uint32_t ph = 0;
+      Ring st;
       TileInfo ti;
       for (int t = blockIdx.x; get_tile<kNTok>(t, mt_off, args, ti); t += gridDim.x) {
         const uint8_t* wsrc = args.wblocks + (static_cast<int64_t>(ti.e) * args.nt + ti.n_tile) *
                                                  static_cast<int64_t>(args.kt) * C::kBlk;
         for (int kt = 0; kt < args.kt; ++kt) {
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], C::kBlk + C::kXBytes);
-          bulk_g2s_hint(smem_w + s * C::kBlk, wsrc + static_cast<int64_t>(kt) * C::kBlk, C::kBlk, &full[s], pol_w);
-          uint8_t* xs = smem_x + s * C::kXBytes;
-          tma_load_2d(xs, &xmap, kt * kTileK, ti.m_start, &full[s]);
-          tma_load_2d(xs + kNTok * 128, &xmap, kt * kTileK + 64, ti.m_start, &full[s]);
-          if (++s == C::kNS) { s = 0; ph ^= 1; }
+          mbar_wait(&empty[st.i], st.ph ^ 1);
+          mbar_arrive_expect_tx(&full[st.i], C::kBlk + C::kXBytes);
+          bulk_g2s_hint(smem_w + st.i * C::kBlk, wsrc + static_cast<int64_t>(kt) * C::kBlk, C::kBlk, &full[st.i],
+                        pol_w);
+          uint8_t* xs = smem_x + st.i * C::kXBytes;
+          tma_load_2d(xs, &xmap, kt * kTileK, ti.m_start, &full[st.i]);
+          tma_load_2d(xs + kNTok * 128, &xmap, kt * kTileK + 64, ti.m_start, &full[st.i]);
+          st.next(C::kNS);
         }
       }
     }
@@ -175,77 +198,93 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = make_idesc_f16(128, kNTok, kBF16);
-      int s = 0, j = 0, a = 0;
-      uint32_t ph = 0, aph = 0, acph = 0;
+      Ring st, ar, acc;
       TileInfo ti;
       for (int t = blockIdx.x; get_tile<kNTok>(t, mt_off, args, ti); t += gridDim.x) {
-        mbar_wait(&accempty[a], acph ^ 1);
-        tc_fence_after();
-        const uint32_t dcol = tbase + a * C::kAccCols;
-        for (int kt = 0; kt < args.kt; ++kt) {
-          mbar_wait(&full[s], ph);
-          mbar_wait(&afull[j], aph);
+        if constexpr (!kScaleEpi) {
+          mbar_wait(&accempty[acc.i], acc.ph ^ 1);
           tc_fence_after();
-          const uint32_t xaddr = smem_u32(smem_x + s * C::kXBytes);
-          const uint32_t acol = tbase + kAcol0 + j * C::kACols;
+        }
+        for (int kt = 0; kt < args.kt; ++kt) {
+          if constexpr (kScaleEpi) {  // one fresh partial per k-tile (= per group)
+            mbar_wait(&accempty[acc.i], acc.ph ^ 1);
+          }
+          mbar_wait(&full[st.i], st.ph);
+          mbar_wait(&afull[ar.i], ar.ph);
+          tc_fence_after();
+          const uint32_t dcol = tbase + acc.i * C::kAccCols;
+          const uint32_t xaddr = smem_u32(smem_x + st.i * C::kXBytes);
+          const uint32_t acol = tbase + kAcol0 + ar.i * C::kACols;
 #pragma unroll
           for (int kk = 0; kk < kTileK / 16; ++kk) {
             const uint64_t bdesc = make_sdesc_sw128(xaddr + (kk >> 2) * (kNTok * 128) + (kk & 3) * 32);
-            const uint32_t acc = (kt | kk) != 0;
-            umma_ts_f16(dcol, acol + kk * 8, bdesc, idesc, acc);
-            if constexpr (kGated) umma_ts_f16(dcol + kNTok, acol + 64 + kk * 8, bdesc, idesc, acc);
+            const uint32_t accum = kScaleEpi ? (kk != 0) : ((kt | kk) != 0);
+            umma_ts_f16(dcol, acol + kk * 8, bdesc, idesc, accum);
+            if constexpr (kGated) umma_ts_f16(dcol + kNTok, acol + 64 + kk * 8, bdesc, idesc, accum);
           }
-          umma_commit(&empty[s]);
-          umma_commit(&aempty[j]);
-          if (++s == C::kNS) { s = 0; ph ^= 1; }
-          if (++j == C::kNumA) { j = 0; aph ^= 1; }
+          umma_commit(&empty[st.i]);
+          umma_commit(&aempty[ar.i]);
+          st.next(C::kNS);
+          ar.next(C::kNumA);
+          if constexpr (kScaleEpi) {
+            umma_commit(&accfull[acc.i]);
+            acc.next(C::kNumAcc);
+          }
         }
-        umma_commit(&accfull[a]);
-        if (++a == C::kNumAcc) { a = 0; acph ^= 1; }
+        if constexpr (!kScaleEpi) {
+          umma_commit(&accfull[acc.i]);
+          acc.next(C::kNumAcc);
+        }
       }
     }
   } else if (warp < kEpiWarp0) {
-    // ------------------------------------------------------------ dequant: int4 smem -> fp16 TMEM
+    // ------------------------------------------------------------ dequant: int4 smem -> TMEM A ring
     const int dw = warp - kDequantWarp0;
     const uint32_t quad = warp & 3;
     const int row = quad * 32 + lane;
     const int c0 = (dw >> 2) * 2;  // this warp's two 32-wide k chunks of the 128-wide tile
     const uint32_t lane_off = (quad * 32) << 16;
-    int s = 0, j = 0;
-    uint32_t ph = 0, aph = 0;
+    const uint32_t code_off = (c0 * kTileRows + row) * 16;
+    Ring st, ar;
     TileInfo ti;
     for (int t = blockIdx.x; get_tile<kNTok>(t, mt_off, args, ti); t += gridDim.x) {
       for (int kt = 0; kt < args.kt; ++kt) {
-        mbar_wait(&full[s], ph);
-        mbar_wait(&aempty[j], aph ^ 1);
-        tc_fence_after();
-        const uint8_t* blk = smem_w + s * C::kBlk;
-        const uint32_t acol = tbase + lane_off + kAcol0 + j * C::kACols;
+        mbar_wait(&full[st.i], st.ph);
+        const uint32_t blk = w_u32 + st.i * C::kBlk;
+        uint4 v[C::kParts][2];
+        uint32_t sb[C::kParts], zb[C::kParts];
 #pragma unroll
         for (int p = 0; p < C::kParts; ++p) {
-          const uint8_t* part = blk + p * kPartBytes;
-          const uint16_t sb = reinterpret_cast<const uint16_t*>(part + kScaleOff)[row];
-          const uint32_t zb = part[kZeroOff + (row >> 1)];
-          const uint32_t z = (row & 1) ? (zb >> 4) : (zb & 15u);
-          const auto ctx = Dq<kBF16>::make(z, sb);
+          const uint32_t part = blk + p * kPartBytes;
+          v[p][0] = lds128(part + code_off);
+          v[p][1] = lds128(part + code_off + kTileRows * 16);
+          zb[p] = lds_u8(part + kZeroOff + (row >> 1));
+          if constexpr (!kScaleEpi) sb[p] = lds_u16(part + kScaleOff + row * 2);
+          else sb[p] = 0;
+        }
+        mbar_wait(&aempty[ar.i], ar.ph ^ 1);
+        tc_fence_after();
+        const uint32_t acol = tbase + lane_off + kAcol0 + ar.i * C::kACols;
+#pragma unroll
+        for (int p = 0; p < C::kParts; ++p) {
+          const uint32_t z = (row & 1) ? (zb[p] >> 4) : (zb[p] & 15u);
+          const auto ctx = Dq<kBF16>::make(z, static_cast<uint16_t>(sb[p]));
 #pragma unroll
           for (int cc = 0; cc < 2; ++cc) {
-            const int c = c0 + cc;
-            const uint4 v = *reinterpret_cast<const uint4*>(part + (c * kTileRows + row) * 16);
             uint32_t r[16];
-            dequant_chunk<kBF16>(v, ctx, r);
-            tmem_st_x16(acol + p * 64 + c * 16, r);
+            dequant_chunk<kBF16, !kScaleEpi>(v[p][cc], ctx, r);
+            tmem_st_x16(acol + p * 64 + (c0 + cc) * 16, r);
           }
         }
         tc_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(&afull[j]);
-          mbar_arrive(&empty[s]);
+          mbar_arrive(&afull[ar.i]);
+          mbar_arrive(&empty[st.i]);
         }
-        if (++s == C::kNS) { s = 0; ph ^= 1; }
-        if (++j == C::kNumA) { j = 0; aph ^= 1; }
+        st.next(C::kNS);
+        ar.next(C::kNumA);
       }
     }
   } else {
@@ -254,43 +293,86 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     const int row = quad * 32 + lane;
     const uint32_t lane_off = (quad * 32) << 16;
     uint16_t* out = reinterpret_cast<uint16_t*>(args.out);
-    int a = 0;
-    uint32_t acph = 0;
+    Ring acc, st;
     TileInfo ti;
     for (int t = blockIdx.x; get_tile<kNTok>(t, mt_off, args, ti); t += gridDim.x) {
-      mbar_wait(&accfull[a], acph);
-      tc_fence_after();
-      const uint32_t dcol = tbase + lane_off + a * C::kAccCols;
       uint16_t* obase = out + static_cast<int64_t>(ti.m_start) * args.ldo + ti.n_tile * kTileRows + row;
-#pragma unroll 1
-      for (int cb = 0; cb < kNTok / 16; ++cb) {
-        uint32_t g[16];
-        tmem_ld_x16(dcol + cb * 16, g);
-        if constexpr (kGated) {
-          uint32_t u[16];
-          tmem_ld_x16(dcol + kNTok + cb * 16, u);
-          tc_wait_ld();
+      if constexpr (kScaleEpi) {
+        float a[C::kParts][kNTok];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int m = cb * 16 + i;
-            if (m < ti.m_rows) {
-              const float gv = __uint_as_float(g[i]), uv = __uint_as_float(u[i]);
-              obase[static_cast<int64_t>(m) * args.ldo] = to_act_bits<kBF16>(silu_f(gv) * uv);
-            }
+        for (int p = 0; p < C::kParts; ++p)
+#pragma unroll
+          for (int i = 0; i < kNTok; ++i) a[p][i] = 0.f;
+        for (int kt = 0; kt < args.kt; ++kt) {
+          mbar_wait(&full[st.i], st.ph);
+          const uint32_t blk = w_u32 + st.i * C::kBlk;
+          float sc[C::kParts];
+#pragma unroll
+          for (int p = 0; p < C::kParts; ++p) sc[p] = act_bits_to_float<kBF16>(lds_u16(blk + p * kPartBytes + kScaleOff + row * 2));
+          mbar_wait(&accfull[acc.i], acc.ph);
+          tc_fence_after();
+          const uint32_t dcol = tbase + lane_off + acc.i * C::kAccCols;
+          uint32_t r[C::kParts][kNTok];
+#pragma unroll
+          for (int p = 0; p < C::kParts; ++p)
+#pragma unroll
+            for (int cb = 0; cb < kNTok / 16; ++cb)
+              tmem_ld_x16(dcol + p * kNTok + cb * 16, *reinterpret_cast<uint32_t(*)[16]>(&r[p][cb * 16]));
+          tc_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&accempty[acc.i]);
+            mbar_arrive(&empty[st.i]);
           }
-        } else {
-          tc_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int m = cb * 16 + i;
-            if (m < ti.m_rows) obase[static_cast<int64_t>(m) * args.ldo] = to_act_bits<kBF16>(__uint_as_float(g[i]));
+          for (int p = 0; p < C::kParts; ++p)
+#pragma unroll
+            for (int i = 0; i < kNTok; ++i) a[p][i] = fmaf(sc[p], __uint_as_float(r[p][i]), a[p][i]);
+          acc.next(C::kNumAcc);
+          st.next(C::kNS);
+        }
+#pragma unroll
+        for (int m = 0; m < kNTok; ++m) {
+          if (m < ti.m_rows) {
+            const float v = kGated ? silu_f(a[0][m]) * a[C::kParts - 1][m] : a[0][m];
+            obase[static_cast<int64_t>(m) * args.ldo] = to_act_bits<kBF16>(v);
           }
         }
+      } else {
+        mbar_wait(&accfull[acc.i], acc.ph);
+        tc_fence_after();
+        const uint32_t dcol = tbase + lane_off + acc.i * C::kAccCols;
+#pragma unroll 1
+        for (int cb = 0; cb < kNTok / 16; ++cb) {
+          uint32_t g[16];
+          tmem_ld_x16(dcol + cb * 16, g);
+          if constexpr (kGated) {
+            uint32_t u[16];
+            tmem_ld_x16(dcol + kNTok + cb * 16, u);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int m = cb * 16 + i;
+              if (m < ti.m_rows) {
+                const float gv = __uint_as_float(g[i]), uv = __uint_as_float(u[i]);
+                obase[static_cast<int64_t>(m) * args.ldo] = to_act_bits<kBF16>(silu_f(gv) * uv);
+              }
+            }
+          } else {
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int m = cb * 16 + i;
+              if (m < ti.m_rows) obase[static_cast<int64_t>(m) * args.ldo] = to_act_bits<kBF16>(__uint_as_float(g[i]));
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&accempty[acc.i]);
+        acc.next(C::kNumAcc);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&accempty[a]);
-      if (++a == C::kNumAcc) { a = 0; acph ^= 1; }
     }
   }
 
@@ -423,10 +505,10 @@ int sm_count() {
   return n;
 }
 
-template <int kNTok, bool kGated, bool kBF16>
+template <int kNTok, bool kGated, bool kBF16, bool kScaleEpi>
 int launch_gemm(const GemmArgs& a, const CUtensorMap& map, int grid, cudaStream_t st) {
-  using C = Cfg<kNTok, kGated>;
-  auto kern = w4a16_moe_gemm_kernel<kNTok, kGated, kBF16>;
+  using C = Cfg<kNTok, kGated, kScaleEpi>;
+  auto kern = w4a16_moe_gemm_kernel<kNTok, kGated, kBF16, kScaleEpi>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
@@ -440,10 +522,10 @@ int launch_gemm(const GemmArgs& a, const CUtensorMap& map, int grid, cudaStream_
 template <bool kGated, bool kBF16>
 int dispatch_ntok(int ntok, const GemmArgs& a, const CUtensorMap& m, int grid, cudaStream_t st) {
   switch (ntok) {
-    case 16: return launch_gemm<16, kGated, kBF16>(a, m, grid, st);
-    case 32: return launch_gemm<32, kGated, kBF16>(a, m, grid, st);
-    case 64: return launch_gemm<64, kGated, kBF16>(a, m, grid, st);
-    case 128: return launch_gemm<128, kGated, kBF16>(a, m, grid, st);
+    case 16: return launch_gemm<16, kGated, kBF16, true>(a, m, grid, st);
+    case 32: return launch_gemm<32, kGated, kBF16, true>(a, m, grid, st);
+    case 64: return launch_gemm<64, kGated, kBF16, false>(a, m, grid, st);
+    case 128: return launch_gemm<128, kGated, kBF16, false>(a, m, grid, st);
     default: return W4_ERR_ARG;
   }
 }

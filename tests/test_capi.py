@@ -1,0 +1,51 @@
+"""C ABI boundary checks that need no GPU: the in-tree library loads and exports every function
+declared in include/*.h, and the host wrappers declare a signature for each of them."""
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _declared():
+    names = set()
+    for h in (ROOT / "include").glob("*.h"):
+        text = re.sub(r"/\*.*?\*/", "", h.read_text(), flags=re.S)
+        names |= set(re.findall(r"\b(w4a16_\w+)\s*\(", text))
+    return names
+
+
+def test_header_declares_the_path():
+    d = _declared()
+    for fn in ("w4a16_grouped_gemm", "w4a16_route_topk", "w4a16_moe_permute", "w4a16_moe_gather",
+               "w4a16_moe_combine", "w4a16_repack_awq", "w4a16_dequant", "w4a16_moe_forward"):
+        assert fn in d
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2504_16214_b200 import _build
+    from paper_2504_16214_b200.moe import _lib
+    _build.build()
+    lib = _lib.load()
+    missing = [n for n in sorted(_declared()) if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(_lib.SIGNATURES) == _declared()
+
+
+def test_pure_host_queries():
+    from paper_2504_16214_b200.moe import _lib
+    lib = _lib.load()
+    assert lib.w4a16_tile_rows() == 128 and lib.w4a16_tile_k() == 128
+    # packed bytes == AWQ payload bytes (codes + fp16 scales + int4 zeros)
+    E, N, K = 256, 4096, 7168
+    assert lib.w4a16_packed_bytes(E, N, K) == E * (N * K // 2 + (K // 128) * N * 2 + (K // 128) * N // 2)
+    assert lib.w4a16_packed_bytes(1, 100, 128) == -1
+    assert lib.w4a16_pick_ntok(512, 256) == 16 and lib.w4a16_pick_ntok(65536, 256) == 128
+
+
+def test_ops_refuse_cpu_tensors():
+    torch = pytest.importorskip("torch")
+    from paper_2504_16214_b200.moe import _lib, ops
+    with pytest.raises(_lib.W4A16Error):
+        ops.moe_permute(torch.zeros(8, dtype=torch.int32), 4)

@@ -1,0 +1,81 @@
+"""CPU tests of the numeric oracle itself (oracle/moe_oracle.py): pinned against vLLM's AWQ packing
+golden vectors and against independent restatements of the rounding/routing/permutation rules."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import moe_oracle as O
+
+GOLD = Path(__file__).resolve().parent / "golden" / "awq_pack_vllm.npz"
+
+
+@pytest.mark.parametrize("shape", ["8x8", "16x64", "128x256"])
+def test_awq_pack_matches_vllm(shape):
+    g = np.load(GOLD)
+    q, packed = g[f"q_{shape}"], g[f"packed_{shape}"]
+    assert np.array_equal(O.awq_pack(q), packed)
+    assert np.array_equal(O.awq_unpack(packed), q)
+
+
+def test_awq_unpack_is_vllm_reverse_order():
+    # column c of a packed word sits at nibble slot [0,4,1,5,2,6,3,7][c] (vllm awq_marlin.py:70-74)
+    q = np.arange(8, dtype=np.uint8)[None, :]
+    w = int(O.awq_pack(q).view(np.uint32)[0, 0])
+    slots = [(w >> (4 * s)) & 15 for s in range(8)]
+    assert slots == [0, 2, 4, 6, 1, 3, 5, 7]
+
+
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+def test_dequant_single_rounding(dt):
+    rng = np.random.default_rng(3)
+    q = rng.integers(0, 16, size=(4, 256), dtype=np.uint8)
+    z = rng.integers(0, 16, size=(4, 2), dtype=np.uint8)
+    s = O.round_act(rng.uniform(-2, 2, size=(4, 2)).astype(np.float32), dt)
+    w = O.dequant(q, z, s, dt)
+    # exact product in float64, one rounding to the act dtype
+    exact = (q.astype(np.float64) - np.repeat(z, 128, 1)) * np.repeat(s.astype(np.float64), 128, 1)
+    assert np.array_equal(w, O.round_act(exact.astype(np.float32), dt))
+    assert np.array_equal(O.act_bits(w, dt), O.act_bits(O.round_act(w, dt), dt))
+
+
+def test_round_bf16_ties_to_even():
+    x = np.array([1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8, -(1.0 + 2 ** -8), 65504.0], np.float32)
+    r = O.round_bf16(x)
+    assert r[0] == 1.0 and r[1] == 1.0 + 2 ** -6 and r[2] == -1.0
+
+
+def test_route_topk_ties_and_weights():
+    lg = np.zeros((2, 6), np.float32)
+    lg[1] = [0.5, 2.0, 2.0, -1.0, 2.0, 0.0]
+    ids, w = O.route_topk(lg, 3, "softmax", renormalize=False)
+    assert ids.tolist() == [[0, 1, 2], [1, 2, 4]]
+    assert np.allclose(w[0], 1 / 6)
+    ids, w = O.route_topk(lg, 2, "sigmoid", renormalize=True)
+    assert ids[1].tolist() == [1, 2] and np.allclose(w.sum(1), 1.0)
+
+
+def test_permute_is_stable_counting_sort():
+    rng = np.random.default_rng(0)
+    ids = rng.integers(-1, 9, size=(50, 4)).astype(np.int32)
+    counts, offsets, sp, pp = O.moe_permute(ids, 8)
+    flat = ids.reshape(-1)
+    valid = np.nonzero((flat >= 0) & (flat < 8))[0]
+    expect = sorted(valid.tolist(), key=lambda i: (flat[i], i))
+    assert sp.tolist() == expect
+    assert counts.tolist() == [int((flat == e).sum()) for e in range(8)]
+    assert all(pp[i] == -1 for i in range(flat.size) if i not in set(valid.tolist()))
+    assert all(sp[pp[i]] == i for i in valid)
+
+
+def test_moe_forward_linearity_in_routing_weights():
+    rng = np.random.default_rng(1)
+    T, E, k, H, I = 5, 4, 2, 128, 128
+    q13, z13, s13 = O.synth_awq_expert_weights(rng, E, 2 * I, H, "f16")
+    q2, z2, s2 = O.synth_awq_expert_weights(rng, E, H, I, "f16")
+    x = O.round_act(rng.standard_normal((T, H)).astype(np.float32), "f16")
+    ids = np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
+    w = np.full((T, k), 0.5, np.float32)
+    y = O.moe_forward(x, O.dequant(q13, z13, s13, "f16"), O.dequant(q2, z2, s2, "f16"), ids, w, "f16")
+    y2 = O.moe_forward_expertwise(x, q13, z13, s13, q2, z2, s2, ids, w, "f16")
+    assert np.array_equal(y, y2)
