@@ -155,6 +155,50 @@ def cpu_oracle_sample(T: int, dtype: str = "f16", budget_s: float = 12.0, seed: 
     }
 
 
+SYNTH_PROGRAMS = {  # P0 fixture, P1 decode CTA tile, P2 prefill CTA tile
+    "P0_mixed_int4": ("ref_mixed_int4.prog", []),
+    "P1_cfg1_tile": ("cfg1_tile.prog", []),
+    "P2_prefill_tile": ("prefill_tile.prog", ["--threads", "256"]),
+}
+
+
+def synth_baseline(repeats: int = 1):
+    """Wall time of the layout synthesizer per program: the reference's own CPU path (``tilesynth``
+    installed in baseline/_ref, when present) vs this re-implementation, each in a fresh process;
+    also checks their reports are byte-identical on this host."""
+    import subprocess
+    progs = ROOT / "tests" / "golden" / "tilesynth" / "programs"
+    ref_path = ROOT / "baseline" / "_ref"
+    code = ("import sys,time;from tilesynth.cli import main;t=time.perf_counter();"
+            "rc=main(sys.argv[1:]);sys.stderr.write('WALL %.6f\\n'%(time.perf_counter()-t));sys.exit(rc)")
+    out = {}
+    for key, (fname, extra) in SYNTH_PROGRAMS.items():
+        row = {}
+        reports = {}
+        for impl, pp in (("reference", ref_path), ("ours", ROOT / "compat")):
+            if impl == "reference" and not (pp / "tilesynth").is_dir():
+                continue
+            times = []
+            for _ in range(repeats):
+                rep = Path(f"/tmp/synth_{impl}_{key}.json")
+                env = dict(os.environ, PYTHONPATH=str(pp), PYTHONDONTWRITEBYTECODE="1")
+                pr = subprocess.run([sys.executable, "-c", code, "--program", str(progs / fname), "--format", "json",
+                                     "--report", str(rep), *extra], capture_output=True, text=True, env=env,
+                                    cwd="/tmp")
+                w = [ln for ln in pr.stderr.splitlines() if ln.startswith("WALL")]
+                if pr.returncode == 0 and w:
+                    times.append(float(w[-1].split()[1]))
+                    reports[impl] = rep.read_text()
+            if times:
+                row[f"{impl}_s"] = round(statistics.median(times), 3)
+        if "ours" in reports:
+            row["best_cycles"] = json.loads(reports["ours"])["best"]["total_cycles"]
+        if len(reports) == 2:
+            row["reports_identical"] = reports["ours"] == reports["reference"]
+        out[key] = row
+    return {"cores_used": 1, "cores_available": len(os.sched_getaffinity(0)), "programs": out}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -338,8 +382,10 @@ def main():
             del xs, ls
 
     cpu = None
+    synth = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_oracle_sample(T, args.dtype)
+        synth = synth_baseline()
 
     if rank == 0:
         line = {
@@ -364,6 +410,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "kernel_ms": {n: round(timer.mean_ms(n), 4) for n in timer.events},
             "sweep": sweep,
+            "layout_synthesis_cpu": synth,
         }
         print(json.dumps(line))
     if world > 1:

@@ -45,12 +45,20 @@ struct GemmArgs {
 // from the dequant (the scale is applied once per group per output instead of once per weight)
 // and is numerically at least as accurate as dequantise-then-MMA. Otherwise (prefill, large token
 // tiles) the dequant applies the scale and the MMA accumulates across k-tiles in TMEM.
-template <int kNTok, bool kGated, bool kScaleEpi>
+// Block modes: how the two 8.5 KB parts of a 17 KB stage are used.
+constexpr int kModePlain = 0;   // one part (one k-group) per stage
+constexpr int kModeGateUp = 1;  // part 0 = gate rows, part 1 = up rows, same k-group (fused SwiGLU)
+constexpr int kModeKPair = 2;   // parts = two consecutive k-groups of the same rows (down proj.)
+
+template <int kNTok, int kMode, bool kScaleEpi>
 struct Cfg {
-  static constexpr int kParts = kGated ? 2 : 1;
+  static constexpr bool kGated = kMode == kModeGateUp;
+  static constexpr int kParts = kMode == kModePlain ? 1 : 2;
+  static constexpr int kGroupsPerStage = kMode == kModeKPair ? 2 : 1;
   static constexpr int kBlk = kParts * kPartBytes;
-  static constexpr int kXBytes = kNTok * kTileK * 2;  // bf16/fp16 X tile, two 64-wide swizzle atoms
-  static constexpr int kAccCols = kParts * kNTok;       // one accumulator / partial stage
+  static constexpr int kXBytes = kGroupsPerStage * kNTok * kTileK * 2;  // X tile, 64-wide 128B-swizzle atoms
+  // one accumulator / partial stage: a partial per part in kScaleEpi mode, else gate|up or one
+  static constexpr int kAccCols = (kScaleEpi || kGated) ? kParts * kNTok : kNTok;
   static constexpr int kACols = kParts * (kTileK / 2);  // fp16 pairs per 32-bit column
   static constexpr int kNumAcc = kScaleEpi ? 4 : ((2 * kAccCols + 2 * kACols <= 512) ? 2 : 1);
   static constexpr int kNumA0 = (512 - kNumAcc * kAccCols) / kACols;
@@ -116,10 +124,12 @@ struct Ring {  // (stage, phase) iterator of an mbarrier ring
   }
 };
 
-template <int kNTok, bool kGated, bool kBF16, bool kScaleEpi>
+template <int kNTok, int kMode, bool kBF16, bool kScaleEpi>
 __global__ void __launch_bounds__(kNumThreads, 1)
     w4a16_moe_gemm_kernel(const GemmArgs args, const __grid_constant__ CUtensorMap xmap) {
-  using C = Cfg<kNTok, kGated, kScaleEpi>;
+  using C = Cfg<kNTok, kMode, kScaleEpi>;
+  constexpr bool kGated = C::kGated;
+  const int n_stages = args.kt / C::kGroupsPerStage;  // stages per tile
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_x = smem;                                  // [NS][kXBytes]
@@ -180,16 +190,19 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       Ring st;
       TileInfo ti;
       for (int t = blockIdx.x; get_tile<kNTok>(t, mt_off, args, ti); t += gridDim.x) {
+        // per (expert, n-tile): kt k-groups of (gated ? 2 : 1) parts, stage j = bytes [j*kBlk, (j+1)*kBlk)
         const uint8_t* wsrc = args.wblocks + (static_cast<int64_t>(ti.e) * args.nt + ti.n_tile) *
-                                                 static_cast<int64_t>(args.kt) * C::kBlk;
-        for (int kt = 0; kt < args.kt; ++kt) {
+                                                 static_cast<int64_t>(args.kt) * (kGated ? 2 : 1) * kPartBytes;
+        for (int j = 0; j < n_stages; ++j) {
           mbar_wait(&empty[st.i], st.ph ^ 1);
           mbar_arrive_expect_tx(&full[st.i], C::kBlk + C::kXBytes);
-          bulk_g2s_hint(smem_w + st.i * C::kBlk, wsrc + static_cast<int64_t>(kt) * C::kBlk, C::kBlk, &full[st.i],
+          bulk_g2s_hint(smem_w + st.i * C::kBlk, wsrc + static_cast<int64_t>(j) * C::kBlk, C::kBlk, &full[st.i],
                         pol_w);
           uint8_t* xs = smem_x + st.i * C::kXBytes;
-          tma_load_2d(xs, &xmap, kt * kTileK, ti.m_start, &full[st.i]);
-          tma_load_2d(xs + kNTok * 128, &xmap, kt * kTileK + 64, ti.m_start, &full[st.i]);
+#pragma unroll
+          for (int h = 0; h < 2 * C::kGroupsPerStage; ++h)
+            tma_load_2d(xs + h * (kNTok * 128), &xmap, j * C::kGroupsPerStage * kTileK + h * 64, ti.m_start,
+                        &full[st.i]);
           st.next(C::kNS);
         }
       }
@@ -205,8 +218,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           mbar_wait(&accempty[acc.i], acc.ph ^ 1);
           tc_fence_after();
         }
-        for (int kt = 0; kt < args.kt; ++kt) {
-          if constexpr (kScaleEpi) {  // one fresh partial per k-tile (= per group)
+        for (int j = 0; j < n_stages; ++j) {
+          if constexpr (kScaleEpi) {  // fresh partials per stage (one per k-group)
             mbar_wait(&accempty[acc.i], acc.ph ^ 1);
           }
           mbar_wait(&full[st.i], st.ph);
@@ -216,11 +229,17 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           const uint32_t xaddr = smem_u32(smem_x + st.i * C::kXBytes);
           const uint32_t acol = tbase + kAcol0 + ar.i * C::kACols;
 #pragma unroll
-          for (int kk = 0; kk < kTileK / 16; ++kk) {
-            const uint64_t bdesc = make_sdesc_sw128(xaddr + (kk >> 2) * (kNTok * 128) + (kk & 3) * 32);
-            const uint32_t accum = kScaleEpi ? (kk != 0) : ((kt | kk) != 0);
-            umma_ts_f16(dcol, acol + kk * 8, bdesc, idesc, accum);
-            if constexpr (kGated) umma_ts_f16(dcol + kNTok, acol + 64 + kk * 8, bdesc, idesc, accum);
+          for (int p = 0; p < C::kParts; ++p) {
+            // k-pair: part p reads the second 128-k half of the X tile; gate/up: both read the same
+            const uint32_t xp = xaddr + (kMode == kModeKPair ? p * 2 * (kNTok * 128) : 0);
+            const uint32_t dp = dcol + ((kScaleEpi || kGated) ? p * kNTok : 0);
+#pragma unroll
+            for (int kk = 0; kk < kTileK / 16; ++kk) {
+              const uint64_t bdesc = make_sdesc_sw128(xp + (kk >> 2) * (kNTok * 128) + (kk & 3) * 32);
+              const uint32_t accum = (kScaleEpi || kGated) ? (kScaleEpi ? (kk != 0) : ((j | kk) != 0))
+                                                           : ((j | p | kk) != 0);
+              umma_ts_f16(dp, acol + p * 64 + kk * 8, bdesc, idesc, accum);
+            }
           }
           umma_commit(&empty[st.i]);
           umma_commit(&aempty[ar.i]);
@@ -248,7 +267,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     Ring st, ar;
     TileInfo ti;
     for (int t = blockIdx.x; get_tile<kNTok>(t, mt_off, args, ti); t += gridDim.x) {
-      for (int kt = 0; kt < args.kt; ++kt) {
+      for (int j = 0; j < n_stages; ++j) {
         mbar_wait(&full[st.i], st.ph);
         const uint32_t blk = w_u32 + st.i * C::kBlk;
         uint4 v[C::kParts][2];
@@ -303,7 +322,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         for (int p = 0; p < C::kParts; ++p)
 #pragma unroll
           for (int i = 0; i < kNTok; ++i) a[p][i] = 0.f;
-        for (int kt = 0; kt < args.kt; ++kt) {
+        for (int j = 0; j < n_stages; ++j) {
           mbar_wait(&full[st.i], st.ph);
           const uint32_t blk = w_u32 + st.i * C::kBlk;
           float sc[C::kParts];
@@ -335,7 +354,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll
         for (int m = 0; m < kNTok; ++m) {
           if (m < ti.m_rows) {
-            const float v = kGated ? silu_f(a[0][m]) * a[C::kParts - 1][m] : a[0][m];
+            float v;
+            if constexpr (kGated) v = silu_f(a[0][m]) * a[1][m];
+            else if constexpr (kMode == kModeKPair) v = a[0][m] + a[1][m];
+            else v = a[0][m];
             obase[static_cast<int64_t>(m) * args.ldo] = to_act_bits<kBF16>(v);
           }
         }
@@ -505,10 +527,10 @@ int sm_count() {
   return n;
 }
 
-template <int kNTok, bool kGated, bool kBF16, bool kScaleEpi>
+template <int kNTok, int kMode, bool kBF16, bool kScaleEpi>
 int launch_gemm(const GemmArgs& a, const CUtensorMap& map, int grid, cudaStream_t st) {
-  using C = Cfg<kNTok, kGated, kScaleEpi>;
-  auto kern = w4a16_moe_gemm_kernel<kNTok, kGated, kBF16, kScaleEpi>;
+  using C = Cfg<kNTok, kMode, kScaleEpi>;
+  auto kern = w4a16_moe_gemm_kernel<kNTok, kMode, kBF16, kScaleEpi>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
@@ -519,13 +541,13 @@ int launch_gemm(const GemmArgs& a, const CUtensorMap& map, int grid, cudaStream_
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
 
-template <bool kGated, bool kBF16>
+template <int kMode, bool kBF16>
 int dispatch_ntok(int ntok, const GemmArgs& a, const CUtensorMap& m, int grid, cudaStream_t st) {
   switch (ntok) {
-    case 16: return launch_gemm<16, kGated, kBF16, true>(a, m, grid, st);
-    case 32: return launch_gemm<32, kGated, kBF16, true>(a, m, grid, st);
-    case 64: return launch_gemm<64, kGated, kBF16, false>(a, m, grid, st);
-    case 128: return launch_gemm<128, kGated, kBF16, false>(a, m, grid, st);
+    case 16: return launch_gemm<16, kMode, kBF16, true>(a, m, grid, st);
+    case 32: return launch_gemm<32, kMode, kBF16, true>(a, m, grid, st);
+    case 64: return launch_gemm<64, kMode, kBF16, false>(a, m, grid, st);
+    case 128: return launch_gemm<128, kMode, kBF16, false>(a, m, grid, st);
     default: return W4_ERR_ARG;
   }
 }
@@ -568,8 +590,12 @@ int w4a16_grouped_gemm(const void* x, int64_t rows, int64_t K, const uint8_t* wb
   a.kt = static_cast<int>(K / kTileK);
   const int grid = sm_count();
   const bool bf = dtype == W4_DTYPE_BF16;
-  if (gated) return bf ? dispatch_ntok<true, true>(ntok, a, map, grid, stream) : dispatch_ntok<true, false>(ntok, a, map, grid, stream);
-  return bf ? dispatch_ntok<false, true>(ntok, a, map, grid, stream) : dispatch_ntok<false, false>(ntok, a, map, grid, stream);
+  if (gated) return bf ? dispatch_ntok<kModeGateUp, true>(ntok, a, map, grid, stream)
+                       : dispatch_ntok<kModeGateUp, false>(ntok, a, map, grid, stream);
+  if (a.kt % 2 == 0) return bf ? dispatch_ntok<kModeKPair, true>(ntok, a, map, grid, stream)
+                               : dispatch_ntok<kModeKPair, false>(ntok, a, map, grid, stream);
+  return bf ? dispatch_ntok<kModePlain, true>(ntok, a, map, grid, stream)
+            : dispatch_ntok<kModePlain, false>(ntok, a, map, grid, stream);
 }
 
 int w4a16_dequant(const uint8_t* wblocks, int64_t num_experts, int64_t n_rows, int64_t K, int parts, int dtype,
