@@ -309,11 +309,13 @@ def main():
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
+        torch.cuda.profiler.start()  # ncu --profile-from-start off captures exactly the timed steps
         ev0.record()
         for _ in range(args.steps):
             step(timer)
         ev1.record()
         barrier()
+        torch.cuda.profiler.stop()
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
     ms = ms_total / args.steps
     value = job_bytes / (ms * 1e-3) / 1e9
