@@ -11,6 +11,8 @@
  *   route:    w4a16_route_topk                         top-k of softmax/sigmoid router scores
  *   permute:  w4a16_moe_permute                        stable counting sort of (token, slot) by expert
  *   gather:   w4a16_moe_gather                         X_perm[p] = x[token(p)]   (128-bit vectors)
+ *             w4a16_moe_gather_sums                    same, plus per-group activation sums (decode)
+ *   sums:     w4a16_group_sums                         per-(group of 128 k, row) sums of an activation
  *   GEMM:     w4a16_grouped_gemm                       per-expert X_e * W_e^T, optional fused SiLU*up
  *   combine:  w4a16_moe_combine                        y[t] = sum_j w[t,j] * Y_perm[pos(t,j)]
  *   EP:       w4a16_ep_pack_counts / w4a16_moe_permute over received rows (NCCL all-to-all is
@@ -83,6 +85,19 @@ int w4a16_moe_permute(const int32_t* topk_ids, int64_t P, int64_t E, int32_t* ex
 int w4a16_moe_gather(const void* x, int64_t H, int64_t topk, const int32_t* sorted_pairs, int64_t rows,
                      const int32_t* row_limit, void* x_perm, cudaStream_t stream);
 
+/* Same as w4a16_moe_gather, and also writes the per-(k-group, row) activation sums the decode-mode
+ * grouped GEMM consumes: xsum fp32 [H/128][w4a16_group_sums_ld(rows)][2] = (C, S) with
+ * S = sum_k x[k] and C = sum_k c_k x[k] over the group's 128 k, c_k the offset of the GEMM's
+ * offset-code dequant (fp16: 1024 for k%8 in {0,1,4,5}, 64 otherwise; bf16: 128). H % 128 == 0. */
+int w4a16_moe_gather_sums(const void* x, int64_t H, int64_t topk, const int32_t* sorted_pairs, int64_t rows,
+                          const int32_t* row_limit, void* x_perm, int dtype, float* xsum, cudaStream_t stream);
+
+/* The sums alone for an activation x [rows][K] (rows >= *row_limit skipped when row_limit != NULL). */
+int w4a16_group_sums(const void* x, int64_t rows, int64_t K, const int32_t* row_limit, int dtype, float* xsum,
+                     cudaStream_t stream);
+/* Row stride (in (C, S) pairs) of the sums array for `rows` rows: rows rounded up to even. */
+int64_t w4a16_group_sums_ld(int64_t rows);
+
 /* y[t][:] = act(sum_j topk_weights[t][j] * Y_perm[pair_pos[t*k+j]][:]), fp32 accumulate in slot
  * order; pairs with pair_pos < 0 contribute nothing. */
 int w4a16_moe_combine(const void* y_perm, int64_t T, int64_t H, int64_t topk, const int32_t* pair_pos,
@@ -92,10 +107,12 @@ int w4a16_moe_combine(const void* y_perm, int64_t T, int64_t H, int64_t topk, co
 /* For each expert e: out[off_e + m][n] = act( sum_k X[off_e + m][k] * W_e[n][k] ), m < counts[e].
  * x [rows][K]; wblocks packed (parts = gated ? 2 : 1, n_rows = gated ? 2*n_out : n_out);
  * gated: out[.., n] = silu(X W_gate^T)[n] * (X W_up^T)[n] (fused SwiGLU). ntok = token tile
- * (16/32/64/128; 0 = pick from rows/num_experts). */
+ * (16/32/64/128; 0 = pick from rows/num_experts). xsum (optional): x's group sums
+ * (w4a16_group_sums layout); with it, 16/32-token tiles run the decode (offset-code) kernel,
+ * without it the scale-in-dequant kernel. */
 int w4a16_grouped_gemm(const void* x, int64_t rows, int64_t K, const uint8_t* wblocks, int64_t num_experts,
                        int64_t n_out, int gated, const int32_t* expert_counts, const int32_t* expert_offsets,
-                       void* out, int dtype, int ntok, cudaStream_t stream);
+                       const float* xsum, void* out, int dtype, int ntok, cudaStream_t stream);
 int w4a16_pick_ntok(int64_t rows, int64_t num_experts);
 
 /* ---- whole layer ------------------------------------------------------------------------------- */

@@ -22,6 +22,8 @@ INCLUDE = ROOT / "include"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", f"-I{INCLUDE}", f"-I{CSRC}"]
+if os.environ.get("W4A16_TRACE"):  # debug build: per-stage clock64 timeline (w4a16_debug_trace)
+    FLAGS.append("-DW4A16_TRACE")
 
 
 def _sources():
@@ -32,8 +34,11 @@ def _deps():
     return _sources() + sorted(CSRC.glob("*.cuh")) + sorted(INCLUDE.glob("*.h")) + [Path(__file__)]
 
 
+STAMP = LIBDIR / "build_flags.txt"
+
+
 def up_to_date() -> bool:
-    if not LIB.exists():
+    if not LIB.exists() or not STAMP.exists() or STAMP.read_text() != " ".join(ARCH + FLAGS):
         return False
     t = LIB.stat().st_mtime
     return all(p.stat().st_mtime <= t for p in _deps())
@@ -62,6 +67,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
     os.replace(tmp, LIB)
+    STAMP.write_text(" ".join(ARCH + FLAGS))
     for o in objs:
         o.unlink(missing_ok=True)
     return LIB

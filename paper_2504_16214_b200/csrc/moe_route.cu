@@ -163,6 +163,60 @@ __global__ void moe_gather_kernel(const uint4* __restrict__ x, int64_t hv, int t
   for (int64_t i = threadIdx.x; i < hv; i += blockDim.x) dst[i] = __ldg(src + i);
 }
 
+// ---------------------------------------------------------------------------------------- group sums
+// Per (quantisation group g of 128 k, row m): C = sum_k c_k x[m,k] and S = sum_k x[m,k] in fp32, where
+// c_k is the offset the grouped GEMM's offset-code dequant leaves on weight k (Dq::offset_bits) --
+// the decode-mode epilogue subtracts C + z*S. Layout xsum [K/128][ld][2].
+template <bool kBF16>
+__device__ __forceinline__ void vec_sums(const uint4& v, float& c, float& s) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  c = 0.f;
+  s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {  // elements 2i, 2i+1 of the 8-vector (k % 8 = 2i, 2i+1)
+    float a, b;
+    if constexpr (kBF16) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+      a = f.x, b = f.y;
+    } else {
+      const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+      a = f.x, b = f.y;
+    }
+    const float off = kBF16 ? 128.f : ((i & 1) ? 64.f : 1024.f);  // == Dq<kBF16>::offset_bits(2i)
+    s += a + b;
+    c = fmaf(off, a + b, c);
+  }
+}
+
+// One CTA (128 threads) per row: thread vectors i = it*128 + tid; the 16 vectors of one group sit on
+// 16 consecutive lanes, reduced with xor shuffles. `src_rows` (gather) maps output row -> input row.
+template <bool kBF16, bool kGather>
+__global__ void group_sums_kernel(const uint4* __restrict__ x, int64_t hv, int topk,
+                                  const int32_t* __restrict__ sorted_pairs, const int32_t* __restrict__ row_limit,
+                                  uint4* __restrict__ xp, int64_t ld, float2* __restrict__ xsum) {
+  const int64_t p = blockIdx.x;
+  if (row_limit && p >= __ldg(row_limit)) return;
+  const uint4* src = kGather ? x + static_cast<int64_t>(__ldg(sorted_pairs + p) / topk) * hv : x + p * hv;
+  uint4* dst = kGather ? xp + p * hv : nullptr;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = 0; base < hv; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool valid = i < hv;
+    float c = 0.f, s = 0.f;
+    if (valid) {
+      const uint4 v = __ldg(src + i);
+      if constexpr (kGather) dst[i] = v;
+      vec_sums<kBF16>(v, c, s);
+    }
+#pragma unroll
+    for (int o = 8; o; o >>= 1) {
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+    }
+    if (valid && (lane & 15) == 0) xsum[(i >> 4) * ld + p] = make_float2(c, s);
+  }
+}
+
 // ---------------------------------------------------------------------------------------- combine
 template <bool kBF16>
 __device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
@@ -274,6 +328,42 @@ int w4a16_moe_gather(const void* x, int64_t H, int64_t topk, const int32_t* sort
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
 
+int w4a16_moe_gather_sums(const void* x, int64_t H, int64_t topk, const int32_t* sorted_pairs, int64_t rows,
+                          const int32_t* row_limit, void* x_perm, int dtype, float* xsum, cudaStream_t stream) {
+  if (!x || !sorted_pairs || !x_perm || !xsum) return W4_ERR_ARG;
+  if (H <= 0 || H % 128 || topk <= 0) return W4_ERR_SHAPE;
+  if (rows <= 0) return W4_OK;
+  const int64_t ld = w4a16_group_sums_ld(rows);
+  auto* xs = reinterpret_cast<float2*>(xsum);
+  if (dtype == W4_DTYPE_BF16)
+    group_sums_kernel<true, true><<<rows, 128, 0, stream>>>(static_cast<const uint4*>(x), H / 8, (int)topk,
+                                                            sorted_pairs, row_limit, static_cast<uint4*>(x_perm), ld, xs);
+  else if (dtype == W4_DTYPE_F16)
+    group_sums_kernel<false, true><<<rows, 128, 0, stream>>>(static_cast<const uint4*>(x), H / 8, (int)topk,
+                                                             sorted_pairs, row_limit, static_cast<uint4*>(x_perm), ld, xs);
+  else
+    return W4_ERR_DTYPE;
+  return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
+}
+
+int w4a16_group_sums(const void* x, int64_t rows, int64_t K, const int32_t* row_limit, int dtype, float* xsum,
+                     cudaStream_t stream) {
+  if (!x || !xsum) return W4_ERR_ARG;
+  if (K <= 0 || K % 128) return W4_ERR_SHAPE;
+  if (rows <= 0) return W4_OK;
+  const int64_t ld = w4a16_group_sums_ld(rows);
+  auto* xs = reinterpret_cast<float2*>(xsum);
+  if (dtype == W4_DTYPE_BF16)
+    group_sums_kernel<true, false><<<rows, 128, 0, stream>>>(static_cast<const uint4*>(x), K / 8, 1, nullptr,
+                                                             row_limit, nullptr, ld, xs);
+  else if (dtype == W4_DTYPE_F16)
+    group_sums_kernel<false, false><<<rows, 128, 0, stream>>>(static_cast<const uint4*>(x), K / 8, 1, nullptr,
+                                                              row_limit, nullptr, ld, xs);
+  else
+    return W4_ERR_DTYPE;
+  return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
+}
+
 int w4a16_moe_combine(const void* y_perm, int64_t T, int64_t H, int64_t topk, const int32_t* pair_pos,
                       const float* topk_weights, int dtype, void* y, cudaStream_t stream) {
   if (!y_perm || !pair_pos || !topk_weights || !y) return W4_ERR_ARG;
@@ -293,8 +383,9 @@ int w4a16_moe_combine(const void* y_perm, int64_t T, int64_t H, int64_t topk, co
 
 int64_t w4a16_moe_workspace_bytes(int64_t T, int64_t topk, int64_t E, int64_t H, int64_t I) {
   const int64_t P = T * topk;
+  const int64_t ld = w4a16_group_sums_ld(P);
   return align256(4 * E) + align256(4 * (E + 1)) + 2 * align256(4 * P) + align256(2 * P * H) +
-         align256(2 * P * I) + align256(2 * P * H);
+         align256(2 * P * I) + align256(2 * P * H) + align256(8 * ld * (H / 128)) + align256(8 * ld * (I / 128));
 }
 
 int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, int64_t topk,
@@ -304,7 +395,9 @@ int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E,
   if (!x || !topk_ids || !topk_weights || !w13 || !w2 || !y || !workspace) return W4_ERR_ARG;
   if (workspace_bytes < w4a16_moe_workspace_bytes(T, topk, E, H, I)) return W4_ERR_WORKSPACE;
   if (T <= 0) return W4_OK;
+  if (H % 128 || I % 128) return W4_ERR_SHAPE;
   const int64_t P = T * topk;
+  const int64_t ld = w4a16_group_sums_ld(P);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
   int32_t* counts = reinterpret_cast<int32_t*>(ws); ws += align256(4 * E);
   int32_t* offsets = reinterpret_cast<int32_t*>(ws); ws += align256(4 * (E + 1));
@@ -312,13 +405,25 @@ int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E,
   int32_t* pos = reinterpret_cast<int32_t*>(ws); ws += align256(4 * P);
   void* xp = ws; ws += align256(2 * P * H);
   void* hp = ws; ws += align256(2 * P * I);
-  void* yp = ws;
+  void* yp = ws; ws += align256(2 * P * H);
+  float* xsum = reinterpret_cast<float*>(ws); ws += align256(8 * ld * (H / 128));
+  float* hsum = reinterpret_cast<float*>(ws);
   int rc;
   if ((rc = w4a16_moe_permute(topk_ids, P, E, counts, offsets, sorted, pos, stream))) return rc;
-  if ((rc = w4a16_moe_gather(x, H, topk, sorted, P, offsets + E, xp, stream))) return rc;
   const int nt = w4a16_pick_ntok(P, E);
-  if ((rc = w4a16_grouped_gemm(xp, P, H, w13, E, I, 1, counts, offsets, hp, dtype, nt, stream))) return rc;
-  if ((rc = w4a16_grouped_gemm(hp, P, I, w2, E, H, 0, counts, offsets, yp, dtype, nt, stream))) return rc;
+  const bool decode = nt <= 32;  // offset-code GEMMs need the per-group activation sums
+  if (decode) {
+    if ((rc = w4a16_moe_gather_sums(x, H, topk, sorted, P, offsets + E, xp, dtype, xsum, stream))) return rc;
+  } else if ((rc = w4a16_moe_gather(x, H, topk, sorted, P, offsets + E, xp, stream))) {
+    return rc;
+  }
+  if ((rc = w4a16_grouped_gemm(xp, P, H, w13, E, I, 1, counts, offsets, decode ? xsum : nullptr, hp, dtype, nt,
+                               stream)))
+    return rc;
+  if (decode && (rc = w4a16_group_sums(hp, P, I, offsets + E, dtype, hsum, stream))) return rc;
+  if ((rc = w4a16_grouped_gemm(hp, P, I, w2, E, H, 0, counts, offsets, decode ? hsum : nullptr, yp, dtype, nt,
+                               stream)))
+    return rc;
   return w4a16_moe_combine(yp, T, H, topk, pos, topk_weights, dtype, y, stream);
 }
 

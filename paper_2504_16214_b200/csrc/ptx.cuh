@@ -62,7 +62,7 @@ W4_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P;\n\t"
       "W4_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, 10000000;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
       "@!P bra W4_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
@@ -98,6 +98,15 @@ W4_DEV uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
+}
+
+// 8-byte cp.async global -> shared (LDGSTS), and an mbarrier arrival once all of this thread's prior
+// cp.async complete (.noinc: the barrier's expected count includes this arrival).
+W4_DEV void cp_async_8(void* dst_smem, const void* src_gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src_gmem) : "memory");
+}
+W4_DEV void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 // 2-D TMA tile load (tensor map in param/const/global space), coordinates innermost first.
@@ -153,6 +162,14 @@ W4_DEV void tmem_ld_x16(uint32_t taddr, uint32_t (&r)[16]) {
       : "memory");
 }
 
+// tcgen05.ld 32 lanes x 32 bit, 4 consecutive columns
+W4_DEV void tmem_ld_x4(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr)
+               : "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05: UMMA
 // D[tmem] (+)= A[tmem] * B[smem desc]; kind::f16 (fp16 or bf16 inputs, fp32 accumulate).
 W4_DEV void umma_ts_f16(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
@@ -161,6 +178,59 @@ W4_DEV void umma_ts_f16(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint3
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// D[tmem] (+)= A[smem desc] * B[smem desc]; kind::f16.
+W4_DEV void umma_ss_f16(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Warp-collective forms: the whole (converged) warp executes them with warp-uniform operands and one
+// elected lane issues -- the operands stay in uniform registers, so back-to-back MMAs issue without
+// the per-instruction waterfall the compiler emits for a lane-0-only region.
+W4_DEV void umma_ts_f16_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Four MMAs under one elect: operand q = base + immediate offset (D/A in TMEM columns, B descriptor
+// in 16-byte units), accumulate flags at run time.
+template <int D0, int D1, int D2, int D3, int A0, int A1, int A2, int A3, int B0, int B1, int B2, int B3>
+W4_DEV void umma4_ts_f16_warp(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t f0, uint32_t f1,
+                              uint32_t f2, uint32_t f3) {
+  asm volatile(
+      "{\n\t.reg .pred e, p0, p1, p2, p3;\n\t"
+      ".reg .b32 d0, d1, d2, d3, a0, a1, a2, a3;\n\t"
+      ".reg .b64 b0, b1, b2, b3;\n\t"
+      "setp.ne.b32 p0, %4, 0;\n\tsetp.ne.b32 p1, %5, 0;\n\tsetp.ne.b32 p2, %6, 0;\n\tsetp.ne.b32 p3, %7, 0;\n\t"
+      "add.u32 d0, %0, %8;\n\tadd.u32 d1, %0, %9;\n\tadd.u32 d2, %0, %10;\n\tadd.u32 d3, %0, %11;\n\t"
+      "add.u32 a0, %1, %12;\n\tadd.u32 a1, %1, %13;\n\tadd.u32 a2, %1, %14;\n\tadd.u32 a3, %1, %15;\n\t"
+      "add.u64 b0, %2, %16;\n\tadd.u64 b1, %2, %17;\n\tadd.u64 b2, %2, %18;\n\tadd.u64 b3, %2, %19;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d0], [a0], b0, %3, p0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], [a1], b1, %3, p1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d2], [a2], b2, %3, p2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [d3], [a3], b3, %3, p3;\n\t}" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(f0), "r"(f1), "r"(f2), "r"(f3), "n"(D0), "n"(D1), "n"(D2), "n"(D3), "n"(A0),
+      "n"(A1), "n"(A2), "n"(A3), "n"(B0), "n"(B1), "n"(B2), "n"(B3)
+      : "memory");
+}
+
+W4_DEV void umma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
       : "memory");
 }
 
@@ -179,11 +249,13 @@ __host__ __device__ constexpr uint32_t make_idesc_f16(uint32_t m, uint32_t n, bo
 
 // Shared-memory matrix descriptor for a K-major operand stored in 128-byte swizzled atoms
 // (8 rows x 128 B, rows contiguous, atoms stacked every 1024 B along M/N).
-W4_DEV uint64_t make_sdesc_sw128(uint32_t smem_addr) {
+// sbo = byte stride between consecutive 8-row groups; sbo = 0 makes every 8-row group read the same
+// atom (a row-periodic operand stored once).
+W4_DEV uint64_t make_sdesc_sw128(uint32_t smem_addr, uint32_t sbo = 1024u) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);       // start address  [0,14)
   d |= static_cast<uint64_t>(1u) << 16;                           // LBO (unused for SW128 K-major)
-  d |= static_cast<uint64_t>(1024u >> 4) << 32;                   // SBO = 1024 B   [32,46)
+  d |= static_cast<uint64_t>(sbo >> 4) << 32;                     // SBO            [32,46)
   d |= static_cast<uint64_t>(1u) << 46;                           // descriptor version (sm_100)
   d |= static_cast<uint64_t>(2u) << 61;                           // SWIZZLE_128B
   return d;

@@ -81,6 +81,20 @@ struct Dq<false> {
     o[2] = *reinterpret_cast<uint32_t*>(&q45);
     o[3] = *reinterpret_cast<uint32_t*>(&q67);
   }
+  // offset codes, LOP3 only: pairs (e0,e1),(e4,e5) come out as 1024 + q, pairs (e2,e3),(e6,e7) as
+  // 64 + q (0x5400 | q << 4: the nibble lands on mantissa bits 4..7, whose weight is 1 at 2^6). Both
+  // are exact fp16 integers; the GEMM removes the offsets and the zero point per (group, token)
+  // with the constant-row MMA (kOffsetRow* below), so no per-weight FP op is needed.
+  static __device__ __forceinline__ void word_raw(uint32_t w, uint32_t* o) {
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(o[0]) : "r"(w), "r"(0x000F000Fu), "r"(0x64006400u));
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(o[1]) : "r"(w), "r"(0x00F000F0u), "r"(0x54005400u));
+    const uint32_t w8 = w >> 8;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(o[2]) : "r"(w8), "r"(0x000F000Fu), "r"(0x64006400u));
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(o[3]) : "r"(w8), "r"(0x00F000F0u), "r"(0x54005400u));
+  }
+  // fp16 bits of the offset carried by element e (0..7) of a word in word_raw's output
+  static __host__ __device__ constexpr uint16_t offset_bits(int e) { return ((e >> 1) & 1) ? 0x5400 : 0x6400; }
+  static constexpr uint16_t kOneBits = 0x3C00;
   static __device__ __forceinline__ void word(uint32_t w, const Ctx& c, uint32_t* o) {
     const uint32_t kMagic = 0x64006400u;
     uint32_t a, b, d, e;
@@ -127,6 +141,14 @@ struct Dq<true> {
       o[i] = *reinterpret_cast<uint32_t*>(&q);
     }
   }
+  // offset codes: every pair comes out as 128 + q (exact bf16 integers)
+  static __device__ __forceinline__ void word_raw(uint32_t w, uint32_t* o) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(o[i]) : "r"(w >> (4 * i)), "r"(0x000F000Fu), "r"(0x43004300u));
+  }
+  static __host__ __device__ constexpr uint16_t offset_bits(int) { return 0x4300; }
+  static constexpr uint16_t kOneBits = 0x3F80;
   static __device__ __forceinline__ void word(uint32_t w, const Ctx& c, uint32_t* o) {
     const uint32_t kMagic = 0x43004300u;
 #pragma unroll
@@ -139,6 +161,15 @@ struct Dq<true> {
     }
   }
 };
+
+// One 16 B chunk (32 consecutive k of one row) as offset codes (see Dq::word_raw), k order.
+template <bool kBF16>
+__device__ __forceinline__ void raw_chunk(const uint4& v, uint32_t (&o)[16]) {
+  Dq<kBF16>::word_raw(v.x, o + 0);
+  Dq<kBF16>::word_raw(v.y, o + 4);
+  Dq<kBF16>::word_raw(v.z, o + 8);
+  Dq<kBF16>::word_raw(v.w, o + 12);
+}
 
 // Dequantise one 16 B chunk (32 consecutive k of one row) into 16 packed pairs, k order:
 // kScaled -> act((q - z) * s) (bit-exact dequant); otherwise the exact integers (q - z).
@@ -160,6 +191,11 @@ __device__ __forceinline__ void dequant_chunk(const uint4& v, const typename Dq<
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float2 lds_f2(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {

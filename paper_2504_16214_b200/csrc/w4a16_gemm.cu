@@ -16,17 +16,23 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include "ptx.cuh"
 #include "w4_format.cuh"
 #include "w4a16_moe.h"
 
 namespace w4 {
 
-constexpr int kNumThreads = 14 * 32;
+constexpr int kNumThreads = 15 * 32;
 constexpr int kDequantWarp0 = 2;
-constexpr int kNumDequantWarps = 8;
+constexpr int kNumDequantWarps = 8;  // two groups of 4 (one warp per TMEM lane quadrant) alternating stages
+constexpr int kDequantGroup = 4;
 constexpr int kEpiWarp0 = 10;
+constexpr int kMmaWarp2 = 14;        // optional second MMA issuer (kDualIssue: odd stages)
+constexpr bool kDualIssue = false;   // two warps issuing tcgen05.mma for alternate stages was observed
+                                     // to hang intermittently; one issuer is the supported layout
 constexpr int kMaxExperts = 1024;
 constexpr int kSmemBudget = 225 * 1024;
 
@@ -36,45 +42,129 @@ struct GemmArgs {
   const int32_t* expert_offsets; // [E+1]; rows of X (and of out) owned by expert e
   void* out;                     // [rows][NT*128] activation dtype
   int64_t ldo;
+  const float* xsum;             // offset mode: (C, S) [kt][sum_ld][2]
+  int64_t sum_ld, rows;
   int num_experts, nt, kt;
 };
 
-// kScaleEpi (decode, small token tiles): the dequant warps produce the exact integers (q - z) and
-// the MMA writes one fp32 partial per k-tile (= per quantisation group) into a TMEM ring; the
-// epilogue warps fold acc += s[row, g] * partial in registers. This removes the per-weight HMUL2
-// from the dequant (the scale is applied once per group per output instead of once per weight)
-// and is numerically at least as accurate as dequantise-then-MMA. Otherwise (prefill, large token
-// tiles) the dequant applies the scale and the MMA accumulates across k-tiles in TMEM.
+// Numeric modes.
+// kOffset (decode, 16/32-token tiles): the dequant warps emit *offset codes* -- the exact integers
+// c_k + q (Dq::word_raw: 5 integer ops per 8 weights, no FP op). Per stage (one quantisation group
+// per part) the MMA writes the fp32 partial P[n,m] = sum_k (c_k + q[n,k]) x[m,k] into a TMEM ring;
+// the per-(group, token) activation sums C[m] = sum_k c_k x[m,k] and S[m] = sum_k x[m,k] arrive
+// with the stage (8-byte cp.async of the caller's xsum by the producer warp's lanes, see
+// w4a16_group_sums), and the epilogue warps fold
+//     acc[n,m] += s[n,g] * (P[n,m] - C[m] - z[n,g] * S[m])     ( = s * sum_k (q - z) x )
+// so scale and zero point cost 3 FFMA per (row, token, group) instead of 2 FP ops per weight pair,
+// and only the tile's real tokens are processed (4-column chunks). At decode token counts the
+// tensor pipe pays ~38 cycles per M128 x N16 x K16 MMA whatever N is (the A-operand read), so the
+// MMA count per weight byte is the budget: exactly one MMA per 128x16 weight slice.
+// Otherwise (prefill, 64/128-token tiles, or no xsum given) the dequant applies zero and scale
+// (bit-exact act((q - z) * s)) and the MMA accumulates across k-groups in TMEM.
 // Block modes: how the two 8.5 KB parts of a 17 KB stage are used.
 constexpr int kModePlain = 0;   // one part (one k-group) per stage
 constexpr int kModeGateUp = 1;  // part 0 = gate rows, part 1 = up rows, same k-group (fused SwiGLU)
 constexpr int kModeKPair = 2;   // parts = two consecutive k-groups of the same rows (down proj.)
+constexpr int kEpiChunk = 4;    // offset-mode epilogue token granularity
 
-template <int kNTok, int kMode, bool kScaleEpi>
+template <int kNTok, int kMode, bool kOffset>
 struct Cfg {
   static constexpr bool kGated = kMode == kModeGateUp;
   static constexpr int kParts = kMode == kModePlain ? 1 : 2;
   static constexpr int kGroupsPerStage = kMode == kModeKPair ? 2 : 1;
   static constexpr int kBlk = kParts * kPartBytes;
   static constexpr int kXBytes = kGroupsPerStage * kNTok * kTileK * 2;  // X tile, 64-wide 128B-swizzle atoms
-  // one accumulator / partial stage: a partial per part in kScaleEpi mode, else gate|up or one
-  static constexpr int kAccCols = (kScaleEpi || kGated) ? kParts * kNTok : kNTok;
+  static constexpr int kSumBytes = kOffset ? kGroupsPerStage * kNTok * 8 : 0;  // (C, S) fp32 per group/token
+  // offset mode: each part's 128-k partial is split over kKSplit independent accumulators (k halves)
+  // so a stage issues kParts * kKSplit interleaved MMA chains -- a dependent chain of small-N MMAs is
+  // bound by the accumulate latency, not by the tensor pipe
+  static constexpr int kKSplit = (kOffset && kNTok == 16) ? 2 : 1;
+  static constexpr int kChainLen = (kTileK / 16) / kKSplit;
+  // one accumulator stage: offset mode = kKSplit partials per part; otherwise gate|up or one
+  // accumulator for the whole tile
+  static constexpr int kAccCols = kOffset ? kParts * kKSplit * kNTok : (kGated ? 2 * kNTok : kNTok);
   static constexpr int kACols = kParts * (kTileK / 2);  // fp16 pairs per 32-bit column
-  static constexpr int kNumAcc = kScaleEpi ? 4 : ((2 * kAccCols + 2 * kACols <= 512) ? 2 : 1);
+  // TMEM budget (512 columns): A ring + accumulator ring
+  static constexpr int kNumA_ = kOffset ? ((3 * kACols + 2 * kAccCols <= 512) ? 3 : 2) : 0;
+  static constexpr int kNumAccO = (512 - kNumA_ * kACols) / kAccCols;
+  static constexpr int kNumAcc = kOffset ? (kNumAccO > 4 ? 4 : kNumAccO)
+                                         : ((2 * kAccCols + 2 * kACols <= 512) ? 2 : 1);
   static constexpr int kNumA0 = (512 - kNumAcc * kAccCols) / kACols;
-  static constexpr int kNumA = kNumA0 > 4 ? 4 : kNumA0;
-  static constexpr int kStageBytes = kBlk + kXBytes;
+  static constexpr int kNumA = kOffset ? kNumA_ : (kNumA0 > 4 ? 4 : kNumA0);
+  static constexpr int kStageBytes = kBlk + kXBytes + kSumBytes;
   static constexpr int kFixed = 2048 + 4 * (kMaxExperts + 1);  // barriers + tile table
   static constexpr int kNS0 = (kSmemBudget - kFixed - 1024) / kStageBytes;
   static constexpr int kNS = kNS0 > 12 ? 12 : kNS0;
-  static constexpr int kEmptyArrivals = kNumDequantWarps + 1 + (kScaleEpi ? 4 : 0);
-  // X ring first (needs 1024 B alignment for the 128B swizzle atoms), then weights.
+  static constexpr int kEmptyArrivals = kDequantGroup + 1 + (kOffset ? 4 : 0);
+  static constexpr int kSumItems = kGroupsPerStage * kNTok;      // 8-byte (C, S) items per stage
+  static constexpr int kFullArrivals = 1 + (kOffset ? 32 : 0);   // expect_tx + the 32 sums cp.async lanes
+  // X ring first (needs 1024 B alignment for the 128B swizzle atoms), sums ring, then weights.
   static constexpr int kSmemBytes = 1024 + kNS * kStageBytes + kFixed;
-  static_assert(kNumA >= 2, "TMEM budget");
+  static_assert(kNumA >= 2 && kNumAcc >= (kOffset ? 2 : 1), "TMEM budget");
+  static_assert(kNumA * kACols + kNumAcc * kAccCols <= 512, "TMEM budget");
   static_assert(kNS >= 2, "smem budget");
   static_assert(kXBytes % 1024 == 0, "X tile alignment");
-  static_assert(!kScaleEpi || kNTok <= 32, "register accumulators");
+  static_assert(!kOffset || kNTok <= 32, "register accumulators");
 };
+
+// MMA q of a stage (q = (u * kKSplit + hs) * kParts + p; kk = hs * kChainLen + u): operand offsets
+// relative to the stage's accumulator column, A-ring column and X descriptor, and the accumulate flag.
+template <int kNTok, int kMode, bool kOffset>
+struct StageMmas {
+  using C = Cfg<kNTok, kMode, kOffset>;
+  static constexpr int kCount = (kTileK / 16) * C::kParts;
+  __host__ __device__ static constexpr int p(int q) { return q % C::kParts; }
+  __host__ __device__ static constexpr int hs(int q) { return (q / C::kParts) % C::kKSplit; }
+  __host__ __device__ static constexpr int u(int q) { return q / (C::kParts * C::kKSplit); }
+  __host__ __device__ static constexpr int kk(int q) { return hs(q) * C::kChainLen + u(q); }
+  __host__ __device__ static constexpr int d(int q) { return kOffset ? (p(q) * C::kKSplit + hs(q)) * kNTok : (C::kGated ? p(q) * kNTok : 0); }
+  __host__ __device__ static constexpr int a(int q) { return p(q) * 64 + kk(q) * 8; }
+  __host__ __device__ static constexpr int b(int q) {  // k-pair: part p reads the second 128-k half of the X tile
+    return ((kMode == kModeKPair ? p(q) * 2 * (kNTok * 128) : 0) + (kk(q) >> 2) * (kNTok * 128) + (kk(q) & 3) * 32) >> 4;
+  }
+  __device__ static __forceinline__ uint32_t flag(int q, uint32_t j) {
+    return kOffset ? (u(q) != 0) : (C::kGated ? ((j | kk(q)) != 0) : ((j | p(q) | kk(q)) != 0));
+  }
+};
+
+template <int kNTok, int kMode, bool kOffset, int kQ>
+__device__ __forceinline__ void issue_mma4(uint32_t dcol, uint32_t acol, uint64_t xdesc, uint32_t idesc, uint32_t j) {
+  using S = StageMmas<kNTok, kMode, kOffset>;
+  umma4_ts_f16_warp<S::d(kQ), S::d(kQ + 1), S::d(kQ + 2), S::d(kQ + 3), S::a(kQ), S::a(kQ + 1), S::a(kQ + 2),
+                    S::a(kQ + 3), S::b(kQ), S::b(kQ + 1), S::b(kQ + 2), S::b(kQ + 3)>(
+      dcol, acol, xdesc, idesc, S::flag(kQ, j), S::flag(kQ + 1, j), S::flag(kQ + 2, j), S::flag(kQ + 3, j));
+}
+
+template <int kNTok, int kMode, bool kOffset, int kQ = 0>
+__device__ __forceinline__ void issue_stage_mmas(uint32_t dcol, uint32_t acol, uint64_t xdesc, uint32_t idesc,
+                                                 uint32_t j) {
+  if constexpr (kQ < StageMmas<kNTok, kMode, kOffset>::kCount) {
+    issue_mma4<kNTok, kMode, kOffset, kQ>(dcol, acol, xdesc, idesc, j);
+    issue_stage_mmas<kNTok, kMode, kOffset, kQ + 4>(dcol, acol, xdesc, idesc, j);
+  }
+}
+
+// Opt-in per-stage timeline of CTA 0 (w4a16_debug_trace): clock64 at each role's sync points.
+__device__ long long* g_w4_trace = nullptr;
+constexpr int kTraceCap = 4096;
+__device__ __forceinline__ void trace_at(long long* tr, int ev, uint32_t idx) {
+#ifndef W4A16_TRACE
+  return;
+#endif
+  if (tr && idx < kTraceCap) {
+    long long c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    tr[ev * kTraceCap + idx] = c;
+  }
+}
+
+// trace build only: per-CTA progress (rows 10..13 of the trace buffer: producer / dequant / MMA /
+// epilogue stages completed, indexed by blockIdx.x), to locate a stuck CTA
+__device__ __forceinline__ void progress_at(int ev, uint32_t n) {
+#ifdef W4A16_TRACE
+  if (g_w4_trace) *reinterpret_cast<volatile long long*>(g_w4_trace + (10 + ev) * kTraceCap + blockIdx.x) = n;
+#endif
+}
 
 struct TileInfo {
   int e, n_tile, m_start, m_rows;
@@ -124,16 +214,17 @@ struct Ring {  // (stage, phase) iterator of an mbarrier ring
   }
 };
 
-template <int kNTok, int kMode, bool kBF16, bool kScaleEpi>
+template <int kNTok, int kMode, bool kBF16, bool kOffset>
 __global__ void __launch_bounds__(kNumThreads, 1)
     w4a16_moe_gemm_kernel(const GemmArgs args, const __grid_constant__ CUtensorMap xmap) {
-  using C = Cfg<kNTok, kMode, kScaleEpi>;
+  using C = Cfg<kNTok, kMode, kOffset>;
   constexpr bool kGated = C::kGated;
   const int n_stages = args.kt / C::kGroupsPerStage;  // stages per tile
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_x = smem;                                  // [NS][kXBytes]
-  uint8_t* smem_w = smem + C::kNS * C::kXBytes;            // [NS][kBlk]
+  uint8_t* smem_s = smem + C::kNS * C::kXBytes;            // [NS][kSumBytes] (offset mode)
+  uint8_t* smem_w = smem_s + C::kNS * C::kSumBytes;        // [NS][kBlk]
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_w + C::kNS * C::kBlk);
   uint64_t* full = bars;
   uint64_t* empty = full + C::kNS;
@@ -146,12 +237,17 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 
   const uint32_t warp = warp_idx();
   const uint32_t lane = lane_id();
+  #ifdef W4A16_TRACE
+  long long* const tr = blockIdx.x == 0 ? g_w4_trace : nullptr;
+#else
+  long long* const tr = nullptr;
+#endif
 
   if (warp == 0) {
     tmem_alloc<512>(tmem_holder);
   } else if (warp == 1 && lane == 0) {
-    for (int i = 0; i < C::kNS; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], C::kEmptyArrivals); }
-    for (int i = 0; i < C::kNumA; ++i) { mbar_init(&afull[i], kNumDequantWarps); mbar_init(&aempty[i], 1); }
+    for (int i = 0; i < C::kNS; ++i) { mbar_init(&full[i], C::kFullArrivals); mbar_init(&empty[i], C::kEmptyArrivals); }
+    for (int i = 0; i < C::kNumA; ++i) { mbar_init(&afull[i], kDequantGroup); mbar_init(&aempty[i], 1); }
     for (int i = 0; i < C::kNumAcc; ++i) { mbar_init(&accfull[i], 1); mbar_init(&accempty[i], 4); }
     fence_mbar_init();
   } else if (warp == 2) {
@@ -185,9 +281,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
+    // lane 0: weight block (1-D bulk copy) + X tile (2-D TMA) on the stage's full barrier (tx bytes);
+    // offset mode: all 32 lanes also copy the stage's (C, S) sums with 8-byte cp.async and arrive on
+    // the same barrier when their copies land.
+    if (kOffset || lane == 0) {
       const uint64_t pol_w = policy_evict_first();
       Ring st;
+      uint32_t pgs = 0;
       TileInfo ti;
       for (int t = blockIdx.x; get_tile<kNTok>(t, mt_off, args, ti); t += gridDim.x) {
         // per (expert, n-tile): kt k-groups of (gated ? 2 : 1) parts, stage j = bytes [j*kBlk, (j+1)*kBlk)
@@ -195,109 +295,159 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                                                  static_cast<int64_t>(args.kt) * (kGated ? 2 : 1) * kPartBytes;
         for (int j = 0; j < n_stages; ++j) {
           mbar_wait(&empty[st.i], st.ph ^ 1);
-          mbar_arrive_expect_tx(&full[st.i], C::kBlk + C::kXBytes);
-          bulk_g2s_hint(smem_w + st.i * C::kBlk, wsrc + static_cast<int64_t>(j) * C::kBlk, C::kBlk, &full[st.i],
-                        pol_w);
-          uint8_t* xs = smem_x + st.i * C::kXBytes;
+          if (lane == 0) {
+            trace_at(tr, 0, pgs++);
+            mbar_arrive_expect_tx(&full[st.i], C::kBlk + C::kXBytes);
+            bulk_g2s_hint(smem_w + st.i * C::kBlk, wsrc + static_cast<int64_t>(j) * C::kBlk, C::kBlk, &full[st.i],
+                          pol_w);
+            uint8_t* xs = smem_x + st.i * C::kXBytes;
 #pragma unroll
-          for (int h = 0; h < 2 * C::kGroupsPerStage; ++h)
-            tma_load_2d(xs + h * (kNTok * 128), &xmap, j * C::kGroupsPerStage * kTileK + h * 64, ti.m_start,
-                        &full[st.i]);
+            for (int h = 0; h < 2 * C::kGroupsPerStage; ++h)
+              tma_load_2d(xs + h * (kNTok * 128), &xmap, j * C::kGroupsPerStage * kTileK + h * 64, ti.m_start,
+                          &full[st.i]);
+          }
+          if constexpr (kOffset) {
+            // all 32 lanes copy and arrive every stage (fewer items than lanes: items are duplicated --
+            // a lane arriving .noinc without its own cp.async in flight was observed never to fire);
+            // rows past the end read row 0 of the group (never used)
+            uint8_t* ss = smem_s + st.i * C::kSumBytes;
+#pragma unroll
+            for (int i0 = 0; i0 < (C::kSumItems > 32 ? C::kSumItems : 32); i0 += 32) {
+              const int i = (i0 + lane) % C::kSumItems;
+              const int g = i / kNTok, m = i % kNTok;
+              const int64_t r = ti.m_start + m < args.rows ? ti.m_start + m : 0;
+              cp_async_8(ss + i * 8,
+                         args.xsum + ((static_cast<int64_t>(j) * C::kGroupsPerStage + g) * args.sum_ld + r) * 2);
+            }
+            cp_async_arrive_noinc(&full[st.i]);
+          }
+          if (lane == 0) progress_at(0, pgs);
           st.next(C::kNS);
         }
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+  } else if (warp == 1 || warp == kMmaWarp2) {
+    // ------------------------------------------------------------ MMA issuer(s)
+    // Offset mode: every stage is self-contained (fresh partials), so two issuing threads take
+    // alternate stages and each one's wait chain (accempty, full, afull) overlaps the other's.
+    // Otherwise one issuer accumulates the whole tile.
+    const uint32_t my_par = warp == 1 ? 0u : 1u;
+    if ((kOffset && kDualIssue) || warp == 1) {  // whole warp; one elected lane issues
       constexpr uint32_t idesc = make_idesc_f16(128, kNTok, kBF16);
       Ring st, ar, acc;
+      uint32_t gs = 0;  // global stage counter (parity selects the issuer in offset mode)
       TileInfo ti;
       for (int t = blockIdx.x; get_tile<kNTok>(t, mt_off, args, ti); t += gridDim.x) {
-        if constexpr (!kScaleEpi) {
+        if constexpr (!kOffset) {
           mbar_wait(&accempty[acc.i], acc.ph ^ 1);
           tc_fence_after();
         }
-        for (int j = 0; j < n_stages; ++j) {
-          if constexpr (kScaleEpi) {  // fresh partials per stage (one per k-group)
+        for (int j = 0; j < n_stages; ++j, ++gs) {
+          if constexpr (kOffset) {  // fresh partials per stage (one per k-group)
+            if (kDualIssue && (gs & 1u) != my_par) {
+              st.next(C::kNS);
+              ar.next(C::kNumA);
+              acc.next(C::kNumAcc);
+              continue;
+            }
             mbar_wait(&accempty[acc.i], acc.ph ^ 1);
           }
           mbar_wait(&full[st.i], st.ph);
           mbar_wait(&afull[ar.i], ar.ph);
           tc_fence_after();
+          trace_at(tr, 4, gs);
           const uint32_t dcol = tbase + acc.i * C::kAccCols;
-          const uint32_t xaddr = smem_u32(smem_x + st.i * C::kXBytes);
+          const uint64_t xdesc = make_sdesc_sw128(smem_u32(smem_x + st.i * C::kXBytes));
           const uint32_t acol = tbase + kAcol0 + ar.i * C::kACols;
-#pragma unroll
-          for (int p = 0; p < C::kParts; ++p) {
-            // k-pair: part p reads the second 128-k half of the X tile; gate/up: both read the same
-            const uint32_t xp = xaddr + (kMode == kModeKPair ? p * 2 * (kNTok * 128) : 0);
-            const uint32_t dp = dcol + ((kScaleEpi || kGated) ? p * kNTok : 0);
-#pragma unroll
-            for (int kk = 0; kk < kTileK / 16; ++kk) {
-              const uint64_t bdesc = make_sdesc_sw128(xp + (kk >> 2) * (kNTok * 128) + (kk & 3) * 32);
-              const uint32_t accum = (kScaleEpi || kGated) ? (kScaleEpi ? (kk != 0) : ((j | kk) != 0))
-                                                           : ((j | p | kk) != 0);
-              umma_ts_f16(dp, acol + p * 64 + kk * 8, bdesc, idesc, accum);
-            }
-          }
-          umma_commit(&empty[st.i]);
-          umma_commit(&aempty[ar.i]);
+          // k-step outer, independent accumulators (gate / up, or the two k-groups of a pair) inner.
+          // kTileK/16 * kParts MMAs, issued four per elect with compile-time operand offsets
+          // (StageMmas::op computes them; see umma4_ts_f16_warp)
+          const uint32_t jf = static_cast<uint32_t>(j);
+          issue_stage_mmas<kNTok, kMode, kOffset>(dcol, acol, xdesc, idesc, jf);
+          trace_at(tr, 5, gs);
+          progress_at(2, gs + 1);
+          umma_commit_warp(&empty[st.i]);
+          umma_commit_warp(&aempty[ar.i]);
           st.next(C::kNS);
           ar.next(C::kNumA);
-          if constexpr (kScaleEpi) {
-            umma_commit(&accfull[acc.i]);
+          if constexpr (kOffset) {
+            umma_commit_warp(&accfull[acc.i]);
             acc.next(C::kNumAcc);
           }
         }
-        if constexpr (!kScaleEpi) {
-          umma_commit(&accfull[acc.i]);
+        if constexpr (!kOffset) {
+          umma_commit_warp(&accfull[acc.i]);
           acc.next(C::kNumAcc);
         }
       }
     }
   } else if (warp < kEpiWarp0) {
     // ------------------------------------------------------------ dequant: int4 smem -> TMEM A ring
+    // Group g (warps 2-5 / 6-9) takes the stages of parity g; inside a group warp w owns the TMEM lane
+    // quadrant w % 4 (32 weight rows) and all four 32-wide k chunks of the 128-wide tile.
     const int dw = warp - kDequantWarp0;
+    const uint32_t my_par = dw / kDequantGroup;
     const uint32_t quad = warp & 3;
     const int row = quad * 32 + lane;
-    const int c0 = (dw >> 2) * 2;  // this warp's two 32-wide k chunks of the 128-wide tile
     const uint32_t lane_off = (quad * 32) << 16;
-    const uint32_t code_off = (c0 * kTileRows + row) * 16;
+    const uint32_t code_off = row * 16;
     Ring st, ar;
+    uint32_t gs = 0;
     TileInfo ti;
     for (int t = blockIdx.x; get_tile<kNTok>(t, mt_off, args, ti); t += gridDim.x) {
-      for (int j = 0; j < n_stages; ++j) {
+      for (int j = 0; j < n_stages; ++j, ++gs) {
+        if ((gs & 1u) != my_par) {
+          st.next(C::kNS);
+          ar.next(C::kNumA);
+          continue;
+        }
         mbar_wait(&full[st.i], st.ph);
+        const bool trd = lane == 0 && quad == 0;
+        if (trd) trace_at(tr, 1, gs);
         const uint32_t blk = w_u32 + st.i * C::kBlk;
-        uint4 v[C::kParts][2];
+        uint4 v[C::kParts][kChunks];
         uint32_t sb[C::kParts], zb[C::kParts];
 #pragma unroll
         for (int p = 0; p < C::kParts; ++p) {
           const uint32_t part = blk + p * kPartBytes;
-          v[p][0] = lds128(part + code_off);
-          v[p][1] = lds128(part + code_off + kTileRows * 16);
-          zb[p] = lds_u8(part + kZeroOff + (row >> 1));
-          if constexpr (!kScaleEpi) sb[p] = lds_u16(part + kScaleOff + row * 2);
-          else sb[p] = 0;
+#pragma unroll
+          for (int c = 0; c < kChunks; ++c) v[p][c] = lds128(part + code_off + c * (kTileRows * 16));
+          if constexpr (!kOffset) {
+            zb[p] = lds_u8(part + kZeroOff + (row >> 1));
+            sb[p] = lds_u16(part + kScaleOff + row * 2);
+          } else {
+            zb[p] = sb[p] = 0;
+          }
         }
         mbar_wait(&aempty[ar.i], ar.ph ^ 1);
         tc_fence_after();
+        if (trd) trace_at(tr, 2, gs);
         const uint32_t acol = tbase + lane_off + kAcol0 + ar.i * C::kACols;
 #pragma unroll
         for (int p = 0; p < C::kParts; ++p) {
-          const uint32_t z = (row & 1) ? (zb[p] >> 4) : (zb[p] & 15u);
-          const auto ctx = Dq<kBF16>::make(z, static_cast<uint16_t>(sb[p]));
+          if constexpr (kOffset) {
 #pragma unroll
-          for (int cc = 0; cc < 2; ++cc) {
-            uint32_t r[16];
-            dequant_chunk<kBF16, !kScaleEpi>(v[p][cc], ctx, r);
-            tmem_st_x16(acol + p * 64 + (c0 + cc) * 16, r);
+            for (int c = 0; c < kChunks; ++c) {
+              uint32_t r[16];
+              raw_chunk<kBF16>(v[p][c], r);
+              tmem_st_x16(acol + p * 64 + c * 16, r);
+            }
+          } else {
+            const uint32_t z = (row & 1) ? (zb[p] >> 4) : (zb[p] & 15u);
+            const auto ctx = Dq<kBF16>::make(z, static_cast<uint16_t>(sb[p]));
+#pragma unroll
+            for (int c = 0; c < kChunks; ++c) {
+              uint32_t r[16];
+              dequant_chunk<kBF16, true>(v[p][c], ctx, r);
+              tmem_st_x16(acol + p * 64 + c * 16, r);
+            }
           }
         }
         tc_wait_st();
         tc_fence_before();
         __syncwarp();
+        if (trd) trace_at(tr, 3, gs);
+        if (trd) progress_at(1, gs + 1);
         if (lane == 0) {
           mbar_arrive(&afull[ar.i]);
           mbar_arrive(&empty[st.i]);
@@ -313,50 +463,81 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     const uint32_t lane_off = (quad * 32) << 16;
     uint16_t* out = reinterpret_cast<uint16_t*>(args.out);
     Ring acc, st;
+    uint32_t egs = 0;
+    const bool tre = lane == 0 && quad == 0;
     TileInfo ti;
     for (int t = blockIdx.x; get_tile<kNTok>(t, mt_off, args, ti); t += gridDim.x) {
+      if (tre) trace_at(tr, 9, egs);
       uint16_t* obase = out + static_cast<int64_t>(ti.m_start) * args.ldo + ti.n_tile * kTileRows + row;
-      if constexpr (kScaleEpi) {
-        float a[C::kParts][kNTok];
+      if constexpr (kOffset) {
+        constexpr int kOuts = kGated ? 2 : 1;  // gate|up accumulators, else one (k-pair parts summed)
+        const int m_rows = ti.m_rows;
+        float a[kOuts][kNTok];
 #pragma unroll
-        for (int p = 0; p < C::kParts; ++p)
+        for (int o = 0; o < kOuts; ++o)
 #pragma unroll
-          for (int i = 0; i < kNTok; ++i) a[p][i] = 0.f;
+          for (int i = 0; i < kNTok; ++i) a[o][i] = 0.f;
         for (int j = 0; j < n_stages; ++j) {
           mbar_wait(&full[st.i], st.ph);
+          if (tre) trace_at(tr, 6, egs);
           const uint32_t blk = w_u32 + st.i * C::kBlk;
-          float sc[C::kParts];
+          const uint32_t sums = smem_u32(smem_s + st.i * C::kSumBytes);
+          float sc[C::kParts], zf[C::kParts];
 #pragma unroll
-          for (int p = 0; p < C::kParts; ++p) sc[p] = act_bits_to_float<kBF16>(lds_u16(blk + p * kPartBytes + kScaleOff + row * 2));
+          for (int p = 0; p < C::kParts; ++p) {
+            const uint32_t part = blk + p * kPartBytes;
+            sc[p] = act_bits_to_float<kBF16>(lds_u16(part + kScaleOff + row * 2));
+            const uint32_t zb = lds_u8(part + kZeroOff + (row >> 1));
+            zf[p] = static_cast<float>((row & 1) ? (zb >> 4) : (zb & 15u));
+          }
           mbar_wait(&accfull[acc.i], acc.ph);
           tc_fence_after();
+          if (tre) trace_at(tr, 7, egs);
           const uint32_t dcol = tbase + lane_off + acc.i * C::kAccCols;
-          uint32_t r[C::kParts][kNTok];
 #pragma unroll
-          for (int p = 0; p < C::kParts; ++p)
+          for (int cb = 0; cb < kNTok / kEpiChunk; ++cb) {
+            if (cb * kEpiChunk < m_rows) {  // warp-uniform: only the tile's real tokens
+              uint32_t r[C::kParts][C::kKSplit][kEpiChunk];
 #pragma unroll
-            for (int cb = 0; cb < kNTok / 16; ++cb)
-              tmem_ld_x16(dcol + p * kNTok + cb * 16, *reinterpret_cast<uint32_t(*)[16]>(&r[p][cb * 16]));
-          tc_wait_ld();
+              for (int p = 0; p < C::kParts; ++p)
+#pragma unroll
+                for (int hs = 0; hs < C::kKSplit; ++hs)
+                  tmem_ld_x4(dcol + (p * C::kKSplit + hs) * kNTok + cb * kEpiChunk, r[p][hs]);
+              tc_wait_ld();
+#pragma unroll
+              for (int i = 0; i < kEpiChunk; ++i) {
+                const int m = cb * kEpiChunk + i;
+#pragma unroll
+                for (int p = 0; p < C::kParts; ++p) {
+                  const int g = kMode == kModeKPair ? p : 0;
+                  const int o = kGated ? p : 0;
+                  const float2 cs = lds_f2(sums + (g * kNTok + m) * 8);  // (C, S), broadcast
+                  float pv = __uint_as_float(r[p][0][i]);
+#pragma unroll
+                  for (int hs = 1; hs < C::kKSplit; ++hs) pv += __uint_as_float(r[p][hs][i]);
+                  const float d = pv - fmaf(zf[p], cs.y, cs.x);
+                  a[o][m] = fmaf(sc[p], d, a[o][m]);
+                }
+              }
+            }
+          }
           tc_fence_before();
           __syncwarp();
+          if (tre) trace_at(tr, 8, egs);
+          ++egs;
+          if (tre) progress_at(3, egs);
           if (lane == 0) {
             mbar_arrive(&accempty[acc.i]);
             mbar_arrive(&empty[st.i]);
           }
-#pragma unroll
-          for (int p = 0; p < C::kParts; ++p)
-#pragma unroll
-            for (int i = 0; i < kNTok; ++i) a[p][i] = fmaf(sc[p], __uint_as_float(r[p][i]), a[p][i]);
           acc.next(C::kNumAcc);
           st.next(C::kNS);
         }
 #pragma unroll
         for (int m = 0; m < kNTok; ++m) {
-          if (m < ti.m_rows) {
+          if (m < m_rows) {
             float v;
             if constexpr (kGated) v = silu_f(a[0][m]) * a[1][m];
-            else if constexpr (kMode == kModeKPair) v = a[0][m] + a[1][m];
             else v = a[0][m];
             obase[static_cast<int64_t>(m) * args.ldo] = to_act_bits<kBF16>(v);
           }
@@ -400,7 +581,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) progress_at(3, 1000000);  // CTA reached the exit barrier
   if (warp == 0) {
+    __syncwarp();  // tcgen05.dealloc is .sync.aligned: the producer's lanes must be reconverged, or the
+                   // columns stay allocated and the next launch's tcgen05.alloc on this SM waits forever
     tc_fence_after();
     tmem_dealloc<512>(tbase);
   }
@@ -527,10 +711,10 @@ int sm_count() {
   return n;
 }
 
-template <int kNTok, int kMode, bool kBF16, bool kScaleEpi>
+template <int kNTok, int kMode, bool kBF16, bool kOffset>
 int launch_gemm(const GemmArgs& a, const CUtensorMap& map, int grid, cudaStream_t st) {
-  using C = Cfg<kNTok, kMode, kScaleEpi>;
-  auto kern = w4a16_moe_gemm_kernel<kNTok, kMode, kBF16, kScaleEpi>;
+  using C = Cfg<kNTok, kMode, kOffset>;
+  auto kern = w4a16_moe_gemm_kernel<kNTok, kMode, kBF16, kOffset>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
@@ -542,10 +726,14 @@ int launch_gemm(const GemmArgs& a, const CUtensorMap& map, int grid, cudaStream_
 }
 
 template <int kMode, bool kBF16>
-int dispatch_ntok(int ntok, const GemmArgs& a, const CUtensorMap& m, int grid, cudaStream_t st) {
+int dispatch_ntok(int ntok, bool offset, const GemmArgs& a, const CUtensorMap& m, int grid, cudaStream_t st) {
+  if (offset) {
+    if (ntok == 16) return launch_gemm<16, kMode, kBF16, true>(a, m, grid, st);
+    if (ntok == 32) return launch_gemm<32, kMode, kBF16, true>(a, m, grid, st);
+  }
   switch (ntok) {
-    case 16: return launch_gemm<16, kMode, kBF16, true>(a, m, grid, st);
-    case 32: return launch_gemm<32, kMode, kBF16, true>(a, m, grid, st);
+    case 16: return launch_gemm<16, kMode, kBF16, false>(a, m, grid, st);
+    case 32: return launch_gemm<32, kMode, kBF16, false>(a, m, grid, st);
     case 64: return launch_gemm<64, kMode, kBF16, false>(a, m, grid, st);
     case 128: return launch_gemm<128, kMode, kBF16, false>(a, m, grid, st);
     default: return W4_ERR_ARG;
@@ -556,29 +744,40 @@ int dispatch_ntok(int ntok, const GemmArgs& a, const CUtensorMap& m, int grid, c
 
 extern "C" {
 
+/* Debug aid (not in the public header's hot path): per-stage clock64 timeline of CTA 0 of every
+ * subsequent grouped-GEMM launch into `buf` (int64 [10][4096], caller-owned, device), or off (null). */
+int w4a16_debug_trace(void* buf) {
+  return cudaMemcpyToSymbol(g_w4_trace, &buf, sizeof(buf)) == cudaSuccess ? W4_OK : W4_ERR_CUDA;
+}
+
 int w4a16_tile_rows(void) { return kTileRows; }
 int w4a16_tile_k(void) { return kTileK; }
 int w4a16_part_bytes(void) { return kPartBytes; }
 
 int w4a16_pick_ntok(int64_t rows, int64_t num_experts) {
-  const int64_t avg = num_experts > 0 ? (rows + num_experts - 1) / num_experts : rows;
-  if (avg <= 16) return 16;
-  if (avg <= 32) return 32;
-  if (avg <= 64) return 64;
+  // Token tile = smallest of 16/32/64/128 that holds a typical expert's rows in ONE m-tile (weights
+  // are streamed once per m-tile): mean + 2.5 sigma of the per-expert count under uniform routing.
+  const double mu = num_experts > 0 ? static_cast<double>(rows) / static_cast<double>(num_experts)
+                                    : static_cast<double>(rows);
+  const double est = mu + 2.5 * sqrt(mu);
+  if (est <= 16.0) return 16;
+  if (est <= 32.0) return 32;
+  if (est <= 64.0) return 64;
   return 128;
 }
 
+int64_t w4a16_group_sums_ld(int64_t rows) { return (rows + 1) & ~int64_t(1); }
+
 int w4a16_grouped_gemm(const void* x, int64_t rows, int64_t K, const uint8_t* wblocks, int64_t num_experts,
                        int64_t n_out, int gated, const int32_t* expert_counts, const int32_t* expert_offsets,
-                       void* out, int dtype, int ntok, cudaStream_t stream) {
+                       const float* xsum, void* out, int dtype, int ntok, cudaStream_t stream) {
   if (!x || !wblocks || !expert_counts || !expert_offsets || !out) return W4_ERR_ARG;
   if (K <= 0 || K % kTileK || n_out <= 0 || n_out % kTileRows) return W4_ERR_SHAPE;
   if (num_experts <= 0 || num_experts > kMaxExperts) return W4_ERR_SHAPE;
   if (dtype != W4_DTYPE_F16 && dtype != W4_DTYPE_BF16) return W4_ERR_DTYPE;
   if (rows <= 0) return W4_OK;
   if (ntok <= 0) ntok = w4a16_pick_ntok(rows, num_experts);
-  CUtensorMap map;
-  if (make_x_map(&map, x, rows, K, ntok) != W4_OK) return W4_ERR_CUDA;
+  if (ntok != 16 && ntok != 32 && ntok != 64 && ntok != 128) return W4_ERR_ARG;
   GemmArgs a;
   a.wblocks = wblocks;
   a.expert_counts = expert_counts;
@@ -588,14 +787,23 @@ int w4a16_grouped_gemm(const void* x, int64_t rows, int64_t K, const uint8_t* wb
   a.num_experts = static_cast<int>(num_experts);
   a.nt = static_cast<int>(n_out / kTileRows);
   a.kt = static_cast<int>(K / kTileK);
+  a.xsum = xsum;
+  a.sum_ld = w4a16_group_sums_ld(rows);
+  a.rows = rows;
+  const int mode = gated ? kModeGateUp : (a.kt % 2 == 0 ? kModeKPair : kModePlain);
+  const bool offset = xsum != nullptr && ntok <= 32;
+  CUtensorMap map;
+  if (make_x_map(&map, x, rows, K, ntok) != W4_OK) return W4_ERR_CUDA;
   const int grid = sm_count();
   const bool bf = dtype == W4_DTYPE_BF16;
-  if (gated) return bf ? dispatch_ntok<kModeGateUp, true>(ntok, a, map, grid, stream)
-                       : dispatch_ntok<kModeGateUp, false>(ntok, a, map, grid, stream);
-  if (a.kt % 2 == 0) return bf ? dispatch_ntok<kModeKPair, true>(ntok, a, map, grid, stream)
-                               : dispatch_ntok<kModeKPair, false>(ntok, a, map, grid, stream);
-  return bf ? dispatch_ntok<kModePlain, true>(ntok, a, map, grid, stream)
-            : dispatch_ntok<kModePlain, false>(ntok, a, map, grid, stream);
+  if (mode == kModeGateUp)
+    return bf ? dispatch_ntok<kModeGateUp, true>(ntok, offset, a, map, grid, stream)
+              : dispatch_ntok<kModeGateUp, false>(ntok, offset, a, map, grid, stream);
+  if (mode == kModeKPair)
+    return bf ? dispatch_ntok<kModeKPair, true>(ntok, offset, a, map, grid, stream)
+              : dispatch_ntok<kModeKPair, false>(ntok, offset, a, map, grid, stream);
+  return bf ? dispatch_ntok<kModePlain, true>(ntok, offset, a, map, grid, stream)
+            : dispatch_ntok<kModePlain, false>(ntok, offset, a, map, grid, stream);
 }
 
 int w4a16_dequant(const uint8_t* wblocks, int64_t num_experts, int64_t n_rows, int64_t K, int parts, int dtype,

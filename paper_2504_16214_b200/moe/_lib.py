@@ -42,10 +42,17 @@ SIGNATURES = {
     "w4a16_moe_permute": (_i, [_p, _i64, _i64, _p, _p, _p, _p, _p]),
     "w4a16_moe_gather": (_i, [_p, _i64, _i64, _p, _i64, _p, _p, _p]),
     "w4a16_moe_combine": (_i, [_p, _i64, _i64, _i64, _p, _p, _i, _p, _p]),
-    "w4a16_grouped_gemm": (_i, [_p, _i64, _i64, _p, _i64, _i64, _i, _p, _p, _p, _i, _i, _p]),
+    "w4a16_moe_gather_sums": (_i, [_p, _i64, _i64, _p, _i64, _p, _p, _i, _p, _p]),
+    "w4a16_group_sums": (_i, [_p, _i64, _i64, _p, _i, _p, _p]),
+    "w4a16_group_sums_ld": (_i64, [_i64]),
+    "w4a16_grouped_gemm": (_i, [_p, _i64, _i64, _p, _i64, _i64, _i, _p, _p, _p, _p, _i, _i, _p]),
     "w4a16_pick_ntok": (_i, [_i64, _i64]),
     "w4a16_moe_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64]),
     "w4a16_moe_forward": (_i, [_p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _i, _p, _p, _i64, _p]),
+}
+# debug aids exported by the library but not part of the public header
+DEBUG_SIGNATURES = {
+    "w4a16_debug_trace": (_i, [_p]),
 }
 
 _lock = threading.Lock()
@@ -64,7 +71,7 @@ def load() -> C.CDLL:
                     f"{LIB_PATH} not built: run `python -m paper_2504_16214_b200._build` "
                     "(there is no CPU fallback for this path)")
             lib = C.CDLL(str(LIB_PATH))
-            for name, (res, args) in SIGNATURES.items():
+            for name, (res, args) in {**SIGNATURES, **DEBUG_SIGNATURES}.items():
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

@@ -61,8 +61,11 @@ class CudaBackend:
     def experts(x, weights, counts, offsets, ntok):
         E, H, I = weights.num_experts, weights.hidden, weights.inter
         nt = ntok or cuda_ops.pick_ntok(x.shape[0], E)
-        h = cuda_ops.grouped_gemm(x, weights.w13.blocks, E, I, True, counts, offsets, nt)
-        return cuda_ops.grouped_gemm(h, weights.w2.blocks, E, H, False, counts, offsets, nt)
+        decode = nt <= 32
+        xs = cuda_ops.group_sums(x) if decode else None
+        h = cuda_ops.grouped_gemm(x, weights.w13.blocks, E, I, True, counts, offsets, nt, xsum=xs)
+        hs = cuda_ops.group_sums(h) if decode else None
+        return cuda_ops.grouped_gemm(h, weights.w2.blocks, E, H, False, counts, offsets, nt, xsum=hs)
 
 
 def moe_w4a16_ep(x: torch.Tensor, weights, topk_weights: torch.Tensor, topk_ids: torch.Tensor, group=None,

@@ -120,15 +120,25 @@ def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, 
     dev = x.device
     with tm.span("permute"):
         counts, offsets, sorted_pairs, pair_pos = ops.moe_permute(topk_ids, E)
-    with tm.span("gather"):
-        xp = ops.moe_gather(x, sorted_pairs, k, P, offsets[E:], out=_ws.get("xp", (P, H), x.dtype, dev))
     nt = ntok or ops.pick_ntok(P, E)
+    decode = nt <= 32  # offset-code GEMMs: per-group activation sums ride along with X and h
+    with tm.span("gather"):
+        xp_buf = _ws.get("xp", (P, H), x.dtype, dev)
+        if decode:
+            xp, xs = ops.moe_gather_sums(x, sorted_pairs, k, P, offsets[E:], out=xp_buf,
+                                         sums=_ws.get("xs", ops.sums_shape(P, H), torch.float32, dev))
+        else:
+            xp, xs = ops.moe_gather(x, sorted_pairs, k, P, offsets[E:], out=xp_buf), None
     with tm.span("gemm_gate_up"):
         h = ops.grouped_gemm(xp, weights.w13.blocks, E, I, True, counts, offsets, nt,
-                             out=_ws.get("h", (P, I), x.dtype, dev))
+                             out=_ws.get("h", (P, I), x.dtype, dev), xsum=xs)
+    hs = None
+    if decode:
+        with tm.span("sums_h"):
+            hs = ops.group_sums(h, offsets[E:], out=_ws.get("hs", ops.sums_shape(P, I), torch.float32, dev))
     with tm.span("gemm_down"):
         yp = ops.grouped_gemm(h, weights.w2.blocks, E, H, False, counts, offsets, nt,
-                              out=_ws.get("yp", (P, H), x.dtype, dev))
+                              out=_ws.get("yp", (P, H), x.dtype, dev), xsum=hs)
     with tm.span("combine"):
         return ops.moe_combine(yp, pair_pos, topk_weights)
 
@@ -148,5 +158,7 @@ def w4a16_linear(x: torch.Tensor, w, ntok: int = 0) -> torch.Tensor:
     dev = x.device
     counts = torch.tensor([M], dtype=torch.int32, device=dev)
     offsets = torch.tensor([0, M], dtype=torch.int32, device=dev)
-    return ops.grouped_gemm(x.contiguous(), w.blocks, 1, w.n_rows, False, counts, offsets,
-                            ntok or ops.pick_ntok(M, 1))
+    nt = ntok or ops.pick_ntok(M, 1)
+    x = x.contiguous()
+    xs = ops.group_sums(x) if nt <= 32 else None
+    return ops.grouped_gemm(x, w.blocks, 1, w.n_rows, False, counts, offsets, nt, xsum=xs)

@@ -106,6 +106,39 @@ def moe_gather(x: torch.Tensor, sorted_pairs: torch.Tensor, topk: int, rows: int
     return out
 
 
+def sums_shape(rows: int, K: int) -> tuple[int, int, int]:
+    """Shape of the per-(k-group, row) activation sums array: [K/128][ld][2] fp32."""
+    return (K // 128, int(_lib.load().w4a16_group_sums_ld(rows)), 2)
+
+
+def moe_gather_sums(x: torch.Tensor, sorted_pairs: torch.Tensor, topk: int, rows: int | None = None,
+                    row_limit: torch.Tensor | None = None, out: torch.Tensor | None = None,
+                    sums: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """moe_gather plus the (C, S) group sums of the gathered rows (decode-mode GEMM input)."""
+    _need_cuda(x, sorted_pairs)
+    rows = sorted_pairs.numel() if rows is None else rows
+    H = x.shape[1]
+    if out is None:
+        out = torch.empty((rows, H), dtype=x.dtype, device=x.device)
+    if sums is None:
+        sums = torch.empty(sums_shape(rows, H), dtype=torch.float32, device=x.device)
+    _lib.call("w4a16_moe_gather_sums", x.data_ptr(), H, topk, sorted_pairs.data_ptr(), rows, _ptr(row_limit),
+              out.data_ptr(), act_code(x.dtype), sums.data_ptr(), _stream())
+    return out, sums
+
+
+def group_sums(x: torch.Tensor, row_limit: torch.Tensor | None = None,
+               out: torch.Tensor | None = None) -> torch.Tensor:
+    """(C, S) sums per (k-group of 128, row) of x [rows, K] (see include/w4a16_moe.h)."""
+    _need_cuda(x)
+    rows, K = x.shape
+    if out is None:
+        out = torch.empty(sums_shape(rows, K), dtype=torch.float32, device=x.device)
+    _lib.call("w4a16_group_sums", x.data_ptr(), rows, K, _ptr(row_limit), act_code(x.dtype), out.data_ptr(),
+              _stream())
+    return out
+
+
 def moe_combine(y_perm: torch.Tensor, pair_pos: torch.Tensor, topk_weights: torch.Tensor,
                 out: torch.Tensor | None = None) -> torch.Tensor:
     _need_cuda(y_perm, pair_pos, topk_weights)
@@ -121,15 +154,16 @@ def moe_combine(y_perm: torch.Tensor, pair_pos: torch.Tensor, topk_weights: torc
 # ------------------------------------------------------------------------------------------ GEMM
 def grouped_gemm(x: torch.Tensor, blocks: torch.Tensor, num_experts: int, n_out: int, gated: bool,
                  expert_counts: torch.Tensor, expert_offsets: torch.Tensor, ntok: int = 0,
-                 out: torch.Tensor | None = None) -> torch.Tensor:
-    """out[off_e + m] = act(x[off_e + m] @ W_e^T) (gated: silu(gate) * up), per expert."""
+                 out: torch.Tensor | None = None, xsum: torch.Tensor | None = None) -> torch.Tensor:
+    """out[off_e + m] = act(x[off_e + m] @ W_e^T) (gated: silu(gate) * up), per expert. ``xsum``
+    (group_sums / moe_gather_sums of x) selects the decode kernel for 16/32-token tiles."""
     _need_cuda(x, blocks, expert_counts, expert_offsets)
     rows, K = x.shape
     if out is None:
         out = torch.empty((rows, n_out), dtype=x.dtype, device=x.device)
     _lib.call("w4a16_grouped_gemm", x.data_ptr(), rows, K, blocks.data_ptr(), num_experts, n_out, int(gated),
-              expert_counts.data_ptr(), expert_offsets.data_ptr(), out.data_ptr(), act_code(x.dtype), ntok,
-              _stream())
+              expert_counts.data_ptr(), expert_offsets.data_ptr(), _ptr(xsum), out.data_ptr(), act_code(x.dtype),
+              ntok, _stream())
     return out
 
 

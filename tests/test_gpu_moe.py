@@ -108,8 +108,28 @@ def test_gather_combine(dt):
     np.testing.assert_allclose(_from_dev_act(y, dt), O.round_act(want, dt), rtol=RTOL, atol=ATOL)
 
 
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+def test_group_sums(dt):
+    """(C, S) per (k-group, row): S = sum x, C = sum c_k x with the decode dequant's offsets."""
+    rng = np.random.default_rng(9)
+    T, k, E, H = 21, 3, 8, 1024
+    ids = np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)
+    x = O.round_act(rng.standard_normal((T, H)).astype(np.float32) * 0.5, dt)
+    ops = _ops()
+    c, o, sp, pp = ops.moe_permute(torch.from_numpy(ids).cuda(), E)
+    xp, xs = ops.moe_gather_sums(_to_dev_act(x, dt), sp, k)
+    _, _, rsp, _ = O.moe_permute(ids, E)
+    xr = x[rsp // k]
+    assert np.array_equal(_from_dev_act(xp, dt), xr)
+    want = O.group_sums(xr, dt)                     # [H/128][rows][2]
+    got = xs.cpu().numpy()[:, :xr.shape[0], :]
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-3)
+    got2 = ops.group_sums(xp).cpu().numpy()[:, :xr.shape[0], :]
+    np.testing.assert_array_equal(got2, got)
+
+
 # ------------------------------------------------------------------------------------------- grouped GEMM
-def _gemm_case(dt, gated, counts, K, N, ntok, seed=0):
+def _gemm_case(dt, gated, counts, K, N, ntok, seed=0, sums=False):
     rng = np.random.default_rng(seed)
     E = len(counts)
     rows = int(sum(counts))
@@ -119,8 +139,10 @@ def _gemm_case(dt, gated, counts, K, N, ntok, seed=0):
     cnt = np.asarray(counts, np.int32)
     off = np.zeros(E + 1, np.int32)
     np.cumsum(cnt, out=off[1:])
-    out = _ops().grouped_gemm(_to_dev_act(x, dt), w.blocks, E, N, gated, torch.from_numpy(cnt).cuda(),
-                              torch.from_numpy(off).cuda(), ntok)
+    xd = _to_dev_act(x, dt)
+    xs = _ops().group_sums(xd) if sums else None
+    out = _ops().grouped_gemm(xd, w.blocks, E, N, gated, torch.from_numpy(cnt).cuda(),
+                              torch.from_numpy(off).cuda(), ntok, xsum=xs)
     torch.cuda.synchronize()
     want = O.grouped_gemm(x, O.dequant(q, z, s, dt), cnt, off, dt, gated)
     return _from_dev_act(out, dt), want
@@ -128,20 +150,40 @@ def _gemm_case(dt, gated, counts, K, N, ntok, seed=0):
 
 @pytest.mark.parametrize("ntok", [16, 32, 64, 128])
 @pytest.mark.parametrize("gated", [False, True])
-def test_grouped_gemm_f16(ntok, gated):
-    got, want = _gemm_case("f16", gated, [5, 0, 17, 1, 40, 130], K=512, N=256, ntok=ntok)
+@pytest.mark.parametrize("sums", [False, True])
+@pytest.mark.parametrize("K", [512, 384])  # k-pair (even K/128) and plain (odd) block modes
+def test_grouped_gemm_f16(ntok, gated, sums, K):
+    got, want = _gemm_case("f16", gated, [5, 0, 17, 1, 40, 130], K=K, N=256, ntok=ntok, sums=sums)
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
 
 
 @pytest.mark.parametrize("gated", [False, True])
-def test_grouped_gemm_bf16(gated):
-    got, want = _gemm_case("bf16", gated, [3, 16, 0, 33], K=384, N=384, ntok=16)
+@pytest.mark.parametrize("sums", [False, True])
+@pytest.mark.parametrize("K", [384, 512])
+def test_grouped_gemm_bf16(gated, sums, K):
+    got, want = _gemm_case("bf16", gated, [3, 16, 0, 33], K=K, N=384, ntok=16, sums=sums)
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=2 * ATOL)
+
+
+@pytest.mark.parametrize("gated", [False, True])
+@pytest.mark.parametrize("sums", [False, True])
+def test_grouped_gemm_ring_wrap(gated, sums):
+    """Enough tiles that every CTA runs several long tiles: the smem / TMEM rings wrap many times."""
+    rng = np.random.default_rng(11)
+    counts = list(rng.integers(1, 5, size=40))
+    got, want = _gemm_case("f16", gated, counts, K=2048, N=1024, ntok=16, seed=12, sums=sums)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+def test_grouped_gemm_decode_shapes():
+    """DeepSeek-R1 down-projection shape (K=2048 -> 8 k-pair stages per tile) in decode mode."""
+    got, want = _gemm_case("f16", False, [2, 1, 3, 0, 2], K=2048, N=512, ntok=16, seed=4, sums=True)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
 
 
 def test_dense_w4a16_linear():
     """Config 1 shape: M=16, N=K=1024, one expert."""
-    got, want = _gemm_case("f16", False, [16], K=1024, N=1024, ntok=16, seed=3)
+    got, want = _gemm_case("f16", False, [16], K=1024, N=1024, ntok=16, seed=3, sums=True)
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
 
 

@@ -79,3 +79,19 @@ def test_moe_forward_linearity_in_routing_weights():
     y = O.moe_forward(x, O.dequant(q13, z13, s13, "f16"), O.dequant(q2, z2, s2, "f16"), ids, w, "f16")
     y2 = O.moe_forward_expertwise(x, q13, z13, s13, q2, z2, s2, ids, w, "f16")
     assert np.array_equal(y, y2)
+
+
+def test_group_sums_restatement():
+    """(C, S) group sums: direct loop vs the vectorised restatement, both dtypes."""
+    rng = np.random.default_rng(3)
+    x = O.round_act(rng.standard_normal((5, 256)).astype(np.float32), "f16")
+    for dt in ("f16", "bf16"):
+        got = O.group_sums(x, dt)
+        assert got.shape == (2, 5, 2)
+        for g in range(2):
+            for r in range(5):
+                xs = x[r, g * 128:(g + 1) * 128].astype(np.float64)
+                c = np.array([128.0 if dt == "bf16" else (64.0 if (k % 8) in (2, 3, 6, 7) else 1024.0)
+                              for k in range(128)])
+                assert np.isclose(got[g, r, 1], xs.sum(), rtol=1e-6, atol=1e-4)
+                assert np.isclose(got[g, r, 0], (c * xs).sum(), rtol=1e-6, atol=1e-2)

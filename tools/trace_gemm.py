@@ -1,0 +1,71 @@
+#!/usr/bin/env python
+"""Per-stage timeline of CTA 0 of one grouped-GEMM launch (w4a16_debug_trace): prints the mean
+interval between the roles' sync points in steady state. --which gate_up|down."""
+import argparse
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+from paper_2504_16214_b200.moe import _lib, ops  # noqa: E402
+from paper_2504_16214_b200.moe.weights import random_packed  # noqa: E402
+
+EV = ["prod_empty_ok", "dq_full_ok", "dq_aempty_ok", "dq_afull_arrive", "mma_ready", "mma_issued",
+      "epi_full_ok", "epi_accfull_ok", "epi_done", "epi_tile_start"]
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--which", default="gate_up")
+ap.add_argument("--experts", type=int, default=224)
+ap.add_argument("--per-expert", type=int, default=2)
+ap.add_argument("--ntok", type=int, default=16)
+a = ap.parse_args()
+H, I = 7168, 2048
+dev = torch.device("cuda", 0)
+E = a.experts
+gd = torch.Generator(device=dev).manual_seed(1)
+gated = a.which == "gate_up"
+N, K = (2 * I, H) if gated else (H, I)
+w = random_packed(E, N, K, gated, torch.float16, gd, dev)
+counts = torch.full((E,), a.per_expert, dtype=torch.int32, device=dev)
+off = torch.zeros(E + 1, dtype=torch.int32, device=dev)
+off[1:] = torch.cumsum(counts, 0)
+x = (torch.randn((E * a.per_expert, K), device=dev) * 0.5).half()
+nout = N // 2 if gated else N
+xs = ops.group_sums(x) if a.ntok <= 32 else None
+for _ in range(2):
+    ops.grouped_gemm(x, w.blocks, E, nout, gated, counts, off, a.ntok, xsum=xs)
+buf = torch.full((14, 4096), -1, dtype=torch.int64, device=dev)
+_lib.call("w4a16_debug_trace", buf.data_ptr())
+torch.cuda.synchronize()
+ops.grouped_gemm(x, w.blocks, E, nout, gated, counts, off, a.ntok, xsum=xs)
+torch.cuda.synchronize()
+_lib.call("w4a16_debug_trace", None)
+t = buf.cpu().numpy()
+n = int((t[4] >= 0).sum())
+t0 = t[t >= 0].min()
+t = np.where(t >= 0, t - t0, -1)
+lo, hi = n // 4, 3 * n // 4
+s = slice(lo, hi)
+print(f"{a.which}: stages traced {n}, steady window [{lo},{hi})")
+per = np.diff(t[4][s]).mean()
+print(f"  stage period (mma_ready diffs)          {per:8.1f} cyc")
+def m(x):
+    return float(np.mean(x))
+print(f"  dequant: full_ok -> aempty_ok            {m(t[2][s] - t[1][s]):8.1f}")
+print(f"  dequant: aempty_ok -> afull arrive       {m(t[3][s] - t[2][s]):8.1f}")
+print(f"  mma: afull arrive -> mma_ready           {m(t[4][s] - t[3][s]):8.1f}")
+print(f"  mma: ready -> issued                     {m(t[5][s] - t[4][s]):8.1f}")
+print(f"  epi: mma_issued -> accfull_ok            {m(t[7][s] - t[5][s]):8.1f}")
+print(f"  epi: accfull_ok -> done                  {m(t[8][s] - t[7][s]):8.1f}")
+print(f"  epi: full_ok -> accfull_ok               {m(t[7][s] - t[6][s]):8.1f}")
+print(f"  producer: empty_ok(gs) - mma_ready(gs)   {m(t[0][s] - t[4][s]):8.1f}")
+print(f"  dq aempty_ok(gs) - mma_issued(gs-3)      {m(t[2][lo + 3:hi] - t[5][lo:hi - 3]):8.1f}")
+print(f"  mma_ready(gs) - epi_done(gs-2)           {m(t[4][lo + 2:hi] - t[8][lo:hi - 2]):8.1f}")
+print(f"  full_ok(dq) - prod_empty_ok (load lat)   {m(t[1][s] - t[0][s]):8.1f}")
+ts = t[9][t[9] >= 0]
+print(f"  tiles traced {len(ts)}")
+print("  first 12 stages (cycles rel.):")
+for i in range(lo, lo + 12):
+    print("   ", i, " ".join(f"{EV[e][:10]}={t[e][i]}" for e in (0, 1, 2, 3, 4, 5, 7, 8)))

@@ -28,7 +28,7 @@ def launch_shares(path: Path) -> str:
     for r in rows[h + 1:]:
         if len(r) > vi:
             v = float(r[vi].replace(",", ""))
-            d[r[ki]].append(v * (1e3 if r[ui] == "msecond" else 1e-3 if r[ui] == "nsecond" else 1.0))
+            d[r[ki]].append(v * {"ms": 1e3, "msecond": 1e3, "ns": 1e-3, "nsecond": 1e-3}.get(r[ui], 1.0))
     tot = sum(sum(v) for v in d.values()) or 1.0
     lines = [f"# ncu --metrics gpu__time_duration.sum --clock-control none (cold, serialised); "
              f"{sum(len(v) for v in d.values())} launches, {tot:.1f} us total", 
@@ -50,14 +50,14 @@ def main():
         shutil.copy(OUT / "bench.json", dst / "bench.json")
     if (OUT / "launches.csv").exists():
         (dst / "launches.txt").write_text(launch_shares(OUT / "launches.csv"))
-    rep = OUT / a.rep
-    if rep.exists():
+    reps = [OUT / r for r in ("prof_gemm0.ncu-rep", "prof_gemm1.ncu-rep", a.rep) if (OUT / r).exists()]
+    summ, hot = [], []
+    for rep in reps:
         py = sys.executable
-        s = subprocess.run([py, str(ROOT / "tools" / "ncu_summary.py"), str(rep)], capture_output=True, text=True).stdout
-        (dst / "ncu_full_summary.txt").write_text(s)
-        h = subprocess.run([py, str(ROOT / "tools" / "ncu_sass_hot.py"), str(rep), "25"], capture_output=True,
-                           text=True).stdout
-        (dst / "ncu_sass_hot.txt").write_text(h)
+        summ.append(subprocess.run([py, str(ROOT / "tools" / "ncu_summary.py"), str(rep)], capture_output=True,
+                                   text=True).stdout)
+        hot.append(subprocess.run([py, str(ROOT / "tools" / "ncu_sass_hot.py"), str(rep), "25"], capture_output=True,
+                                  text=True).stdout)
         raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         rows = list(csv.reader(io.StringIO(raw)))
         hdr, units = rows[0], rows[1]
@@ -75,6 +75,9 @@ def main():
             elif "w4a16_moe_gemm_kernel" in name:
                 traffic[f"gemm_down_T{a.tokens}"] = int(b)
         tr_path.write_text(json.dumps(traffic, indent=1, sort_keys=True) + "\n")
+    if summ:
+        (dst / "ncu_full_summary.txt").write_text("".join(summ))
+        (dst / "ncu_sass_hot.txt").write_text("".join(hot))
     print("wrote", dst)
 
 
