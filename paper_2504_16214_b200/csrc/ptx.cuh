@@ -68,6 +68,84 @@ W4_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// ---------------------------------------------------------------- clusters (CTA pairs)
+W4_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+W4_DEV uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+W4_DEV uint32_t nclusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of `bar` in CTA `rank` of this cluster
+W4_DEV uint32_t mapa_shared(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+W4_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+W4_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "W4_WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra W4_WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// Wait for two barrier phases at once: both try_waits are in flight together, so a ready barrier
+// costs its latency once instead of once per barrier (a completed phase stays completed until the
+// waiter consumes it, so re-testing is safe).
+W4_DEV void mbar_wait2_cluster(uint64_t* b0, uint32_t ph0, uint64_t* b1, uint32_t ph1) {
+  asm volatile(
+      "{\n\t.reg .pred P0, P1;\n\t"
+      "W4_WAIT2_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P0, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%2], %3;\n\t"
+      "@!P0 bra W4_WAIT2_%=;\n\t"
+      "@!P1 bra W4_WAIT2_%=;\n\t}" ::"r"(smem_u32(b0)),
+      "r"(ph0), "r"(smem_u32(b1)), "r"(ph1)
+      : "memory");
+}
+
+// Warp-wide forms: the whole (converged) warp waits and branches on a vote, so ptxas sees uniform
+// control flow afterwards and keeps warp-uniform values in uniform registers (MMA operands).
+W4_DEV void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P, Q;\n\t"
+      "W4_WAITW_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], %1;\n\t"
+      "vote.sync.all.pred Q, P, 0xffffffff;\n\t"
+      "@!Q bra.uni W4_WAITW_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+W4_DEV void mbar_wait2_warp(uint64_t* b0, uint32_t ph0, uint64_t* b1, uint32_t ph1) {
+  asm volatile(
+      "{\n\t.reg .pred P0, P1, P, Q;\n\t"
+      "W4_WAIT2W_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P0, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%2], %3;\n\t"
+      "and.pred P, P0, P1;\n\t"
+      "vote.sync.all.pred Q, P, 0xffffffff;\n\t"
+      "@!Q bra.uni W4_WAIT2W_%=;\n\t}" ::"r"(smem_u32(b0)),
+      "r"(ph0), "r"(smem_u32(b1)), "r"(ph1)
+      : "memory");
+}
+
+W4_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- bulk copies (async proxy)
 // 1-D bulk copy global -> shared, completion counted on an mbarrier (bytes % 16 == 0).
 W4_DEV void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
@@ -129,6 +207,17 @@ W4_DEV void tmem_alloc(uint32_t* dst_smem) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
                "n"(kCols));
   asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+
+template <uint32_t kCols>
+W4_DEV void tmem_alloc_pair(uint32_t* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(kCols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+}
+template <uint32_t kCols>
+W4_DEV void tmem_dealloc_pair(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols));
 }
 
 template <uint32_t kCols>
@@ -203,26 +292,22 @@ W4_DEV void umma_ts_f16_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, 
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// Four MMAs under one elect: operand q = base + immediate offset (D/A in TMEM columns, B descriptor
-// in 16-byte units), accumulate flags at run time.
-template <int D0, int D1, int D2, int D3, int A0, int A1, int A2, int A3, int B0, int B1, int B2, int B3>
-W4_DEV void umma4_ts_f16_warp(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t f0, uint32_t f1,
-                              uint32_t f2, uint32_t f3) {
+// single-thread commit for a CTA pair (caller elected)
+W4_DEV void umma_commit_pair(uint64_t* bar) {
   asm volatile(
-      "{\n\t.reg .pred e, p0, p1, p2, p3;\n\t"
-      ".reg .b32 d0, d1, d2, d3, a0, a1, a2, a3;\n\t"
-      ".reg .b64 b0, b1, b2, b3;\n\t"
-      "setp.ne.b32 p0, %4, 0;\n\tsetp.ne.b32 p1, %5, 0;\n\tsetp.ne.b32 p2, %6, 0;\n\tsetp.ne.b32 p3, %7, 0;\n\t"
-      "add.u32 d0, %0, %8;\n\tadd.u32 d1, %0, %9;\n\tadd.u32 d2, %0, %10;\n\tadd.u32 d3, %0, %11;\n\t"
-      "add.u32 a0, %1, %12;\n\tadd.u32 a1, %1, %13;\n\tadd.u32 a2, %1, %14;\n\tadd.u32 a3, %1, %15;\n\t"
-      "add.u64 b0, %2, %16;\n\tadd.u64 b1, %2, %17;\n\tadd.u64 b2, %2, %18;\n\tadd.u64 b3, %2, %19;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+// commit for a CTA pair: arrive on the barrier at the same smem offset in both CTAs (mask 0b11)
+W4_DEV void umma_commit_pair_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [d0], [a0], b0, %3, p0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [d1], [a1], b1, %3, p1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [d2], [a2], b2, %3, p2;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [d3], [a3], b3, %3, p3;\n\t}" ::"r"(d),
-      "r"(a), "l"(b), "r"(idesc), "r"(f0), "r"(f1), "r"(f2), "r"(f3), "n"(D0), "n"(D1), "n"(D2), "n"(D3), "n"(A0),
-      "n"(A1), "n"(A2), "n"(A3), "n"(B0), "n"(B1), "n"(B2), "n"(B3)
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::
+          "r"(smem_u32(bar)), "h"(static_cast<uint16_t>(3))
       : "memory");
 }
 

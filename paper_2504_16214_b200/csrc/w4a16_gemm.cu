@@ -21,18 +21,16 @@
 #include <cstdlib>
 #include "ptx.cuh"
 #include "w4_format.cuh"
+#include "mma_stage.cuh"
 #include "w4a16_moe.h"
 
 namespace w4 {
 
-constexpr int kNumThreads = 15 * 32;
+constexpr int kNumThreads = 14 * 32;
 constexpr int kDequantWarp0 = 2;
 constexpr int kNumDequantWarps = 8;  // two groups of 4 (one warp per TMEM lane quadrant) alternating stages
 constexpr int kDequantGroup = 4;
 constexpr int kEpiWarp0 = 10;
-constexpr int kMmaWarp2 = 14;        // optional second MMA issuer (kDualIssue: odd stages)
-constexpr bool kDualIssue = false;   // two warps issuing tcgen05.mma for alternate stages was observed
-                                     // to hang intermittently; one issuer is the supported layout
 constexpr int kMaxExperts = 1024;
 constexpr int kSmemBudget = 225 * 1024;
 
@@ -67,13 +65,19 @@ constexpr int kModeGateUp = 1;  // part 0 = gate rows, part 1 = up rows, same k-
 constexpr int kModeKPair = 2;   // parts = two consecutive k-groups of the same rows (down proj.)
 constexpr int kEpiChunk = 4;    // offset-mode epilogue token granularity
 
-template <int kNTok, int kMode, bool kOffset>
+// kPair: a CTA pair (cluster of 2 on one TPC) runs tcgen05.mma.cta_group::2 -- M = 256 weight rows
+// (each CTA dequantises its own 128-row n-tile into its own TMEM), N = kNTok tokens with each CTA
+// holding kNTok/2 rows of the X tile; one leader thread issues for both, halving MMA instructions
+// and issuer waits per weight byte.
+template <int kNTok, int kMode, bool kOffset, bool kPair = false>
 struct Cfg {
   static constexpr bool kGated = kMode == kModeGateUp;
+  static constexpr int kCG = kPair ? 2 : 1;
+  static constexpr int kXRows = kNTok / kCG;  // X rows held by this CTA
   static constexpr int kParts = kMode == kModePlain ? 1 : 2;
   static constexpr int kGroupsPerStage = kMode == kModeKPair ? 2 : 1;
   static constexpr int kBlk = kParts * kPartBytes;
-  static constexpr int kXBytes = kGroupsPerStage * kNTok * kTileK * 2;  // X tile, 64-wide 128B-swizzle atoms
+  static constexpr int kXBytes = kGroupsPerStage * kXRows * kTileK * 2;  // X tile, 64-wide 128B-swizzle atoms
   static constexpr int kSumBytes = kOffset ? kGroupsPerStage * kNTok * 8 : 0;  // (C, S) fp32 per group/token
   // offset mode: each part's 128-k partial is split over kKSplit independent accumulators (k halves)
   // so a stage issues kParts * kKSplit interleaved MMA chains -- a dependent chain of small-N MMAs is
@@ -98,6 +102,8 @@ struct Cfg {
   static constexpr int kEmptyArrivals = kDequantGroup + 1 + (kOffset ? 4 : 0);
   static constexpr int kSumItems = kGroupsPerStage * kNTok;      // 8-byte (C, S) items per stage
   static constexpr int kFullArrivals = 1 + (kOffset ? 32 : 0);   // expect_tx + the 32 sums cp.async lanes
+  static constexpr int kAFullArrivals = kDequantGroup * kCG;     // dequant groups of both CTAs (leader)
+  static constexpr int kAccEmptyArrivals = 4 * kCG;              // epilogue warps of both CTAs (leader)
   // X ring first (needs 1024 B alignment for the 128B swizzle atoms), sums ring, then weights.
   static constexpr int kSmemBytes = 1024 + kNS * kStageBytes + kFixed;
   static_assert(kNumA >= 2 && kNumAcc >= (kOffset ? 2 : 1), "TMEM budget");
@@ -106,43 +112,6 @@ struct Cfg {
   static_assert(kXBytes % 1024 == 0, "X tile alignment");
   static_assert(!kOffset || kNTok <= 32, "register accumulators");
 };
-
-// MMA q of a stage (q = (u * kKSplit + hs) * kParts + p; kk = hs * kChainLen + u): operand offsets
-// relative to the stage's accumulator column, A-ring column and X descriptor, and the accumulate flag.
-template <int kNTok, int kMode, bool kOffset>
-struct StageMmas {
-  using C = Cfg<kNTok, kMode, kOffset>;
-  static constexpr int kCount = (kTileK / 16) * C::kParts;
-  __host__ __device__ static constexpr int p(int q) { return q % C::kParts; }
-  __host__ __device__ static constexpr int hs(int q) { return (q / C::kParts) % C::kKSplit; }
-  __host__ __device__ static constexpr int u(int q) { return q / (C::kParts * C::kKSplit); }
-  __host__ __device__ static constexpr int kk(int q) { return hs(q) * C::kChainLen + u(q); }
-  __host__ __device__ static constexpr int d(int q) { return kOffset ? (p(q) * C::kKSplit + hs(q)) * kNTok : (C::kGated ? p(q) * kNTok : 0); }
-  __host__ __device__ static constexpr int a(int q) { return p(q) * 64 + kk(q) * 8; }
-  __host__ __device__ static constexpr int b(int q) {  // k-pair: part p reads the second 128-k half of the X tile
-    return ((kMode == kModeKPair ? p(q) * 2 * (kNTok * 128) : 0) + (kk(q) >> 2) * (kNTok * 128) + (kk(q) & 3) * 32) >> 4;
-  }
-  __device__ static __forceinline__ uint32_t flag(int q, uint32_t j) {
-    return kOffset ? (u(q) != 0) : (C::kGated ? ((j | kk(q)) != 0) : ((j | p(q) | kk(q)) != 0));
-  }
-};
-
-template <int kNTok, int kMode, bool kOffset, int kQ>
-__device__ __forceinline__ void issue_mma4(uint32_t dcol, uint32_t acol, uint64_t xdesc, uint32_t idesc, uint32_t j) {
-  using S = StageMmas<kNTok, kMode, kOffset>;
-  umma4_ts_f16_warp<S::d(kQ), S::d(kQ + 1), S::d(kQ + 2), S::d(kQ + 3), S::a(kQ), S::a(kQ + 1), S::a(kQ + 2),
-                    S::a(kQ + 3), S::b(kQ), S::b(kQ + 1), S::b(kQ + 2), S::b(kQ + 3)>(
-      dcol, acol, xdesc, idesc, S::flag(kQ, j), S::flag(kQ + 1, j), S::flag(kQ + 2, j), S::flag(kQ + 3, j));
-}
-
-template <int kNTok, int kMode, bool kOffset, int kQ = 0>
-__device__ __forceinline__ void issue_stage_mmas(uint32_t dcol, uint32_t acol, uint64_t xdesc, uint32_t idesc,
-                                                 uint32_t j) {
-  if constexpr (kQ < StageMmas<kNTok, kMode, kOffset>::kCount) {
-    issue_mma4<kNTok, kMode, kOffset, kQ>(dcol, acol, xdesc, idesc, j);
-    issue_stage_mmas<kNTok, kMode, kOffset, kQ + 4>(dcol, acol, xdesc, idesc, j);
-  }
-}
 
 // Opt-in per-stage timeline of CTA 0 (w4a16_debug_trace): clock64 at each role's sync points.
 __device__ long long* g_w4_trace = nullptr;
@@ -170,23 +139,25 @@ struct TileInfo {
   int e, n_tile, m_start, m_rows;
 };
 
-// Static persistent schedule: tile t -> (expert, n-tile, m-tile); m-tiles of one (expert, n-tile)
-// are adjacent so concurrently running CTAs share that weight block through L2.
-template <int kNTok>
-__device__ __forceinline__ bool get_tile(int t, const int* mt_off, const GemmArgs& a, TileInfo& ti) {
-  const int total = mt_off[a.num_experts] * a.nt;
+// Static persistent schedule: tile t -> (expert, n-tile group, m-tile); m-tiles of one (expert, n-tile)
+// are adjacent so concurrently running CTAs share that weight block through L2. kNSplit = 2 for CTA
+// pairs: tile t covers n-tiles 2g and 2g+1, CTA rank r of the pair takes n-tile 2g + r.
+template <int kNTok, int kNSplit>
+__device__ __forceinline__ bool get_tile(int t, const int* mt_off, const GemmArgs& a, uint32_t rank, TileInfo& ti) {
+  const int ntg = a.nt / kNSplit;
+  const int total = mt_off[a.num_experts] * ntg;
   if (t >= total) return false;
-  int lo = 0, hi = a.num_experts;  // find e with mt_off[e]*nt <= t < mt_off[e+1]*nt
+  int lo = 0, hi = a.num_experts;  // find e with mt_off[e]*ntg <= t < mt_off[e+1]*ntg
   while (hi - lo > 1) {
     int mid = (lo + hi) >> 1;
-    if (mt_off[mid] * a.nt <= t) lo = mid; else hi = mid;
+    if (mt_off[mid] * ntg <= t) lo = mid; else hi = mid;
   }
   const int e = lo;
   const int me = mt_off[e + 1] - mt_off[e];
-  const int local = t - mt_off[e] * a.nt;
-  const int m_tile = local % me;
+  const int local = t - mt_off[e] * ntg;
+  const int m_tile = me == 1 ? 0 : local % me;
   ti.e = e;
-  ti.n_tile = local / me;
+  ti.n_tile = (me == 1 ? local : local / me) * kNSplit + static_cast<int>(rank);
   ti.m_start = __ldg(a.expert_offsets + e) + m_tile * kNTok;
   ti.m_rows = min(kNTok, __ldg(a.expert_counts + e) - m_tile * kNTok);
   return true;
@@ -214,10 +185,10 @@ struct Ring {  // (stage, phase) iterator of an mbarrier ring
   }
 };
 
-template <int kNTok, int kMode, bool kBF16, bool kOffset>
+template <int kNTok, int kMode, bool kBF16, bool kOffset, bool kPair>
 __global__ void __launch_bounds__(kNumThreads, 1)
     w4a16_moe_gemm_kernel(const GemmArgs args, const __grid_constant__ CUtensorMap xmap) {
-  using C = Cfg<kNTok, kMode, kOffset>;
+  using C = Cfg<kNTok, kMode, kOffset, kPair>;
   constexpr bool kGated = C::kGated;
   const int n_stages = args.kt / C::kGroupsPerStage;  // stages per tile
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -237,6 +208,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 
   const uint32_t warp = warp_idx();
   const uint32_t lane = lane_id();
+  const uint32_t rank = kPair ? cluster_ctarank() : 0u;  // CTA rank in the pair (0 = leader, issues MMAs)
+  const int tile0 = kPair ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
+  const int tstride = kPair ? static_cast<int>(nclusters_x()) : static_cast<int>(gridDim.x);
   #ifdef W4A16_TRACE
   long long* const tr = blockIdx.x == 0 ? g_w4_trace : nullptr;
 #else
@@ -244,11 +218,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #endif
 
   if (warp == 0) {
-    tmem_alloc<512>(tmem_holder);
+    if constexpr (kPair) tmem_alloc_pair<512>(tmem_holder);
+    else tmem_alloc<512>(tmem_holder);
   } else if (warp == 1 && lane == 0) {
     for (int i = 0; i < C::kNS; ++i) { mbar_init(&full[i], C::kFullArrivals); mbar_init(&empty[i], C::kEmptyArrivals); }
-    for (int i = 0; i < C::kNumA; ++i) { mbar_init(&afull[i], kDequantGroup); mbar_init(&aempty[i], 1); }
-    for (int i = 0; i < C::kNumAcc; ++i) { mbar_init(&accfull[i], 1); mbar_init(&accempty[i], 4); }
+    for (int i = 0; i < C::kNumA; ++i) { mbar_init(&afull[i], C::kAFullArrivals); mbar_init(&aempty[i], 1); }
+    for (int i = 0; i < C::kNumAcc; ++i) { mbar_init(&accfull[i], 1); mbar_init(&accempty[i], C::kAccEmptyArrivals); }
     fence_mbar_init();
   } else if (warp == 2) {
     // m-tile prefix over experts (E <= 1024): each lane scans a contiguous slice, then a warp scan.
@@ -273,7 +248,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     tma_prefetch_desc(&xmap);
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) cluster_sync_all();  // the peer's barriers must exist before remote arrivals
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
   constexpr uint32_t kAcol0 = C::kNumAcc * C::kAccCols;  // first column of the TMEM A ring
@@ -289,7 +265,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       Ring st;
       uint32_t pgs = 0;
       TileInfo ti;
-      for (int t = blockIdx.x; get_tile<kNTok>(t, mt_off, args, ti); t += gridDim.x) {
+      for (int t = tile0; get_tile<kNTok, C::kCG>(t, mt_off, args, rank, ti); t += tstride) {
         // per (expert, n-tile): kt k-groups of (gated ? 2 : 1) parts, stage j = bytes [j*kBlk, (j+1)*kBlk)
         const uint8_t* wsrc = args.wblocks + (static_cast<int64_t>(ti.e) * args.nt + ti.n_tile) *
                                                  static_cast<int64_t>(args.kt) * (kGated ? 2 : 1) * kPartBytes;
@@ -303,8 +279,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             uint8_t* xs = smem_x + st.i * C::kXBytes;
 #pragma unroll
             for (int h = 0; h < 2 * C::kGroupsPerStage; ++h)
-              tma_load_2d(xs + h * (kNTok * 128), &xmap, j * C::kGroupsPerStage * kTileK + h * 64, ti.m_start,
-                          &full[st.i]);
+              tma_load_2d(xs + h * (C::kXRows * 128), &xmap, j * C::kGroupsPerStage * kTileK + h * 64,
+                          ti.m_start + static_cast<int>(rank) * C::kXRows, &full[st.i]);
           }
           if constexpr (kOffset) {
             // all 32 lanes copy and arrive every stage (fewer items than lanes: items are duplicated --
@@ -326,57 +302,59 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
       }
     }
-  } else if (warp == 1 || warp == kMmaWarp2) {
-    // ------------------------------------------------------------ MMA issuer(s)
-    // Offset mode: every stage is self-contained (fresh partials), so two issuing threads take
-    // alternate stages and each one's wait chain (accempty, full, afull) overlaps the other's.
-    // Otherwise one issuer accumulates the whole tile.
-    const uint32_t my_par = warp == 1 ? 0u : 1u;
-    if ((kOffset && kDualIssue) || warp == 1) {  // whole warp; one elected lane issues
-      constexpr uint32_t idesc = make_idesc_f16(128, kNTok, kBF16);
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA of a pair)
+    // whole warp runs the loop; one elected lane issues. Waiting on afull (all dequant warps of the
+    // pair arrived, each after its own full barrier) also covers the stage's X tile(s).
+    if (!kPair || rank == 0) {
+      constexpr uint32_t idesc = make_idesc_f16(128 * C::kCG, kNTok, kBF16);
+      // provably warp-uniform bases (shfl from lane 0): ptxas keeps the MMA operands in uniform registers
+      const uint32_t tb_u = __shfl_sync(0xffffffffu, tbase, 0);
+      const uint32_t xs_u = __shfl_sync(0xffffffffu, smem_u32(smem_x), 0);
       Ring st, ar, acc;
-      uint32_t gs = 0;  // global stage counter (parity selects the issuer in offset mode)
+      uint32_t gs = 0;
       TileInfo ti;
-      for (int t = blockIdx.x; get_tile<kNTok>(t, mt_off, args, ti); t += gridDim.x) {
+      for (int t = tile0; get_tile<kNTok, C::kCG>(t, mt_off, args, rank, ti); t += tstride) {
         if constexpr (!kOffset) {
-          mbar_wait(&accempty[acc.i], acc.ph ^ 1);
+          mbar_wait_warp(&accempty[acc.i], acc.ph ^ 1);
           tc_fence_after();
         }
         for (int j = 0; j < n_stages; ++j, ++gs) {
-          if constexpr (kOffset) {  // fresh partials per stage (one per k-group)
-            if (kDualIssue && (gs & 1u) != my_par) {
-              st.next(C::kNS);
-              ar.next(C::kNumA);
-              acc.next(C::kNumAcc);
-              continue;
-            }
-            mbar_wait(&accempty[acc.i], acc.ph ^ 1);
-          }
-          mbar_wait(&full[st.i], st.ph);
-          mbar_wait(&afull[ar.i], ar.ph);
+          if constexpr (kOffset)  // fresh partials per stage: accumulator slot free + A slot filled
+            mbar_wait2_warp(&accempty[acc.i], acc.ph ^ 1, &afull[ar.i], ar.ph);
+          else
+            mbar_wait_warp(&afull[ar.i], ar.ph);
           tc_fence_after();
           trace_at(tr, 4, gs);
-          const uint32_t dcol = tbase + acc.i * C::kAccCols;
-          const uint64_t xdesc = make_sdesc_sw128(smem_u32(smem_x + st.i * C::kXBytes));
-          const uint32_t acol = tbase + kAcol0 + ar.i * C::kACols;
-          // k-step outer, independent accumulators (gate / up, or the two k-groups of a pair) inner.
-          // kTileK/16 * kParts MMAs, issued four per elect with compile-time operand offsets
-          // (StageMmas::op computes them; see umma4_ts_f16_warp)
-          const uint32_t jf = static_cast<uint32_t>(j);
-          issue_stage_mmas<kNTok, kMode, kOffset>(dcol, acol, xdesc, idesc, jf);
-          trace_at(tr, 5, gs);
+          const uint32_t dcol = tb_u + acc.i * C::kAccCols;
+          const uint64_t xdesc = make_sdesc_sw128(xs_u + st.i * C::kXBytes);
+          const uint32_t acol = tb_u + kAcol0 + ar.i * C::kACols;
+          // one elected lane issues the stage's MMAs (generated PTX block, mma_stage.cuh) and commits
+          if (elect_one()) {
+            StageAsm<kNTok, kMode, C::kCG, kOffset>::issue(dcol, acol, xdesc, idesc, static_cast<uint32_t>(j));
+            trace_at(tr, 5, gs);
+            if constexpr (kPair) {
+              umma_commit_pair(&empty[st.i]);
+              umma_commit_pair(&aempty[ar.i]);
+              if constexpr (kOffset) umma_commit_pair(&accfull[acc.i]);
+            } else {
+              umma_commit(&empty[st.i]);
+              umma_commit(&aempty[ar.i]);
+              if constexpr (kOffset) umma_commit(&accfull[acc.i]);
+            }
+          }
+          __syncwarp();
           progress_at(2, gs + 1);
-          umma_commit_warp(&empty[st.i]);
-          umma_commit_warp(&aempty[ar.i]);
           st.next(C::kNS);
           ar.next(C::kNumA);
-          if constexpr (kOffset) {
-            umma_commit_warp(&accfull[acc.i]);
-            acc.next(C::kNumAcc);
-          }
+          if constexpr (kOffset) acc.next(C::kNumAcc);
         }
         if constexpr (!kOffset) {
-          umma_commit_warp(&accfull[acc.i]);
+          if (elect_one()) {
+            if constexpr (kPair) umma_commit_pair(&accfull[acc.i]);
+            else umma_commit(&accfull[acc.i]);
+          }
+          __syncwarp();
           acc.next(C::kNumAcc);
         }
       }
@@ -394,7 +372,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     Ring st, ar;
     uint32_t gs = 0;
     TileInfo ti;
-    for (int t = blockIdx.x; get_tile<kNTok>(t, mt_off, args, ti); t += gridDim.x) {
+    for (int t = tile0; get_tile<kNTok, C::kCG>(t, mt_off, args, rank, ti); t += tstride) {
       for (int j = 0; j < n_stages; ++j, ++gs) {
         if ((gs & 1u) != my_par) {
           st.next(C::kNS);
@@ -419,7 +397,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             zb[p] = sb[p] = 0;
           }
         }
-        mbar_wait(&aempty[ar.i], ar.ph ^ 1);
+        mbar_wait_cluster(&aempty[ar.i], ar.ph ^ 1);
         tc_fence_after();
         if (trd) trace_at(tr, 2, gs);
         const uint32_t acol = tbase + lane_off + kAcol0 + ar.i * C::kACols;
@@ -449,7 +427,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         if (trd) trace_at(tr, 3, gs);
         if (trd) progress_at(1, gs + 1);
         if (lane == 0) {
-          mbar_arrive(&afull[ar.i]);
+          if constexpr (kPair) mbar_arrive_cluster(mapa_shared(&afull[ar.i], 0));
+          else mbar_arrive(&afull[ar.i]);
           mbar_arrive(&empty[st.i]);
         }
         st.next(C::kNS);
@@ -466,7 +445,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     uint32_t egs = 0;
     const bool tre = lane == 0 && quad == 0;
     TileInfo ti;
-    for (int t = blockIdx.x; get_tile<kNTok>(t, mt_off, args, ti); t += gridDim.x) {
+    for (int t = tile0; get_tile<kNTok, C::kCG>(t, mt_off, args, rank, ti); t += tstride) {
       if (tre) trace_at(tr, 9, egs);
       uint16_t* obase = out + static_cast<int64_t>(ti.m_start) * args.ldo + ti.n_tile * kTileRows + row;
       if constexpr (kOffset) {
@@ -490,7 +469,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             const uint32_t zb = lds_u8(part + kZeroOff + (row >> 1));
             zf[p] = static_cast<float>((row & 1) ? (zb >> 4) : (zb & 15u));
           }
-          mbar_wait(&accfull[acc.i], acc.ph);
+          mbar_wait_cluster(&accfull[acc.i], acc.ph);
           tc_fence_after();
           if (tre) trace_at(tr, 7, egs);
           const uint32_t dcol = tbase + lane_off + acc.i * C::kAccCols;
@@ -527,7 +506,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           ++egs;
           if (tre) progress_at(3, egs);
           if (lane == 0) {
-            mbar_arrive(&accempty[acc.i]);
+            if constexpr (kPair) mbar_arrive_cluster(mapa_shared(&accempty[acc.i], 0));
+            else mbar_arrive(&accempty[acc.i]);
             mbar_arrive(&empty[st.i]);
           }
           acc.next(C::kNumAcc);
@@ -543,7 +523,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           }
         }
       } else {
-        mbar_wait(&accfull[acc.i], acc.ph);
+        mbar_wait_cluster(&accfull[acc.i], acc.ph);
         tc_fence_after();
         const uint32_t dcol = tbase + lane_off + acc.i * C::kAccCols;
 #pragma unroll 1
@@ -573,20 +553,29 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&accempty[acc.i]);
+        if (lane == 0) {
+          if constexpr (kPair) mbar_arrive_cluster(mapa_shared(&accempty[acc.i], 0));
+          else mbar_arrive(&accempty[acc.i]);
+        }
         acc.next(C::kNumAcc);
       }
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) {
+    __syncwarp();
+    cluster_sync_all();  // both CTAs done: no MMA reads this TMEM and no remote arrival is in flight
+  } else {
+    __syncthreads();
+  }
   if (threadIdx.x == 0) progress_at(3, 1000000);  // CTA reached the exit barrier
   if (warp == 0) {
     __syncwarp();  // tcgen05.dealloc is .sync.aligned: the producer's lanes must be reconverged, or the
                    // columns stay allocated and the next launch's tcgen05.alloc on this SM waits forever
     tc_fence_after();
-    tmem_dealloc<512>(tbase);
+    if constexpr (kPair) tmem_dealloc_pair<512>(tbase);
+    else tmem_dealloc<512>(tbase);
   }
 }
 
@@ -711,33 +700,61 @@ int sm_count() {
   return n;
 }
 
-template <int kNTok, int kMode, bool kBF16, bool kOffset>
-int launch_gemm(const GemmArgs& a, const CUtensorMap& map, int grid, cudaStream_t st) {
-  using C = Cfg<kNTok, kMode, kOffset>;
-  auto kern = w4a16_moe_gemm_kernel<kNTok, kMode, kBF16, kOffset>;
+template <int kNTok, int kMode, bool kBF16, bool kOffset, bool kPair>
+int launch_gemm(const GemmArgs& a, const void* x, int64_t rows, int64_t K, int grid, cudaStream_t st) {
+  using C = Cfg<kNTok, kMode, kOffset, kPair>;
+  auto kern = w4a16_moe_gemm_kernel<kNTok, kMode, kBF16, kOffset, kPair>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
       return W4_ERR_CUDA;
     attr = true;
   }
-  kern<<<grid, kNumThreads, C::kSmemBytes, st>>>(a, map);
+  CUtensorMap map;
+  if (make_x_map(&map, x, rows, K, C::kXRows) != W4_OK) return W4_ERR_CUDA;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kPair ? (grid & ~1) : grid);
+  cfg.blockDim = dim3(kNumThreads);
+  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kPair ? 2 : 1;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = kPair ? 1 : 0;
+  if (cudaLaunchKernelEx(&cfg, kern, a, map) != cudaSuccess) return W4_ERR_CUDA;
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
 
 template <int kMode, bool kBF16>
-int dispatch_ntok(int ntok, bool offset, const GemmArgs& a, const CUtensorMap& m, int grid, cudaStream_t st) {
+int dispatch_ntok(int ntok, bool offset, bool pair, const GemmArgs& a, const void* x, int64_t rows, int64_t K,
+                  int grid, cudaStream_t st) {
+  if (offset && pair) {
+    if (ntok == 16) return launch_gemm<16, kMode, kBF16, true, true>(a, x, rows, K, grid, st);
+    if (ntok == 32) return launch_gemm<32, kMode, kBF16, true, true>(a, x, rows, K, grid, st);
+  }
   if (offset) {
-    if (ntok == 16) return launch_gemm<16, kMode, kBF16, true>(a, m, grid, st);
-    if (ntok == 32) return launch_gemm<32, kMode, kBF16, true>(a, m, grid, st);
+    if (ntok == 16) return launch_gemm<16, kMode, kBF16, true, false>(a, x, rows, K, grid, st);
+    if (ntok == 32) return launch_gemm<32, kMode, kBF16, true, false>(a, x, rows, K, grid, st);
   }
   switch (ntok) {
-    case 16: return launch_gemm<16, kMode, kBF16, false>(a, m, grid, st);
-    case 32: return launch_gemm<32, kMode, kBF16, false>(a, m, grid, st);
-    case 64: return launch_gemm<64, kMode, kBF16, false>(a, m, grid, st);
-    case 128: return launch_gemm<128, kMode, kBF16, false>(a, m, grid, st);
+    case 16: return launch_gemm<16, kMode, kBF16, false, false>(a, x, rows, K, grid, st);
+    case 32: return launch_gemm<32, kMode, kBF16, false, false>(a, x, rows, K, grid, st);
+    case 64: return launch_gemm<64, kMode, kBF16, false, false>(a, x, rows, K, grid, st);
+    case 128: return launch_gemm<128, kMode, kBF16, false, false>(a, x, rows, K, grid, st);
     default: return W4_ERR_ARG;
   }
+}
+
+// Experiment knob: W4A16_PAIR=1 runs the decode kernel on CTA pairs.
+bool pairs_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("W4A16_PAIR");
+    return e && atoi(e) != 0;
+  }();
+  return on;
 }
 
 }  // namespace
@@ -792,18 +809,19 @@ int w4a16_grouped_gemm(const void* x, int64_t rows, int64_t K, const uint8_t* wb
   a.rows = rows;
   const int mode = gated ? kModeGateUp : (a.kt % 2 == 0 ? kModeKPair : kModePlain);
   const bool offset = xsum != nullptr && ntok <= 32;
-  CUtensorMap map;
-  if (make_x_map(&map, x, rows, K, ntok) != W4_OK) return W4_ERR_CUDA;
+  // CTA pairs (cta_group::2) measured slower at decode token counts (an M=256 x N=16 MMA with 8-row B
+  // halves executes ~4x slower than two M=128 ones): opt-in only (W4A16_PAIR=1)
+  const bool pair = offset && a.nt % 2 == 0 && pairs_enabled();
   const int grid = sm_count();
   const bool bf = dtype == W4_DTYPE_BF16;
   if (mode == kModeGateUp)
-    return bf ? dispatch_ntok<kModeGateUp, true>(ntok, offset, a, map, grid, stream)
-              : dispatch_ntok<kModeGateUp, false>(ntok, offset, a, map, grid, stream);
+    return bf ? dispatch_ntok<kModeGateUp, true>(ntok, offset, pair, a, x, rows, K, grid, stream)
+              : dispatch_ntok<kModeGateUp, false>(ntok, offset, pair, a, x, rows, K, grid, stream);
   if (mode == kModeKPair)
-    return bf ? dispatch_ntok<kModeKPair, true>(ntok, offset, a, map, grid, stream)
-              : dispatch_ntok<kModeKPair, false>(ntok, offset, a, map, grid, stream);
-  return bf ? dispatch_ntok<kModePlain, true>(ntok, offset, a, map, grid, stream)
-            : dispatch_ntok<kModePlain, false>(ntok, offset, a, map, grid, stream);
+    return bf ? dispatch_ntok<kModeKPair, true>(ntok, offset, pair, a, x, rows, K, grid, stream)
+              : dispatch_ntok<kModeKPair, false>(ntok, offset, pair, a, x, rows, K, grid, stream);
+  return bf ? dispatch_ntok<kModePlain, true>(ntok, offset, pair, a, x, rows, K, grid, stream)
+            : dispatch_ntok<kModePlain, false>(ntok, offset, pair, a, x, rows, K, grid, stream);
 }
 
 int w4a16_dequant(const uint8_t* wblocks, int64_t num_experts, int64_t n_rows, int64_t K, int parts, int dtype,
