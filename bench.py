@@ -304,7 +304,6 @@ def main():
     for _ in range(args.warmup):
         step()
     barrier()
-    timer = KernelTimer()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -312,7 +311,7 @@ def main():
         torch.cuda.profiler.start()  # ncu --profile-from-start off captures exactly the timed steps
         ev0.record()
         for _ in range(args.steps):
-            step(timer)
+            step()
         ev1.record()
         barrier()
         torch.cuda.profiler.stop()
@@ -320,6 +319,11 @@ def main():
     ms = ms_total / args.steps
     value = job_bytes / (ms * 1e-3) / 1e9
     tflops = job_flops / (ms * 1e-3) / 1e12
+    # per-kernel device times (separate pass: the bracketing events add small gaps between launches)
+    timer = KernelTimer()
+    for _ in range(args.steps):
+        step(timer)
+    barrier()
     hbm_peak, tc_peak, tc_sus, peak_src = peaks()
 
     # dominant kernel: gate/up grouped GEMM (2/3 of the weight bytes). Algorithmic bytes per launch

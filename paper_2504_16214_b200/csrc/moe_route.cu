@@ -251,12 +251,14 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-// One CTA per token; accumulate the k expert rows in slot order in fp32.
+// grid (T, H/8 / blockDim): each thread owns one 16-byte vector of one token and accumulates the k
+// expert rows in slot order in fp32 (enough CTAs to saturate HBM even at decode token counts).
 template <bool kBF16>
 __global__ void moe_combine_kernel(const uint4* __restrict__ yp, int64_t hv, int topk,
                                    const int32_t* __restrict__ pair_pos, const float* __restrict__ wts,
                                    uint4* __restrict__ y) {
   const int64_t t = blockIdx.x;
+  const int64_t i = static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x;
   constexpr int kMaxK = 32;
   __shared__ int pos[kMaxK];
   __shared__ float wt[kMaxK];
@@ -265,17 +267,16 @@ __global__ void moe_combine_kernel(const uint4* __restrict__ yp, int64_t hv, int
     wt[threadIdx.x] = wts[t * topk + threadIdx.x];
   }
   __syncthreads();
-  for (int64_t i = threadIdx.x; i < hv; i += blockDim.x) {
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int j = 0; j < topk; ++j) {
-      if (pos[j] < 0) continue;
-      float f[8];
-      unpack8<kBF16>(__ldg(yp + static_cast<int64_t>(pos[j]) * hv + i), f);
+  if (i >= hv) return;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int j = 0; j < topk; ++j) {
+    if (pos[j] < 0) continue;
+    float f[8];
+    unpack8<kBF16>(__ldg(yp + static_cast<int64_t>(pos[j]) * hv + i), f);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = fmaf(wt[j], f[q], acc[q]);
-    }
-    y[t * hv + i] = pack8<kBF16>(acc);
+    for (int q = 0; q < 8; ++q) acc[q] = fmaf(wt[j], f[q], acc[q]);
   }
+  y[t * hv + i] = pack8<kBF16>(acc);
 }
 
 }  // namespace w4
@@ -370,12 +371,13 @@ int w4a16_moe_combine(const void* y_perm, int64_t T, int64_t H, int64_t topk, co
   if (H <= 0 || H % 8 || topk <= 0 || topk > 32) return W4_ERR_SHAPE;
   if (T <= 0) return W4_OK;
   const int thr = 128;
+  const dim3 grid(static_cast<unsigned>(T), static_cast<unsigned>((H / 8 + thr - 1) / thr));
   if (dtype == W4_DTYPE_BF16)
-    moe_combine_kernel<true><<<T, thr, 0, stream>>>(static_cast<const uint4*>(y_perm), H / 8, (int)topk, pair_pos,
-                                                    topk_weights, static_cast<uint4*>(y));
+    moe_combine_kernel<true><<<grid, thr, 0, stream>>>(static_cast<const uint4*>(y_perm), H / 8, (int)topk,
+                                                       pair_pos, topk_weights, static_cast<uint4*>(y));
   else if (dtype == W4_DTYPE_F16)
-    moe_combine_kernel<false><<<T, thr, 0, stream>>>(static_cast<const uint4*>(y_perm), H / 8, (int)topk, pair_pos,
-                                                     topk_weights, static_cast<uint4*>(y));
+    moe_combine_kernel<false><<<grid, thr, 0, stream>>>(static_cast<const uint4*>(y_perm), H / 8, (int)topk,
+                                                        pair_pos, topk_weights, static_cast<uint4*>(y));
   else
     return W4_ERR_DTYPE;
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;

@@ -32,6 +32,7 @@ constexpr int kNumDequantWarps = 8;  // two groups of 4 (one warp per TMEM lane 
 constexpr int kDequantGroup = 4;
 constexpr int kEpiWarp0 = 10;
 constexpr int kMaxExperts = 1024;
+constexpr int kTileTab = 512;  // per-CTA tile table entries in smem (later tiles are searched on the fly)
 constexpr int kSmemBudget = 225 * 1024;
 
 struct GemmArgs {
@@ -96,7 +97,7 @@ struct Cfg {
   static constexpr int kNumA0 = (512 - kNumAcc * kAccCols) / kACols;
   static constexpr int kNumA = kOffset ? kNumA_ : (kNumA0 > 4 ? 4 : kNumA0);
   static constexpr int kStageBytes = kBlk + kXBytes + kSumBytes;
-  static constexpr int kFixed = 2048 + 4 * (kMaxExperts + 1);  // barriers + tile table
+  static constexpr int kFixed = 2048 + 4 * (kMaxExperts + 2) + 8 * kTileTab;  // barriers, m-tile prefix, tiles
   static constexpr int kNS0 = (kSmemBudget - kFixed - 1024) / kStageBytes;
   static constexpr int kNS = kNS0 > 12 ? 12 : kNS0;
   static constexpr int kEmptyArrivals = kDequantGroup + 1 + (kOffset ? 4 : 0);
@@ -163,6 +164,31 @@ __device__ __forceinline__ bool get_tile(int t, const int* mt_off, const GemmArg
   return true;
 }
 
+// Packed tile: w0 = e | (m_rows - 1) << 10 | n_tile << 17, w1 = m_start.
+__device__ __forceinline__ uint2 pack_tile(const TileInfo& ti) {
+  return make_uint2(static_cast<uint32_t>(ti.e) | static_cast<uint32_t>(ti.m_rows - 1) << 10 |
+                        static_cast<uint32_t>(ti.n_tile) << 17,
+                    static_cast<uint32_t>(ti.m_start));
+}
+__device__ __forceinline__ void unpack_tile(uint2 p, TileInfo& ti) {
+  ti.e = p.x & 1023u;
+  ti.m_rows = static_cast<int>((p.x >> 10) & 127u) + 1;
+  ti.n_tile = static_cast<int>(p.x >> 17);
+  ti.m_start = static_cast<int>(p.y);
+}
+
+// The CTA's i-th tile (t = tile0 + i * tstride): from the smem table when i < kTileTab, else searched.
+template <int kNTok, int kNSplit>
+__device__ __forceinline__ bool tile_at(int i, int n_tiles, int tile0, int tstride, const uint2* tab, const int* mt_off,
+                                        const GemmArgs& a, uint32_t rank, TileInfo& ti) {
+  if (i >= n_tiles) return false;
+  if (i < kTileTab) {
+    unpack_tile(tab[i], ti);
+    return true;
+  }
+  return get_tile<kNTok, kNSplit>(tile0 + i * tstride, mt_off, a, rank, ti);
+}
+
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
 
 template <bool kBF16>
@@ -205,6 +231,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   uint64_t* accempty = accfull + C::kNumAcc;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accempty + C::kNumAcc);
   int* mt_off = reinterpret_cast<int*>(bars + 256);
+  uint2* tile_tab = reinterpret_cast<uint2*>(mt_off + kMaxExperts + 2);  // 8-byte aligned (odd int count + 1)
+  int* n_tiles_sm = mt_off + kMaxExperts + 1;
 
   const uint32_t warp = warp_idx();
   const uint32_t lane = lane_id();
@@ -244,6 +272,16 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       run += (__ldg(args.expert_counts + e) + kNTok - 1) / kNTok;
     }
     if (lane == 31) mt_off[E] = incl;
+    __syncwarp();
+    // this CTA's tiles t = tile0 + i * tstride, the first kTileTab of them tabulated
+    const int total = mt_off[E] * (args.nt / C::kCG);
+    const int n_tiles = tile0 < total ? (total - tile0 + tstride - 1) / tstride : 0;
+    if (lane == 0) *n_tiles_sm = n_tiles;
+    for (int i = lane; i < min(n_tiles, kTileTab); i += 32) {
+      TileInfo ti;
+      get_tile<kNTok, C::kCG>(tile0 + i * tstride, mt_off, args, rank, ti);
+      tile_tab[i] = pack_tile(ti);
+    }
   } else if (warp == 3 && lane == 0) {
     tma_prefetch_desc(&xmap);
   }
@@ -252,6 +290,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
+  const int n_tiles = *n_tiles_sm;
   constexpr uint32_t kAcol0 = C::kNumAcc * C::kAccCols;  // first column of the TMEM A ring
   const uint32_t w_u32 = smem_u32(smem_w);
 
@@ -265,7 +304,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       Ring st;
       uint32_t pgs = 0;
       TileInfo ti;
-      for (int t = tile0; get_tile<kNTok, C::kCG>(t, mt_off, args, rank, ti); t += tstride) {
+      for (int it = 0; tile_at<kNTok, C::kCG>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
         // per (expert, n-tile): kt k-groups of (gated ? 2 : 1) parts, stage j = bytes [j*kBlk, (j+1)*kBlk)
         const uint8_t* wsrc = args.wblocks + (static_cast<int64_t>(ti.e) * args.nt + ti.n_tile) *
                                                  static_cast<int64_t>(args.kt) * (kGated ? 2 : 1) * kPartBytes;
@@ -314,7 +353,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       Ring st, ar, acc;
       uint32_t gs = 0;
       TileInfo ti;
-      for (int t = tile0; get_tile<kNTok, C::kCG>(t, mt_off, args, rank, ti); t += tstride) {
+      for (int it = 0; tile_at<kNTok, C::kCG>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
         if constexpr (!kOffset) {
           mbar_wait_warp(&accempty[acc.i], acc.ph ^ 1);
           tc_fence_after();
@@ -372,7 +411,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     Ring st, ar;
     uint32_t gs = 0;
     TileInfo ti;
-    for (int t = tile0; get_tile<kNTok, C::kCG>(t, mt_off, args, rank, ti); t += tstride) {
+    for (int it = 0; tile_at<kNTok, C::kCG>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
       for (int j = 0; j < n_stages; ++j, ++gs) {
         if ((gs & 1u) != my_par) {
           st.next(C::kNS);
@@ -445,7 +484,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     uint32_t egs = 0;
     const bool tre = lane == 0 && quad == 0;
     TileInfo ti;
-    for (int t = tile0; get_tile<kNTok, C::kCG>(t, mt_off, args, rank, ti); t += tstride) {
+    for (int it = 0; tile_at<kNTok, C::kCG>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
       if (tre) trace_at(tr, 9, egs);
       uint16_t* obase = out + static_cast<int64_t>(ti.m_start) * args.ldo + ti.n_tile * kTileRows + row;
       if constexpr (kOffset) {

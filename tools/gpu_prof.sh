@@ -5,7 +5,7 @@ T=${1:-64}
 mkdir -p gpurun_out
 python -m paper_2504_16214_b200._build
 timeout 600 python -m pytest tests/test_gpu_moe.py -x -q 2>&1 | tail -3
-timeout 600 python bench.py --steps 50 --warmup 5 --no-cpu --tokens $T > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
+timeout 900 python bench.py --tokens $T > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 python tools/summarize_bench.py gpurun_out/bench.json
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off -c 400 --csv --log-file gpurun_out/launches.csv \
    python bench.py --steps 2 --warmup 1 --no-sweep --no-cpu --tokens $T > /dev/null 2>&1; echo "ncu launches rc=$?"

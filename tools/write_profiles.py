@@ -70,10 +70,10 @@ def main():
             for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                 i = hdr.index(key)
                 b += float(r[i]) * scale[units[i]]
-            if "w4a16_moe_gemm_kernel" in name and ", 1," in name.replace("(int)", ""):
-                traffic[f"gemm_gate_up_T{a.tokens}"] = int(b)
-            elif "w4a16_moe_gemm_kernel" in name:
-                traffic[f"gemm_down_T{a.tokens}"] = int(b)
+            if "w4a16_moe_gemm_kernel" in name:
+                targs = name.replace("(int)", "").replace("(bool)", "").split("<", 1)[1].split(">")[0].split(",")
+                mode = int(targs[1])  # template <kNTok, kMode, ...>: 1 = gate/up, 2 = k-pair down, 0 = plain
+                traffic[f"gemm_{'gate_up' if mode == 1 else 'down'}_T{a.tokens}"] = int(b)
         tr_path.write_text(json.dumps(traffic, indent=1, sort_keys=True) + "\n")
     if summ:
         (dst / "ncu_full_summary.txt").write_text("".join(summ))
