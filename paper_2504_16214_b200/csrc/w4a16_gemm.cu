@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // whole warp runs the loop; one elected lane issues. Waiting on afull (all dequant warps of the
     // pair arrived, each after its own full barrier) also covers the stage's X tile(s).
     if (!kPair || rank == 0) {
-      constexpr uint32_t idesc = make_idesc_f16(128 * C::kCG, kNTok, kBF16);
+      constexpr uint32_t idesc_full = make_idesc_f16(128 * C::kCG, kNTok, kBF16);
       // provably warp-uniform bases (shfl from lane 0): ptxas keeps the MMA operands in uniform registers
       const uint32_t tb_u = __shfl_sync(0xffffffffu, tbase, 0);
       const uint32_t xs_u = __shfl_sync(0xffffffffu, smem_u32(smem_x), 0);
@@ -354,6 +354,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       uint32_t gs = 0;
       TileInfo ti;
       for (int it = 0; tile_at<kNTok, C::kCG>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
+        // MMA N sized to the tile's real tokens (multiple of 16 per CTA of the group): an expert's last,
+        // partial m-tile costs tensor time in proportion to its rows, not to kNTok
+        const uint32_t n_mma = min(kNTok, (ti.m_rows + 16 * C::kCG - 1) / (16 * C::kCG) * (16 * C::kCG));
+        const uint32_t idesc = (idesc_full & ~(0x3Fu << 17)) | ((n_mma >> 3) << 17);
         if constexpr (!kOffset) {
           mbar_wait_warp(&accempty[acc.i], acc.ph ^ 1);
           tc_fence_after();
@@ -778,6 +782,10 @@ int dispatch_ntok(int ntok, bool offset, bool pair, const GemmArgs& a, const voi
     if (ntok == 16) return launch_gemm<16, kMode, kBF16, true, false>(a, x, rows, K, grid, st);
     if (ntok == 32) return launch_gemm<32, kMode, kBF16, true, false>(a, x, rows, K, grid, st);
   }
+  if (pair) {
+    if (ntok == 64) return launch_gemm<64, kMode, kBF16, false, true>(a, x, rows, K, grid, st);
+    if (ntok == 128) return launch_gemm<128, kMode, kBF16, false, true>(a, x, rows, K, grid, st);
+  }
   switch (ntok) {
     case 16: return launch_gemm<16, kMode, kBF16, false, false>(a, x, rows, K, grid, st);
     case 32: return launch_gemm<32, kMode, kBF16, false, false>(a, x, rows, K, grid, st);
@@ -785,6 +793,15 @@ int dispatch_ntok(int ntok, bool offset, bool pair, const GemmArgs& a, const voi
     case 128: return launch_gemm<128, kMode, kBF16, false, false>(a, x, rows, K, grid, st);
     default: return W4_ERR_ARG;
   }
+}
+
+// Experiment knob: W4A16_PREFILL_PAIR=1 runs the prefill (64/128-token) kernels on CTA pairs.
+bool prefill_pairs_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("W4A16_PREFILL_PAIR");
+    return e && atoi(e) != 0;
+  }();
+  return on;
 }
 
 // Experiment knob: W4A16_PAIR=1 runs the decode kernel on CTA pairs.
@@ -850,7 +867,7 @@ int w4a16_grouped_gemm(const void* x, int64_t rows, int64_t K, const uint8_t* wb
   const bool offset = xsum != nullptr && ntok <= 32;
   // CTA pairs (cta_group::2) measured slower at decode token counts (an M=256 x N=16 MMA with 8-row B
   // halves executes ~4x slower than two M=128 ones): opt-in only (W4A16_PAIR=1)
-  const bool pair = offset && a.nt % 2 == 0 && pairs_enabled();
+  const bool pair = a.nt % 2 == 0 && (offset ? pairs_enabled() : prefill_pairs_enabled());
   const int grid = sm_count();
   const bool bf = dtype == W4_DTYPE_BF16;
   if (mode == kModeGateUp)

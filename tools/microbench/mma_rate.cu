@@ -6,7 +6,7 @@
 #include "ptx.cuh"
 using namespace w4;
 
-template <int N, bool kTS, int kChains, int kStWarps = 0>
+template <int N, bool kTS, int kChains, int kStWarps = 0, int kSmemWarps = 0>
 __global__ void mma_rate(int iters, long long* out) {
   __shared__ __align__(1024) uint8_t smem[2 * 16384 + 1024];
   __shared__ uint32_t holder;
@@ -42,6 +42,14 @@ __global__ void mma_rate(int iters, long long* out) {
     mbar_wait(&bar, 0);
     long long t2 = clock64();
     if (threadIdx.x == 32) { out[0] = t1 - t0; out[1] = t2 - t0; }
+  } else if (warp >= 2 + kStWarps && warp < 2 + kStWarps + kSmemWarps) {
+    // shared-memory write traffic into the B buffer region's tail (like TMA landing the next tiles)
+    uint4* dst = reinterpret_cast<uint4*>(smem + 8192);
+    const uint4 v = make_uint4(0x3c003c00u, 0x3c003c00u, 0x3c003c00u, 0x3c003c00u);
+    for (int it = 0; it < iters * 16; ++it) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) dst[((threadIdx.x & 31) + c * 32) & 511] = v;
+    }
   } else if (warp >= 2 && warp < 2 + kStWarps) {
     // concurrent tcgen05.st traffic into columns 384..511 (like the dequant warps): each warp writes its
     // lane quadrant, 16 columns per instruction, 8 instructions per "stage"
@@ -63,23 +71,23 @@ __global__ void mma_rate(int iters, long long* out) {
   if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tb); }
 }
 
-template <int N, bool kTS, int kChains, int kStWarps = 0>
+template <int N, bool kTS, int kChains, int kStWarps = 0, int kSmemWarps = 0>
 void run(long long* d) {
   const int iters = 200;
   cudaMemset(d, 0, 32);
-  mma_rate<N, kTS, kChains, kStWarps><<<1, 64 + 32 * kStWarps>>>(iters, d);
+  mma_rate<N, kTS, kChains, kStWarps, kSmemWarps><<<1, 64 + 32 * (kStWarps + kSmemWarps)>>>(iters, d);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[3];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-  printf("N=%3d %s chains=%d st_warps=%d : issue %.1f cyc/mma, complete %.1f cyc/mma; st %.1f cyc per 8xSTTM %s\n", N,
-         kTS ? "ts" : "ss", kChains, kStWarps, (double)h[0] / (iters * 16), (double)h[1] / (iters * 16),
+  printf("smemw=%d N=%3d %s chains=%d st_warps=%d : issue %.1f cyc/mma, complete %.1f cyc/mma; st %.1f cyc per 8xSTTM %s\n", N,
+         kSmemWarps, kTS ? "ts" : "ss", kChains, kStWarps, (double)h[0] / (iters * 16), (double)h[1] / (iters * 16),
          kStWarps ? (double)h[2] / (iters * 4) : 0.0, e == cudaSuccess ? "" : cudaGetErrorString(e));
 }
 
 int main() {
   long long* d;
   cudaMalloc(&d, 64);
-  run<16, true, 4>(d); run<16, true, 4, 4>(d); run<16, true, 4, 8>(d); run<32, true, 4, 4>(d);
-  run<128, true, 4, 4>(d);
+  run<128, true, 2>(d); run<128, true, 2, 4>(d); run<128, true, 2, 4, 4>(d); run<128, true, 2, 8, 4>(d);
+  run<64, true, 2>(d); run<64, true, 2, 4, 4>(d); run<16, true, 4, 4, 4>(d);
   return 0;
 }
