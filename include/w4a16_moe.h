@@ -80,6 +80,14 @@ int w4a16_route_topk(const float* logits, int64_t T, int64_t E, int64_t k, int s
 int w4a16_moe_permute(const int32_t* topk_ids, int64_t P, int64_t E, int32_t* expert_counts,
                       int32_t* expert_offsets, int32_t* sorted_pairs, int32_t* pair_pos, cudaStream_t stream);
 
+/* Same result as w4a16_moe_permute, parallel over many CTAs for large P (histogram -> scan ->
+ * ranked scatter). ws: caller workspace of w4a16_moe_permute_ws_bytes(P, E) bytes; with a smaller
+ * (or NULL) workspace, or small P, it runs the single-CTA kernel. */
+int w4a16_moe_permute_ws(const int32_t* topk_ids, int64_t P, int64_t E, int32_t* expert_counts,
+                         int32_t* expert_offsets, int32_t* sorted_pairs, int32_t* pair_pos, void* ws,
+                         int64_t ws_bytes, cudaStream_t stream);
+int64_t w4a16_moe_permute_ws_bytes(int64_t P, int64_t E);
+
 /* X_perm[p][:] = x[sorted_pairs[p] / topk][:] for p < rows, and p < *row_limit when row_limit (a
  * device pointer, e.g. expert_offsets + E) is non-null -- rows past it are left untouched. */
 int w4a16_moe_gather(const void* x, int64_t H, int64_t topk, const int32_t* sorted_pairs, int64_t rows,

@@ -150,6 +150,109 @@ __global__ void __launch_bounds__(kPermThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------- permute (multi-CTA)
+// Large P: the pairs are cut into chunks of kChunk; (1) per-chunk expert histograms, (2) one CTA scans
+// them in (expert, chunk) order into per-chunk bases, (3) each chunk scatters its pairs with the same
+// warp-ranked stable order as the single-CTA kernel. Same output as moe_permute_kernel.
+constexpr int kChunk = 2048;
+
+__global__ void __launch_bounds__(512) permute_hist_kernel(const int32_t* __restrict__ ids, int P, int E,
+                                                           int32_t* __restrict__ ws) {
+  extern __shared__ int hist[];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) hist[e] = 0;
+  __syncthreads();
+  const int beg = blockIdx.x * kChunk, end = min(P, beg + kChunk);
+  for (int i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    const int e = ids[i];
+    if (e >= 0 && e < E) atomicAdd(&hist[e], 1);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) ws[static_cast<int64_t>(blockIdx.x) * E + e] = hist[e];
+}
+
+// one CTA of 1024 threads; thread e owns expert e (E <= 1024)
+__global__ void __launch_bounds__(1024) permute_scan_kernel(int nb, int E, int32_t* __restrict__ ws,
+                                                            int32_t* __restrict__ counts,
+                                                            int32_t* __restrict__ offsets) {
+  __shared__ int wsum[32];
+  const int e = threadIdx.x, lane = e & 31, warp = e >> 5;
+  int total = 0;
+  if (e < E)
+    for (int b = 0; b < nb; ++b) total += ws[static_cast<int64_t>(b) * E + e];
+  int incl = total;  // block-wide inclusive scan over experts
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int w = wsum[lane], wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += v;
+    }
+    wsum[lane] = wi - w;  // exclusive warp prefix
+  }
+  __syncthreads();
+  const int excl = incl - total + wsum[warp];
+  if (e < E) {
+    counts[e] = total;
+    offsets[e] = excl;
+    int run = excl;
+    for (int b = 0; b < nb; ++b) {  // per-chunk base of expert e
+      const int64_t idx = static_cast<int64_t>(b) * E + e;
+      const int c = ws[idx];
+      ws[idx] = run;
+      run += c;
+    }
+    if (e == E - 1) offsets[E] = run;
+  }
+}
+
+__global__ void __launch_bounds__(kPermThreads, 1)
+    permute_scatter_kernel(const int32_t* __restrict__ ids, int P, int E, const int32_t* __restrict__ ws,
+                           int32_t* __restrict__ sorted_pairs, int32_t* __restrict__ pair_pos) {
+  extern __shared__ int sm[];
+  int* base = sm;                    // [E]
+  int* wcnt = base + E;              // [kPermWarps][E]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < E; e += kPermThreads) base[e] = ws[static_cast<int64_t>(blockIdx.x) * E + e];
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int cbeg = blockIdx.x * kChunk, cend = min(P, cbeg + kChunk);
+  for (int start = cbeg; start < cend; start += kPermThreads) {
+    for (int x = tid; x < kPermWarps * E; x += kPermThreads) wcnt[x] = 0;
+    __syncthreads();
+    const int i = start + tid;
+    int e = i < cend ? ids[i] : -1;
+    if (e >= E) e = -1;
+    const unsigned same = __match_any_sync(0xffffffffu, e);
+    const int lrank = __popc(same & lt_mask);
+    if (e >= 0 && lrank == 0) wcnt[warp * E + e] = __popc(same);
+    __syncthreads();
+    if (i < cend) {
+      if (e >= 0) {
+        int pre = 0;
+        for (int w = 0; w < warp; ++w) pre += wcnt[w * E + e];
+        const int pos = base[e] + pre + lrank;
+        sorted_pairs[pos] = i;
+        pair_pos[i] = pos;
+      } else {
+        pair_pos[i] = -1;
+      }
+    }
+    __syncthreads();
+    for (int x = tid; x < E; x += kPermThreads) {
+      int s2 = 0;
+      for (int w = 0; w < kPermWarps; ++w) s2 += wcnt[w * E + x];
+      base[x] += s2;
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------------------------------- gather
 // One CTA per permuted row, 128-bit vectors (H % 8 == 0).
 __global__ void moe_gather_kernel(const uint4* __restrict__ x, int64_t hv, int topk,
@@ -319,6 +422,33 @@ int w4a16_moe_permute(const int32_t* topk_ids, int64_t P, int64_t E, int32_t* ex
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
 
+int64_t w4a16_moe_permute_ws_bytes(int64_t P, int64_t E) {
+  return 4 * ((P + kChunk - 1) / kChunk) * E;
+}
+
+int w4a16_moe_permute_ws(const int32_t* topk_ids, int64_t P, int64_t E, int32_t* expert_counts,
+                         int32_t* expert_offsets, int32_t* sorted_pairs, int32_t* pair_pos, void* ws,
+                         int64_t ws_bytes, cudaStream_t stream) {
+  if (!ws || ws_bytes < w4a16_moe_permute_ws_bytes(P, E) || P <= 2 * kChunk)
+    return w4a16_moe_permute(topk_ids, P, E, expert_counts, expert_offsets, sorted_pairs, pair_pos, stream);
+  if (!topk_ids || !expert_counts || !expert_offsets || !sorted_pairs || !pair_pos) return W4_ERR_ARG;
+  if (E <= 0 || E > 1024 || P > (int64_t(1) << 30)) return W4_ERR_SHAPE;
+  const int nb = static_cast<int>((P + kChunk - 1) / kChunk);
+  int32_t* w = static_cast<int32_t*>(ws);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(permute_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             sizeof(int) * (1024 + kPermWarps * 1024)) != cudaSuccess)
+      return W4_ERR_CUDA;
+    attr = true;
+  }
+  permute_hist_kernel<<<nb, 512, sizeof(int) * E, stream>>>(topk_ids, (int)P, (int)E, w);
+  permute_scan_kernel<<<1, 1024, 0, stream>>>(nb, (int)E, w, expert_counts, expert_offsets);
+  permute_scatter_kernel<<<nb, kPermThreads, sizeof(int) * (E + kPermWarps * E), stream>>>(
+      topk_ids, (int)P, (int)E, w, sorted_pairs, pair_pos);
+  return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
+}
+
 int w4a16_moe_gather(const void* x, int64_t H, int64_t topk, const int32_t* sorted_pairs, int64_t rows,
                      const int32_t* row_limit, void* x_perm, cudaStream_t stream) {
   if (!x || !sorted_pairs || !x_perm) return W4_ERR_ARG;
@@ -387,7 +517,8 @@ int64_t w4a16_moe_workspace_bytes(int64_t T, int64_t topk, int64_t E, int64_t H,
   const int64_t P = T * topk;
   const int64_t ld = w4a16_group_sums_ld(P);
   return align256(4 * E) + align256(4 * (E + 1)) + 2 * align256(4 * P) + align256(2 * P * H) +
-         align256(2 * P * I) + align256(2 * P * H) + align256(8 * ld * (H / 128)) + align256(8 * ld * (I / 128));
+         align256(2 * P * I) + align256(2 * P * H) + align256(8 * ld * (H / 128)) + align256(8 * ld * (I / 128)) +
+         align256(w4a16_moe_permute_ws_bytes(P, E));
 }
 
 int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, int64_t topk,
@@ -409,9 +540,12 @@ int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E,
   void* hp = ws; ws += align256(2 * P * I);
   void* yp = ws; ws += align256(2 * P * H);
   float* xsum = reinterpret_cast<float*>(ws); ws += align256(8 * ld * (H / 128));
-  float* hsum = reinterpret_cast<float*>(ws);
+  float* hsum = reinterpret_cast<float*>(ws); ws += align256(8 * ld * (I / 128));
+  void* pws = ws;
   int rc;
-  if ((rc = w4a16_moe_permute(topk_ids, P, E, counts, offsets, sorted, pos, stream))) return rc;
+  if ((rc = w4a16_moe_permute_ws(topk_ids, P, E, counts, offsets, sorted, pos, pws,
+                                 w4a16_moe_permute_ws_bytes(P, E), stream)))
+    return rc;
   const int nt = w4a16_pick_ntok(P, E);
   const bool decode = nt <= 32;  // offset-code GEMMs need the per-group activation sums
   if (decode) {

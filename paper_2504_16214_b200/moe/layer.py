@@ -119,7 +119,8 @@ def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, 
     P = T * k
     dev = x.device
     with tm.span("permute"):
-        counts, offsets, sorted_pairs, pair_pos = ops.moe_permute(topk_ids, E)
+        counts, offsets, sorted_pairs, pair_pos = ops.moe_permute(
+            topk_ids, E, _ws.get("perm_ws", (max(ops.permute_ws_bytes(P, E), 1),), torch.uint8, dev))
     nt = ntok or ops.pick_ntok(P, E)
     decode = nt <= 32  # offset-code GEMMs: per-group activation sums ride along with X and h
     with tm.span("gather"):

@@ -77,8 +77,9 @@ def route_topk(logits: torch.Tensor, k: int, scoring: str = "softmax", renormali
     return ids, wts
 
 
-def moe_permute(topk_ids: torch.Tensor, num_experts: int):
-    """-> (expert_counts [E], expert_offsets [E+1], sorted_pairs [P], pair_pos [P]) int32."""
+def moe_permute(topk_ids: torch.Tensor, num_experts: int, workspace: torch.Tensor | None = None):
+    """-> (expert_counts [E], expert_offsets [E+1], sorted_pairs [P], pair_pos [P]) int32. Large P runs
+    the multi-CTA kernel when a workspace of permute_ws_bytes(P, E) bytes is given (or allocated)."""
     _need_cuda(topk_ids)
     if topk_ids.dtype != torch.int32:
         raise _lib.W4A16Error("topk_ids must be int32")
@@ -88,9 +89,17 @@ def moe_permute(topk_ids: torch.Tensor, num_experts: int):
     offsets = torch.empty(num_experts + 1, dtype=torch.int32, device=dev)
     sorted_pairs = torch.empty(max(P, 1), dtype=torch.int32, device=dev)
     pair_pos = torch.empty(max(P, 1), dtype=torch.int32, device=dev)
-    _lib.call("w4a16_moe_permute", topk_ids.data_ptr(), P, num_experts, counts.data_ptr(), offsets.data_ptr(),
-              sorted_pairs.data_ptr(), pair_pos.data_ptr(), _stream())
+    wsb = permute_ws_bytes(P, num_experts)
+    if workspace is None or workspace.numel() * workspace.element_size() < wsb:
+        workspace = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev)
+    _lib.call("w4a16_moe_permute_ws", topk_ids.data_ptr(), P, num_experts, counts.data_ptr(), offsets.data_ptr(),
+              sorted_pairs.data_ptr(), pair_pos.data_ptr(), workspace.data_ptr(),
+              workspace.numel() * workspace.element_size(), _stream())
     return counts, offsets, sorted_pairs[:P], pair_pos[:P]
+
+
+def permute_ws_bytes(P: int, num_experts: int) -> int:
+    return int(_lib.load().w4a16_moe_permute_ws_bytes(P, num_experts))
 
 
 def moe_gather(x: torch.Tensor, sorted_pairs: torch.Tensor, topk: int, rows: int | None = None,

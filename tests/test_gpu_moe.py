@@ -71,7 +71,8 @@ def test_route_topk(scoring, renorm, E, k):
 
 
 # ------------------------------------------------------------------------------------------- permute
-@pytest.mark.parametrize("P,E", [(1, 4), (64 * 8, 256), (3000, 256), (5000, 7), (65536, 256), (2048, 1024)])
+@pytest.mark.parametrize("P,E", [(1, 4), (64 * 8, 256), (3000, 256), (5000, 7), (65536, 256), (2048, 1024),
+                                 (20000, 1024), (9001, 3), (131072, 128)])
 def test_permute_bit_exact(P, E):
     rng = np.random.default_rng(P + E)
     ids = rng.integers(0, E, size=P).astype(np.int32)
