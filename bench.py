@@ -237,6 +237,7 @@ def main():
     ap.add_argument("--dtype", choices=["f16", "bf16"], default="f16")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of a CUDA graph")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -270,6 +271,19 @@ def main():
     def step(timer=None, xx=x, ll=lg):
         return fused_moe_w4a16(xx, ll, weights, K_DS, "softmax", True, ep_group=group, timer=timer)
 
+    # single GPU: the whole layer step captured once in a CUDA graph (decode-serving mode; every
+    # kernel still runs per replay). EP (N > 1) reads split sizes on the host, so it runs eagerly.
+    graphed = None
+    if world == 1 and not args.no_graph:
+        from paper_2504_16214_b200.moe import FusedMoEGraph
+        graphed = FusedMoEGraph(weights, T, K_DS, "softmax", True, tdt, dev)
+        graphed(x, lg)
+
+    def timed_step(xx=x, ll=lg):
+        if graphed is not None:
+            return graphed(xx, ll)
+        return step(None, xx, ll)
+
     def barrier():
         if world > 1:
             dist.barrier()
@@ -301,8 +315,11 @@ def main():
     job_bytes = layer_bytes(e_touched, T_job, H_DS, I_DS, K_DS)
     job_flops = layer_flops(T_job, K_DS, H_DS, I_DS)
 
+    if graphed is not None:
+        graphed.x.copy_(x)
+        graphed.logits.copy_(lg)
     for _ in range(args.warmup):
-        step()
+        timed_step(None, None) if graphed is not None else step()
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -311,7 +328,7 @@ def main():
         torch.cuda.profiler.start()  # ncu --profile-from-start off captures exactly the timed steps
         ev0.record()
         for _ in range(args.steps):
-            step()
+            timed_step(None, None) if graphed is not None else step()
         ev1.record()
         barrier()
         torch.cuda.profiler.stop()
@@ -319,7 +336,10 @@ def main():
     ms = ms_total / args.steps
     value = job_bytes / (ms * 1e-3) / 1e9
     tflops = job_flops / (ms * 1e-3) / 1e12
-    # per-kernel device times (separate pass: the bracketing events add small gaps between launches)
+    # per-kernel device times (separate eager pass: the bracketing events add small gaps between launches)
+    for _ in range(2):
+        step()
+    barrier()
     timer = KernelTimer()
     for _ in range(args.steps):
         step(timer)
@@ -341,24 +361,31 @@ def main():
     # ---- end to end through the public API with host buffers (H2D inputs, D2H output)
     y_host = torch.empty((T, H_DS), dtype=tdt).pin_memory()
     for _ in range(2):
-        xx = x_host.to(dev, non_blocking=True)
-        ll = lg_host.to(dev, non_blocking=True)
-        y_host.copy_(step(None, xx, ll), non_blocking=True)
+        if graphed is not None:
+            y_host.copy_(graphed(x_host, lg_host), non_blocking=True)  # H2D into the graph's inputs
+        else:
+            xx = x_host.to(dev, non_blocking=True)
+            ll = lg_host.to(dev, non_blocking=True)
+            y_host.copy_(step(None, xx, ll), non_blocking=True)
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        xx = x_host.to(dev, non_blocking=True)
-        ll = lg_host.to(dev, non_blocking=True)
-        y_host.copy_(step(None, xx, ll), non_blocking=True)
+        if graphed is not None:
+            y_host.copy_(graphed(x_host, lg_host), non_blocking=True)
+        else:
+            xx = x_host.to(dev, non_blocking=True)
+            ll = lg_host.to(dev, non_blocking=True)
+            y_host.copy_(step(None, xx, ll), non_blocking=True)
     e1.record()
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
     e2e = {"value": round(job_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
            "h2d_bytes_per_step": x_host.numel() * x_host.element_size() + lg_host.numel() * 4,
            "d2h_bytes_per_step": y_host.numel() * y_host.element_size(), "ms_per_step": round(e2e_ms, 4),
-           "api": "paper_2504_16214_b200.moe.fused_moe_w4a16"}
+           "api": ("paper_2504_16214_b200.moe.FusedMoEGraph (CUDA graph of fused_moe_w4a16)" if graphed is not None
+                   else "paper_2504_16214_b200.moe.fused_moe_w4a16")}
 
     # ---- regime sweep (1 GPU only): decode .. prefill, same weights
     sweep = []
@@ -368,15 +395,18 @@ def main():
             ls = torch.randn((Ts, E_DS), generator=g).to(dev)
             _, sid = select_experts(ls, K_DS, "softmax", True)
             et = int(torch.unique(sid).numel())
+            from paper_2504_16214_b200.moe import FusedMoEGraph
+            gs_ = FusedMoEGraph(weights, Ts, K_DS, "softmax", True, tdt, dev)
+            gs_(xs, ls)
             for _ in range(2):
-                fused_moe_w4a16(xs, ls, weights, K_DS, "softmax", True)
+                gs_()
             torch.cuda.synchronize()
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             reps = 5
             a.record()
             for _ in range(reps):
-                fused_moe_w4a16(xs, ls, weights, K_DS, "softmax", True)
+                gs_()
             b.record()
             torch.cuda.synchronize()
             sm = a.elapsed_time(b) / reps
@@ -385,7 +415,7 @@ def main():
                           "GB/s": round(by / sm / 1e6, 1), "TFLOP/s": round(fl / sm / 1e9, 2),
                           "hbm_frac": round(by / sm / 1e6 / hbm_peak, 4),
                           "tc_frac": round(fl / sm / 1e9 / tc_peak, 4)})
-            del xs, ls
+            del xs, ls, gs_
 
     cpu = None
     synth = None

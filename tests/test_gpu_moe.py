@@ -208,3 +208,24 @@ def test_moe_layer(dt, T, E, k, H, I):
     assert np.array_equal(ids.cpu().numpy(), rid)
     want = O.moe_forward(x, O.dequant(q13, z13, s13, dt), O.dequant(q2, z2, s2, dt), rid, rw, dt)
     np.testing.assert_allclose(_from_dev_act(y, dt), want, rtol=RTOL, atol=ATOL)
+
+
+def test_fused_moe_graph_matches_eager():
+    """The CUDA-graph-captured layer replays the same kernels: identical output to the eager call,
+    and new inputs copied into the graph take effect."""
+    from paper_2504_16214_b200.moe import FusedMoEGraph, fused_moe_w4a16
+    from paper_2504_16214_b200.moe.weights import MoEWeights
+    rng = np.random.default_rng(21)
+    T, E, k, H, I, dt = 12, 16, 4, 512, 256, "f16"
+    q13, z13, s13 = O.synth_awq_expert_weights(rng, E, 2 * I, H, dt)
+    q2, z2, s2 = O.synth_awq_expert_weights(rng, E, H, I, dt)
+    weights = MoEWeights(_packed(q13, z13, s13, dt, True), _packed(q2, z2, s2, dt, False))
+    g = FusedMoEGraph(weights, T, k, "softmax", True, torch.float16)
+    for seed in (1, 2):
+        r = np.random.default_rng(seed)
+        x = _to_dev_act(O.round_act(r.standard_normal((T, H)).astype(np.float32) * 0.5, dt), dt)
+        lg = torch.from_numpy(r.standard_normal((T, E)).astype(np.float32)).cuda()
+        want = fused_moe_w4a16(x, lg, weights, k, "softmax", True).clone()
+        got = g(x, lg)
+        torch.cuda.synchronize()
+        assert torch.equal(got, want)
