@@ -90,12 +90,14 @@ struct Cfg {
   static constexpr int kAccCols = kOffset ? kParts * kKSplit * kNTok : (kGated ? 2 * kNTok : kNTok);
   static constexpr int kACols = kParts * (kTileK / 2);  // fp16 pairs per 32-bit column
   // TMEM budget (512 columns): A ring + accumulator ring
-  static constexpr int kNumA_ = kOffset ? ((3 * kACols + 2 * kAccCols <= 512) ? 3 : 2) : 0;
+  // 3 A slots if two accumulator stages still fit, else 2; the gated prefill projection (56-stage
+  // tiles) instead prefers 3 A slots (dequant / MMA overlap) over a second accumulator stage
+  // (epilogue / next-tile overlap, once per long tile); the short k-pair tiles need two.
+  static constexpr int kNumA_ = (kOffset || !kGated) ? ((3 * kACols + 2 * kAccCols <= 512) ? 3 : 2)
+                                                    : ((3 * kACols + kAccCols <= 512) ? 3 : 2);
   static constexpr int kNumAccO = (512 - kNumA_ * kACols) / kAccCols;
-  static constexpr int kNumAcc = kOffset ? (kNumAccO > 4 ? 4 : kNumAccO)
-                                         : ((2 * kAccCols + 2 * kACols <= 512) ? 2 : 1);
-  static constexpr int kNumA0 = (512 - kNumAcc * kAccCols) / kACols;
-  static constexpr int kNumA = kOffset ? kNumA_ : (kNumA0 > 4 ? 4 : kNumA0);
+  static constexpr int kNumAcc = kNumAccO > (kOffset ? 4 : 2) ? (kOffset ? 4 : 2) : kNumAccO;
+  static constexpr int kNumA = kNumA_;
   static constexpr int kStageBytes = kBlk + kXBytes + kSumBytes;
   static constexpr int kFixed = 2048 + 4 * (kMaxExperts + 2) + 8 * kTileTab;  // barriers, m-tile prefix, tiles
   static constexpr int kNS0 = (kSmemBudget - kFixed - 1024) / kStageBytes;
