@@ -238,6 +238,8 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of a CUDA graph")
+    ap.add_argument("--ep", action="store_true",
+                    help="run the expert-parallel path (NCCL process group, all-to-all) even on one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -254,8 +256,13 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if world > 1 or args.ep:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            dist.init_process_group("nccl", device_id=dev, rank=0, world_size=1)
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         group = dist.group.WORLD
     tdt = torch.float16 if args.dtype == "f16" else torch.bfloat16
     T = args.tokens
@@ -274,7 +281,7 @@ def main():
     # single GPU: the whole layer step captured once in a CUDA graph (decode-serving mode; every
     # kernel still runs per replay). EP (N > 1) reads split sizes on the host, so it runs eagerly.
     graphed = None
-    if world == 1 and not args.no_graph:
+    if group is None and not args.no_graph:
         from paper_2504_16214_b200.moe import FusedMoEGraph
         graphed = FusedMoEGraph(weights, T, K_DS, "softmax", True, tdt, dev)
         graphed(x, lg)
@@ -351,7 +358,7 @@ def main():
     per_rank_touched = int(touched[lo:hi].sum().item()) if world > 1 else e_touched
     k_bytes = per_rank_touched * w_bytes(2 * I_DS, H_DS) + T_job * K_DS // world * (H_DS + I_DS) * 2
     k_ms = timer.mean_ms("gemm_gate_up")
-    k_gbs = k_bytes / (k_ms * 1e-3) / 1e9
+    k_gbs = k_bytes / (k_ms * 1e-3) / 1e9 if k_ms > 0 else 0.0
     traffic = None
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
@@ -449,7 +456,7 @@ def main():
             "layout_synthesis_cpu": synth,
         }
         print(json.dumps(line))
-    if world > 1:
+    if group is not None:
         dist.destroy_process_group()
     return 0
 

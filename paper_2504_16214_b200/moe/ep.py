@@ -45,11 +45,13 @@ def plan_dispatch(global_counts: torch.Tensor, world: int, group=None) -> Dispat
     return DispatchPlan(both[:world], both[world:], recv.view(world, e_local))
 
 
-def local_expert_ids(recv_counts: torch.Tensor) -> torch.Tensor:
-    """Local expert id of every received row (rows arrive grouped by source, then by expert)."""
+def local_expert_ids(recv_counts: torch.Tensor, n_recv: int | None = None) -> torch.Tensor:
+    """Local expert id of every received row (rows arrive grouped by source, then by expert).
+    ``n_recv`` (the host-known total) avoids a device->host synchronisation."""
     world, e_local = recv_counts.shape
     experts = torch.arange(e_local, device=recv_counts.device, dtype=torch.int32).repeat(world)
-    return torch.repeat_interleave(experts, recv_counts.reshape(-1).to(torch.int64)).to(torch.int32)
+    return torch.repeat_interleave(experts, recv_counts.reshape(-1).to(torch.int64),
+                                   output_size=n_recv).to(torch.int32)
 
 
 class CudaBackend:
@@ -58,14 +60,18 @@ class CudaBackend:
     combine = staticmethod(cuda_ops.moe_combine)
 
     @staticmethod
-    def experts(x, weights, counts, offsets, ntok):
+    def experts(x, weights, counts, offsets, ntok, timer=None):
+        from .layer import _NOTIMER
+        tm = timer or _NOTIMER
         E, H, I = weights.num_experts, weights.hidden, weights.inter
         nt = ntok or cuda_ops.pick_ntok(x.shape[0], E)
         decode = nt <= 32
         xs = cuda_ops.group_sums(x) if decode else None
-        h = cuda_ops.grouped_gemm(x, weights.w13.blocks, E, I, True, counts, offsets, nt, xsum=xs)
+        with tm.span("gemm_gate_up"):
+            h = cuda_ops.grouped_gemm(x, weights.w13.blocks, E, I, True, counts, offsets, nt, xsum=xs)
         hs = cuda_ops.group_sums(h) if decode else None
-        return cuda_ops.grouped_gemm(h, weights.w2.blocks, E, H, False, counts, offsets, nt, xsum=hs)
+        with tm.span("gemm_down"):
+            return cuda_ops.grouped_gemm(h, weights.w2.blocks, E, H, False, counts, offsets, nt, xsum=hs)
 
 
 def moe_w4a16_ep(x: torch.Tensor, weights, topk_weights: torch.Tensor, topk_ids: torch.Tensor, group=None,
@@ -90,10 +96,10 @@ def moe_w4a16_ep(x: torch.Tensor, weights, topk_weights: torch.Tensor, topk_ids:
     recv_x = x.new_empty((n_recv, H))
     dist.all_to_all_single(recv_x, send_x, plan.recv_splits, plan.send_splits, group=group)
     # 5: local expert order + grouped GEMMs
-    lid = local_expert_ids(plan.recv_counts)
+    lid = local_expert_ids(plan.recv_counts, n_recv)
     l_counts, l_offsets, l_sorted, l_pos = backend.permute(lid, e_local)
     xl = backend.gather(recv_x, l_sorted, 1, n_recv) if n_recv else recv_x
-    yl = backend.experts(xl, weights, l_counts, l_offsets, ntok) if n_recv else recv_x
+    yl = backend.experts(xl, weights, l_counts, l_offsets, ntok, timer) if n_recv else recv_x
     # 6: back to arrival order, combine exchange, weighted reduction
     y_recv = backend.gather(yl, l_pos, 1, n_recv) if n_recv else recv_x
     y_back = x.new_empty((T * k, H))

@@ -53,7 +53,7 @@ class CpuBackend:
         return torch.from_numpy(O.round_act(y.numpy(), "f16"))
 
     @staticmethod
-    def experts(x, weights, counts, offsets, ntok):
+    def experts(x, weights, counts, offsets, ntok, timer=None):
         h = O.grouped_gemm(x.numpy(), weights.w13d, counts.numpy(), offsets.numpy(), "f16", gated=True)
         y = O.grouped_gemm(h, weights.w2d, counts.numpy(), offsets.numpy(), "f16", gated=False)
         return torch.from_numpy(y)
