@@ -865,7 +865,9 @@ int w4a16_grouped_gemm(const void* x, int64_t rows, int64_t K, const uint8_t* wb
   a.xsum = xsum;
   a.sum_ld = w4a16_group_sums_ld(rows);
   a.rows = rows;
-  const int mode = gated ? kModeGateUp : (a.kt % 2 == 0 ? kModeKPair : kModePlain);
+  // k-pair (two k-groups per 17 KB stage) for decode tiles; at 64/128 tokens the X tile dominates a
+  // stage (64 KB for a k-pair at 128 tokens -> only 2 smem stages), so 128-token tiles use one group per stage
+  const int mode = gated ? kModeGateUp : ((a.kt % 2 == 0 && ntok <= 64) ? kModeKPair : kModePlain);
   const bool offset = xsum != nullptr && ntok <= 32;
   // CTA pairs (cta_group::2) measured slower at decode token counts (an M=256 x N=16 MMA with 8-row B
   // halves executes ~4x slower than two M=128 ones): opt-in only (W4A16_PAIR=1)
