@@ -341,6 +341,7 @@ def main():
         torch.cuda.profiler.stop()
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
     ms = ms_total / args.steps
+    hbm_peak, tc_peak, tc_sus, peak_src = peaks()
     value = job_bytes / (ms * 1e-3) / 1e9
     tflops = job_flops / (ms * 1e-3) / 1e12
     # per-kernel device times (separate eager pass: the bracketing events add small gaps between launches)
@@ -351,8 +352,6 @@ def main():
     for _ in range(args.steps):
         step(timer)
     barrier()
-    hbm_peak, tc_peak, tc_sus, peak_src = peaks()
-
     # dominant kernel: gate/up grouped GEMM (2/3 of the weight bytes). Algorithmic bytes per launch
     # = this rank's touched W13 blocks + X_perm read + H write.
     per_rank_touched = int(touched[lo:hi].sum().item()) if world > 1 else e_touched
@@ -421,7 +420,8 @@ def main():
             sweep.append({"tokens": Ts, "experts_touched": et, "ms": round(sm, 4),
                           "GB/s": round(by / sm / 1e6, 1), "TFLOP/s": round(fl / sm / 1e9, 2),
                           "hbm_frac": round(by / sm / 1e6 / hbm_peak, 4),
-                          "tc_frac": round(fl / sm / 1e9 / tc_peak, 4)})
+                          "tc_frac": round(fl / sm / 1e9 / tc_peak, 4),
+                          "tc_frac_sustained": round(fl / sm / 1e9 / tc_sus, 4) if tc_sus else None})
             del xs, ls, gs_
 
     cpu = None
