@@ -388,6 +388,11 @@ using namespace w4;
 
 namespace {
 inline int64_t align256(int64_t b) { return (b + 255) & ~int64_t(255); }
+int64_t splitk_bytes(int64_t P, int64_t E, int64_t H, int64_t I) {
+  const int nt = w4a16_pick_ntok(P, E);
+  const int64_t a = w4a16_grouped_gemm_ws_bytes(P, H, E, I, 1, nt), b = w4a16_grouped_gemm_ws_bytes(P, I, E, H, 0, nt);
+  return a > b ? a : b;
+}
 }  // namespace
 
 extern "C" {
@@ -518,7 +523,7 @@ int64_t w4a16_moe_workspace_bytes(int64_t T, int64_t topk, int64_t E, int64_t H,
   const int64_t ld = w4a16_group_sums_ld(P);
   return align256(4 * E) + align256(4 * (E + 1)) + 2 * align256(4 * P) + align256(2 * P * H) +
          align256(2 * P * I) + align256(2 * P * H) + align256(8 * ld * (H / 128)) + align256(8 * ld * (I / 128)) +
-         align256(w4a16_moe_permute_ws_bytes(P, E));
+         align256(w4a16_moe_permute_ws_bytes(P, E)) + align256(splitk_bytes(P, E, H, I));
 }
 
 int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, int64_t topk,
@@ -541,7 +546,9 @@ int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E,
   void* yp = ws; ws += align256(2 * P * H);
   float* xsum = reinterpret_cast<float*>(ws); ws += align256(8 * ld * (H / 128));
   float* hsum = reinterpret_cast<float*>(ws); ws += align256(8 * ld * (I / 128));
-  void* pws = ws;
+  void* pws = ws; ws += align256(w4a16_moe_permute_ws_bytes(P, E));
+  void* kws = ws;
+  const int64_t kws_bytes = splitk_bytes(P, E, H, I);
   int rc;
   if ((rc = w4a16_moe_permute_ws(topk_ids, P, E, counts, offsets, sorted, pos, pws,
                                  w4a16_moe_permute_ws_bytes(P, E), stream)))
@@ -553,12 +560,12 @@ int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E,
   } else if ((rc = w4a16_moe_gather(x, H, topk, sorted, P, offsets + E, xp, stream))) {
     return rc;
   }
-  if ((rc = w4a16_grouped_gemm(xp, P, H, w13, E, I, 1, counts, offsets, decode ? xsum : nullptr, hp, dtype, nt,
-                               stream)))
+  if ((rc = w4a16_grouped_gemm_ws(xp, P, H, w13, E, I, 1, counts, offsets, decode ? xsum : nullptr, hp, dtype, nt,
+                                  kws, kws_bytes, stream)))
     return rc;
   if (decode && (rc = w4a16_group_sums(hp, P, I, offsets + E, dtype, hsum, stream))) return rc;
-  if ((rc = w4a16_grouped_gemm(hp, P, I, w2, E, H, 0, counts, offsets, decode ? hsum : nullptr, yp, dtype, nt,
-                               stream)))
+  if ((rc = w4a16_grouped_gemm_ws(hp, P, I, w2, E, H, 0, counts, offsets, decode ? hsum : nullptr, yp, dtype, nt,
+                                  kws, kws_bytes, stream)))
     return rc;
   return w4a16_moe_combine(yp, T, H, topk, pos, topk_weights, dtype, y, stream);
 }

@@ -16,6 +16,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -44,6 +45,9 @@ struct GemmArgs {
   const float* xsum;             // offset mode: (C, S) [kt][sum_ld][2]
   int64_t sum_ld, rows;
   int num_experts, nt, kt;
+  int splits;                    // split-K factor (decode mode; 1 = none)
+  float* part;                   // splits > 1: fp32 partials [splits][rows][part_ld]
+  int64_t part_ld;               // (gated ? 2 : 1) * n_out
 };
 
 // Numeric modes.
@@ -139,7 +143,7 @@ __device__ __forceinline__ void progress_at(int ev, uint32_t n) {
 }
 
 struct TileInfo {
-  int e, n_tile, m_start, m_rows;
+  int e, n_tile, m_start, m_rows, split;
 };
 
 // Static persistent schedule: tile t -> (expert, n-tile group, m-tile); m-tiles of one (expert, n-tile)
@@ -148,8 +152,10 @@ struct TileInfo {
 template <int kNTok, int kNSplit>
 __device__ __forceinline__ bool get_tile(int t, const int* mt_off, const GemmArgs& a, uint32_t rank, TileInfo& ti) {
   const int ntg = a.nt / kNSplit;
-  const int total = mt_off[a.num_experts] * ntg;
+  const int total = mt_off[a.num_experts] * ntg * a.splits;
   if (t >= total) return false;
+  ti.split = t % a.splits;  // split-K units of one tile are adjacent
+  t /= a.splits;
   int lo = 0, hi = a.num_experts;  // find e with mt_off[e]*ntg <= t < mt_off[e+1]*ntg
   while (hi - lo > 1) {
     int mid = (lo + hi) >> 1;
@@ -166,17 +172,19 @@ __device__ __forceinline__ bool get_tile(int t, const int* mt_off, const GemmArg
   return true;
 }
 
-// Packed tile: w0 = e | (m_rows - 1) << 10 | n_tile << 17, w1 = m_start.
+// Packed tile: w0 = e | (m_rows - 1) << 10 | n_tile << 17, w1 = m_start | split << 20 (split-K
+// launches have rows < 2^20; without split-K split is 0 and m_start uses all 32 bits).
 __device__ __forceinline__ uint2 pack_tile(const TileInfo& ti) {
   return make_uint2(static_cast<uint32_t>(ti.e) | static_cast<uint32_t>(ti.m_rows - 1) << 10 |
                         static_cast<uint32_t>(ti.n_tile) << 17,
-                    static_cast<uint32_t>(ti.m_start));
+                    static_cast<uint32_t>(ti.m_start) | static_cast<uint32_t>(ti.split) << 20);
 }
 __device__ __forceinline__ void unpack_tile(uint2 p, TileInfo& ti) {
   ti.e = p.x & 1023u;
   ti.m_rows = static_cast<int>((p.x >> 10) & 127u) + 1;
   ti.n_tile = static_cast<int>(p.x >> 17);
-  ti.m_start = static_cast<int>(p.y);
+  ti.m_start = static_cast<int>(p.y & 0xFFFFFu);
+  ti.split = static_cast<int>(p.y >> 20);
 }
 
 // The CTA's i-th tile (t = tile0 + i * tstride): from the smem table when i < kTileTab, else searched.
@@ -219,6 +227,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   using C = Cfg<kNTok, kMode, kOffset, kPair>;
   constexpr bool kGated = C::kGated;
   const int n_stages = args.kt / C::kGroupsPerStage;  // stages per tile
+  // split-K: unit (tile, split) covers stages [stage_beg, stage_end) of the tile
+  auto stage_beg = [&](const TileInfo& t) { return t.split * n_stages / args.splits; };
+  auto stage_end = [&](const TileInfo& t) { return (t.split + 1) * n_stages / args.splits; };
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_x = smem;                                  // [NS][kXBytes]
@@ -276,7 +287,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     if (lane == 31) mt_off[E] = incl;
     __syncwarp();
     // this CTA's tiles t = tile0 + i * tstride, the first kTileTab of them tabulated
-    const int total = mt_off[E] * (args.nt / C::kCG);
+    const int total = mt_off[E] * (args.nt / C::kCG) * args.splits;
     const int n_tiles = tile0 < total ? (total - tile0 + tstride - 1) / tstride : 0;
     if (lane == 0) *n_tiles_sm = n_tiles;
     for (int i = lane; i < min(n_tiles, kTileTab); i += 32) {
@@ -310,7 +321,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         // per (expert, n-tile): kt k-groups of (gated ? 2 : 1) parts, stage j = bytes [j*kBlk, (j+1)*kBlk)
         const uint8_t* wsrc = args.wblocks + (static_cast<int64_t>(ti.e) * args.nt + ti.n_tile) *
                                                  static_cast<int64_t>(args.kt) * (kGated ? 2 : 1) * kPartBytes;
-        for (int j = 0; j < n_stages; ++j) {
+        for (int j = stage_beg(ti); j < stage_end(ti); ++j) {
           mbar_wait(&empty[st.i], st.ph ^ 1);
           if (lane == 0) {
             trace_at(tr, 0, pgs++);
@@ -364,7 +375,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           mbar_wait_warp(&accempty[acc.i], acc.ph ^ 1);
           tc_fence_after();
         }
-        for (int j = 0; j < n_stages; ++j, ++gs) {
+        for (int j = stage_beg(ti); j < stage_end(ti); ++j, ++gs) {
           if constexpr (kOffset)  // fresh partials per stage: accumulator slot free + A slot filled
             mbar_wait2_warp(&accempty[acc.i], acc.ph ^ 1, &afull[ar.i], ar.ph);
           else
@@ -418,7 +429,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     uint32_t gs = 0;
     TileInfo ti;
     for (int it = 0; tile_at<kNTok, C::kCG>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
-      for (int j = 0; j < n_stages; ++j, ++gs) {
+      for (int j = stage_beg(ti); j < stage_end(ti); ++j, ++gs) {
         if ((gs & 1u) != my_par) {
           st.next(C::kNS);
           ar.next(C::kNumA);
@@ -501,7 +512,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         for (int o = 0; o < kOuts; ++o)
 #pragma unroll
           for (int i = 0; i < kNTok; ++i) a[o][i] = 0.f;
-        for (int j = 0; j < n_stages; ++j) {
+        for (int j = stage_beg(ti); j < stage_end(ti); ++j) {
           mbar_wait(&full[st.i], st.ph);
           if (tre) trace_at(tr, 6, egs);
           const uint32_t blk = w_u32 + st.i * C::kBlk;
@@ -558,13 +569,25 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           acc.next(C::kNumAcc);
           st.next(C::kNS);
         }
+        if (args.splits > 1) {  // split-K: fp32 partials, summed (and activated) by splitk_finalize
+          float* pbase = args.part + (static_cast<int64_t>(ti.split) * args.rows + ti.m_start) * args.part_ld +
+                         ti.n_tile * kTileRows + row;
 #pragma unroll
-        for (int m = 0; m < kNTok; ++m) {
-          if (m < m_rows) {
-            float v;
-            if constexpr (kGated) v = silu_f(a[0][m]) * a[1][m];
-            else v = a[0][m];
-            obase[static_cast<int64_t>(m) * args.ldo] = to_act_bits<kBF16>(v);
+          for (int m = 0; m < kNTok; ++m) {
+            if (m < m_rows) {
+#pragma unroll
+              for (int o = 0; o < kOuts; ++o) pbase[static_cast<int64_t>(m) * args.part_ld + o * args.ldo] = a[o][m];
+            }
+          }
+        } else {
+#pragma unroll
+          for (int m = 0; m < kNTok; ++m) {
+            if (m < m_rows) {
+              float v;
+              if constexpr (kGated) v = silu_f(a[0][m]) * a[1][m];
+              else v = a[0][m];
+              obase[static_cast<int64_t>(m) * args.ldo] = to_act_bits<kBF16>(v);
+            }
           }
         }
       } else {
@@ -622,6 +645,37 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     if constexpr (kPair) tmem_dealloc_pair<512>(tbase);
     else tmem_dealloc<512>(tbase);
   }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Split-K finalize: out[r][n] = act(f(sum_s part[s][r][...])), f = silu(gate) * up when gated, for
+// rows r < *row_limit. One thread per 4 outputs.
+template <bool kBF16, bool kGated>
+__global__ void splitk_finalize_kernel(const float* __restrict__ part, int splits, int64_t rows, int64_t n_out,
+                                       const int32_t* __restrict__ row_limit, uint16_t* __restrict__ out) {
+  const int64_t r = blockIdx.y;
+  if (r >= __ldg(row_limit)) return;
+  const int64_t n = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+  if (n >= n_out) return;
+  const int64_t ld = (kGated ? 2 : 1) * n_out;
+  float4 g = make_float4(0.f, 0.f, 0.f, 0.f), u = g;
+  for (int sidx = 0; sidx < splits; ++sidx) {
+    const float* pr = part + (static_cast<int64_t>(sidx) * rows + r) * ld + n;
+    const float4 a = *reinterpret_cast<const float4*>(pr);
+    g.x += a.x, g.y += a.y, g.z += a.z, g.w += a.w;
+    if constexpr (kGated) {
+      const float4 b = *reinterpret_cast<const float4*>(pr + n_out);
+      u.x += b.x, u.y += b.y, u.z += b.z, u.w += b.w;
+    }
+  }
+  float v[4] = {g.x, g.y, g.z, g.w};
+  if constexpr (kGated) {
+    v[0] = silu_f(g.x) * u.x, v[1] = silu_f(g.y) * u.y, v[2] = silu_f(g.z) * u.z, v[3] = silu_f(g.w) * u.w;
+  }
+  uint2 o;
+  o.x = static_cast<uint32_t>(to_act_bits<kBF16>(v[0])) | static_cast<uint32_t>(to_act_bits<kBF16>(v[1])) << 16;
+  o.y = static_cast<uint32_t>(to_act_bits<kBF16>(v[2])) | static_cast<uint32_t>(to_act_bits<kBF16>(v[3])) << 16;
+  *reinterpret_cast<uint2*>(out + r * n_out + n) = o;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -739,8 +793,9 @@ int sm_count() {
   static int n = 0;
   if (!n) {
     int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) !=
+                                                  cudaSuccess || n <= 0)
+      n = 148;  // no device (planning queries on a build host): B200
   }
   return n;
 }
@@ -817,6 +872,45 @@ bool pairs_enabled() {
 
 }  // namespace
 
+namespace {
+// Split-K factor for a decode-mode launch: with few (expert, n-tile) tiles the 148 SMs are not all
+// busy (T = 1 touches 8 DS-R1 experts -> 128 gate/up tiles; Mixtral decode -> 64 down tiles of 56
+// stages). Minimise waves x (stages per unit + per-unit overhead) over S, from an upper estimate
+// of the tile count (touched experts <= min(E, rows)).
+int choose_splits(int64_t rows, int64_t num_experts, int nt, int n_stages, int grid) {
+  const int64_t tiles = std::min<int64_t>(num_experts, rows) * nt;
+  if (tiles >= 2 * grid || n_stages < 4) return 1;
+  double best = 1e30;
+  int best_s = 1;
+  for (int sp = 1; sp <= std::min(16, n_stages / 2); ++sp) {
+    const int64_t units = tiles * sp;
+    const double waves = static_cast<double>((units + grid - 1) / grid);
+    const double cost = waves * (static_cast<double>(n_stages) / sp + 1.5) + (sp > 1 ? 1.0 : 0.0);
+    if (cost < best - 1e-9) { best = cost; best_s = sp; }
+  }
+  return best_s;
+}
+
+struct GemmPlan {
+  int ntok, mode, splits;
+  bool offset;
+};
+
+GemmPlan plan_gemm(int64_t rows, int64_t K, int64_t num_experts, int64_t n_out, int gated, bool has_xsum,
+                   int ntok) {
+  GemmPlan pl;
+  pl.ntok = ntok > 0 ? ntok : w4a16_pick_ntok(rows, num_experts);
+  const int kt = static_cast<int>(K / kTileK), nt = static_cast<int>(n_out / kTileRows);
+  pl.offset = has_xsum && pl.ntok <= 32;
+  // k-pair (two k-groups per 17 KB stage) for decode tiles; at 128 tokens the X tile dominates a stage
+  // (64 KB for a k-pair -> only 2 smem stages), so 128-token tiles use one group per stage
+  pl.mode = gated ? kModeGateUp : ((kt % 2 == 0 && pl.ntok <= 64) ? kModeKPair : kModePlain);
+  const int n_stages = kt / (pl.mode == kModeKPair ? 2 : 1);
+  pl.splits = (pl.offset && rows < (1 << 20)) ? choose_splits(rows, num_experts, nt, n_stages, sm_count()) : 1;
+  return pl;
+}
+}  // namespace
+
 extern "C" {
 
 /* Debug aid (not in the public header's hot path): per-stage clock64 timeline of CTA 0 of every
@@ -843,16 +937,27 @@ int w4a16_pick_ntok(int64_t rows, int64_t num_experts) {
 
 int64_t w4a16_group_sums_ld(int64_t rows) { return (rows + 1) & ~int64_t(1); }
 
-int w4a16_grouped_gemm(const void* x, int64_t rows, int64_t K, const uint8_t* wblocks, int64_t num_experts,
-                       int64_t n_out, int gated, const int32_t* expert_counts, const int32_t* expert_offsets,
-                       const float* xsum, void* out, int dtype, int ntok, cudaStream_t stream) {
+
+int64_t w4a16_grouped_gemm_ws_bytes(int64_t rows, int64_t K, int64_t num_experts, int64_t n_out, int gated,
+                                    int ntok) {
+  if (rows <= 0 || K % kTileK || n_out % kTileRows || num_experts <= 0) return 0;
+  const GemmPlan pl = plan_gemm(rows, K, num_experts, n_out, gated, true, ntok);
+  return pl.splits > 1 ? static_cast<int64_t>(pl.splits) * rows * (gated ? 2 : 1) * n_out * 4 : 0;
+}
+
+int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t* wblocks, int64_t num_experts,
+                          int64_t n_out, int gated, const int32_t* expert_counts, const int32_t* expert_offsets,
+                          const float* xsum, void* out, int dtype, int ntok, void* ws, int64_t ws_bytes,
+                          cudaStream_t stream) {
   if (!x || !wblocks || !expert_counts || !expert_offsets || !out) return W4_ERR_ARG;
   if (K <= 0 || K % kTileK || n_out <= 0 || n_out % kTileRows) return W4_ERR_SHAPE;
   if (num_experts <= 0 || num_experts > kMaxExperts) return W4_ERR_SHAPE;
   if (dtype != W4_DTYPE_F16 && dtype != W4_DTYPE_BF16) return W4_ERR_DTYPE;
   if (rows <= 0) return W4_OK;
-  if (ntok <= 0) ntok = w4a16_pick_ntok(rows, num_experts);
-  if (ntok != 16 && ntok != 32 && ntok != 64 && ntok != 128) return W4_ERR_ARG;
+  if (ntok != 0 && ntok != 16 && ntok != 32 && ntok != 64 && ntok != 128) return W4_ERR_ARG;
+  GemmPlan pl = plan_gemm(rows, K, num_experts, n_out, gated, xsum != nullptr, ntok);
+  const int64_t need = pl.splits > 1 ? static_cast<int64_t>(pl.splits) * rows * (gated ? 2 : 1) * n_out * 4 : 0;
+  if (pl.splits > 1 && (!ws || ws_bytes < need)) pl.splits = 1;  // no / too small workspace: no split-K
   GemmArgs a;
   a.wblocks = wblocks;
   a.expert_counts = expert_counts;
@@ -865,23 +970,43 @@ int w4a16_grouped_gemm(const void* x, int64_t rows, int64_t K, const uint8_t* wb
   a.xsum = xsum;
   a.sum_ld = w4a16_group_sums_ld(rows);
   a.rows = rows;
-  // k-pair (two k-groups per 17 KB stage) for decode tiles; at 64/128 tokens the X tile dominates a
-  // stage (64 KB for a k-pair at 128 tokens -> only 2 smem stages), so 128-token tiles use one group per stage
-  const int mode = gated ? kModeGateUp : ((a.kt % 2 == 0 && ntok <= 64) ? kModeKPair : kModePlain);
-  const bool offset = xsum != nullptr && ntok <= 32;
+  a.splits = pl.splits;
+  a.part = static_cast<float*>(ws);
+  a.part_ld = (gated ? 2 : 1) * n_out;
   // CTA pairs (cta_group::2) measured slower at decode token counts (an M=256 x N=16 MMA with 8-row B
   // halves executes ~4x slower than two M=128 ones): opt-in only (W4A16_PAIR=1)
-  const bool pair = a.nt % 2 == 0 && (offset ? pairs_enabled() : prefill_pairs_enabled());
+  const bool pair = pl.splits == 1 && a.nt % 2 == 0 && (pl.offset ? pairs_enabled() : prefill_pairs_enabled());
   const int grid = sm_count();
   const bool bf = dtype == W4_DTYPE_BF16;
-  if (mode == kModeGateUp)
-    return bf ? dispatch_ntok<kModeGateUp, true>(ntok, offset, pair, a, x, rows, K, grid, stream)
-              : dispatch_ntok<kModeGateUp, false>(ntok, offset, pair, a, x, rows, K, grid, stream);
-  if (mode == kModeKPair)
-    return bf ? dispatch_ntok<kModeKPair, true>(ntok, offset, pair, a, x, rows, K, grid, stream)
-              : dispatch_ntok<kModeKPair, false>(ntok, offset, pair, a, x, rows, K, grid, stream);
-  return bf ? dispatch_ntok<kModePlain, true>(ntok, offset, pair, a, x, rows, K, grid, stream)
-            : dispatch_ntok<kModePlain, false>(ntok, offset, pair, a, x, rows, K, grid, stream);
+  int rc;
+  if (pl.mode == kModeGateUp)
+    rc = bf ? dispatch_ntok<kModeGateUp, true>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream)
+            : dispatch_ntok<kModeGateUp, false>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream);
+  else if (pl.mode == kModeKPair)
+    rc = bf ? dispatch_ntok<kModeKPair, true>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream)
+            : dispatch_ntok<kModeKPair, false>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream);
+  else
+    rc = bf ? dispatch_ntok<kModePlain, true>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream)
+            : dispatch_ntok<kModePlain, false>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream);
+  if (rc != W4_OK || pl.splits == 1) return rc;
+  const int thr = 128;
+  const dim3 fgrid(static_cast<unsigned>((n_out / 4 + thr - 1) / thr), static_cast<unsigned>(rows));
+  auto* o = static_cast<uint16_t*>(out);
+  const int32_t* lim = expert_offsets + num_experts;
+  if (gated)
+    bf ? splitk_finalize_kernel<true, true><<<fgrid, thr, 0, stream>>>(a.part, pl.splits, rows, n_out, lim, o)
+       : splitk_finalize_kernel<false, true><<<fgrid, thr, 0, stream>>>(a.part, pl.splits, rows, n_out, lim, o);
+  else
+    bf ? splitk_finalize_kernel<true, false><<<fgrid, thr, 0, stream>>>(a.part, pl.splits, rows, n_out, lim, o)
+       : splitk_finalize_kernel<false, false><<<fgrid, thr, 0, stream>>>(a.part, pl.splits, rows, n_out, lim, o);
+  return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
+}
+
+int w4a16_grouped_gemm(const void* x, int64_t rows, int64_t K, const uint8_t* wblocks, int64_t num_experts,
+                       int64_t n_out, int gated, const int32_t* expert_counts, const int32_t* expert_offsets,
+                       const float* xsum, void* out, int dtype, int ntok, cudaStream_t stream) {
+  return w4a16_grouped_gemm_ws(x, rows, K, wblocks, num_experts, n_out, gated, expert_counts, expert_offsets, xsum,
+                               out, dtype, ntok, nullptr, 0, stream);
 }
 
 int w4a16_dequant(const uint8_t* wblocks, int64_t num_experts, int64_t n_rows, int64_t K, int parts, int dtype,

@@ -130,16 +130,20 @@ def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, 
                                          sums=_ws.get("xs", ops.sums_shape(P, H), torch.float32, dev))
         else:
             xp, xs = ops.moe_gather(x, sorted_pairs, k, P, offsets[E:], out=xp_buf), None
+    def splitk_ws(K: int, n_out: int, gated: bool):
+        b = ops.gemm_ws_bytes(P, K, E, n_out, gated, nt) if decode else 0
+        return _ws.get("splitk", (b,), torch.uint8, dev) if b else None
+
     with tm.span("gemm_gate_up"):
         h = ops.grouped_gemm(xp, weights.w13.blocks, E, I, True, counts, offsets, nt,
-                             out=_ws.get("h", (P, I), x.dtype, dev), xsum=xs)
+                             out=_ws.get("h", (P, I), x.dtype, dev), xsum=xs, workspace=splitk_ws(H, I, True))
     hs = None
     if decode:
         with tm.span("sums_h"):
             hs = ops.group_sums(h, offsets[E:], out=_ws.get("hs", ops.sums_shape(P, I), torch.float32, dev))
     with tm.span("gemm_down"):
         yp = ops.grouped_gemm(h, weights.w2.blocks, E, H, False, counts, offsets, nt,
-                              out=_ws.get("yp", (P, H), x.dtype, dev), xsum=hs)
+                              out=_ws.get("yp", (P, H), x.dtype, dev), xsum=hs, workspace=splitk_ws(I, H, False))
     with tm.span("combine"):
         return ops.moe_combine(yp, pair_pos, topk_weights)
 

@@ -130,7 +130,7 @@ def test_group_sums(dt):
 
 
 # ------------------------------------------------------------------------------------------- grouped GEMM
-def _gemm_case(dt, gated, counts, K, N, ntok, seed=0, sums=False):
+def _gemm_case(dt, gated, counts, K, N, ntok, seed=0, sums=False, splitk=False):
     rng = np.random.default_rng(seed)
     E = len(counts)
     rows = int(sum(counts))
@@ -142,8 +142,13 @@ def _gemm_case(dt, gated, counts, K, N, ntok, seed=0, sums=False):
     np.cumsum(cnt, out=off[1:])
     xd = _to_dev_act(x, dt)
     xs = _ops().group_sums(xd) if sums else None
+    ws = None
+    if splitk:
+        wsb = _ops().gemm_ws_bytes(rows, K, E, N, gated, ntok)
+        assert wsb > 0, "expected a split-K plan"
+        ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
     out = _ops().grouped_gemm(xd, w.blocks, E, N, gated, torch.from_numpy(cnt).cuda(),
-                              torch.from_numpy(off).cuda(), ntok, xsum=xs)
+                              torch.from_numpy(off).cuda(), ntok, xsum=xs, workspace=ws)
     torch.cuda.synchronize()
     want = O.grouped_gemm(x, O.dequant(q, z, s, dt), cnt, off, dt, gated)
     return _from_dev_act(out, dt), want
@@ -174,6 +179,16 @@ def test_grouped_gemm_ring_wrap(gated, sums):
     counts = list(rng.integers(1, 5, size=40))
     got, want = _gemm_case("f16", gated, counts, K=2048, N=1024, ntok=16, seed=12, sums=sums)
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
+@pytest.mark.parametrize("gated,K,N", [(True, 2048, 1024), (False, 4096, 512), (False, 1920, 256)])
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+def test_grouped_gemm_splitk(gated, K, N, dt):
+    """Few tiles (1-2 experts, a few tokens): the decode GEMM splits K over CTAs into fp32 partials
+    and a finalize kernel (k-pair, gated and plain block modes)."""
+    got, want = _gemm_case(dt, gated, [2, 0, 3] if gated else [1, 2], K=K, N=N, ntok=16, seed=8, sums=True,
+                           splitk=True)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=(2 if dt == "bf16" else 1) * ATOL)
 
 
 def test_grouped_gemm_decode_shapes():

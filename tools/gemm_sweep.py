@@ -12,11 +12,12 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
+E_DS = K_DS = H_DS = I_DS = 0  # layer shape, set from --model
 
 
 def main():
     import torch
-    from bench import E_DS, K_DS, H_DS, I_DS, w_bytes
+    from bench import w_bytes
     from paper_2504_16214_b200.moe import moe_w4a16, random_moe_weights, select_experts
     from paper_2504_16214_b200.moe.layer import KernelTimer
     ap = argparse.ArgumentParser()
@@ -24,7 +25,11 @@ def main():
     ap.add_argument("--ntok", default="0")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--dtype", default="f16")
+    ap.add_argument("--model", default="ds", choices=["ds", "mixtral", "qwen3"])
     a = ap.parse_args()
+    global E_DS, K_DS, H_DS, I_DS
+    E_DS, K_DS, H_DS, I_DS = {"ds": (256, 8, 7168, 2048), "mixtral": (8, 2, 4096, 14336),
+                              "qwen3": (128, 8, 2048, 768)}[a.model]
     dev = torch.device("cuda", 0)
     tdt = torch.float16 if a.dtype == "f16" else torch.bfloat16
     w = random_moe_weights(E_DS, H_DS, I_DS, tdt, device=dev, seed=7)
