@@ -13,57 +13,51 @@
 namespace w4 {
 
 // ---------------------------------------------------------------------------------------- top-k
-// One warp per token; lane l holds logits l, l+32, ... (E <= 1024, k <= 32).
+// One warp per token; lane l holds logits l, l+32, ... (kPer per lane = power of two >= E/32, padded
+// with -inf). Selection compares raw logits (softmax / sigmoid are monotone), ties -> lower expert id.
+template <int kPer>
 __global__ void route_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int scoring, int renorm,
                                   int32_t* __restrict__ ids, float* __restrict__ wts) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= T) return;
   const float* row = logits + static_cast<int64_t>(warp) * E;
-  constexpr int kMaxPer = 32;
-  float v[kMaxPer];
-  const int per = (E + 31) / 32;
+  float v[kPer];
   float mx = -INFINITY;
 #pragma unroll
-  for (int i = 0; i < kMaxPer; ++i) {
-    if (i < per) {
-      const int e = lane + 32 * i;
-      v[i] = e < E ? row[e] : -INFINITY;
-      mx = fmaxf(mx, v[i]);
-    }
+  for (int i = 0; i < kPer; ++i) {
+    const int e = lane + 32 * i;
+    v[i] = e < E ? __ldg(row + e) : -INFINITY;
+    mx = fmaxf(mx, v[i]);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   float denom = 0.f;
   if (scoring == W4_SCORE_SOFTMAX) {
 #pragma unroll
-    for (int i = 0; i < kMaxPer; ++i)
-      if (i < per && lane + 32 * i < E) denom += expf(v[i] - mx);
+    for (int i = 0; i < kPer; ++i) denom += lane + 32 * i < E ? __expf(v[i] - mx) : 0.f;
 #pragma unroll
     for (int o = 16; o; o >>= 1) denom += __shfl_xor_sync(0xffffffffu, denom, o);
   }
-  uint32_t taken = 0;  // bit i: v[i] already selected
-  float sel_sum = 0.f;
-  float my_w = 0.f;
+  float sel_sum = 0.f, my_w = 0.f;
   int my_id = 0;
+  uint32_t taken = 0;  // bit i: v[i] already selected (explicit, so -inf logits stay selectable once)
   for (int j = 0; j < k; ++j) {
     float best = -INFINITY;
     int bidx = 0x7fffffff;
 #pragma unroll
-    for (int i = 0; i < kMaxPer; ++i) {
+    for (int i = 0; i < kPer; ++i) {  // lane-local best; ascending i = ascending expert id
       const int e = lane + 32 * i;
-      if (i < per && e < E && !((taken >> i) & 1u)) {
-        if (v[i] > best || (v[i] == best && e < bidx) || bidx == 0x7fffffff) { best = v[i]; bidx = e; }
-      }
+      if (e < E && !((taken >> i) & 1u) && (bidx == 0x7fffffff || v[i] > best)) { best = v[i]; bidx = e; }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       const float ob = __shfl_xor_sync(0xffffffffu, best, o);
       const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
-      if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+      if (oi != 0x7fffffff && (bidx == 0x7fffffff || ob > best || (ob == best && oi < bidx))) { best = ob; bidx = oi; }
     }
     if ((bidx & 31) == lane) taken |= 1u << (bidx >> 5);
-    const float w = scoring == W4_SCORE_SOFTMAX ? expf(best - mx) / denom : 1.0f / (1.0f + expf(-best));
+    const float w = scoring == W4_SCORE_SOFTMAX ? __expf(best - mx) / denom : 1.0f / (1.0f + __expf(-best));
     sel_sum += w;
     if (lane == j) { my_w = w; my_id = bidx; }
   }
@@ -403,10 +397,19 @@ int w4a16_route_topk(const float* logits, int64_t T, int64_t E, int64_t k, int s
   if (E <= 0 || E > 1024 || k <= 0 || k > 32 || k > E) return W4_ERR_SHAPE;
   if (scoring != W4_SCORE_SOFTMAX && scoring != W4_SCORE_SIGMOID) return W4_ERR_ARG;
   if (T <= 0) return W4_OK;
-  const int thr = 256;
+  const int thr = 128;
   const int64_t blocks = (T * 32 + thr - 1) / thr;
-  route_topk_kernel<<<blocks, thr, 0, stream>>>(logits, (int)T, (int)E, (int)k, scoring, renormalize, topk_ids,
-                                                topk_weights);
+  const int per = static_cast<int>((E + 31) / 32);
+#define W4_ROUTE(P)                                                                                             \
+  route_topk_kernel<P><<<blocks, thr, 0, stream>>>(logits, (int)T, (int)E, (int)k, scoring, renormalize, topk_ids, \
+                                                   topk_weights)
+  if (per <= 1) W4_ROUTE(1);
+  else if (per <= 2) W4_ROUTE(2);
+  else if (per <= 4) W4_ROUTE(4);
+  else if (per <= 8) W4_ROUTE(8);
+  else if (per <= 16) W4_ROUTE(16);
+  else W4_ROUTE(32);
+#undef W4_ROUTE
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
 

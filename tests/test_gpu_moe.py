@@ -64,6 +64,9 @@ def test_route_topk(scoring, renorm, E, k):
     lg = rng.standard_normal((T, E)).astype(np.float32)
     lg[3, :] = 0.25                                  # all tied -> ids 0..k-1
     lg[5, E // 2] = lg[5, E // 3] = lg[5].max() + 1  # tie at the top
+    lg[7, 1::2] = -np.inf                            # masked experts (half the row)
+    lg[8, :] = -np.inf                               # fully masked row: ties -> ids 0..k-1 ...
+    lg[8, :k] = 0.0                                  # ... except k finite ones
     ids, w = _ops().route_topk(torch.from_numpy(lg).cuda(), k, scoring, renorm)
     rid, rw = O.route_topk(lg, k, scoring, renorm)
     assert np.array_equal(ids.cpu().numpy(), rid)
