@@ -1,0 +1,36 @@
+// Kernel launches with Programmatic Dependent Launch (PDL): each hot-path kernel is launched with
+// programmatic stream serialization, so its launch and prologue (TMEM allocation, barrier init,
+// descriptor prefetch) overlap the tail of the previous kernel in the stream; the kernel executes
+// griddep_wait() before it reads anything the previous kernel wrote. W4A16_NO_PDL=1 disables it.
+#pragma once
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+namespace w4 {
+
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("W4A16_NO_PDL");
+    return !(e && atoi(e) != 0);
+  }();
+  return on;
+}
+
+template <typename Kern, typename... Args>
+cudaError_t launch_pdl(Kern kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+}  // namespace w4

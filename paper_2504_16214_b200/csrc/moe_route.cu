@@ -8,6 +8,7 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 #include "ptx.cuh"
+#include "launch.cuh"
 #include "w4a16_moe.h"
 
 namespace w4 {
@@ -18,6 +19,7 @@ namespace w4 {
 template <int kPer>
 __global__ void route_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int scoring, int renorm,
                                   int32_t* __restrict__ ids, float* __restrict__ wts) {
+  griddep_wait();  // PDL: inputs written by the previous kernel in the stream
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= T) return;
@@ -79,6 +81,7 @@ __global__ void __launch_bounds__(kPermThreads, 1)
     moe_permute_kernel(const int32_t* __restrict__ ids, int P, int E, int32_t* __restrict__ counts,
                        int32_t* __restrict__ offsets, int32_t* __restrict__ sorted_pairs,
                        int32_t* __restrict__ pair_pos) {
+  griddep_wait();  // PDL: inputs written by the previous kernel in the stream
   extern __shared__ int sm[];
   int* cnt = sm;                     // [E]
   int* base = cnt + E;               // [E]
@@ -152,6 +155,7 @@ constexpr int kChunk = 2048;
 
 __global__ void __launch_bounds__(512) permute_hist_kernel(const int32_t* __restrict__ ids, int P, int E,
                                                            int32_t* __restrict__ ws) {
+  griddep_wait();  // PDL: inputs written by the previous kernel in the stream
   extern __shared__ int hist[];
   for (int e = threadIdx.x; e < E; e += blockDim.x) hist[e] = 0;
   __syncthreads();
@@ -168,6 +172,7 @@ __global__ void __launch_bounds__(512) permute_hist_kernel(const int32_t* __rest
 __global__ void __launch_bounds__(1024) permute_scan_kernel(int nb, int E, int32_t* __restrict__ ws,
                                                             int32_t* __restrict__ counts,
                                                             int32_t* __restrict__ offsets) {
+  griddep_wait();  // PDL: inputs written by the previous kernel in the stream
   __shared__ int wsum[32];
   const int e = threadIdx.x, lane = e & 31, warp = e >> 5;
   int total = 0;
@@ -209,6 +214,7 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int nb, int E, int32
 __global__ void __launch_bounds__(kPermThreads, 1)
     permute_scatter_kernel(const int32_t* __restrict__ ids, int P, int E, const int32_t* __restrict__ ws,
                            int32_t* __restrict__ sorted_pairs, int32_t* __restrict__ pair_pos) {
+  griddep_wait();  // PDL: inputs written by the previous kernel in the stream
   extern __shared__ int sm[];
   int* base = sm;                    // [E]
   int* wcnt = base + E;              // [kPermWarps][E]
@@ -252,6 +258,7 @@ __global__ void __launch_bounds__(kPermThreads, 1)
 __global__ void moe_gather_kernel(const uint4* __restrict__ x, int64_t hv, int topk,
                                   const int32_t* __restrict__ sorted_pairs, const int32_t* __restrict__ row_limit,
                                   uint4* __restrict__ xp) {
+  griddep_wait();  // PDL: inputs written by the previous kernel in the stream
   const int64_t p = blockIdx.x;
   if (row_limit && p >= __ldg(row_limit)) return;
   const int64_t t = __ldg(sorted_pairs + p) / topk;
@@ -291,6 +298,7 @@ template <bool kBF16, bool kGather>
 __global__ void group_sums_kernel(const uint4* __restrict__ x, int64_t hv, int topk,
                                   const int32_t* __restrict__ sorted_pairs, const int32_t* __restrict__ row_limit,
                                   uint4* __restrict__ xp, int64_t ld, float2* __restrict__ xsum) {
+  griddep_wait();  // PDL: inputs written by the previous kernel in the stream
   const int64_t p = blockIdx.x;
   if (row_limit && p >= __ldg(row_limit)) return;
   const uint4* src = kGather ? x + static_cast<int64_t>(__ldg(sorted_pairs + p) / topk) * hv : x + p * hv;
@@ -354,6 +362,7 @@ template <bool kBF16>
 __global__ void moe_combine_kernel(const uint4* __restrict__ yp, int64_t hv, int topk,
                                    const int32_t* __restrict__ pair_pos, const float* __restrict__ wts,
                                    uint4* __restrict__ y) {
+  griddep_wait();  // PDL: inputs written by the previous kernel in the stream
   const int64_t t = blockIdx.x;
   const int64_t i = static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x;
   constexpr int kMaxK = 32;
@@ -401,7 +410,7 @@ int w4a16_route_topk(const float* logits, int64_t T, int64_t E, int64_t k, int s
   const int64_t blocks = (T * 32 + thr - 1) / thr;
   const int per = static_cast<int>((E + 31) / 32);
 #define W4_ROUTE(P)                                                                                             \
-  route_topk_kernel<P><<<blocks, thr, 0, stream>>>(logits, (int)T, (int)E, (int)k, scoring, renormalize, topk_ids, \
+  launch_pdl(route_topk_kernel<P>, blocks, thr, 0, stream, logits, (int)T, (int)E, (int)k, scoring, renormalize, topk_ids, \
                                                    topk_weights)
   if (per <= 1) W4_ROUTE(1);
   else if (per <= 2) W4_ROUTE(2);
@@ -425,7 +434,7 @@ int w4a16_moe_permute(const int32_t* topk_ids, int64_t P, int64_t E, int32_t* ex
       return W4_ERR_CUDA;
     attr = true;
   }
-  moe_permute_kernel<<<1, kPermThreads, smem, stream>>>(topk_ids, (int)P, (int)E, expert_counts, expert_offsets,
+  launch_pdl(moe_permute_kernel, 1, kPermThreads, smem, stream, topk_ids, (int)P, (int)E, expert_counts, expert_offsets,
                                                          sorted_pairs, pair_pos);
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
@@ -450,9 +459,9 @@ int w4a16_moe_permute_ws(const int32_t* topk_ids, int64_t P, int64_t E, int32_t*
       return W4_ERR_CUDA;
     attr = true;
   }
-  permute_hist_kernel<<<nb, 512, sizeof(int) * E, stream>>>(topk_ids, (int)P, (int)E, w);
-  permute_scan_kernel<<<1, 1024, 0, stream>>>(nb, (int)E, w, expert_counts, expert_offsets);
-  permute_scatter_kernel<<<nb, kPermThreads, sizeof(int) * (E + kPermWarps * E), stream>>>(
+  launch_pdl(permute_hist_kernel, nb, 512, sizeof(int) * E, stream, topk_ids, (int)P, (int)E, w);
+  launch_pdl(permute_scan_kernel, 1, 1024, 0, stream, nb, (int)E, w, expert_counts, expert_offsets);
+  launch_pdl(permute_scatter_kernel, nb, kPermThreads, sizeof(int) * (E + kPermWarps * E), stream, 
       topk_ids, (int)P, (int)E, w, sorted_pairs, pair_pos);
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
@@ -462,7 +471,7 @@ int w4a16_moe_gather(const void* x, int64_t H, int64_t topk, const int32_t* sort
   if (!x || !sorted_pairs || !x_perm) return W4_ERR_ARG;
   if (H <= 0 || H % 8 || topk <= 0) return W4_ERR_SHAPE;
   if (rows <= 0) return W4_OK;
-  moe_gather_kernel<<<rows, 128, 0, stream>>>(static_cast<const uint4*>(x), H / 8, (int)topk, sorted_pairs,
+  launch_pdl(moe_gather_kernel, rows, 128, 0, stream, static_cast<const uint4*>(x), H / 8, (int)topk, sorted_pairs,
                                                row_limit, static_cast<uint4*>(x_perm));
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
@@ -475,10 +484,10 @@ int w4a16_moe_gather_sums(const void* x, int64_t H, int64_t topk, const int32_t*
   const int64_t ld = w4a16_group_sums_ld(rows);
   auto* xs = reinterpret_cast<float2*>(xsum);
   if (dtype == W4_DTYPE_BF16)
-    group_sums_kernel<true, true><<<rows, 128, 0, stream>>>(static_cast<const uint4*>(x), H / 8, (int)topk,
+    launch_pdl(group_sums_kernel<true, true>, rows, 128, 0, stream, static_cast<const uint4*>(x), H / 8, (int)topk,
                                                             sorted_pairs, row_limit, static_cast<uint4*>(x_perm), ld, xs);
   else if (dtype == W4_DTYPE_F16)
-    group_sums_kernel<false, true><<<rows, 128, 0, stream>>>(static_cast<const uint4*>(x), H / 8, (int)topk,
+    launch_pdl(group_sums_kernel<false, true>, rows, 128, 0, stream, static_cast<const uint4*>(x), H / 8, (int)topk,
                                                              sorted_pairs, row_limit, static_cast<uint4*>(x_perm), ld, xs);
   else
     return W4_ERR_DTYPE;
@@ -493,10 +502,10 @@ int w4a16_group_sums(const void* x, int64_t rows, int64_t K, const int32_t* row_
   const int64_t ld = w4a16_group_sums_ld(rows);
   auto* xs = reinterpret_cast<float2*>(xsum);
   if (dtype == W4_DTYPE_BF16)
-    group_sums_kernel<true, false><<<rows, 128, 0, stream>>>(static_cast<const uint4*>(x), K / 8, 1, nullptr,
+    launch_pdl(group_sums_kernel<true, false>, rows, 128, 0, stream, static_cast<const uint4*>(x), K / 8, 1, nullptr,
                                                              row_limit, nullptr, ld, xs);
   else if (dtype == W4_DTYPE_F16)
-    group_sums_kernel<false, false><<<rows, 128, 0, stream>>>(static_cast<const uint4*>(x), K / 8, 1, nullptr,
+    launch_pdl(group_sums_kernel<false, false>, rows, 128, 0, stream, static_cast<const uint4*>(x), K / 8, 1, nullptr,
                                                               row_limit, nullptr, ld, xs);
   else
     return W4_ERR_DTYPE;
@@ -511,10 +520,10 @@ int w4a16_moe_combine(const void* y_perm, int64_t T, int64_t H, int64_t topk, co
   const int thr = 128;
   const dim3 grid(static_cast<unsigned>(T), static_cast<unsigned>((H / 8 + thr - 1) / thr));
   if (dtype == W4_DTYPE_BF16)
-    moe_combine_kernel<true><<<grid, thr, 0, stream>>>(static_cast<const uint4*>(y_perm), H / 8, (int)topk,
+    launch_pdl(moe_combine_kernel<true>, grid, thr, 0, stream, static_cast<const uint4*>(y_perm), H / 8, (int)topk,
                                                        pair_pos, topk_weights, static_cast<uint4*>(y));
   else if (dtype == W4_DTYPE_F16)
-    moe_combine_kernel<false><<<grid, thr, 0, stream>>>(static_cast<const uint4*>(y_perm), H / 8, (int)topk,
+    launch_pdl(moe_combine_kernel<false>, grid, thr, 0, stream, static_cast<const uint4*>(y_perm), H / 8, (int)topk,
                                                         pair_pos, topk_weights, static_cast<uint4*>(y));
   else
     return W4_ERR_DTYPE;

@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include "ptx.cuh"
+#include "launch.cuh"
 #include "w4_format.cuh"
 #include "mma_stage.cuh"
 #include "w4a16_moe.h"
@@ -267,6 +268,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     for (int i = 0; i < C::kNumAcc; ++i) { mbar_init(&accfull[i], 1); mbar_init(&accempty[i], C::kAccEmptyArrivals); }
     fence_mbar_init();
   } else if (warp == 2) {
+    // PDL: TMEM allocation and barrier init above overlap the previous kernel; expert counts / X / sums
+    // are its outputs. Other roles touch them only after the __syncthreads below.
+    griddep_wait();
     // m-tile prefix over experts (E <= 1024): each lane scans a contiguous slice, then a warp scan.
     const int E = args.num_experts;
     const int per = (E + 31) / 32;
@@ -653,6 +657,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 template <bool kBF16, bool kGated>
 __global__ void splitk_finalize_kernel(const float* __restrict__ part, int splits, int64_t rows, int64_t n_out,
                                        const int32_t* __restrict__ row_limit, uint16_t* __restrict__ out) {
+  griddep_wait();  // PDL
   const int64_t r = blockIdx.y;
   if (r >= __ldg(row_limit)) return;
   const int64_t n = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
@@ -817,13 +822,20 @@ int launch_gemm(const GemmArgs& a, const void* x, int64_t rows, int64_t K, int g
   cfg.blockDim = dim3(kNumThreads);
   cfg.dynamicSmemBytes = C::kSmemBytes;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = kPair ? 2 : 1;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  if (kPair) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 2;
+    at[na].val.clusterDim.y = 1;
+    at[na++].val.clusterDim.z = 1;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = kPair ? 1 : 0;
+  cfg.numAttrs = na;
   if (cudaLaunchKernelEx(&cfg, kern, a, map) != cudaSuccess) return W4_ERR_CUDA;
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
@@ -994,11 +1006,11 @@ int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t*
   auto* o = static_cast<uint16_t*>(out);
   const int32_t* lim = expert_offsets + num_experts;
   if (gated)
-    bf ? splitk_finalize_kernel<true, true><<<fgrid, thr, 0, stream>>>(a.part, pl.splits, rows, n_out, lim, o)
-       : splitk_finalize_kernel<false, true><<<fgrid, thr, 0, stream>>>(a.part, pl.splits, rows, n_out, lim, o);
+    bf ? launch_pdl(splitk_finalize_kernel<true, true>, fgrid, thr, 0, stream, a.part, pl.splits, rows, n_out, lim, o)
+       : launch_pdl(splitk_finalize_kernel<false, true>, fgrid, thr, 0, stream, a.part, pl.splits, rows, n_out, lim, o);
   else
-    bf ? splitk_finalize_kernel<true, false><<<fgrid, thr, 0, stream>>>(a.part, pl.splits, rows, n_out, lim, o)
-       : splitk_finalize_kernel<false, false><<<fgrid, thr, 0, stream>>>(a.part, pl.splits, rows, n_out, lim, o);
+    bf ? launch_pdl(splitk_finalize_kernel<true, false>, fgrid, thr, 0, stream, a.part, pl.splits, rows, n_out, lim, o)
+       : launch_pdl(splitk_finalize_kernel<false, false>, fgrid, thr, 0, stream, a.part, pl.splits, rows, n_out, lim, o);
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
 
