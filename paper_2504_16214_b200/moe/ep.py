@@ -65,7 +65,8 @@ class CudaBackend:
         tm = timer or _NOTIMER
         E, H, I = weights.num_experts, weights.hidden, weights.inter
         nt = ntok or cuda_ops.pick_ntok(x.shape[0], E)
-        decode = nt <= 32
+        from .layer import _DECODE_MAX_NTOK
+        decode = nt <= _DECODE_MAX_NTOK
         xs = cuda_ops.group_sums(x) if decode else None
         with tm.span("gemm_gate_up"):
             h = cuda_ops.grouped_gemm(x, weights.w13.blocks, E, I, True, counts, offsets, nt, xsum=xs)

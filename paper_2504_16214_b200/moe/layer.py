@@ -48,6 +48,8 @@ class _Workspace:
 
 
 _ws = _Workspace()
+# largest token tile that runs the offset-code (decode) GEMM; larger tiles dequantise with the scale
+_DECODE_MAX_NTOK = int(__import__("os").environ.get("W4A16_DECODE_MAX_NTOK", "16"))
 
 
 class KernelTimer:
@@ -122,7 +124,7 @@ def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, 
         counts, offsets, sorted_pairs, pair_pos = ops.moe_permute(
             topk_ids, E, _ws.get("perm_ws", (max(ops.permute_ws_bytes(P, E), 1),), torch.uint8, dev))
     nt = ntok or ops.pick_ntok(P, E)
-    decode = nt <= 32  # offset-code GEMMs: per-group activation sums ride along with X and h
+    decode = nt <= _DECODE_MAX_NTOK  # offset-code GEMMs: per-group activation sums ride along with X and h
     with tm.span("gather"):
         xp_buf = _ws.get("xp", (P, H), x.dtype, dev)
         if decode:
@@ -197,5 +199,5 @@ def w4a16_linear(x: torch.Tensor, w, ntok: int = 0) -> torch.Tensor:
     offsets = torch.tensor([0, M], dtype=torch.int32, device=dev)
     nt = ntok or ops.pick_ntok(M, 1)
     x = x.contiguous()
-    xs = ops.group_sums(x) if nt <= 32 else None
+    xs = ops.group_sums(x) if nt <= _DECODE_MAX_NTOK else None
     return ops.grouped_gemm(x, w.blocks, 1, w.n_rows, False, counts, offsets, nt, xsum=xs)
