@@ -227,6 +227,85 @@ def run_reference(args):
 
 
 # --------------------------------------------------------------------------------------------- GPU
+def _graph_ms(fn, reps: int = 10) -> float:
+    """Device ms per call of fn captured once in a CUDA graph (warm-up, capture, timed replays)."""
+    import torch
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(2):
+            fn()
+    torch.cuda.current_stream().wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def other_configs(dev, hbm_peak: float, tc_peak: float):
+    """BASELINE.json configs 2, 3, 5 on one GPU (graphed; synthetic weights of the named shapes):
+    the dense Llama-3-8B W4A16 linear and the Mixtral-8x7B / Qwen3-30B-A3B MoE layers."""
+    import torch
+    from paper_2504_16214_b200.moe import FusedMoEGraph, random_moe_weights, select_experts, w4a16_linear
+    from paper_2504_16214_b200.moe.weights import random_packed
+    out = {}
+    g = torch.Generator().manual_seed(3)
+    gd = torch.Generator(device=dev).manual_seed(3)
+    # config 2: dense K=4096, N=14336
+    w = random_packed(1, 14336, 4096, False, torch.float16, gd, dev)
+    rows = []
+    for M in (1, 16, 256, 4096):
+        x = (torch.randn((M, 4096), generator=g) * 0.5).half().to(dev)
+        w4a16_linear(x, w)  # eager first call: cached routing tensors, workspace
+        torch.cuda.synchronize()
+        ms = _graph_ms(lambda: w4a16_linear(x, w))
+        by, fl = w_bytes(14336, 4096) + 2 * M * (4096 + 14336), 2 * M * 4096 * 14336
+        rows.append({"M": M, "ms": round(ms, 4), "GB/s": round(by / ms / 1e6, 1), "TFLOP/s": round(fl / ms / 1e9, 2),
+                     "hbm_frac": round(by / ms / 1e6 / hbm_peak, 4), "tc_frac": round(fl / ms / 1e9 / tc_peak, 4)})
+    out["llama3_8b_dense_K4096_N14336"] = rows
+    del w
+    # configs 3 and 5: MoE layers
+    for name, (E, k, H, I), Ts in (("mixtral_8x7b", (8, 2, 4096, 14336), (1, 16, 256, 1024, 8192)),
+                                   ("qwen3_30b_a3b", (128, 8, 2048, 768), (1, 16, 256, 1024, 8192))):
+        wm = random_moe_weights(E, H, I, torch.float16, device=dev, seed=4)
+        rows = []
+        for T in Ts:
+            x = (torch.randn((T, H), generator=g) * 0.5).half().to(dev)
+            lg = torch.randn((T, E), generator=g).to(dev)
+            _, ids = select_experts(lg, k, "softmax", True)
+            et = int(torch.unique(ids).numel())
+            gr = FusedMoEGraph(wm, T, k, "softmax", True, torch.float16, dev)
+            gr(x, lg)
+            for _ in range(3):
+                gr()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(10):
+                gr()
+            b.record()
+            torch.cuda.synchronize()
+            ms = a.elapsed_time(b) / 10
+            by, fl = layer_bytes(et, T, H, I, k), layer_flops(T, k, H, I)
+            rows.append({"tokens": T, "experts_touched": et, "ms": round(ms, 4), "GB/s": round(by / ms / 1e6, 1),
+                         "TFLOP/s": round(fl / ms / 1e9, 2), "hbm_frac": round(by / ms / 1e6 / hbm_peak, 4),
+                         "tc_frac": round(fl / ms / 1e9 / tc_peak, 4)})
+            del gr
+        out[name] = rows
+        del wm
+        torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -424,6 +503,10 @@ def main():
                           "tc_frac_sustained": round(fl / sm / 1e9 / tc_sus, 4) if tc_sus else None})
             del xs, ls, gs_
 
+    configs = None
+    if world == 1 and not args.no_sweep and group is None:
+        configs = other_configs(dev, hbm_peak, tc_peak)
+
     cpu = None
     synth = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -453,6 +536,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "kernel_ms": {n: round(timer.mean_ms(n), 4) for n in timer.events},
             "sweep": sweep,
+            "other_configs": configs,
             "layout_synthesis_cpu": synth,
         }
         print(json.dumps(line))

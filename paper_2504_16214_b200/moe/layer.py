@@ -190,14 +190,23 @@ class FusedMoEGraph:
         return self.y
 
 
+_LINEAR_ROUTING: dict = {}
+
+
 def w4a16_linear(x: torch.Tensor, w, ntok: int = 0) -> torch.Tensor:
     """Dense W4A16 linear y = x @ W^T (one "expert"; BASELINE config 2). ``w`` is a PackedW4 with
     num_experts == 1 and parts == 1."""
     M, K = x.shape
     dev = x.device
-    counts = torch.tensor([M], dtype=torch.int32, device=dev)
-    offsets = torch.tensor([0, M], dtype=torch.int32, device=dev)
+    key = (M, str(dev))
+    if key not in _LINEAR_ROUTING:  # cached: no host->device copy per call (CUDA-graph capturable)
+        _LINEAR_ROUTING[key] = (torch.tensor([M], dtype=torch.int32, device=dev),
+                                torch.tensor([0, M], dtype=torch.int32, device=dev))
+    counts, offsets = _LINEAR_ROUTING[key]
     nt = ntok or ops.pick_ntok(M, 1)
     x = x.contiguous()
-    xs = ops.group_sums(x) if nt <= _DECODE_MAX_NTOK else None
-    return ops.grouped_gemm(x, w.blocks, 1, w.n_rows, False, counts, offsets, nt, xsum=xs)
+    decode = nt <= _DECODE_MAX_NTOK
+    xs = ops.group_sums(x) if decode else None
+    wsb = ops.gemm_ws_bytes(M, K, 1, w.n_rows, False, nt) if decode else 0
+    ws = _ws.get("linear_splitk", (wsb,), torch.uint8, dev) if wsb else None
+    return ops.grouped_gemm(x, w.blocks, 1, w.n_rows, False, counts, offsets, nt, xsum=xs, workspace=ws)

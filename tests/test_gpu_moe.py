@@ -206,6 +206,22 @@ def test_dense_w4a16_linear():
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
 
 
+@pytest.mark.parametrize("M", [1, 16, 200])
+def test_dense_w4a16_linear_llama_shape(M):
+    """BASELINE config 2: Llama-3-8B linear K=4096, N=14336 through the public dense entry point
+    (decode mode + split-K at small M, scale-in-dequant at larger M)."""
+    from paper_2504_16214_b200.moe import w4a16_linear
+    rng = np.random.default_rng(M)
+    N, K = 14336, 4096
+    q, z, s = O.synth_awq_expert_weights(rng, 1, N, K, "f16")
+    w = _packed(q, z, s, "f16", False)
+    x = O.round_act(rng.standard_normal((M, K)).astype(np.float32) * 0.5, "f16")
+    got = _from_dev_act(w4a16_linear(_to_dev_act(x, "f16"), w), "f16")
+    torch.cuda.synchronize()
+    want = O.round_act(x @ O.dequant(q, z, s, "f16")[0].T, "f16")
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
 # ------------------------------------------------------------------------------------------- layer
 @pytest.mark.parametrize("dt", ["f16", "bf16"])
 @pytest.mark.parametrize("T,E,k,H,I", [(1, 8, 2, 256, 384), (24, 16, 4, 512, 256), (130, 8, 2, 256, 256),
