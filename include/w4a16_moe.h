@@ -127,11 +127,12 @@ int w4a16_pick_ntok(int64_t rows, int64_t num_experts);
  * cannot fill the GPU (e.g. one token touching 8 experts): the k-groups of a tile are split over
  * several CTAs writing fp32 partials to ws, then summed (and SiLU*up applied) by a finalize kernel.
  * ws_bytes >= w4a16_grouped_gemm_ws_bytes(...) (0 when no split is planned); a smaller workspace
- * just disables split-K. */
+ * just disables split-K. osum (optional): also produce the output's group sums (w4a16_group_sums
+ * layout) -- the next GEMM's xsum; the decode gate/up epilogue computes them in place. */
 int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t* wblocks, int64_t num_experts,
                           int64_t n_out, int gated, const int32_t* expert_counts, const int32_t* expert_offsets,
-                          const float* xsum, void* out, int dtype, int ntok, void* ws, int64_t ws_bytes,
-                          cudaStream_t stream);
+                          const float* xsum, float* osum, void* out, int dtype, int ntok, void* ws,
+                          int64_t ws_bytes, cudaStream_t stream);
 int64_t w4a16_grouped_gemm_ws_bytes(int64_t rows, int64_t K, int64_t num_experts, int64_t n_out, int gated,
                                     int ntok);
 

@@ -572,12 +572,11 @@ int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E,
   } else if ((rc = w4a16_moe_gather(x, H, topk, sorted, P, offsets + E, xp, stream))) {
     return rc;
   }
-  if ((rc = w4a16_grouped_gemm_ws(xp, P, H, w13, E, I, 1, counts, offsets, decode ? xsum : nullptr, hp, dtype, nt,
-                                  kws, kws_bytes, stream)))
+  if ((rc = w4a16_grouped_gemm_ws(xp, P, H, w13, E, I, 1, counts, offsets, decode ? xsum : nullptr,
+                                  decode ? hsum : nullptr, hp, dtype, nt, kws, kws_bytes, stream)))
     return rc;
-  if (decode && (rc = w4a16_group_sums(hp, P, I, offsets + E, dtype, hsum, stream))) return rc;
-  if ((rc = w4a16_grouped_gemm_ws(hp, P, I, w2, E, H, 0, counts, offsets, decode ? hsum : nullptr, yp, dtype, nt,
-                                  kws, kws_bytes, stream)))
+  if ((rc = w4a16_grouped_gemm_ws(hp, P, I, w2, E, H, 0, counts, offsets, decode ? hsum : nullptr, nullptr, yp,
+                                  dtype, nt, kws, kws_bytes, stream)))
     return rc;
   return w4a16_moe_combine(yp, T, H, topk, pos, topk_weights, dtype, y, stream);
 }

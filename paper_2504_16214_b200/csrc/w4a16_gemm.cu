@@ -53,6 +53,7 @@ struct GemmArgs {
   int splits;                    // split-K factor (decode mode; 1 = none)
   float* part;                   // splits > 1: fp32 partials [splits][rows][part_ld]
   int64_t part_ld;               // (gated ? 2 : 1) * n_out
+  float2* osum;                  // gated decode: (C, S) sums of the output h [nt][sum_ld] (next GEMM's xsum)
 };
 
 // Numeric modes.
@@ -108,7 +109,8 @@ struct Cfg {
   static constexpr int kNumAcc = kNumAccO > (kOffset ? 4 : 2) ? (kOffset ? 4 : 2) : kNumAccO;
   static constexpr int kNumA = kNumA_;
   static constexpr int kStageBytes = kBlk + kXBytes + kSumBytes;
-  static constexpr int kFixed = 2048 + 4 * (kMaxExperts + 2) + 8 * kTileTab;  // barriers, m-tile prefix, tiles
+  // barriers, m-tile prefix, tile table, epilogue cross-warp reduction scratch (4 warps x 16 x float2)
+  static constexpr int kFixed = 2048 + 4 * (kMaxExperts + 2) + 8 * kTileTab + 512;
   static constexpr int kNS0 = (kSmemBudget - kFixed - 1024) / kStageBytes;
   static constexpr int kNS = kNS0 > 12 ? 12 : kNS0;
   static constexpr int kEmptyArrivals = kDequantGroup + 1 + (kOffset ? 4 : 0);
@@ -251,6 +253,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   int* mt_off = reinterpret_cast<int*>(bars + 256);
   uint2* tile_tab = reinterpret_cast<uint2*>(mt_off + kMaxExperts + 2);  // 8-byte aligned (odd int count + 1)
   int* n_tiles_sm = mt_off + kMaxExperts + 1;
+  float2* red_sm = reinterpret_cast<float2*>(tile_tab + kTileTab);  // [4 warps][16 tokens]
 
   const uint32_t warp = warp_idx();
   const uint32_t lane = lane_id();
@@ -588,13 +591,49 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             }
           }
         } else {
+          float hv[kNTok];  // the stored (rounded) outputs, for the fused sums below
 #pragma unroll
           for (int m = 0; m < kNTok; ++m) {
+            hv[m] = 0.f;
             if (m < m_rows) {
               float v;
               if constexpr (kGated) v = silu_f(a[0][m]) * a[1][m];
               else v = a[0][m];
-              obase[static_cast<int64_t>(m) * args.ldo] = to_act_bits<kBF16>(v);
+              const uint16_t bits = to_act_bits<kBF16>(v);
+              obase[static_cast<int64_t>(m) * args.ldo] = bits;
+              hv[m] = act_bits_to_float<kBF16>(bits);
+            }
+          }
+          if constexpr (kGated && kNTok <= 16) {
+            if (args.osum != nullptr) {
+              // The tile's 128 rows are exactly one k-group of the next (down) GEMM: its per-token
+              // (C, S) = (sum_r c_r h_r, sum_r h_r), c_r the decode offset of k = r (Dq::offset_bits).
+              const float cr = act_bits_to_float<kBF16>(Dq<kBF16>::offset_bits(row & 7));
+              const uint32_t ew = warp - kEpiWarp0;
+#pragma unroll
+              for (int m = 0; m < kNTok; ++m) {
+                if (m < m_rows) {  // warp-uniform
+                  float sc = cr * hv[m], ss = hv[m];
+#pragma unroll
+                  for (int o = 16; o; o >>= 1) {
+                    sc += __shfl_xor_sync(0xffffffffu, sc, o);
+                    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+                  }
+                  if (lane == 0) red_sm[ew * 16 + m] = make_float2(sc, ss);
+                }
+              }
+              named_bar_sync(1, 128);  // the 4 epilogue warps
+              if (ew == 0 && static_cast<int>(lane) < m_rows) {
+                float2 t = red_sm[lane];
+#pragma unroll
+                for (int w2 = 1; w2 < 4; ++w2) {
+                  const float2 u = red_sm[w2 * 16 + lane];
+                  t.x += u.x;
+                  t.y += u.y;
+                }
+                args.osum[static_cast<int64_t>(ti.n_tile) * args.sum_ld + ti.m_start + lane] = t;
+              }
+              named_bar_sync(1, 128);  // scratch reused by the next tile
             }
           }
         }
@@ -957,7 +996,7 @@ int64_t w4a16_grouped_gemm_ws_bytes(int64_t rows, int64_t K, int64_t num_experts
 
 int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t* wblocks, int64_t num_experts,
                           int64_t n_out, int gated, const int32_t* expert_counts, const int32_t* expert_offsets,
-                          const float* xsum, void* out, int dtype, int ntok, void* ws, int64_t ws_bytes,
+                          const float* xsum, float* osum, void* out, int dtype, int ntok, void* ws, int64_t ws_bytes,
                           cudaStream_t stream) {
   if (!x || !wblocks || !expert_counts || !expert_offsets || !out) return W4_ERR_ARG;
   if (K <= 0 || K % kTileK || n_out <= 0 || n_out % kTileRows) return W4_ERR_SHAPE;
@@ -983,6 +1022,9 @@ int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t*
   a.splits = pl.splits;
   a.part = static_cast<float*>(ws);
   a.part_ld = (gated ? 2 : 1) * n_out;
+  // the decode gate/up epilogue writes the output's group sums itself; otherwise a sums pass follows
+  const bool fused_osum = osum != nullptr && gated && pl.offset && pl.ntok <= 16 && pl.splits == 1;
+  a.osum = fused_osum ? reinterpret_cast<float2*>(osum) : nullptr;
   // CTA pairs (cta_group::2) measured slower at decode token counts (an M=256 x N=16 MMA with 8-row B
   // halves executes ~4x slower than two M=128 ones): opt-in only (W4A16_PAIR=1)
   const bool pair = pl.splits == 1 && a.nt % 2 == 0 && (pl.offset ? pairs_enabled() : prefill_pairs_enabled());
@@ -998,7 +1040,8 @@ int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t*
   else
     rc = bf ? dispatch_ntok<kModePlain, true>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream)
             : dispatch_ntok<kModePlain, false>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream);
-  if (rc != W4_OK || pl.splits == 1) return rc;
+  if (rc != W4_OK) return rc;
+  if (pl.splits > 1) {
   const int thr = 128;
   const dim3 fgrid(static_cast<unsigned>((n_out / 4 + thr - 1) / thr), static_cast<unsigned>(rows));
   auto* o = static_cast<uint16_t*>(out);
@@ -1009,14 +1052,18 @@ int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t*
   else
     bf ? launch_pdl(splitk_finalize_kernel<true, false>, fgrid, thr, 0, stream, a.part, pl.splits, rows, n_out, lim, o)
        : launch_pdl(splitk_finalize_kernel<false, false>, fgrid, thr, 0, stream, a.part, pl.splits, rows, n_out, lim, o);
-  return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
+    if (cudaGetLastError() != cudaSuccess) return W4_ERR_CUDA;
+  }
+  if (osum != nullptr && !fused_osum)
+    return w4a16_group_sums(out, rows, n_out, expert_offsets + num_experts, dtype, osum, stream);
+  return W4_OK;
 }
 
 int w4a16_grouped_gemm(const void* x, int64_t rows, int64_t K, const uint8_t* wblocks, int64_t num_experts,
                        int64_t n_out, int gated, const int32_t* expert_counts, const int32_t* expert_offsets,
                        const float* xsum, void* out, int dtype, int ntok, cudaStream_t stream) {
   return w4a16_grouped_gemm_ws(x, rows, K, wblocks, num_experts, n_out, gated, expert_counts, expert_offsets, xsum,
-                               out, dtype, ntok, nullptr, 0, stream);
+                               nullptr, out, dtype, ntok, nullptr, 0, stream);
 }
 
 int w4a16_dequant(const uint8_t* wblocks, int64_t num_experts, int64_t n_rows, int64_t K, int parts, int dtype,

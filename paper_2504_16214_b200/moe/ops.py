@@ -164,18 +164,19 @@ def moe_combine(y_perm: torch.Tensor, pair_pos: torch.Tensor, topk_weights: torc
 def grouped_gemm(x: torch.Tensor, blocks: torch.Tensor, num_experts: int, n_out: int, gated: bool,
                  expert_counts: torch.Tensor, expert_offsets: torch.Tensor, ntok: int = 0,
                  out: torch.Tensor | None = None, xsum: torch.Tensor | None = None,
-                 workspace: torch.Tensor | None = None) -> torch.Tensor:
+                 workspace: torch.Tensor | None = None, osum: torch.Tensor | None = None) -> torch.Tensor:
     """out[off_e + m] = act(x[off_e + m] @ W_e^T) (gated: silu(gate) * up), per expert. ``xsum``
     (group_sums / moe_gather_sums of x) selects the decode kernel for 16/32-token tiles; a
-    ``workspace`` of gemm_ws_bytes(...) bytes enables split-K when few tiles exist."""
+    ``workspace`` of gemm_ws_bytes(...) bytes enables split-K when few tiles exist; ``osum`` (shape
+    sums_shape(rows, n_out)) receives the output's group sums (the next GEMM's xsum)."""
     _need_cuda(x, blocks, expert_counts, expert_offsets)
     rows, K = x.shape
     if out is None:
         out = torch.empty((rows, n_out), dtype=x.dtype, device=x.device)
     wsb = 0 if workspace is None else workspace.numel() * workspace.element_size()
     _lib.call("w4a16_grouped_gemm_ws", x.data_ptr(), rows, K, blocks.data_ptr(), num_experts, n_out, int(gated),
-              expert_counts.data_ptr(), expert_offsets.data_ptr(), _ptr(xsum), out.data_ptr(), act_code(x.dtype),
-              ntok, _ptr(workspace), wsb, _stream())
+              expert_counts.data_ptr(), expert_offsets.data_ptr(), _ptr(xsum), _ptr(osum), out.data_ptr(),
+              act_code(x.dtype), ntok, _ptr(workspace), wsb, _stream())
     return out
 
 

@@ -194,6 +194,33 @@ def test_grouped_gemm_splitk(gated, K, N, dt):
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=(2 if dt == "bf16" else 1) * ATOL)
 
 
+@pytest.mark.parametrize("splitk", [False, True])
+def test_gate_up_output_sums(splitk):
+    """The gated GEMM also emits its output's (C, S) group sums (fused in the decode epilogue, or a
+    sums pass after split-K): equal to group_sums of the output."""
+    rng = np.random.default_rng(31)
+    E, N, K, dt = 3, 1024, 2048, "f16"
+    counts = [2, 0, 3] if splitk else [5, 16, 9]
+    q, z, s = O.synth_awq_expert_weights(rng, E, 2 * N, K, dt)
+    w = _packed(q, z, s, dt, True)
+    rows = int(sum(counts))
+    cnt = np.asarray(counts, np.int32)
+    off = np.zeros(E + 1, np.int32)
+    np.cumsum(cnt, out=off[1:])
+    xd = _to_dev_act(O.round_act(rng.standard_normal((rows, K)).astype(np.float32) * 0.5, dt), dt)
+    ops = _ops()
+    xs = ops.group_sums(xd)
+    hs = torch.full(ops.sums_shape(rows, N), float("nan"), dtype=torch.float32, device="cuda")
+    wsb = ops.gemm_ws_bytes(rows, K, E, N, True, 16)
+    assert wsb > 0  # few tiles: a split is planned; without a workspace the fused epilogue path runs
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda") if splitk else None
+    h = ops.grouped_gemm(xd, w.blocks, E, N, True, torch.from_numpy(cnt).cuda(), torch.from_numpy(off).cuda(), 16,
+                         xsum=xs, workspace=ws, osum=hs)
+    want = ops.group_sums(h).cpu().numpy()[:, :rows]
+    got = hs.cpu().numpy()[:, :rows]
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=2e-2)
+
+
 def test_grouped_gemm_decode_shapes():
     """DeepSeek-R1 down-projection shape (K=2048 -> 8 k-pair stages per tile) in decode mode."""
     got, want = _gemm_case("f16", False, [2, 1, 3, 0, 2], K=2048, N=512, ntok=16, seed=4, sums=True)
