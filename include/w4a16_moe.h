@@ -88,6 +88,13 @@ int w4a16_moe_permute_ws(const int32_t* topk_ids, int64_t P, int64_t E, int32_t*
                          int64_t ws_bytes, cudaStream_t stream);
 int64_t w4a16_moe_permute_ws_bytes(int64_t P, int64_t E);
 
+/* Expert parallelism, receiver side: rows arrive grouped by (source rank, local expert) with counts
+ * recv_counts [world][local_experts] (device). Produces the local-expert order, stable by source rank
+ * then arrival: l_counts [E_l], l_offsets [E_l+1], l_sorted [n] (arrival row of each expert-ordered
+ * row), l_pos [n] (expert-ordered position of each arrival row). world * E_l <= 4096. */
+int w4a16_ep_local_order(const int32_t* recv_counts, int64_t world, int64_t local_experts, int32_t* l_counts,
+                         int32_t* l_offsets, int32_t* l_sorted, int32_t* l_pos, cudaStream_t stream);
+
 /* X_perm[p][:] = x[sorted_pairs[p] / topk][:] for p < rows, and p < *row_limit when row_limit (a
  * device pointer, e.g. expert_offsets + E) is non-null -- rows past it are left untouched. */
 int w4a16_moe_gather(const void* x, int64_t H, int64_t topk, const int32_t* sorted_pairs, int64_t rows,
@@ -128,11 +135,13 @@ int w4a16_pick_ntok(int64_t rows, int64_t num_experts);
  * several CTAs writing fp32 partials to ws, then summed (and SiLU*up applied) by a finalize kernel.
  * ws_bytes >= w4a16_grouped_gemm_ws_bytes(...) (0 when no split is planned); a smaller workspace
  * just disables split-K. osum (optional): also produce the output's group sums (w4a16_group_sums
- * layout) -- the next GEMM's xsum; the decode gate/up epilogue computes them in place. */
+ * layout) -- the next GEMM's xsum; the decode gate/up epilogue computes them in place. out_rows
+ * (optional): row i of the result is written to out row out_rows[i] (e.g. straight back into
+ * expert-parallel arrival order); not combinable with osum. */
 int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t* wblocks, int64_t num_experts,
                           int64_t n_out, int gated, const int32_t* expert_counts, const int32_t* expert_offsets,
-                          const float* xsum, float* osum, void* out, int dtype, int ntok, void* ws,
-                          int64_t ws_bytes, cudaStream_t stream);
+                          const float* xsum, float* osum, const int32_t* out_rows, void* out, int dtype, int ntok,
+                          void* ws, int64_t ws_bytes, cudaStream_t stream);
 int64_t w4a16_grouped_gemm_ws_bytes(int64_t rows, int64_t K, int64_t num_experts, int64_t n_out, int gated,
                                     int ntok);
 

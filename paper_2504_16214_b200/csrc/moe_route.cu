@@ -253,6 +253,104 @@ __global__ void __launch_bounds__(kPermThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------- EP local order
+// Expert parallelism, receiver side: rows arrive grouped by (source rank r, local expert e) with
+// counts cnt[r][e]. Produce the local-expert order (stable by source rank, then arrival):
+// l_counts[e], l_offsets[E_l+1], l_sorted[p] = arrival row of expert-ordered row p, l_pos[i] = p.
+// One CTA; world * E_l <= kEpMaxCells.
+constexpr int kEpMaxCells = 4096;  // static smem: 2 x 16 KB of cell arrays
+
+__global__ void __launch_bounds__(1024) ep_local_order_kernel(const int32_t* __restrict__ recv_counts, int world,
+                                                              int el, int32_t* __restrict__ l_counts,
+                                                              int32_t* __restrict__ l_offsets,
+                                                              int32_t* __restrict__ l_sorted,
+                                                              int32_t* __restrict__ l_pos) {
+  griddep_wait();  // PDL
+  __shared__ int cnt[kEpMaxCells];
+  __shared__ int arr[kEpMaxCells];  // arrival offset of cell (r, e)
+  __shared__ int wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cells = world * el;
+  for (int c = tid; c < cells; c += 1024) cnt[c] = recv_counts[c];
+  __syncthreads();
+  // exclusive scan of cnt in flat (r, e) order -> arrival offsets: thread t owns cells
+  // [t*per, (t+1)*per), one block scan over the per-thread sums
+  {
+    const int per = (cells + 1023) / 1024;
+    const int beg = min(cells, tid * per), end = min(cells, beg + per);
+    int tsum = 0;
+    for (int c = beg; c < end; ++c) tsum += cnt[c];
+    int incl = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int w = wsum[lane];
+      int wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += t;
+      }
+      wsum[lane] = wi - w;
+    }
+    __syncthreads();
+    int run = incl - tsum + wsum[warp];
+    for (int c = beg; c < end; ++c) {
+      arr[c] = run;
+      run += cnt[c];
+    }
+    __syncthreads();
+  }
+  // per-expert totals and exclusive offsets (thread e), then per-(r, e) expert-order bases
+  __shared__ int loff[1024];
+  int lc = 0;
+  if (tid < el)
+    for (int r = 0; r < world; ++r) lc += cnt[r * el + tid];
+  int incl = lc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int w = wsum[lane];
+    int wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    wsum[lane] = wi - w;
+  }
+  __syncthreads();
+  if (tid < el) {
+    const int off = incl - lc + wsum[warp];
+    loff[tid] = off;
+    l_counts[tid] = lc;
+    l_offsets[tid] = off;
+    if (tid == el - 1) l_offsets[el] = off + lc;
+  }
+  __syncthreads();
+  // fill: warp w handles cells w, w+32, ...; expert-order base of (r, e) = loff[e] + sum_{r'<r} cnt[r'][e]
+  for (int c = warp; c < cells; c += 32) {
+    const int r = c / el, e = c - r * el;
+    int b = loff[e];
+    for (int r2 = 0; r2 < r; ++r2) b += cnt[r2 * el + e];
+    const int a0 = arr[c], n = cnt[c];
+    for (int j = lane; j < n; j += 32) {
+      l_sorted[b + j] = a0 + j;
+      l_pos[a0 + j] = b + j;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------------- gather
 // One CTA per permuted row, 128-bit vectors (H % 8 == 0).
 __global__ void moe_gather_kernel(const uint4* __restrict__ x, int64_t hv, int topk,
@@ -466,6 +564,16 @@ int w4a16_moe_permute_ws(const int32_t* topk_ids, int64_t P, int64_t E, int32_t*
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
 
+int w4a16_ep_local_order(const int32_t* recv_counts, int64_t world, int64_t local_experts, int32_t* l_counts,
+                         int32_t* l_offsets, int32_t* l_sorted, int32_t* l_pos, cudaStream_t stream) {
+  if (!recv_counts || !l_counts || !l_offsets || !l_sorted || !l_pos) return W4_ERR_ARG;
+  if (world <= 0 || local_experts <= 0 || local_experts > 1024 || world * local_experts > kEpMaxCells)
+    return W4_ERR_SHAPE;
+  launch_pdl(ep_local_order_kernel, 1, 1024, 0, stream, recv_counts, (int)world, (int)local_experts, l_counts,
+             l_offsets, l_sorted, l_pos);
+  return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
+}
+
 int w4a16_moe_gather(const void* x, int64_t H, int64_t topk, const int32_t* sorted_pairs, int64_t rows,
                      const int32_t* row_limit, void* x_perm, cudaStream_t stream) {
   if (!x || !sorted_pairs || !x_perm) return W4_ERR_ARG;
@@ -573,10 +681,10 @@ int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E,
     return rc;
   }
   if ((rc = w4a16_grouped_gemm_ws(xp, P, H, w13, E, I, 1, counts, offsets, decode ? xsum : nullptr,
-                                  decode ? hsum : nullptr, hp, dtype, nt, kws, kws_bytes, stream)))
+                                  decode ? hsum : nullptr, nullptr, hp, dtype, nt, kws, kws_bytes, stream)))
     return rc;
-  if ((rc = w4a16_grouped_gemm_ws(hp, P, I, w2, E, H, 0, counts, offsets, decode ? hsum : nullptr, nullptr, yp,
-                                  dtype, nt, kws, kws_bytes, stream)))
+  if ((rc = w4a16_grouped_gemm_ws(hp, P, I, w2, E, H, 0, counts, offsets, decode ? hsum : nullptr, nullptr, nullptr,
+                                  yp, dtype, nt, kws, kws_bytes, stream)))
     return rc;
   return w4a16_moe_combine(yp, T, H, topk, pos, topk_weights, dtype, y, stream);
 }

@@ -54,6 +54,7 @@ struct GemmArgs {
   float* part;                   // splits > 1: fp32 partials [splits][rows][part_ld]
   int64_t part_ld;               // (gated ? 2 : 1) * n_out
   float2* osum;                  // gated decode: (C, S) sums of the output h [nt][sum_ld] (next GEMM's xsum)
+  const int32_t* out_rows;       // optional: output row of input row i (scatter, e.g. back to EP arrival order)
 };
 
 // Numeric modes.
@@ -514,7 +515,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     TileInfo ti;
     for (int it = 0; tile_at<kNTok, C::kCG>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
       if (tre) trace_at(tr, 9, egs);
-      uint16_t* obase = out + static_cast<int64_t>(ti.m_start) * args.ldo + ti.n_tile * kTileRows + row;
+      uint16_t* ocol = out + ti.n_tile * kTileRows + row;
+      // output row of the tile's token m (identity, or scattered through args.out_rows)
+      auto orow = [&](int m) -> int64_t {
+        const int64_t i = static_cast<int64_t>(ti.m_start) + m;
+        return (args.out_rows ? static_cast<int64_t>(__ldg(args.out_rows + i)) : i) * args.ldo;
+      };
       if constexpr (kOffset) {
         constexpr int kOuts = kGated ? 2 : 1;  // gate|up accumulators, else one (k-pair parts summed)
         const int m_rows = ti.m_rows;
@@ -600,7 +606,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               if constexpr (kGated) v = silu_f(a[0][m]) * a[1][m];
               else v = a[0][m];
               const uint16_t bits = to_act_bits<kBF16>(v);
-              obase[static_cast<int64_t>(m) * args.ldo] = bits;
+              ocol[orow(m)] = bits;
               hv[m] = act_bits_to_float<kBF16>(bits);
             }
           }
@@ -654,7 +660,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               const int m = cb * 16 + i;
               if (m < ti.m_rows) {
                 const float gv = __uint_as_float(g[i]), uv = __uint_as_float(u[i]);
-                obase[static_cast<int64_t>(m) * args.ldo] = to_act_bits<kBF16>(silu_f(gv) * uv);
+                ocol[orow(m)] = to_act_bits<kBF16>(silu_f(gv) * uv);
               }
             }
           } else {
@@ -662,7 +668,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               const int m = cb * 16 + i;
-              if (m < ti.m_rows) obase[static_cast<int64_t>(m) * args.ldo] = to_act_bits<kBF16>(__uint_as_float(g[i]));
+              if (m < ti.m_rows) ocol[orow(m)] = to_act_bits<kBF16>(__uint_as_float(g[i]));
             }
           }
         }
@@ -699,7 +705,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 // rows r < *row_limit. One thread per 4 outputs.
 template <bool kBF16, bool kGated>
 __global__ void splitk_finalize_kernel(const float* __restrict__ part, int splits, int64_t rows, int64_t n_out,
-                                       const int32_t* __restrict__ row_limit, uint16_t* __restrict__ out) {
+                                       const int32_t* __restrict__ row_limit, const int32_t* __restrict__ out_rows,
+                                       uint16_t* __restrict__ out) {
   griddep_wait();  // PDL
   const int64_t r = blockIdx.y;
   if (r >= __ldg(row_limit)) return;
@@ -723,7 +730,8 @@ __global__ void splitk_finalize_kernel(const float* __restrict__ part, int split
   uint2 o;
   o.x = static_cast<uint32_t>(to_act_bits<kBF16>(v[0])) | static_cast<uint32_t>(to_act_bits<kBF16>(v[1])) << 16;
   o.y = static_cast<uint32_t>(to_act_bits<kBF16>(v[2])) | static_cast<uint32_t>(to_act_bits<kBF16>(v[3])) << 16;
-  *reinterpret_cast<uint2*>(out + r * n_out + n) = o;
+  const int64_t orow = out_rows ? static_cast<int64_t>(__ldg(out_rows + r)) : r;
+  *reinterpret_cast<uint2*>(out + orow * n_out + n) = o;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -996,8 +1004,8 @@ int64_t w4a16_grouped_gemm_ws_bytes(int64_t rows, int64_t K, int64_t num_experts
 
 int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t* wblocks, int64_t num_experts,
                           int64_t n_out, int gated, const int32_t* expert_counts, const int32_t* expert_offsets,
-                          const float* xsum, float* osum, void* out, int dtype, int ntok, void* ws, int64_t ws_bytes,
-                          cudaStream_t stream) {
+                          const float* xsum, float* osum, const int32_t* out_rows, void* out, int dtype, int ntok,
+                          void* ws, int64_t ws_bytes, cudaStream_t stream) {
   if (!x || !wblocks || !expert_counts || !expert_offsets || !out) return W4_ERR_ARG;
   if (K <= 0 || K % kTileK || n_out <= 0 || n_out % kTileRows) return W4_ERR_SHAPE;
   if (num_experts <= 0 || num_experts > kMaxExperts) return W4_ERR_SHAPE;
@@ -1025,6 +1033,8 @@ int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t*
   // the decode gate/up epilogue writes the output's group sums itself; otherwise a sums pass follows
   const bool fused_osum = osum != nullptr && gated && pl.offset && pl.ntok <= 16 && pl.splits == 1;
   a.osum = fused_osum ? reinterpret_cast<float2*>(osum) : nullptr;
+  a.out_rows = out_rows;
+  if (out_rows && osum) return W4_ERR_ARG;  // sums of a scattered output are not supported
   // CTA pairs (cta_group::2) measured slower at decode token counts (an M=256 x N=16 MMA with 8-row B
   // halves executes ~4x slower than two M=128 ones): opt-in only (W4A16_PAIR=1)
   const bool pair = pl.splits == 1 && a.nt % 2 == 0 && (pl.offset ? pairs_enabled() : prefill_pairs_enabled());
@@ -1047,11 +1057,11 @@ int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t*
   auto* o = static_cast<uint16_t*>(out);
   const int32_t* lim = expert_offsets + num_experts;
   if (gated)
-    bf ? launch_pdl(splitk_finalize_kernel<true, true>, fgrid, thr, 0, stream, a.part, pl.splits, rows, n_out, lim, o)
-       : launch_pdl(splitk_finalize_kernel<false, true>, fgrid, thr, 0, stream, a.part, pl.splits, rows, n_out, lim, o);
+    bf ? launch_pdl(splitk_finalize_kernel<true, true>, fgrid, thr, 0, stream, a.part, pl.splits, rows, n_out, lim, out_rows, o)
+       : launch_pdl(splitk_finalize_kernel<false, true>, fgrid, thr, 0, stream, a.part, pl.splits, rows, n_out, lim, out_rows, o);
   else
-    bf ? launch_pdl(splitk_finalize_kernel<true, false>, fgrid, thr, 0, stream, a.part, pl.splits, rows, n_out, lim, o)
-       : launch_pdl(splitk_finalize_kernel<false, false>, fgrid, thr, 0, stream, a.part, pl.splits, rows, n_out, lim, o);
+    bf ? launch_pdl(splitk_finalize_kernel<true, false>, fgrid, thr, 0, stream, a.part, pl.splits, rows, n_out, lim, out_rows, o)
+       : launch_pdl(splitk_finalize_kernel<false, false>, fgrid, thr, 0, stream, a.part, pl.splits, rows, n_out, lim, out_rows, o);
     if (cudaGetLastError() != cudaSuccess) return W4_ERR_CUDA;
   }
   if (osum != nullptr && !fused_osum)
@@ -1063,7 +1073,7 @@ int w4a16_grouped_gemm(const void* x, int64_t rows, int64_t K, const uint8_t* wb
                        int64_t n_out, int gated, const int32_t* expert_counts, const int32_t* expert_offsets,
                        const float* xsum, void* out, int dtype, int ntok, cudaStream_t stream) {
   return w4a16_grouped_gemm_ws(x, rows, K, wblocks, num_experts, n_out, gated, expert_counts, expert_offsets, xsum,
-                               nullptr, out, dtype, ntok, nullptr, 0, stream);
+                               nullptr, nullptr, out, dtype, ntok, nullptr, 0, stream);
 }
 
 int w4a16_dequant(const uint8_t* wblocks, int64_t num_experts, int64_t n_rows, int64_t K, int parts, int dtype,

@@ -56,11 +56,15 @@ def local_expert_ids(recv_counts: torch.Tensor, n_recv: int | None = None) -> to
 
 class CudaBackend:
     permute = staticmethod(cuda_ops.moe_permute)
+    local_order = staticmethod(cuda_ops.ep_local_order)  # one kernel: receiver-side local expert order
+    scatter_out = True  # the down GEMM writes arrival order directly
     gather = staticmethod(cuda_ops.moe_gather)
     combine = staticmethod(cuda_ops.moe_combine)
 
     @staticmethod
-    def experts(x, weights, counts, offsets, ntok, timer=None):
+    def experts(x, weights, counts, offsets, ntok, timer=None, out_rows=None):
+        """Both grouped GEMMs; with ``out_rows`` the down projection writes its rows scattered
+        through it (straight back to arrival order)."""
         from .layer import _NOTIMER
         tm = timer or _NOTIMER
         E, H, I = weights.num_experts, weights.hidden, weights.inter
@@ -72,7 +76,8 @@ class CudaBackend:
             h = cuda_ops.grouped_gemm(x, weights.w13.blocks, E, I, True, counts, offsets, nt, xsum=xs)
         hs = cuda_ops.group_sums(h) if decode else None
         with tm.span("gemm_down"):
-            return cuda_ops.grouped_gemm(h, weights.w2.blocks, E, H, False, counts, offsets, nt, xsum=hs)
+            return cuda_ops.grouped_gemm(h, weights.w2.blocks, E, H, False, counts, offsets, nt, xsum=hs,
+                                         out_rows=out_rows)
 
 
 def moe_w4a16_ep(x: torch.Tensor, weights, topk_weights: torch.Tensor, topk_ids: torch.Tensor, group=None,
@@ -97,12 +102,20 @@ def moe_w4a16_ep(x: torch.Tensor, weights, topk_weights: torch.Tensor, topk_ids:
     recv_x = x.new_empty((n_recv, H))
     dist.all_to_all_single(recv_x, send_x, plan.recv_splits, plan.send_splits, group=group)
     # 5: local expert order + grouped GEMMs
-    lid = local_expert_ids(plan.recv_counts, n_recv)
-    l_counts, l_offsets, l_sorted, l_pos = backend.permute(lid, e_local)
+    if hasattr(backend, "local_order"):
+        l_counts, l_offsets, l_sorted, l_pos = backend.local_order(plan.recv_counts, n_recv)
+    else:  # generic: ids of the received rows, then the stable permutation
+        lid = local_expert_ids(plan.recv_counts, n_recv)
+        l_counts, l_offsets, l_sorted, l_pos = backend.permute(lid, e_local)
     xl = backend.gather(recv_x, l_sorted, 1, n_recv) if n_recv else recv_x
-    yl = backend.experts(xl, weights, l_counts, l_offsets, ntok, timer) if n_recv else recv_x
-    # 6: back to arrival order, combine exchange, weighted reduction
-    y_recv = backend.gather(yl, l_pos, 1, n_recv) if n_recv else recv_x
+    # 6: the down GEMM scatters its rows straight back to arrival order; combine exchange, reduction
+    if not n_recv:
+        y_recv = recv_x
+    elif getattr(backend, "scatter_out", False):
+        y_recv = backend.experts(xl, weights, l_counts, l_offsets, ntok, timer, out_rows=l_sorted)
+    else:
+        yl = backend.experts(xl, weights, l_counts, l_offsets, ntok, timer)
+        y_recv = backend.gather(yl, l_pos, 1, n_recv)
     y_back = x.new_empty((T * k, H))
     dist.all_to_all_single(y_back, y_recv, plan.send_splits, plan.recv_splits, group=group)
     return backend.combine(y_back, pair_pos, topk_weights)

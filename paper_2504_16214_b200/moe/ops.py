@@ -115,6 +115,21 @@ def moe_gather(x: torch.Tensor, sorted_pairs: torch.Tensor, topk: int, rows: int
     return out
 
 
+def ep_local_order(recv_counts: torch.Tensor, n_recv: int):
+    """recv_counts [world, E_l] int32 (device) -> (l_counts [E_l], l_offsets [E_l+1], l_sorted [n],
+    l_pos [n]) int32: the received rows' local-expert order (see include/w4a16_moe.h)."""
+    _need_cuda(recv_counts)
+    world, el = recv_counts.shape
+    dev = recv_counts.device
+    l_counts = torch.empty(el, dtype=torch.int32, device=dev)
+    l_offsets = torch.empty(el + 1, dtype=torch.int32, device=dev)
+    l_sorted = torch.empty(max(n_recv, 1), dtype=torch.int32, device=dev)
+    l_pos = torch.empty(max(n_recv, 1), dtype=torch.int32, device=dev)
+    _lib.call("w4a16_ep_local_order", recv_counts.contiguous().data_ptr(), world, el, l_counts.data_ptr(),
+              l_offsets.data_ptr(), l_sorted.data_ptr(), l_pos.data_ptr(), _stream())
+    return l_counts, l_offsets, l_sorted[:n_recv], l_pos[:n_recv]
+
+
 def sums_shape(rows: int, K: int) -> tuple[int, int, int]:
     """Shape of the per-(k-group, row) activation sums array: [K/128][ld][2] fp32."""
     return (K // 128, int(_lib.load().w4a16_group_sums_ld(rows)), 2)
@@ -164,19 +179,21 @@ def moe_combine(y_perm: torch.Tensor, pair_pos: torch.Tensor, topk_weights: torc
 def grouped_gemm(x: torch.Tensor, blocks: torch.Tensor, num_experts: int, n_out: int, gated: bool,
                  expert_counts: torch.Tensor, expert_offsets: torch.Tensor, ntok: int = 0,
                  out: torch.Tensor | None = None, xsum: torch.Tensor | None = None,
-                 workspace: torch.Tensor | None = None, osum: torch.Tensor | None = None) -> torch.Tensor:
+                 workspace: torch.Tensor | None = None, osum: torch.Tensor | None = None,
+                 out_rows: torch.Tensor | None = None) -> torch.Tensor:
     """out[off_e + m] = act(x[off_e + m] @ W_e^T) (gated: silu(gate) * up), per expert. ``xsum``
     (group_sums / moe_gather_sums of x) selects the decode kernel for 16/32-token tiles; a
     ``workspace`` of gemm_ws_bytes(...) bytes enables split-K when few tiles exist; ``osum`` (shape
-    sums_shape(rows, n_out)) receives the output's group sums (the next GEMM's xsum)."""
+    sums_shape(rows, n_out)) receives the output's group sums (the next GEMM's xsum); ``out_rows``
+    (int32 [rows]) scatters result row i to out row out_rows[i]."""
     _need_cuda(x, blocks, expert_counts, expert_offsets)
     rows, K = x.shape
     if out is None:
         out = torch.empty((rows, n_out), dtype=x.dtype, device=x.device)
     wsb = 0 if workspace is None else workspace.numel() * workspace.element_size()
     _lib.call("w4a16_grouped_gemm_ws", x.data_ptr(), rows, K, blocks.data_ptr(), num_experts, n_out, int(gated),
-              expert_counts.data_ptr(), expert_offsets.data_ptr(), _ptr(xsum), _ptr(osum), out.data_ptr(),
-              act_code(x.dtype), ntok, _ptr(workspace), wsb, _stream())
+              expert_counts.data_ptr(), expert_offsets.data_ptr(), _ptr(xsum), _ptr(osum), _ptr(out_rows),
+              out.data_ptr(), act_code(x.dtype), ntok, _ptr(workspace), wsb, _stream())
     return out
 
 

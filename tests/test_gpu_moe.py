@@ -290,3 +290,43 @@ def test_fused_moe_graph_matches_eager():
         got = g(x, lg)
         torch.cuda.synchronize()
         assert torch.equal(got, want)
+
+
+@pytest.mark.parametrize("world,el", [(1, 256), (2, 128), (8, 32), (4, 3)])
+def test_ep_local_order(world, el):
+    """Receiver-side local-expert order from the received counts == ids + stable permutation."""
+    from paper_2504_16214_b200.moe.ep import local_expert_ids
+    rng = np.random.default_rng(world * 100 + el)
+    cnt = rng.integers(0, 6, size=(world, el)).astype(np.int32)
+    cnt[0, 0] = 0
+    n = int(cnt.sum())
+    rc = torch.from_numpy(cnt).cuda()
+    got = _ops().ep_local_order(rc, n)
+    lid = local_expert_ids(rc, n).cpu().numpy()
+    want = O.moe_permute(lid, el)
+    for g, w in zip(got, want):
+        assert np.array_equal(g.cpu().numpy()[:len(w)], w)
+
+
+@pytest.mark.parametrize("ntok,splitk", [(16, False), (16, True), (64, False)])
+def test_grouped_gemm_out_rows(ntok, splitk):
+    """out_rows scatters result rows (the EP down GEMM writes arrival order directly): equals the
+    plain output permuted."""
+    rng = np.random.default_rng(41)
+    E, N, K, dt = 2, 512, 1024, "f16"
+    counts = [3, 2] if ntok == 16 else [40, 30]
+    q, z, s = O.synth_awq_expert_weights(rng, E, N, K, dt)
+    w = _packed(q, z, s, dt, False)
+    rows = int(sum(counts))
+    cnt = torch.tensor(counts, dtype=torch.int32).cuda()
+    off = torch.tensor([0, counts[0], rows], dtype=torch.int32).cuda()
+    xd = _to_dev_act(O.round_act(rng.standard_normal((rows, K)).astype(np.float32) * 0.5, dt), dt)
+    ops = _ops()
+    xs = ops.group_sums(xd) if ntok == 16 else None
+    wsb = ops.gemm_ws_bytes(rows, K, E, N, False, ntok) if splitk else 0
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda") if wsb else None
+    perm = torch.from_numpy(rng.permutation(rows).astype(np.int32)).cuda()
+    plain = ops.grouped_gemm(xd, w.blocks, E, N, False, cnt, off, ntok, xsum=xs, workspace=ws)
+    scat = ops.grouped_gemm(xd, w.blocks, E, N, False, cnt, off, ntok, xsum=xs, workspace=ws, out_rows=perm)
+    torch.cuda.synchronize()
+    assert torch.equal(scat[perm.long()], plain)
