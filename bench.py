@@ -362,8 +362,7 @@ def main():
     graphed = None
     if group is None and not args.no_graph:
         from paper_2504_16214_b200.moe import FusedMoEGraph
-        graphed = FusedMoEGraph(weights, T, K_DS, "softmax", True, tdt, dev)
-        graphed(x, lg)
+        graphed = FusedMoEGraph(weights, T, K_DS, "softmax", True, tdt, dev, x=x, router_logits=lg)
 
     def timed_step(xx=x, ll=lg):
         if graphed is not None:

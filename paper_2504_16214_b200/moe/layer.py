@@ -167,10 +167,15 @@ class FusedMoEGraph:
     graph's own buffers; the returned output tensor is the graph's (overwritten by the next call)."""
 
     def __init__(self, weights: MoEWeights, tokens: int, top_k: int, scoring: str = "softmax",
-                 renormalize: bool = False, dtype: torch.dtype = torch.float16, device=None):
+                 renormalize: bool = False, dtype: torch.dtype = torch.float16, device=None,
+                 x: torch.Tensor | None = None, router_logits: torch.Tensor | None = None):
         dev = torch.device(device) if device is not None else weights.w13.blocks.device
         self.x = torch.zeros((tokens, weights.hidden), dtype=dtype, device=dev)
         self.logits = torch.randn((tokens, weights.num_experts), device=dev)
+        if x is not None:  # warm up / capture on the caller's first inputs (same routing as served)
+            self.x.copy_(x)
+        if router_logits is not None:
+            self.logits.copy_(router_logits)
         args = (weights, top_k, scoring, renormalize)
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream(dev))
