@@ -75,6 +75,7 @@ struct GemmArgs {
 constexpr int kModePlain = 0;   // one part (one k-group) per stage
 constexpr int kModeGateUp = 1;  // part 0 = gate rows, part 1 = up rows, same k-group (fused SwiGLU)
 constexpr int kModeKPair = 2;   // parts = two consecutive k-groups of the same rows (down proj.)
+constexpr int kModeNPair = 3;   // parts = one k-group of two adjacent n-tiles sharing the X tile (prefill)
 constexpr int kEpiChunk = 4;    // offset-mode epilogue token granularity
 
 // kPair: a CTA pair (cluster of 2 on one TPC) runs tcgen05.mma.cta_group::2 -- M = 256 weight rows
@@ -87,6 +88,7 @@ struct Cfg {
   static constexpr int kCG = kPair ? 2 : 1;
   static constexpr int kXRows = kNTok / kCG;  // X rows held by this CTA
   static constexpr int kParts = kMode == kModePlain ? 1 : 2;
+  static constexpr int kNPer = kMode == kModeNPair ? 2 : 1;  // n-tiles per (CTA) tile
   static constexpr int kGroupsPerStage = kMode == kModeKPair ? 2 : 1;
   static constexpr int kBlk = kParts * kPartBytes;
   static constexpr int kXBytes = kGroupsPerStage * kXRows * kTileK * 2;  // X tile, 64-wide 128B-swizzle atoms
@@ -98,14 +100,14 @@ struct Cfg {
   static constexpr int kChainLen = (kTileK / 16) / kKSplit;
   // one accumulator stage: offset mode = kKSplit partials per part; otherwise gate|up or one
   // accumulator for the whole tile
-  static constexpr int kAccCols = kOffset ? kParts * kKSplit * kNTok : (kGated ? 2 * kNTok : kNTok);
+  static constexpr int kAccCols = kOffset ? kParts * kKSplit * kNTok : ((kGated || kNPer == 2) ? 2 * kNTok : kNTok);
   static constexpr int kACols = kParts * (kTileK / 2);  // fp16 pairs per 32-bit column
   // TMEM budget (512 columns): A ring + accumulator ring
   // 3 A slots if two accumulator stages still fit, else 2; the gated prefill projection (56-stage
   // tiles) instead prefers 3 A slots (dequant / MMA overlap) over a second accumulator stage
   // (epilogue / next-tile overlap, once per long tile); the short k-pair tiles need two.
-  static constexpr int kNumA_ = (kOffset || !kGated) ? ((3 * kACols + 2 * kAccCols <= 512) ? 3 : 2)
-                                                    : ((3 * kACols + kAccCols <= 512) ? 3 : 2);
+  static constexpr int kNumA_ = (kOffset || !(kGated || kNPer == 2)) ? ((3 * kACols + 2 * kAccCols <= 512) ? 3 : 2)
+                                                                   : ((3 * kACols + kAccCols <= 512) ? 3 : 2);
   static constexpr int kNumAccO = (512 - kNumA_ * kACols) / kAccCols;
   static constexpr int kNumAcc = kNumAccO > (kOffset ? 4 : 2) ? (kOffset ? 4 : 2) : kNumAccO;
   static constexpr int kNumA = kNumA_;
@@ -157,9 +159,9 @@ struct TileInfo {
 // Static persistent schedule: tile t -> (expert, n-tile group, m-tile); m-tiles of one (expert, n-tile)
 // are adjacent so concurrently running CTAs share that weight block through L2. kNSplit = 2 for CTA
 // pairs: tile t covers n-tiles 2g and 2g+1, CTA rank r of the pair takes n-tile 2g + r.
-template <int kNTok, int kNSplit>
+template <int kNTok, int kNSplit, int kNPer = 1>
 __device__ __forceinline__ bool get_tile(int t, const int* mt_off, const GemmArgs& a, uint32_t rank, TileInfo& ti) {
-  const int ntg = a.nt / kNSplit;
+  const int ntg = a.nt / (kNSplit * kNPer);
   const int total = mt_off[a.num_experts] * ntg * a.splits;
   if (t >= total) return false;
   ti.split = t % a.splits;  // split-K units of one tile are adjacent
@@ -174,7 +176,7 @@ __device__ __forceinline__ bool get_tile(int t, const int* mt_off, const GemmArg
   const int local = t - mt_off[e] * ntg;
   const int m_tile = me == 1 ? 0 : local % me;
   ti.e = e;
-  ti.n_tile = (me == 1 ? local : local / me) * kNSplit + static_cast<int>(rank);
+  ti.n_tile = ((me == 1 ? local : local / me) * kNSplit + static_cast<int>(rank)) * kNPer;
   ti.m_start = __ldg(a.expert_offsets + e) + m_tile * kNTok;
   ti.m_rows = min(kNTok, __ldg(a.expert_counts + e) - m_tile * kNTok);
   return true;
@@ -196,7 +198,7 @@ __device__ __forceinline__ void unpack_tile(uint2 p, TileInfo& ti) {
 }
 
 // The CTA's i-th tile (t = tile0 + i * tstride): from the smem table when i < kTileTab, else searched.
-template <int kNTok, int kNSplit>
+template <int kNTok, int kNSplit, int kNPer = 1>
 __device__ __forceinline__ bool tile_at(int i, int n_tiles, int tile0, int tstride, const uint2* tab, const int* mt_off,
                                         const GemmArgs& a, uint32_t rank, TileInfo& ti) {
   if (i >= n_tiles) return false;
@@ -204,7 +206,7 @@ __device__ __forceinline__ bool tile_at(int i, int n_tiles, int tile0, int tstri
     unpack_tile(tab[i], ti);
     return true;
   }
-  return get_tile<kNTok, kNSplit>(tile0 + i * tstride, mt_off, a, rank, ti);
+  return get_tile<kNTok, kNSplit, kNPer>(tile0 + i * tstride, mt_off, a, rank, ti);
 }
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
@@ -299,12 +301,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     if (lane == 31) mt_off[E] = incl;
     __syncwarp();
     // this CTA's tiles t = tile0 + i * tstride, the first kTileTab of them tabulated
-    const int total = mt_off[E] * (args.nt / C::kCG) * args.splits;
+    const int total = mt_off[E] * (args.nt / (C::kCG * C::kNPer)) * args.splits;
     const int n_tiles = tile0 < total ? (total - tile0 + tstride - 1) / tstride : 0;
     if (lane == 0) *n_tiles_sm = n_tiles;
     for (int i = lane; i < min(n_tiles, kTileTab); i += 32) {
       TileInfo ti;
-      get_tile<kNTok, C::kCG>(tile0 + i * tstride, mt_off, args, rank, ti);
+      get_tile<kNTok, C::kCG, C::kNPer>(tile0 + i * tstride, mt_off, args, rank, ti);
       tile_tab[i] = pack_tile(ti);
     }
   } else if (warp == 3 && lane == 0) {
@@ -329,7 +331,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       Ring st;
       uint32_t pgs = 0;
       TileInfo ti;
-      for (int it = 0; tile_at<kNTok, C::kCG>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
+      for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
         // per (expert, n-tile): kt k-groups of (gated ? 2 : 1) parts, stage j = bytes [j*kBlk, (j+1)*kBlk)
         const uint8_t* wsrc = args.wblocks + (static_cast<int64_t>(ti.e) * args.nt + ti.n_tile) *
                                                  static_cast<int64_t>(args.kt) * (kGated ? 2 : 1) * kPartBytes;
@@ -338,8 +340,15 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           if (lane == 0) {
             trace_at(tr, 0, pgs++);
             mbar_arrive_expect_tx(&full[st.i], C::kBlk + C::kXBytes);
-            bulk_g2s_hint(smem_w + st.i * C::kBlk, wsrc + static_cast<int64_t>(j) * C::kBlk, C::kBlk, &full[st.i],
-                          pol_w);
+            if constexpr (C::kNPer == 2) {  // k-group j of n-tiles n_tile and n_tile + 1 (blocks kt apart)
+              bulk_g2s_hint(smem_w + st.i * C::kBlk, wsrc + static_cast<int64_t>(j) * kPartBytes, kPartBytes,
+                            &full[st.i], pol_w);
+              bulk_g2s_hint(smem_w + st.i * C::kBlk + kPartBytes,
+                            wsrc + (static_cast<int64_t>(args.kt) + j) * kPartBytes, kPartBytes, &full[st.i], pol_w);
+            } else {
+              bulk_g2s_hint(smem_w + st.i * C::kBlk, wsrc + static_cast<int64_t>(j) * C::kBlk, C::kBlk, &full[st.i],
+                            pol_w);
+            }
             uint8_t* xs = smem_x + st.i * C::kXBytes;
 #pragma unroll
             for (int h = 0; h < 2 * C::kGroupsPerStage; ++h)
@@ -378,7 +387,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       Ring st, ar, acc;
       uint32_t gs = 0;
       TileInfo ti;
-      for (int it = 0; tile_at<kNTok, C::kCG>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
+      for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
         // MMA N sized to the tile's real tokens (multiple of 16 per CTA of the group): an expert's last,
         // partial m-tile costs tensor time in proportion to its rows, not to kNTok
         const uint32_t n_mma = min(kNTok, (ti.m_rows + 16 * C::kCG - 1) / (16 * C::kCG) * (16 * C::kCG));
@@ -399,7 +408,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           const uint32_t acol = tb_u + kAcol0 + ar.i * C::kACols;
           // one elected lane issues the stage's MMAs (generated PTX block, mma_stage.cuh) and commits
           if (elect_one()) {
-            StageAsm<kNTok, kMode, C::kCG, kOffset>::issue(dcol, acol, xdesc, idesc, static_cast<uint32_t>(j));
+            StageAsm<kNTok, (kMode == kModeNPair ? kModeGateUp : kMode), C::kCG, kOffset>::issue(
+                dcol, acol, xdesc, idesc, static_cast<uint32_t>(j));
             trace_at(tr, 5, gs);
             if constexpr (kPair) {
               umma_commit_pair(&empty[st.i]);
@@ -440,7 +450,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     Ring st, ar;
     uint32_t gs = 0;
     TileInfo ti;
-    for (int it = 0; tile_at<kNTok, C::kCG>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
+    for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
       for (int j = stage_beg(ti); j < stage_end(ti); ++j, ++gs) {
         if ((gs & 1u) != my_par) {
           st.next(C::kNS);
@@ -513,7 +523,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     uint32_t egs = 0;
     const bool tre = lane == 0 && quad == 0;
     TileInfo ti;
-    for (int it = 0; tile_at<kNTok, C::kCG>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
+    for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
       if (tre) trace_at(tr, 9, egs);
       uint16_t* ocol = out + ti.n_tile * kTileRows + row;
       // output row of the tile's token m (identity, or scattered through args.out_rows)
@@ -661,6 +671,19 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               if (m < ti.m_rows) {
                 const float gv = __uint_as_float(g[i]), uv = __uint_as_float(u[i]);
                 ocol[orow(m)] = to_act_bits<kBF16>(silu_f(gv) * uv);
+              }
+            }
+          } else if constexpr (C::kNPer == 2) {  // second accumulator = the next n-tile's columns
+            uint32_t u[16];
+            tmem_ld_x16(dcol + kNTok + cb * 16, u);
+            tc_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int m = cb * 16 + i;
+              if (m < ti.m_rows) {
+                const int64_t o = orow(m);
+                ocol[o] = to_act_bits<kBF16>(__uint_as_float(g[i]));
+                ocol[o + kTileRows] = to_act_bits<kBF16>(__uint_as_float(u[i]));
               }
             }
           } else {
@@ -909,6 +932,23 @@ int dispatch_ntok(int ntok, bool offset, bool pair, const GemmArgs& a, const voi
   }
 }
 
+template <int kMode, bool kBF16>
+int dispatch_prefill(int ntok, const GemmArgs& a, const void* x, int64_t rows, int64_t K, int grid, cudaStream_t st) {
+  if (ntok == 64) return launch_gemm<64, kMode, kBF16, false, false>(a, x, rows, K, grid, st);
+  if (ntok == 128) return launch_gemm<128, kMode, kBF16, false, false>(a, x, rows, K, grid, st);
+  return W4_ERR_ARG;
+}
+
+// n-pair block mode from this token tile up (W4A16_NPAIR_MIN_NTOK, default 128; 0 disables)
+int npair_min_ntok() {
+  static const int v = [] {
+    const char* e = getenv("W4A16_NPAIR_MIN_NTOK");
+    const int x = e ? atoi(e) : 128;
+    return x <= 0 ? 1 << 30 : x;
+  }();
+  return v;
+}
+
 // Experiment knob: W4A16_PREFILL_PAIR=1 runs the prefill (64/128-token) kernels on CTA pairs.
 bool prefill_pairs_enabled() {
   static const bool on = [] {
@@ -962,6 +1002,8 @@ GemmPlan plan_gemm(int64_t rows, int64_t K, int64_t num_experts, int64_t n_out, 
   // k-pair (two k-groups per 17 KB stage) for decode tiles; at 128 tokens the X tile dominates a stage
   // (64 KB for a k-pair -> only 2 smem stages), so 128-token tiles use one group per stage
   pl.mode = gated ? kModeGateUp : ((kt % 2 == 0 && pl.ntok <= 64) ? kModeKPair : kModePlain);
+  // prefill down projection: two n-tiles per stage share the X tile (halves the X smem traffic)
+  if (!gated && !pl.offset && pl.ntok >= npair_min_ntok() && nt % 2 == 0) pl.mode = kModeNPair;
   const int n_stages = kt / (pl.mode == kModeKPair ? 2 : 1);
   pl.splits = (pl.offset && rows < (1 << 20)) ? choose_splits(rows, num_experts, nt, n_stages, sm_count()) : 1;
   return pl;
@@ -1047,6 +1089,9 @@ int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t*
   else if (pl.mode == kModeKPair)
     rc = bf ? dispatch_ntok<kModeKPair, true>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream)
             : dispatch_ntok<kModeKPair, false>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream);
+  else if (pl.mode == kModeNPair)
+    rc = bf ? dispatch_prefill<kModeNPair, true>(pl.ntok, a, x, rows, K, grid, stream)
+            : dispatch_prefill<kModeNPair, false>(pl.ntok, a, x, rows, K, grid, stream);
   else
     rc = bf ? dispatch_ntok<kModePlain, true>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream)
             : dispatch_ntok<kModePlain, false>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream);
