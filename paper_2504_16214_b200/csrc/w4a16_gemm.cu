@@ -569,11 +569,14 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll
               for (int i = 0; i < kEpiChunk; ++i) {
                 const int m = cb * kEpiChunk + i;
+                float2 csg[C::kGroupsPerStage];  // (C, S) of token m per k-group of the stage (broadcast)
+#pragma unroll
+                for (int g = 0; g < C::kGroupsPerStage; ++g) csg[g] = lds_f2(sums + (g * kNTok + m) * 8);
 #pragma unroll
                 for (int p = 0; p < C::kParts; ++p) {
                   const int g = kMode == kModeKPair ? p : 0;
                   const int o = kGated ? p : 0;
-                  const float2 cs = lds_f2(sums + (g * kNTok + m) * 8);  // (C, S), broadcast
+                  const float2 cs = csg[g];
                   float pv = __uint_as_float(r[p][0][i]);
 #pragma unroll
                   for (int hs = 1; hs < C::kKSplit; ++hs) pv += __uint_as_float(r[p][hs][i]);
