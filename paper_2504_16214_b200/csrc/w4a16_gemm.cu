@@ -39,6 +39,10 @@ constexpr int kTileTab = 512;  // per-CTA tile table entries in smem (later tile
 // k-group), which beats the dequant's per-weight scale only at <= 16 tokens (measured: 32-token tiles
 // are 10-25 % faster with the scale applied in the dequant).
 constexpr int kDecodeMaxNTok = 16;
+#ifndef W4A16_KSPLIT
+#define W4A16_KSPLIT 1
+#endif
+constexpr bool kKSplitEnv = W4A16_KSPLIT != 0;  // experiment: -DW4A16_KSPLIT=0
 constexpr int kSmemBudget = 225 * 1024;
 
 struct GemmArgs {
@@ -96,7 +100,7 @@ struct Cfg {
   // offset mode: each part's 128-k partial is split over kKSplit independent accumulators (k halves)
   // so a stage issues kParts * kKSplit interleaved MMA chains -- a dependent chain of small-N MMAs is
   // bound by the accumulate latency, not by the tensor pipe
-  static constexpr int kKSplit = (kOffset && kNTok == 16) ? 2 : 1;
+  static constexpr int kKSplit = (kOffset && kNTok == 16 && kKSplitEnv) ? 2 : 1;
   static constexpr int kChainLen = (kTileK / 16) / kKSplit;
   // one accumulator stage: offset mode = kKSplit partials per part; otherwise gate|up or one
   // accumulator for the whole tile
@@ -408,7 +412,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           const uint32_t acol = tb_u + kAcol0 + ar.i * C::kACols;
           // one elected lane issues the stage's MMAs (generated PTX block, mma_stage.cuh) and commits
           if (elect_one()) {
-            StageAsm<kNTok, (kMode == kModeNPair ? kModeGateUp : kMode), C::kCG, kOffset>::issue(
+            StageAsm<kNTok, (kMode == kModeNPair ? kModeGateUp : kMode), C::kCG, kOffset, C::kKSplit>::issue(
                 dcol, acol, xdesc, idesc, static_cast<uint32_t>(j));
             trace_at(tr, 5, gs);
             if constexpr (kPair) {
