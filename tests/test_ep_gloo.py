@@ -1,4 +1,4 @@
-"""Expert-parallel exchange plumbing on CPU: world_size 2 over ``gloo``.
+"""Expert-parallel exchange plumbing on CPU: world_size 2 and 4 over ``gloo``.
 
 The product path runs the CUDA ops; here ``moe_w4a16_ep`` gets a CPU backend built from the oracle
 so the dispatch plan, the two all-to-alls, the receiver-side local-expert permutation and the
@@ -59,13 +59,13 @@ class CpuBackend:
         return torch.from_numpy(y)
 
 
-def _inputs():
+def _inputs(world=2):
     rng = np.random.default_rng(11)
     q13, z13, s13 = O.synth_awq_expert_weights(rng, E, 2 * I, H, "f16")
     q2, z2, s2 = O.synth_awq_expert_weights(rng, E, H, I, "f16")
     w13, w2 = O.dequant(q13, z13, s13, "f16"), O.dequant(q2, z2, s2, "f16")
     xs, ids, wts = [], [], []
-    for r in range(2):  # each rank routes its own T tokens
+    for r in range(world):  # each rank routes its own T tokens
         xs.append(O.round_act(rng.standard_normal((T, H)).astype(np.float32), "f16"))
         lg = rng.standard_normal((T, E)).astype(np.float32)
         i, w = O.route_topk(lg, K_TOP, "softmax", True)
@@ -78,7 +78,7 @@ def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2504_16214_b200.moe.ep import moe_w4a16_ep, shard_bounds
-    w13, w2, xs, ids, wts = _inputs()
+    w13, w2, xs, ids, wts = _inputs(world)
     lo, hi = shard_bounds(E, world, rank)
     y = moe_w4a16_ep(torch.from_numpy(xs[rank]), _W(w13[lo:hi], w2[lo:hi]), torch.from_numpy(wts[rank]),
                      torch.from_numpy(ids[rank]), backend=CpuBackend)
@@ -86,19 +86,20 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-def test_ep_world2_matches_single_process_oracle():
+@pytest.mark.parametrize("world", [2, 4])
+def test_ep_matches_single_process_oracle(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
     got = dict(q.get(timeout=300) for _ in procs)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    w13, w2, xs, ids, wts = _inputs()
-    for r in range(2):
+    w13, w2, xs, ids, wts = _inputs(world)
+    for r in range(world):
         want = O.moe_forward(xs[r], w13, w2, ids[r], wts[r], "f16")
         # per-rank GEMMs see different row batches (BLAS blocking) -> last-ulp fp16 differences only
         np.testing.assert_allclose(got[r], want, rtol=2e-3, atol=1e-4)

@@ -330,3 +330,41 @@ def test_grouped_gemm_out_rows(ntok, splitk):
     scat = ops.grouped_gemm(xd, w.blocks, E, N, False, cnt, off, ntok, xsum=xs, workspace=ws, out_rows=perm)
     torch.cuda.synchronize()
     assert torch.equal(scat[perm.long()], plain)
+
+
+@pytest.mark.parametrize("T", [3, 40, 600])
+def test_c_abi_moe_forward(T):
+    """The one-call C entry point w4a16_moe_forward (caller workspace, precomputed routing) through
+    ctypes == the oracle layer (decode, 32/64-token and split-K plans depending on T)."""
+    import ctypes
+    from paper_2504_16214_b200.moe import _lib
+    from paper_2504_16214_b200.moe.weights import MoEWeights
+    lib = _lib.load()
+    lib.w4a16_moe_workspace_bytes.restype = ctypes.c_int64
+    lib.w4a16_moe_workspace_bytes.argtypes = [ctypes.c_int64] * 5
+    lib.w4a16_moe_forward.restype = ctypes.c_int
+    p, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    lib.w4a16_moe_forward.argtypes = [p, i64, i64, i64, i64, i64, p, p, p, p, i32, p, p, i64, p]
+    rng = np.random.default_rng(T)
+    E, k, H, I, dt = 16, 4, 512, 256, "f16"
+    q13, z13, s13 = O.synth_awq_expert_weights(rng, E, 2 * I, H, dt)
+    q2, z2, s2 = O.synth_awq_expert_weights(rng, E, H, I, dt)
+    w = MoEWeights(_packed(q13, z13, s13, dt, True), _packed(q2, z2, s2, dt, False))
+    x = O.round_act(rng.standard_normal((T, H)).astype(np.float32) * 0.5, dt)
+    lg = rng.standard_normal((T, E)).astype(np.float32)
+    ids, wts = O.route_topk(lg, k, "softmax", True)
+    xd = _to_dev_act(x, dt)
+    idd, wd = torch.from_numpy(ids).cuda(), torch.from_numpy(wts).cuda()
+    y = torch.empty_like(xd)
+    wsb = lib.w4a16_moe_workspace_bytes(T, k, E, H, I)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    rc = lib.w4a16_moe_forward(xd.data_ptr(), T, H, I, E, k, idd.data_ptr(), wd.data_ptr(), w.w13.blocks.data_ptr(),
+                               w.w2.blocks.data_ptr(), 0, y.data_ptr(), ws.data_ptr(), wsb,
+                               torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    torch.cuda.synchronize()
+    want = O.moe_forward(x, O.dequant(q13, z13, s13, dt), O.dequant(q2, z2, s2, dt), ids, wts, dt)
+    np.testing.assert_allclose(_from_dev_act(y, dt), want, rtol=RTOL, atol=ATOL)
+    assert lib.w4a16_moe_forward(xd.data_ptr(), T, H, I, E, k, idd.data_ptr(), wd.data_ptr(), w.w13.blocks.data_ptr(),
+                                 w.w2.blocks.data_ptr(), 0, y.data_ptr(), ws.data_ptr(), wsb - 1,
+                                 torch.cuda.current_stream().cuda_stream) == -6  # W4_ERR_WORKSPACE
