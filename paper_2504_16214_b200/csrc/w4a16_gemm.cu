@@ -44,6 +44,15 @@ constexpr int kDecodeMaxNTok = 16;
 #endif
 constexpr bool kKSplitEnv = W4A16_KSPLIT != 0;  // experiment: -DW4A16_KSPLIT=0
 constexpr int kSmemBudget = 225 * 1024;
+#ifndef W4A16_SPLITA
+#define W4A16_SPLITA 0
+#endif
+constexpr bool kSplitAEnv = W4A16_SPLITA != 0;  // experiment: per-part TMEM A units at prefill
+#ifndef W4A16_DQEXP
+#define W4A16_DQEXP 0
+#endif
+// experiment (prefill dequant): 1 = store raw codes (no FP math), 2 = no TMEM stores at all
+constexpr int kDqExp = W4A16_DQEXP;
 
 struct GemmArgs {
   const uint8_t* wblocks;        // [E][NT][KT][parts * kPartBytes]
@@ -105,19 +114,30 @@ struct Cfg {
   // one accumulator stage: offset mode = kKSplit partials per part; otherwise gate|up or one
   // accumulator for the whole tile
   static constexpr int kAccCols = kOffset ? kParts * kKSplit * kNTok : ((kGated || kNPer == 2) ? 2 * kNTok : kNTok);
-  static constexpr int kACols = kParts * (kTileK / 2);  // fp16 pairs per 32-bit column
+  // Prefill two-part stages use a split A ring: one 64-column TMEM unit per part, released per part
+  // by the MMA, so the dequant of the next part overlaps the MMAs of this one (with whole-stage
+  // slots the gate/up tile ran ~1300-1800 cycles per 1024-cycle stage: a slot was held for a whole
+  // dequant + MMA round trip and two slots did not cover it; tools/trace_gemm.py).
+  static constexpr bool kSplitA = kSplitAEnv && !kOffset && kParts == 2;
+  static constexpr int kAUnits = kSplitA ? kParts : 1;  // A-ring slots per stage
+  static constexpr int kACols = (kSplitA ? 1 : kParts) * (kTileK / 2);  // fp16 pairs per 32-bit column
   // TMEM budget (512 columns): A ring + accumulator ring
   // 3 A slots if two accumulator stages still fit, else 2; the gated prefill projection (56-stage
   // tiles) instead prefers 3 A slots (dequant / MMA overlap) over a second accumulator stage
   // (epilogue / next-tile overlap, once per long tile); the short k-pair tiles need two.
+  // Split ring: two accumulator stages if 6 units still fit, then as many units as fit (<= 8).
   static constexpr int kNumA_ = (kOffset || !(kGated || kNPer == 2)) ? ((3 * kACols + 2 * kAccCols <= 512) ? 3 : 2)
                                                                    : ((3 * kACols + kAccCols <= 512) ? 3 : 2);
+  static constexpr int kNumAccS = (2 * kAccCols + 6 * kACols <= 512) ? 2 : 1;
+  static constexpr int kNumAS = (512 - kNumAccS * kAccCols) / kACols > 8 ? 8 : (512 - kNumAccS * kAccCols) / kACols;
   static constexpr int kNumAccO = (512 - kNumA_ * kACols) / kAccCols;
-  static constexpr int kNumAcc = kNumAccO > (kOffset ? 4 : 2) ? (kOffset ? 4 : 2) : kNumAccO;
-  static constexpr int kNumA = kNumA_;
+  static constexpr int kNumAcc = kSplitA ? kNumAccS : (kNumAccO > (kOffset ? 4 : 2) ? (kOffset ? 4 : 2) : kNumAccO);
+  static constexpr int kNumA = kSplitA ? kNumAS : kNumA_;
   static constexpr int kStageBytes = kBlk + kXBytes + kSumBytes;
   // barriers, m-tile prefix, tile table, epilogue cross-warp reduction scratch (4 warps x 16 x float2)
-  static constexpr int kFixed = 2048 + 4 * (kMaxExperts + 2) + 8 * kTileTab + 512;
+  // prefill epilogue: per-warp staging of a 16-token x 32-column output block (x2 for n-pair tiles)
+  static constexpr int kEpiStageBytes = kOffset ? 0 : 4 * 1024 * (kNPer == 2 ? 2 : 1);  // [4 warps][...], 16 B aligned
+  static constexpr int kFixed = 2048 + 4 * (kMaxExperts + 2) + 8 * kTileTab + 512 + 16 + kEpiStageBytes;
   static constexpr int kNS0 = (kSmemBudget - kFixed - 1024) / kStageBytes;
   static constexpr int kNS = kNS0 > 12 ? 12 : kNS0;
   static constexpr int kEmptyArrivals = kDequantGroup + 1 + (kOffset ? 4 : 0);
@@ -127,7 +147,7 @@ struct Cfg {
   static constexpr int kAccEmptyArrivals = 4 * kCG;              // epilogue warps of both CTAs (leader)
   // X ring first (needs 1024 B alignment for the 128B swizzle atoms), sums ring, then weights.
   static constexpr int kSmemBytes = 1024 + kNS * kStageBytes + kFixed;
-  static_assert(kNumA >= 2 && kNumAcc >= (kOffset ? 2 : 1), "TMEM budget");
+  static_assert(kNumA >= 2 * kAUnits && kNumAcc >= (kOffset ? 2 : 1), "TMEM budget");
   static_assert(kNumA * kACols + kNumAcc * kAccCols <= 512, "TMEM budget");
   static_assert(kNS >= 2, "smem budget");
   static_assert(kXBytes % 1024 == 0, "X tile alignment");
@@ -136,6 +156,7 @@ struct Cfg {
 
 // Opt-in per-stage timeline of CTA 0 (w4a16_debug_trace): clock64 at each role's sync points.
 __device__ long long* g_w4_trace = nullptr;
+__device__ int g_w4_trace_cta = 0;  // which CTA the timeline follows
 constexpr int kTraceCap = 4096;
 __device__ __forceinline__ void trace_at(long long* tr, int ev, uint32_t idx) {
 #ifndef W4A16_TRACE
@@ -213,7 +234,9 @@ __device__ __forceinline__ bool tile_at(int i, int n_tiles, int tile0, int tstri
   return get_tile<kNTok, kNSplit, kNPer>(tile0 + i * tstride, mt_off, a, rank, ti);
 }
 
-__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+// fast reciprocal division (exp overflow -> +inf -> 0, the limit): no IEEE slow-path branch, so the
+// epilogue's per-token chains stay branch-free and interleave
+__device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 template <bool kBF16>
 __device__ __forceinline__ uint16_t to_act_bits(float v) {
@@ -261,6 +284,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   uint2* tile_tab = reinterpret_cast<uint2*>(mt_off + kMaxExperts + 2);  // 8-byte aligned (odd int count + 1)
   int* n_tiles_sm = mt_off + kMaxExperts + 1;
   float2* red_sm = reinterpret_cast<float2*>(tile_tab + kTileTab);  // [4 warps][16 tokens]
+  uint8_t* epi_sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(red_sm + 64) + 15) & ~uintptr_t(15));
 
   const uint32_t warp = warp_idx();
   const uint32_t lane = lane_id();
@@ -268,7 +292,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   const int tile0 = kPair ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
   const int tstride = kPair ? static_cast<int>(nclusters_x()) : static_cast<int>(gridDim.x);
   #ifdef W4A16_TRACE
-  long long* const tr = blockIdx.x == 0 ? g_w4_trace : nullptr;
+  long long* const tr = static_cast<int>(blockIdx.x) == g_w4_trace_cta ? g_w4_trace : nullptr;
 #else
   long long* const tr = nullptr;
 #endif
@@ -339,6 +363,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         // per (expert, n-tile): kt k-groups of (gated ? 2 : 1) parts, stage j = bytes [j*kBlk, (j+1)*kBlk)
         const uint8_t* wsrc = args.wblocks + (static_cast<int64_t>(ti.e) * args.nt + ti.n_tile) *
                                                  static_cast<int64_t>(args.kt) * (kGated ? 2 : 1) * kPartBytes;
+        // CTA pair: an MMA of N columns takes its first N/2 from the leader's X rows and the next N/2 from
+        // the peer's, so the peer's X rows start at token N/2 of the tile (N = the tile's MMA N, below)
+        const int x_row0 = ti.m_start + static_cast<int>(rank) *
+                                            (min(kNTok, (ti.m_rows + 16 * C::kCG - 1) / (16 * C::kCG) * (16 * C::kCG)) / 2);
         for (int j = stage_beg(ti); j < stage_end(ti); ++j) {
           mbar_wait(&empty[st.i], st.ph ^ 1);
           if (lane == 0) {
@@ -357,7 +385,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll
             for (int h = 0; h < 2 * C::kGroupsPerStage; ++h)
               tma_load_2d(xs + h * (C::kXRows * 128), &xmap, j * C::kGroupsPerStage * kTileK + h * 64,
-                          ti.m_start + static_cast<int>(rank) * C::kXRows, &full[st.i]);
+                          x_row0, &full[st.i]);
           }
           if constexpr (kOffset) {
             // all 32 lanes copy and arrive every stage (fewer items than lanes: items are duplicated --
@@ -399,8 +427,41 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         if constexpr (!kOffset) {
           mbar_wait_warp(&accempty[acc.i], acc.ph ^ 1);
           tc_fence_after();
+          trace_at(tr, 6, it);
         }
         for (int j = stage_beg(ti); j < stage_end(ti); ++j, ++gs) {
+          if constexpr (C::kSplitA) {
+            // one A unit per part: wait, issue its 8 MMAs, release it; the stage's smem after part 1
+            const uint32_t dcol = tb_u + acc.i * C::kAccCols;
+            const uint64_t xdesc = make_sdesc_sw128(xs_u + st.i * C::kXBytes);
+#pragma unroll
+            for (int p = 0; p < C::kParts; ++p) {
+              mbar_wait_warp(&afull[ar.i], ar.ph);
+              tc_fence_after();
+              if (p == 0) trace_at(tr, 4, gs);
+              const uint32_t acol = tb_u + kAcol0 + ar.i * C::kACols;
+              // gate|up or the two n-tiles: own accumulators; k-pair: part 1 reads the second X k-group
+              const uint32_t d = dcol + (kMode == kModeKPair ? 0u : static_cast<uint32_t>(p * kNTok));
+              const uint64_t b = xdesc + (kMode == kModeKPair ? static_cast<uint64_t>(p * C::kXRows * 16) : 0ull);
+              const uint32_t accf = (j != 0 || (kMode == kModeKPair && p == 1)) ? 1u : 0u;
+              if (elect_one()) {
+                PartAsm<C::kXRows, C::kCG>::issue(d, acol, b, idesc, accf);
+                if constexpr (kPair) {
+                  umma_commit_pair(&aempty[ar.i]);
+                  if (p == C::kParts - 1) umma_commit_pair(&empty[st.i]);
+                } else {
+                  umma_commit(&aempty[ar.i]);
+                  if (p == C::kParts - 1) umma_commit(&empty[st.i]);
+                }
+              }
+              __syncwarp();
+              ar.next(C::kNumA);
+            }
+            trace_at(tr, 5, gs);
+            progress_at(2, gs + 1);
+            st.next(C::kNS);
+            continue;
+          }
           if constexpr (kOffset)  // fresh partials per stage: accumulator slot free + A slot filled
             mbar_wait2_warp(&accempty[acc.i], acc.ph ^ 1, &afull[ar.i], ar.ph);
           else
@@ -458,7 +519,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       for (int j = stage_beg(ti); j < stage_end(ti); ++j, ++gs) {
         if ((gs & 1u) != my_par) {
           st.next(C::kNS);
-          ar.next(C::kNumA);
+#pragma unroll
+          for (int u = 0; u < C::kAUnits; ++u) ar.next(C::kNumA);
           continue;
         }
         mbar_wait(&full[st.i], st.ph);
@@ -479,6 +541,37 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             zb[p] = sb[p] = 0;
           }
         }
+        if constexpr (C::kSplitA) {
+          // one A unit per part, handed to the MMA as soon as it is written
+#pragma unroll
+          for (int p = 0; p < C::kParts; ++p) {
+            mbar_wait_cluster(&aempty[ar.i], ar.ph ^ 1);
+            tc_fence_after();
+            if (trd && p == 0) trace_at(tr, 2, gs);
+            const uint32_t acol = tbase + lane_off + kAcol0 + ar.i * C::kACols;
+            const uint32_t z = (row & 1) ? (zb[p] >> 4) : (zb[p] & 15u);
+            const auto ctx = Dq<kBF16>::make(z, static_cast<uint16_t>(sb[p]));
+#pragma unroll
+            for (int c = 0; c < kChunks; ++c) {
+              uint32_t r[16];
+              dequant_chunk<kBF16, true>(v[p][c], ctx, r);
+              tmem_st_x16(acol + c * 16, r);
+            }
+            tc_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if constexpr (kPair) mbar_arrive_cluster(mapa_shared(&afull[ar.i], 0));
+              else mbar_arrive(&afull[ar.i]);
+            }
+            ar.next(C::kNumA);
+          }
+          if (trd) trace_at(tr, 3, gs);
+          if (trd) progress_at(1, gs + 1);
+          if (lane == 0) mbar_arrive(&empty[st.i]);
+          st.next(C::kNS);
+          continue;
+        }
         mbar_wait_cluster(&aempty[ar.i], ar.ph ^ 1);
         tc_fence_after();
         if (trd) trace_at(tr, 2, gs);
@@ -498,8 +591,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll
             for (int c = 0; c < kChunks; ++c) {
               uint32_t r[16];
-              dequant_chunk<kBF16, true>(v[p][c], ctx, r);
-              tmem_st_x16(acol + p * 64 + c * 16, r);
+              if constexpr (kDqExp == 0) dequant_chunk<kBF16, true>(v[p][c], ctx, r);
+              else raw_chunk<kBF16>(v[p][c], r);
+              if constexpr (kDqExp != 2) tmem_st_x16(acol + p * 64 + c * 16, r);
+              else if (r[0] == 0x12345u && r[5] == 0x777u) tmem_st_x16(acol + p * 64 + c * 16, r);
             }
           }
         }
@@ -534,6 +629,42 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       auto orow = [&](int m) -> int64_t {
         const int64_t i = static_cast<int64_t>(ti.m_start) + m;
         return (args.out_rows ? static_cast<int64_t>(__ldg(args.out_rows + i)) : i) * args.ldo;
+      };
+      // Stores of 16 tokens: lane l (< 16) computes token m0 + l's output row offset once, the values of
+      // all 16 tokens are computed branch-free first, then 16 predicated stores (one 64 B row segment
+      // per warp each). Per-token `if (m < rows) { compute; store }` blocks serialised a ~200-cycle
+      // dependent chain per token (27k cycles per 128x128 tile, measured with tools/trace_gemm.py).
+      auto row_off16 = [&](int m0) -> int64_t {
+        const int mm = m0 + static_cast<int>(lane & 15);
+        return mm < ti.m_rows ? orow(mm) : 0;
+      };
+      auto store16 = [&](int m0, int64_t ro, const uint16_t (&hb)[16], int col_off) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int64_t o = __shfl_sync(0xffffffffu, ro, i);
+          if (m0 + i < ti.m_rows) ocol[o + col_off] = hb[i];
+        }
+      };
+      // Prefill: the warp's 16-token x 32-column block goes through shared memory (token-major, 64 B per
+      // token) and out as 16-byte stores, 2 per lane: 16 2-byte stores per lane issued ~1 per 125 cycles.
+      uint8_t* const my_stage = epi_sm + (warp - kEpiWarp0) * (C::kEpiStageBytes / 4);
+      auto store16_staged = [&](int m0, int64_t ro, const uint16_t (&hb)[16], int col_off, int buf) {
+        uint8_t* sb = my_stage + buf * 1024;
+        const uint32_t sa = smem_u32(sb);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(sa + i * 64 + lane * 2), "h"(hb[i]) : "memory");
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int sgi = static_cast<int>(lane) + 32 * j;  // 16-byte segment: token sgi / 4, quarter sgi % 4
+          const int t = sgi >> 2, q = sgi & 3;
+          const int64_t o = __shfl_sync(0xffffffffu, ro, t);
+          const uint4 v = lds128(sa + t * 64 + q * 16);
+          if (m0 + t < ti.m_rows)
+            *reinterpret_cast<uint4*>(ocol - lane + o + col_off + q * 8) = v;
+        }
+        __syncwarp();  // the staging block is rewritten by the next call
       };
       if constexpr (kOffset) {
         constexpr int kOuts = kGated ? 2 : 1;  // gate|up accumulators, else one (k-pair parts summed)
@@ -616,16 +747,19 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         } else {
           float hv[kNTok];  // the stored (rounded) outputs, for the fused sums below
 #pragma unroll
-          for (int m = 0; m < kNTok; ++m) {
-            hv[m] = 0.f;
-            if (m < m_rows) {
+          for (int m0 = 0; m0 < kNTok; m0 += 16) {
+            const int64_t ro = row_off16(m0);
+            uint16_t hb[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int m = m0 + i;
               float v;
               if constexpr (kGated) v = silu_f(a[0][m]) * a[1][m];
               else v = a[0][m];
-              const uint16_t bits = to_act_bits<kBF16>(v);
-              ocol[orow(m)] = bits;
-              hv[m] = act_bits_to_float<kBF16>(bits);
+              hb[i] = to_act_bits<kBF16>(v);
+              hv[m] = m < m_rows ? act_bits_to_float<kBF16>(hb[i]) : 0.f;
             }
+            store16(m0, ro, hb, 0);
           }
           if constexpr (kGated && kNTok <= 16) {
             if (args.osum != nullptr) {
@@ -663,47 +797,46 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       } else {
         mbar_wait_cluster(&accfull[acc.i], acc.ph);
         tc_fence_after();
+        if (tre) trace_at(tr, 7, it);
         const uint32_t dcol = tbase + lane_off + acc.i * C::kAccCols;
 #pragma unroll 1
         for (int cb = 0; cb < kNTok / 16; ++cb) {
           uint32_t g[16];
           tmem_ld_x16(dcol + cb * 16, g);
+          const int64_t ro = row_off16(cb * 16);
+          uint16_t hb[16];
           if constexpr (kGated) {
             uint32_t u[16];
             tmem_ld_x16(dcol + kNTok + cb * 16, u);
             tc_wait_ld();
+            if (tre) trace_at(tr, 14, it * 32 + cb * 2);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int m = cb * 16 + i;
-              if (m < ti.m_rows) {
-                const float gv = __uint_as_float(g[i]), uv = __uint_as_float(u[i]);
-                ocol[orow(m)] = to_act_bits<kBF16>(silu_f(gv) * uv);
-              }
-            }
+            for (int i = 0; i < 16; ++i)
+              hb[i] = to_act_bits<kBF16>(silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]));
+            store16_staged(cb * 16, ro, hb, 0, 0);
+            if (tre) trace_at(tr, 14, it * 32 + cb * 2 + 1);
           } else if constexpr (C::kNPer == 2) {  // second accumulator = the next n-tile's columns
             uint32_t u[16];
             tmem_ld_x16(dcol + kNTok + cb * 16, u);
             tc_wait_ld();
+            uint16_t hu[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
-              const int m = cb * 16 + i;
-              if (m < ti.m_rows) {
-                const int64_t o = orow(m);
-                ocol[o] = to_act_bits<kBF16>(__uint_as_float(g[i]));
-                ocol[o + kTileRows] = to_act_bits<kBF16>(__uint_as_float(u[i]));
-              }
+              hb[i] = to_act_bits<kBF16>(__uint_as_float(g[i]));
+              hu[i] = to_act_bits<kBF16>(__uint_as_float(u[i]));
             }
+            store16_staged(cb * 16, ro, hb, 0, 0);
+            store16_staged(cb * 16, ro, hu, kTileRows, 1);
           } else {
             tc_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const int m = cb * 16 + i;
-              if (m < ti.m_rows) ocol[orow(m)] = to_act_bits<kBF16>(__uint_as_float(g[i]));
-            }
+            for (int i = 0; i < 16; ++i) hb[i] = to_act_bits<kBF16>(__uint_as_float(g[i]));
+            store16_staged(cb * 16, ro, hb, 0, 0);
           }
         }
         tc_fence_before();
         __syncwarp();
+        if (tre) trace_at(tr, 8, it);
         if (lane == 0) {
           if constexpr (kPair) mbar_arrive_cluster(mapa_shared(&accempty[acc.i], 0));
           else mbar_arrive(&accempty[acc.i]);
@@ -877,6 +1010,7 @@ int make_x_map(CUtensorMap* map, const void* x, int64_t rows, int64_t K, int box
 
 int sm_count() {
   static int n = 0;
+  if (!n && getenv("W4A16_GRID")) n = atoi(getenv("W4A16_GRID"));  // debug: persistent grid override
   if (!n) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) !=
@@ -1024,6 +1158,9 @@ extern "C" {
 int w4a16_debug_trace(void* buf) {
   return cudaMemcpyToSymbol(g_w4_trace, &buf, sizeof(buf)) == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
+int w4a16_debug_trace_cta(int cta) {
+  return cudaMemcpyToSymbol(g_w4_trace_cta, &cta, sizeof(cta)) == cudaSuccess ? W4_OK : W4_ERR_CUDA;
+}
 
 int w4a16_tile_rows(void) { return kTileRows; }
 int w4a16_tile_k(void) { return kTileK; }
@@ -1059,6 +1196,8 @@ int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t*
   if (K <= 0 || K % kTileK || n_out <= 0 || n_out % kTileRows) return W4_ERR_SHAPE;
   if (num_experts <= 0 || num_experts > kMaxExperts) return W4_ERR_SHAPE;
   if (dtype != W4_DTYPE_F16 && dtype != W4_DTYPE_BF16) return W4_ERR_DTYPE;
+  // TMA reads of x and the epilogue's 16-byte stores
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out)) & 15) return W4_ERR_ARG;
   if (rows <= 0) return W4_OK;
   if (ntok != 0 && ntok != 16 && ntok != 32 && ntok != 64 && ntok != 128) return W4_ERR_ARG;
   GemmPlan pl = plan_gemm(rows, K, num_experts, n_out, gated, xsum != nullptr, ntok);

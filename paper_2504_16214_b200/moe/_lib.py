@@ -59,6 +59,7 @@ SIGNATURES = {
 # debug aids exported by the library but not part of the public header
 DEBUG_SIGNATURES = {
     "w4a16_debug_trace": (_i, [_p]),
+    "w4a16_debug_trace_cta": (_i, [_i]),
 }
 
 _lock = threading.Lock()

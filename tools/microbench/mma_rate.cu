@@ -6,15 +6,16 @@
 #include "ptx.cuh"
 using namespace w4;
 
-template <int N, bool kTS, int kChains, int kStWarps = 0, int kSmemWarps = 0>
+template <int N, bool kTS, int kChains, int kStWarps = 0, int kSmemWarps = 0, int kCommits = 0>
 __global__ void mma_rate(int iters, long long* out) {
   __shared__ __align__(1024) uint8_t smem[2 * 16384 + 1024];
   __shared__ uint32_t holder;
   __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t cbar[4];
   const int warp = threadIdx.x / 32;
   for (int i = threadIdx.x; i < (2 * 16384) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0x3c003c00u;
   if (warp == 0) tmem_alloc<512>(&holder);
-  if (threadIdx.x == 32) { mbar_init(&bar, 1); fence_mbar_init(); }
+  if (threadIdx.x == 32) { mbar_init(&bar, 1); for (int i = 0; i < 4; ++i) mbar_init(&cbar[i], 1); fence_mbar_init(); }
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -35,6 +36,8 @@ __global__ void mma_rate(int iters, long long* out) {
                        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
                        "l"(adesc + (k & 3) * 2), "l"(bdesc + (k & 3) * 2), "r"(idesc) : "memory");
         }
+        // kCommits commits per 16 MMAs (never waited on): does a commit serialise the MMA pipe?
+        if (kCommits > 0 && (k + 1) % (16 / (kCommits > 0 ? kCommits : 1)) == 0) umma_commit_warp(&cbar[k & 3]);
       }
     }
     long long t1 = clock64();
@@ -71,14 +74,15 @@ __global__ void mma_rate(int iters, long long* out) {
   if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tb); }
 }
 
-template <int N, bool kTS, int kChains, int kStWarps = 0, int kSmemWarps = 0>
+template <int N, bool kTS, int kChains, int kStWarps = 0, int kSmemWarps = 0, int kCommits = 0>
 void run(long long* d) {
   const int iters = 200;
   cudaMemset(d, 0, 32);
-  mma_rate<N, kTS, kChains, kStWarps, kSmemWarps><<<1, 64 + 32 * (kStWarps + kSmemWarps)>>>(iters, d);
+  mma_rate<N, kTS, kChains, kStWarps, kSmemWarps, kCommits><<<1, 64 + 32 * (kStWarps + kSmemWarps)>>>(iters, d);
   cudaError_t e = cudaDeviceSynchronize();
   long long h[3];
   cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  printf("commits/16=%d ", kCommits);
   printf("smemw=%d N=%3d %s chains=%d st_warps=%d : issue %.1f cyc/mma, complete %.1f cyc/mma; st %.1f cyc per 8xSTTM %s\n", N,
          kSmemWarps, kTS ? "ts" : "ss", kChains, kStWarps, (double)h[0] / (iters * 16), (double)h[1] / (iters * 16),
          kStWarps ? (double)h[2] / (iters * 4) : 0.0, e == cudaSuccess ? "" : cudaGetErrorString(e));
@@ -88,6 +92,8 @@ int main() {
   long long* d;
   cudaMalloc(&d, 64);
   run<128, true, 2>(d); run<128, true, 2, 4>(d); run<128, true, 2, 4, 4>(d); run<128, true, 2, 8, 4>(d);
+  run<128, true, 2, 0, 0, 1>(d); run<128, true, 2, 0, 0, 2>(d); run<128, true, 2, 0, 0, 4>(d);
+  run<16, true, 4, 0, 0, 1>(d); run<16, true, 4, 0, 0, 4>(d);
   run<64, true, 2>(d); run<64, true, 2, 4, 4>(d); run<16, true, 4, 4, 4>(d);
   return 0;
 }

@@ -20,6 +20,8 @@ ap.add_argument("--which", default="gate_up")
 ap.add_argument("--experts", type=int, default=224)
 ap.add_argument("--per-expert", type=int, default=2)
 ap.add_argument("--ntok", type=int, default=16)
+ap.add_argument("--cta", type=int, default=0, help="CTA whose timeline is recorded")
+ap.add_argument("--xscale", type=float, default=0.5, help="0 = all-zero activations (data-dependent power probe)")
 a = ap.parse_args()
 H, I = 7168, 2048
 dev = torch.device("cuda", 0)
@@ -31,12 +33,13 @@ w = random_packed(E, N, K, gated, torch.float16, gd, dev)
 counts = torch.full((E,), a.per_expert, dtype=torch.int32, device=dev)
 off = torch.zeros(E + 1, dtype=torch.int32, device=dev)
 off[1:] = torch.cumsum(counts, 0)
-x = (torch.randn((E * a.per_expert, K), device=dev) * 0.5).half()
+x = (torch.randn((E * a.per_expert, K), device=dev) * a.xscale).half()
 nout = N // 2 if gated else N
 xs = ops.group_sums(x) if a.ntok <= 32 else None
 for _ in range(2):
     ops.grouped_gemm(x, w.blocks, E, nout, gated, counts, off, a.ntok, xsum=xs)
-buf = torch.full((14, 4096), -1, dtype=torch.int64, device=dev)
+buf = torch.full((16, 4096), -1, dtype=torch.int64, device=dev)
+_lib.call("w4a16_debug_trace_cta", a.cta)
 _lib.call("w4a16_debug_trace", buf.data_ptr())
 torch.cuda.synchronize()
 ops.grouped_gemm(x, w.blocks, E, nout, gated, counts, off, a.ntok, xsum=xs)
@@ -64,6 +67,15 @@ print(f"  producer: empty_ok(gs) - mma_ready(gs)   {m(t[0][s] - t[4][s]):8.1f}")
 print(f"  dq aempty_ok(gs) - mma_issued(gs-3)      {m(t[2][lo + 3:hi] - t[5][lo:hi - 3]):8.1f}")
 print(f"  mma_ready(gs) - epi_done(gs-2)           {m(t[4][lo + 2:hi] - t[8][lo:hi - 2]):8.1f}")
 print(f"  full_ok(dq) - prod_empty_ok (load lat)   {m(t[1][s] - t[0][s]):8.1f}")
+if a.ntok > 32:  # prefill: per-tile epilogue (events 6-8 indexed by tile)
+    nt_ = int((t[7] >= 0).sum())
+    if nt_ > 2:
+        print(f"  prefill tiles {nt_}: epilogue accfull_ok -> done   {m(t[8][:nt_] - t[7][:nt_]):8.1f}")
+        print(f"  MMA tile start (accempty ok) - prev accfull_ok  {m(t[6][1:nt_] - t[7][:nt_ - 1]):8.1f}")
+        e = t[14][: nt_ * 32].reshape(nt_, 32)[1:-1]
+        print("  epilogue per 16-token chunk: [ld-wait done, stores done] rel. to accfull_ok, mean over tiles:")
+        print("   ", np.round((e - t[7][1:nt_ - 1, None]).mean(0)).astype(int).tolist())
+        print(f"  tile period                                     {m(np.diff(t[7][:nt_])):8.1f}")
 ts = t[9][t[9] >= 0]
 print(f"  tiles traced {len(ts)}")
 print("  first 12 stages (cycles rel.):")
