@@ -251,6 +251,14 @@ W4_DEV void tmem_ld_x16(uint32_t taddr, uint32_t (&r)[16]) {
       : "memory");
 }
 
+// Orders later uses of tcgen05.ld destination registers after the tcgen05.wait::ld that precedes this
+// call: the (volatile) empty asm "rewrites" them, so the compiler cannot hoist their consumers above it.
+W4_DEV void reg_fence16(uint32_t (&r)[16]) {
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]));
+}
+
 // tcgen05.ld 32 lanes x 32 bit, 4 consecutive columns
 W4_DEV void tmem_ld_x4(uint32_t taddr, uint32_t (&r)[4]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"

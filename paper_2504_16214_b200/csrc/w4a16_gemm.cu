@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   uint64_t* accfull = aempty + C::kNumA;
   uint64_t* accempty = accfull + C::kNumAcc;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accempty + C::kNumAcc);
+  uint64_t* trbar = accempty + C::kNumAcc + 2;  // trace builds: per-stage MMA completion (8-deep ring)
   int* mt_off = reinterpret_cast<int*>(bars + 256);
   uint2* tile_tab = reinterpret_cast<uint2*>(mt_off + kMaxExperts + 2);  // 8-byte aligned (odd int count + 1)
   int* n_tiles_sm = mt_off + kMaxExperts + 1;
@@ -304,6 +305,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     for (int i = 0; i < C::kNS; ++i) { mbar_init(&full[i], C::kFullArrivals); mbar_init(&empty[i], C::kEmptyArrivals); }
     for (int i = 0; i < C::kNumA; ++i) { mbar_init(&afull[i], C::kAFullArrivals); mbar_init(&aempty[i], 1); }
     for (int i = 0; i < C::kNumAcc; ++i) { mbar_init(&accfull[i], 1); mbar_init(&accempty[i], C::kAccEmptyArrivals); }
+#ifdef W4A16_TRACE
+    for (int i = 0; i < 8; ++i) mbar_init(&trbar[i], 1);
+#endif
     fence_mbar_init();
   } else if (warp == 2) {
     // PDL: TMEM allocation and barrier init above overlap the previous kernel; expert counts / X / sums
@@ -354,6 +358,17 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // lane 0: weight block (1-D bulk copy) + X tile (2-D TMA) on the stage's full barrier (tx bytes);
     // offset mode: all 32 lanes also copy the stage's (C, S) sums with 8-byte cp.async and arrive on
     // the same barrier when their copies land.
+#ifdef W4A16_TRACE
+    if (!kOffset && lane == 1 && tr && !kPair) {  // MMA completion times (trace event 15)
+      uint32_t n = 0;
+      TileInfo ti;
+      for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it)
+        for (int j = stage_beg(ti); j < stage_end(ti); ++j, ++n) {
+          mbar_wait(&trbar[n & 7], (n >> 3) & 1);
+          trace_at(tr, 15, n);
+        }
+    }
+#endif
     if (kOffset || lane == 0) {
       const uint64_t pol_w = policy_evict_first();
       Ring st;
@@ -476,6 +491,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             StageAsm<kNTok, (kMode == kModeNPair ? kModeGateUp : kMode), C::kCG, kOffset, C::kKSplit>::issue(
                 dcol, acol, xdesc, idesc, static_cast<uint32_t>(j));
             trace_at(tr, 5, gs);
+#ifdef W4A16_TRACE
+            if (!kOffset && !kPair && tr) umma_commit(&trbar[gs & 7]);
+#endif
             if constexpr (kPair) {
               umma_commit_pair(&empty[st.i]);
               umma_commit_pair(&aempty[ar.i]);
@@ -799,16 +817,21 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         tc_fence_after();
         if (tre) trace_at(tr, 7, it);
         const uint32_t dcol = tbase + lane_off + acc.i * C::kAccCols;
-#pragma unroll 1
-        for (int cb = 0; cb < kNTok / 16; ++cb) {
-          uint32_t g[16];
+        constexpr bool kTwo = kGated || C::kNPer == 2;  // two accumulators: gate|up, or two n-tiles
+        constexpr int kNChunks = kNTok / 16;
+        auto load = [&](int cb, uint32_t (&g)[16], uint32_t (&u)[16]) {
           tmem_ld_x16(dcol + cb * 16, g);
+          if constexpr (kTwo) tmem_ld_x16(dcol + kNTok + cb * 16, u);
+        };
+        auto landed = [&](uint32_t (&g)[16], uint32_t (&u)[16]) {
+          tc_wait_ld();
+          reg_fence16(g);
+          if constexpr (kTwo) reg_fence16(u);
+        };
+        auto process = [&](int cb, const uint32_t (&g)[16], const uint32_t (&u)[16]) {
           const int64_t ro = row_off16(cb * 16);
           uint16_t hb[16];
           if constexpr (kGated) {
-            uint32_t u[16];
-            tmem_ld_x16(dcol + kNTok + cb * 16, u);
-            tc_wait_ld();
             if (tre) trace_at(tr, 14, it * 32 + cb * 2);
 #pragma unroll
             for (int i = 0; i < 16; ++i)
@@ -816,9 +839,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             store16_staged(cb * 16, ro, hb, 0, 0);
             if (tre) trace_at(tr, 14, it * 32 + cb * 2 + 1);
           } else if constexpr (C::kNPer == 2) {  // second accumulator = the next n-tile's columns
-            uint32_t u[16];
-            tmem_ld_x16(dcol + kNTok + cb * 16, u);
-            tc_wait_ld();
             uint16_t hu[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -828,10 +848,26 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             store16_staged(cb * 16, ro, hb, 0, 0);
             store16_staged(cb * 16, ro, hu, kTileRows, 1);
           } else {
-            tc_wait_ld();
 #pragma unroll
             for (int i = 0; i < 16; ++i) hb[i] = to_act_bits<kBF16>(__uint_as_float(g[i]));
             store16_staged(cb * 16, ro, hb, 0, 0);
+          }
+        };
+        // TMEM loads of chunk cb + 1 overlap the conversion and stores of chunk cb (two register sets)
+        uint32_t gA[16], uA[16], gB[16], uB[16];
+        load(0, gA, uA);
+        landed(gA, uA);
+        if constexpr (kNChunks == 1) {
+          process(0, gA, uA);
+        } else {
+#pragma unroll 1
+          for (int cb = 0; cb < kNChunks; cb += 2) {
+            load(cb + 1, gB, uB);
+            process(cb, gA, uA);
+            landed(gB, uB);
+            if (cb + 2 < kNChunks) load(cb + 2, gA, uA);
+            process(cb + 1, gB, uB);
+            landed(gA, uA);
           }
         }
         tc_fence_before();

@@ -76,6 +76,13 @@ if a.ntok > 32:  # prefill: per-tile epilogue (events 6-8 indexed by tile)
         print("  epilogue per 16-token chunk: [ld-wait done, stores done] rel. to accfull_ok, mean over tiles:")
         print("   ", np.round((e - t[7][1:nt_ - 1, None]).mean(0)).astype(int).tolist())
         print(f"  tile period                                     {m(np.diff(t[7][:nt_])):8.1f}")
+if (t[15] >= 0).sum() > 8:  # MMA completion per stage (non-offset, trace build)
+    c = t[15][s]
+    print(f"  MMA complete period                              {np.diff(c).mean():8.1f}")
+    print(f"  MMA complete(gs) - issued(gs)                    {m(c - t[5][s]):8.1f}")
+    busy = np.minimum(np.diff(c), c[1:] - t[5][lo + 1:hi])
+    print(f"  stage exec est. (complete - max(prev complete, issued)) {m(busy):8.1f}")
+    print(f"  MMA issued(gs) - complete(gs-1) (<0: queued behind)      {m(t[5][lo + 1:hi] - c[:-1]):8.1f}")
 ts = t[9][t[9] >= 0]
 print(f"  tiles traced {len(ts)}")
 print("  first 12 stages (cycles rel.):")
