@@ -136,7 +136,7 @@ struct Cfg {
   static constexpr int kStageBytes = kBlk + kXBytes + kSumBytes;
   // barriers, m-tile prefix, tile table, epilogue cross-warp reduction scratch (4 warps x 16 x float2)
   // prefill epilogue: per-warp staging of a 16-token x 32-column output block (x2 for n-pair tiles)
-  static constexpr int kEpiStageBytes = kOffset ? 0 : 4 * 1024 * (kNPer == 2 ? 2 : 1);  // [4 warps][...], 16 B aligned
+  static constexpr int kEpiStageBytes = 4 * 1024 * (kNPer == 2 ? 2 : 1);  // [4 warps][...], 16 B aligned
   static constexpr int kFixed = 2048 + 4 * (kMaxExperts + 2) + 8 * kTileTab + 512 + 16 + kEpiStageBytes;
   static constexpr int kNS0 = (kSmemBudget - kFixed - 1024) / kStageBytes;
   static constexpr int kNS = kNS0 > 12 ? 12 : kNS0;
@@ -648,23 +648,16 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         const int64_t i = static_cast<int64_t>(ti.m_start) + m;
         return (args.out_rows ? static_cast<int64_t>(__ldg(args.out_rows + i)) : i) * args.ldo;
       };
-      // Stores of 16 tokens: lane l (< 16) computes token m0 + l's output row offset once, the values of
-      // all 16 tokens are computed branch-free first, then 16 predicated stores (one 64 B row segment
-      // per warp each). Per-token `if (m < rows) { compute; store }` blocks serialised a ~200-cycle
-      // dependent chain per token (27k cycles per 128x128 tile, measured with tools/trace_gemm.py).
+      // Stores of 16 tokens: lane l (< 16) computes token m0 + l's output row offset once and the values
+      // of all 16 tokens are computed branch-free first (per-token `if (m < rows) { compute; store }`
+      // blocks serialised a ~200-cycle dependent chain per token: 27k cycles per 128x128 tile, measured
+      // with tools/trace_gemm.py).
       auto row_off16 = [&](int m0) -> int64_t {
         const int mm = m0 + static_cast<int>(lane & 15);
         return mm < ti.m_rows ? orow(mm) : 0;
       };
-      auto store16 = [&](int m0, int64_t ro, const uint16_t (&hb)[16], int col_off) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int64_t o = __shfl_sync(0xffffffffu, ro, i);
-          if (m0 + i < ti.m_rows) ocol[o + col_off] = hb[i];
-        }
-      };
-      // Prefill: the warp's 16-token x 32-column block goes through shared memory (token-major, 64 B per
-      // token) and out as 16-byte stores, 2 per lane: 16 2-byte stores per lane issued ~1 per 125 cycles.
+      // The warp's 16-token x 32-column block then goes through shared memory (token-major, 64 B per
+      // token) and out as 16-byte stores, 2 per lane (16 2-byte stores per lane issued ~1 per 125 cycles).
       uint8_t* const my_stage = epi_sm + (warp - kEpiWarp0) * (C::kEpiStageBytes / 4);
       auto store16_staged = [&](int m0, int64_t ro, const uint16_t (&hb)[16], int col_off, int buf) {
         uint8_t* sb = my_stage + buf * 1024;
@@ -777,7 +770,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               hb[i] = to_act_bits<kBF16>(v);
               hv[m] = m < m_rows ? act_bits_to_float<kBF16>(hb[i]) : 0.f;
             }
-            store16(m0, ro, hb, 0);
+            store16_staged(m0, ro, hb, 0, 0);
           }
           if constexpr (kGated && kNTok <= 16) {
             if (args.osum != nullptr) {
