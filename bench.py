@@ -444,31 +444,37 @@ def main():
 
     # ---- end to end through the public API with host buffers (H2D inputs, D2H output)
     y_host = torch.empty((T, H_DS), dtype=tdt).pin_memory()
-    for _ in range(2):
-        if graphed is not None:
-            y_host.copy_(graphed(x_host, lg_host), non_blocking=True)  # H2D into the graph's inputs
+    pipe = None
+    if graphed is not None:  # serving loop: H2D of step i+1 and D2H of step i overlap step i's layer
+        from paper_2504_16214_b200.moe import FusedMoEPipeline
+        pipe = FusedMoEPipeline(weights, T, K_DS, "softmax", True, tdt, dev, x=x, router_logits=lg)
+
+    def e2e_steps(n):
+        if pipe is not None:
+            pipe.start()
+            for _ in range(n):
+                pipe(x_host, lg_host, y_host)
+            pipe.finish()
         else:
-            xx = x_host.to(dev, non_blocking=True)
-            ll = lg_host.to(dev, non_blocking=True)
-            y_host.copy_(step(None, xx, ll), non_blocking=True)
+            for _ in range(n):
+                xx = x_host.to(dev, non_blocking=True)
+                ll = lg_host.to(dev, non_blocking=True)
+                y_host.copy_(step(None, xx, ll), non_blocking=True)
+
+    e2e_steps(3)
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(args.steps):
-        if graphed is not None:
-            y_host.copy_(graphed(x_host, lg_host), non_blocking=True)
-        else:
-            xx = x_host.to(dev, non_blocking=True)
-            ll = lg_host.to(dev, non_blocking=True)
-            y_host.copy_(step(None, xx, ll), non_blocking=True)
+    e2e_steps(args.steps)
     e1.record()
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
     e2e = {"value": round(job_bytes / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
            "h2d_bytes_per_step": x_host.numel() * x_host.element_size() + lg_host.numel() * 4,
            "d2h_bytes_per_step": y_host.numel() * y_host.element_size(), "ms_per_step": round(e2e_ms, 4),
-           "api": ("paper_2504_16214_b200.moe.FusedMoEGraph (CUDA graph of fused_moe_w4a16)" if graphed is not None
+           "api": ("paper_2504_16214_b200.moe.FusedMoEPipeline (CUDA-graph layer steps, H2D/D2H on copy streams "
+                   "overlapping the neighbouring steps)" if graphed is not None
                    else "paper_2504_16214_b200.moe.fused_moe_w4a16")}
 
     # ---- regime sweep (1 GPU only): decode .. prefill, same weights

@@ -1,9 +1,10 @@
 """W4A16 mixture-of-experts operator on B200 (sm_100a CUDA kernels behind a C ABI)."""
-from .layer import FusedMoEGraph, fused_moe_w4a16, moe_w4a16, select_experts, w4a16_linear
+from .layer import FusedMoEGraph, FusedMoEPipeline, fused_moe_w4a16, moe_w4a16, select_experts, w4a16_linear
 from .weights import MoEWeights, PackedW4, pack_awq, pack_moe_awq, random_moe_weights
 
 __all__ = [
     "FusedMoEGraph",
+    "FusedMoEPipeline",
     "MoEWeights",
     "PackedW4",
     "fused_moe_w4a16",

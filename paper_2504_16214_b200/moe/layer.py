@@ -197,6 +197,73 @@ class FusedMoEGraph:
         return self.y
 
 
+class FusedMoEPipeline:
+    """Serving loop over host batches with the copies off the critical path: the host->device copy
+    of step i+1 and the device->host copy of step i run on their own streams while step i's layer
+    (a FusedMoEGraph replay) runs. Two graph slots (own input and output buffers; weights and
+    workspaces shared, replays serialised on the caller's stream) make that safe:
+
+        pipe = FusedMoEPipeline(weights, tokens, top_k, ...)
+        pipe.start()
+        for x_h, lg_h, y_h in batches:   # pinned host tensors
+            pipe(x_h, lg_h, y_h)         # enqueue only: H2D, layer, D2H
+        pipe.finish()                    # the caller's stream now waits for the last D2H
+
+    Every step still moves its own inputs in and its own output out; only the overlap changes."""
+
+    def __init__(self, weights: MoEWeights, tokens: int, top_k: int, scoring: str = "softmax",
+                 renormalize: bool = False, dtype: torch.dtype = torch.float16, device=None,
+                 x: torch.Tensor | None = None, router_logits: torch.Tensor | None = None):
+        self.dev = torch.device(device) if device is not None else weights.w13.blocks.device
+        self.slots = [FusedMoEGraph(weights, tokens, top_k, scoring, renormalize, dtype, self.dev, x, router_logits)
+                      for _ in range(2)]
+        self.h2d = torch.cuda.Stream(device=self.dev)
+        self.d2h = torch.cuda.Stream(device=self.dev)
+        self.i = 0
+        self._reset_events()
+
+    def _reset_events(self):
+        mk = lambda: [torch.cuda.Event(), torch.cuda.Event()]  # noqa: E731
+        self.h2d_done, self.comp_done, self.d2h_done = mk(), mk(), mk()
+        self.used = [False, False]
+
+    def start(self):
+        """Order the copy streams after everything already queued on the caller's stream."""
+        cur = torch.cuda.current_stream(self.dev)
+        self.h2d.wait_stream(cur)
+        self.d2h.wait_stream(cur)
+
+    def __call__(self, x_host: torch.Tensor, logits_host: torch.Tensor, y_host: torch.Tensor) -> torch.Tensor:
+        s = self.i & 1
+        self.i += 1
+        g = self.slots[s]
+        cur = torch.cuda.current_stream(self.dev)
+        if self.used[s]:  # the slot's inputs are free once its previous replay is done
+            self.h2d.wait_event(self.comp_done[s])
+        with torch.cuda.stream(self.h2d):
+            g.x.copy_(x_host, non_blocking=True)
+            g.logits.copy_(logits_host, non_blocking=True)
+            self.h2d_done[s].record(self.h2d)
+        cur.wait_event(self.h2d_done[s])
+        if self.used[s]:  # and its output once the previous device->host copy is done
+            cur.wait_event(self.d2h_done[s])
+        g.graph.replay()
+        self.comp_done[s].record(cur)
+        self.d2h.wait_event(self.comp_done[s])
+        with torch.cuda.stream(self.d2h):
+            y_host.copy_(g.y, non_blocking=True)
+            self.d2h_done[s].record(self.d2h)
+        self.used[s] = True
+        return y_host
+
+    def finish(self):
+        """The caller's stream waits for every queued copy (y_host of every step is then valid once
+        that stream reaches this point)."""
+        cur = torch.cuda.current_stream(self.dev)
+        cur.wait_stream(self.d2h)
+        cur.wait_stream(self.h2d)
+
+
 _LINEAR_ROUTING: dict = {}
 
 

@@ -292,6 +292,33 @@ def test_fused_moe_graph_matches_eager():
         assert torch.equal(got, want)
 
 
+def test_fused_moe_pipeline_matches_eager():
+    """The copy-overlapped serving loop (two graph slots, H2D / D2H streams): every step's host output
+    equals the eager layer on that step's host inputs, across slot reuse."""
+    from paper_2504_16214_b200.moe import FusedMoEPipeline, fused_moe_w4a16
+    from paper_2504_16214_b200.moe.weights import MoEWeights
+    rng = np.random.default_rng(22)
+    T, E, k, H, I, dt = 12, 16, 4, 512, 256, "f16"
+    q13, z13, s13 = O.synth_awq_expert_weights(rng, E, 2 * I, H, dt)
+    q2, z2, s2 = O.synth_awq_expert_weights(rng, E, H, I, dt)
+    weights = MoEWeights(_packed(q13, z13, s13, dt, True), _packed(q2, z2, s2, dt, False))
+    pipe = FusedMoEPipeline(weights, T, k, "softmax", True, torch.float16)
+    xs, lgs, ys = [], [], []
+    for seed in range(5):
+        r = np.random.default_rng(100 + seed)
+        xs.append(_to_dev_act(O.round_act(r.standard_normal((T, H)).astype(np.float32) * 0.5, dt), dt).cpu().pin_memory())
+        lgs.append(torch.from_numpy(r.standard_normal((T, E)).astype(np.float32)).pin_memory())
+        ys.append(torch.empty((T, H), dtype=torch.float16).pin_memory())
+    pipe.start()
+    for x, lg, y in zip(xs, lgs, ys):
+        pipe(x, lg, y)
+    pipe.finish()
+    torch.cuda.synchronize()
+    for x, lg, y in zip(xs, lgs, ys):
+        want = fused_moe_w4a16(x.cuda(), lg.cuda(), weights, k, "softmax", True).cpu()
+        assert torch.equal(y, want)
+
+
 @pytest.mark.parametrize("world,el", [(1, 256), (2, 128), (8, 32), (4, 3)])
 def test_ep_local_order(world, el):
     """Receiver-side local-expert order from the received counts == ids + stable permutation."""

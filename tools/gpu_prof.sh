@@ -14,3 +14,8 @@ for skip in 0 1; do
      -o gpurun_out/prof_gemm$skip -f python bench.py --steps 1 --warmup 0 --no-sweep --no-cpu --tokens $T > gpurun_out/ncu_full$skip.log 2>&1
   echo "ncu full $skip rc=$?"; tail -2 gpurun_out/ncu_full$skip.log
 done
+# prefill: one 128-token gate/up launch (64 experts x 256 rows, full tiles)
+timeout 420 ncu --set full --clock-control none --import-source on -k regex:w4a16_moe_gemm -s 2 -c 1 \
+   -o gpurun_out/prof_prefill -f python tools/prof_one.py --which gate_up --experts 64 --per-expert 256 --ntok 128 --reps 3 --sums 0 \
+   > gpurun_out/ncu_prefill.log 2>&1
+echo "ncu prefill rc=$?"; tail -2 gpurun_out/ncu_prefill.log

@@ -46,13 +46,13 @@ ops.grouped_gemm(x, w.blocks, E, nout, gated, counts, off, a.ntok, xsum=xs)
 torch.cuda.synchronize()
 _lib.call("w4a16_debug_trace", None)
 t = buf.cpu().numpy()
-n = int((t[4] >= 0).sum())
+n = int(max((t[4] >= 0).sum(), (t[1] >= 0).sum()))  # the peer CTA of a pair records no MMA events
 t0 = t[t >= 0].min()
 t = np.where(t >= 0, t - t0, -1)
 lo, hi = n // 4, 3 * n // 4
 s = slice(lo, hi)
 print(f"{a.which}: stages traced {n}, steady window [{lo},{hi})")
-per = np.diff(t[4][s]).mean()
+per = np.diff(t[4][s] if (t[4] >= 0).sum() else t[1][s]).mean()
 print(f"  stage period (mma_ready diffs)          {per:8.1f} cyc")
 def m(x):
     return float(np.mean(x))

@@ -50,7 +50,8 @@ def main():
         shutil.copy(OUT / "bench.json", dst / "bench.json")
     if (OUT / "launches.csv").exists():
         (dst / "launches.txt").write_text(launch_shares(OUT / "launches.csv"))
-    reps = [OUT / r for r in ("prof_gemm0.ncu-rep", "prof_gemm1.ncu-rep", a.rep) if (OUT / r).exists()]
+    reps = [OUT / r for r in ("prof_gemm0.ncu-rep", "prof_gemm1.ncu-rep", "prof_prefill.ncu-rep", a.rep)
+            if (OUT / r).exists()]
     summ, hot = [], []
     for rep in reps:
         py = sys.executable
@@ -73,7 +74,8 @@ def main():
             if "w4a16_moe_gemm_kernel" in name:
                 targs = name.replace("(int)", "").replace("(bool)", "").split("<", 1)[1].split(">")[0].split(",")
                 mode = int(targs[1])  # template <kNTok, kMode, ...>: 1 = gate/up, 2 = k-pair down, 0 = plain
-                traffic[f"gemm_{'gate_up' if mode == 1 else 'down'}_T{a.tokens}"] = int(b)
+                sfx = "prefill_ntok128" if "prefill" in rep.name else f"T{a.tokens}"
+                traffic[f"gemm_{'gate_up' if mode == 1 else 'down'}_{sfx}"] = int(b)
         tr_path.write_text(json.dumps(traffic, indent=1, sort_keys=True) + "\n")
     if summ:
         (dst / "ncu_full_summary.txt").write_text("".join(summ))
