@@ -47,7 +47,9 @@ constexpr int kSmemBudget = 225 * 1024;
 #ifndef W4A16_SPLITA
 #define W4A16_SPLITA 0
 #endif
-constexpr bool kSplitAEnv = W4A16_SPLITA != 0;  // experiment: per-part TMEM A units at prefill
+// experiment (-DW4A16_SPLITA=1): prefill k-half TMEM A units; measured slower (gate/up T=8192 3.57 vs
+// 3.43 ms), see the Cfg comment
+constexpr bool kSplitAEnv = W4A16_SPLITA != 0;
 #ifndef W4A16_DQEXP
 #define W4A16_DQEXP 0
 #endif
@@ -114,12 +116,16 @@ struct Cfg {
   // one accumulator stage: offset mode = kKSplit partials per part; otherwise gate|up or one
   // accumulator for the whole tile
   static constexpr int kAccCols = kOffset ? kParts * kKSplit * kNTok : ((kGated || kNPer == 2) ? 2 * kNTok : kNTok);
-  // Prefill two-part stages use a split A ring: one 64-column TMEM unit per part, released per part
-  // by the MMA, so the dequant of the next part overlaps the MMAs of this one (with whole-stage
-  // slots the gate/up tile ran ~1300-1800 cycles per 1024-cycle stage: a slot was held for a whole
-  // dequant + MMA round trip and two slots did not cover it; tools/trace_gemm.py).
+  // Prefill two-part stages use a split A ring: one 64-column TMEM unit per k half of the stage
+  // (both parts' k = 64h .. 64h+63), converted by dequant group h and released per unit by the MMA.
+  // With whole-stage slots the MMA waited for each stage's dequant: TMEM fits only two 128-column
+  // slots beside the 256-column gate|up accumulator, and a slot is busy for a whole dequant + MMA
+  // round trip (stage period ~1440 cycles for 1024 of MMA, tools/trace_gemm.py). With half-stage
+  // units the same 256 columns hold four units and each unit's round trip is half as long -- but the
+  // measured stage period got longer (~1750 cycles: the MMA warp idles on the second group's units),
+  // so this stays an experiment.
   static constexpr bool kSplitA = kSplitAEnv && !kOffset && kParts == 2;
-  static constexpr int kAUnits = kSplitA ? kParts : 1;  // A-ring slots per stage
+  static constexpr int kAUnits = kSplitA ? 2 : 1;  // A-ring slots per stage
   static constexpr int kACols = (kSplitA ? 1 : kParts) * (kTileK / 2);  // fp16 pairs per 32-bit column
   // TMEM budget (512 columns): A ring + accumulator ring
   // 3 A slots if two accumulator stages still fit, else 2; the gated prefill projection (56-stage
@@ -140,10 +146,12 @@ struct Cfg {
   static constexpr int kFixed = 2048 + 4 * (kMaxExperts + 2) + 8 * kTileTab + 512 + 16 + kEpiStageBytes;
   static constexpr int kNS0 = (kSmemBudget - kFixed - 1024) / kStageBytes;
   static constexpr int kNS = kNS0 > 12 ? 12 : kNS0;
-  static constexpr int kEmptyArrivals = kDequantGroup + 1 + (kOffset ? 4 : 0);
+  // dequant warps reading a stage's smem: one group, or both (split ring: group h converts k half h)
+  static constexpr int kDqPerStage = kSplitA ? 2 * kDequantGroup : kDequantGroup;
+  static constexpr int kEmptyArrivals = kDqPerStage + 1 + (kOffset ? 4 : 0);
   static constexpr int kSumItems = kGroupsPerStage * kNTok;      // 8-byte (C, S) items per stage
   static constexpr int kFullArrivals = 1 + (kOffset ? 32 : 0);   // expect_tx + the 32 sums cp.async lanes
-  static constexpr int kAFullArrivals = kDequantGroup * kCG;     // dequant groups of both CTAs (leader)
+  static constexpr int kAFullArrivals = kDequantGroup * kCG;     // one dequant group of both CTAs (leader)
   static constexpr int kAccEmptyArrivals = 4 * kCG;              // epilogue warps of both CTAs (leader)
   // X ring first (needs 1024 B alignment for the 128B swizzle atoms), sums ring, then weights.
   static constexpr int kSmemBytes = 1024 + kNS * kStageBytes + kFixed;
@@ -446,33 +454,36 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
         for (int j = stage_beg(ti); j < stage_end(ti); ++j, ++gs) {
           if constexpr (C::kSplitA) {
-            // one A unit per part: wait, issue its 8 MMAs, release it; the stage's smem after part 1
+            // one A unit per k half: wait, issue its 8 MMAs (both parts), release it; the stage's smem
+            // (X tile) after the second half
             const uint32_t dcol = tb_u + acc.i * C::kAccCols;
+            const uint32_t d1 = dcol + (kMode == kModeKPair ? 0u : static_cast<uint32_t>(kNTok));
             const uint64_t xdesc = make_sdesc_sw128(xs_u + st.i * C::kXBytes);
 #pragma unroll
-            for (int p = 0; p < C::kParts; ++p) {
+            for (int h = 0; h < 2; ++h) {
               mbar_wait_warp(&afull[ar.i], ar.ph);
               tc_fence_after();
-              if (p == 0) trace_at(tr, 4, gs);
+              if (h == 0) trace_at(tr, 4, gs);
               const uint32_t acol = tb_u + kAcol0 + ar.i * C::kACols;
-              // gate|up or the two n-tiles: own accumulators; k-pair: part 1 reads the second X k-group
-              const uint32_t d = dcol + (kMode == kModeKPair ? 0u : static_cast<uint32_t>(p * kNTok));
-              const uint64_t b = xdesc + (kMode == kModeKPair ? static_cast<uint64_t>(p * C::kXRows * 16) : 0ull);
-              const uint32_t accf = (j != 0 || (kMode == kModeKPair && p == 1)) ? 1u : 0u;
+              const uint64_t b = xdesc + static_cast<uint64_t>(h * C::kXRows * 8);  // X k half h
+              const uint32_t accf = (j != 0 || h != 0) ? 1u : 0u;
               if (elect_one()) {
-                PartAsm<C::kXRows, C::kCG>::issue(d, acol, b, idesc, accf);
+                HalfAsm<C::kXRows, C::kCG, kMode == kModeKPair>::issue(dcol, d1, acol, b, accf, idesc);
                 if constexpr (kPair) {
                   umma_commit_pair(&aempty[ar.i]);
-                  if (p == C::kParts - 1) umma_commit_pair(&empty[st.i]);
+                  if (h == 1) umma_commit_pair(&empty[st.i]);
                 } else {
                   umma_commit(&aempty[ar.i]);
-                  if (p == C::kParts - 1) umma_commit(&empty[st.i]);
+                  if (h == 1) umma_commit(&empty[st.i]);
                 }
+                if (h == 1) trace_at(tr, 5, gs);
+#ifdef W4A16_TRACE
+                if (h == 1 && !kPair && tr) umma_commit(&trbar[gs & 7]);
+#endif
               }
               __syncwarp();
               ar.next(C::kNumA);
             }
-            trace_at(tr, 5, gs);
             progress_at(2, gs + 1);
             st.next(C::kNS);
             continue;
@@ -522,27 +533,32 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
   } else if (warp < kEpiWarp0) {
     // ------------------------------------------------------------ dequant: int4 smem -> TMEM A ring
-    // Group g (warps 2-5 / 6-9) takes the stages of parity g; inside a group warp w owns the TMEM lane
-    // quadrant w % 4 (32 weight rows) and all four 32-wide k chunks of the 128-wide tile.
+    // Whole-stage ring: group g (warps 2-5 / 6-9) takes the stages of parity g. Split ring (prefill):
+    // group h converts k half h (chunks 2h, 2h+1 of both parts) of every stage into A unit 2s+h.
+    // Inside a group warp w owns the TMEM lane quadrant w % 4 (32 weight rows).
     const int dw = warp - kDequantWarp0;
     const uint32_t my_par = dw / kDequantGroup;
     const uint32_t quad = warp & 3;
     const int row = quad * 32 + lane;
     const uint32_t lane_off = (quad * 32) << 16;
     const uint32_t code_off = row * 16;
+    constexpr int kMyChunks = C::kSplitA ? kChunks / 2 : kChunks;  // 32-k chunks this warp converts
+    const int c0 = C::kSplitA ? static_cast<int>(my_par) * kMyChunks : 0;
     Ring st, ar;
+    if constexpr (C::kSplitA) {
+      if (my_par) ar.next(C::kNumA);  // group 1 starts at the stage's second unit
+    }
     uint32_t gs = 0;
     TileInfo ti;
     for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
       for (int j = stage_beg(ti); j < stage_end(ti); ++j, ++gs) {
-        if ((gs & 1u) != my_par) {
+        if (!C::kSplitA && (gs & 1u) != my_par) {
           st.next(C::kNS);
-#pragma unroll
-          for (int u = 0; u < C::kAUnits; ++u) ar.next(C::kNumA);
+          ar.next(C::kNumA);
           continue;
         }
         mbar_wait(&full[st.i], st.ph);
-        const bool trd = lane == 0 && quad == 0;
+        const bool trd = lane == 0 && quad == 0 && my_par == (C::kSplitA ? 0u : (gs & 1u));
         if (trd) trace_at(tr, 1, gs);
         const uint32_t blk = w_u32 + st.i * C::kBlk;
         uint4 v[C::kParts][kChunks];
@@ -551,7 +567,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         for (int p = 0; p < C::kParts; ++p) {
           const uint32_t part = blk + p * kPartBytes;
 #pragma unroll
-          for (int c = 0; c < kChunks; ++c) v[p][c] = lds128(part + code_off + c * (kTileRows * 16));
+          for (int c = 0; c < kMyChunks; ++c) v[p][c] = lds128(part + code_off + (c0 + c) * (kTileRows * 16));
           if constexpr (!kOffset) {
             zb[p] = lds_u8(part + kZeroOff + (row >> 1));
             sb[p] = lds_u16(part + kScaleOff + row * 2);
@@ -560,34 +576,35 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           }
         }
         if constexpr (C::kSplitA) {
-          // one A unit per part, handed to the MMA as soon as it is written
+          // unit layout: part p's two chunks at columns p * 32 + {0, 16}
+          mbar_wait_cluster(&aempty[ar.i], ar.ph ^ 1);
+          tc_fence_after();
+          if (trd) trace_at(tr, 2, gs);
+          const uint32_t acol = tbase + lane_off + kAcol0 + ar.i * C::kACols;
 #pragma unroll
           for (int p = 0; p < C::kParts; ++p) {
-            mbar_wait_cluster(&aempty[ar.i], ar.ph ^ 1);
-            tc_fence_after();
-            if (trd && p == 0) trace_at(tr, 2, gs);
-            const uint32_t acol = tbase + lane_off + kAcol0 + ar.i * C::kACols;
             const uint32_t z = (row & 1) ? (zb[p] >> 4) : (zb[p] & 15u);
             const auto ctx = Dq<kBF16>::make(z, static_cast<uint16_t>(sb[p]));
 #pragma unroll
-            for (int c = 0; c < kChunks; ++c) {
+            for (int c = 0; c < kMyChunks; ++c) {
               uint32_t r[16];
               dequant_chunk<kBF16, true>(v[p][c], ctx, r);
-              tmem_st_x16(acol + c * 16, r);
+              tmem_st_x16(acol + p * 32 + c * 16, r);
             }
-            tc_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-              if constexpr (kPair) mbar_arrive_cluster(mapa_shared(&afull[ar.i], 0));
-              else mbar_arrive(&afull[ar.i]);
-            }
-            ar.next(C::kNumA);
           }
+          tc_wait_st();
+          tc_fence_before();
+          __syncwarp();
           if (trd) trace_at(tr, 3, gs);
           if (trd) progress_at(1, gs + 1);
-          if (lane == 0) mbar_arrive(&empty[st.i]);
+          if (lane == 0) {
+            if constexpr (kPair) mbar_arrive_cluster(mapa_shared(&afull[ar.i], 0));
+            else mbar_arrive(&afull[ar.i]);
+            mbar_arrive(&empty[st.i]);
+          }
           st.next(C::kNS);
+          ar.next(C::kNumA);
+          ar.next(C::kNumA);
           continue;
         }
         mbar_wait_cluster(&aempty[ar.i], ar.ph ^ 1);
@@ -611,8 +628,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               uint32_t r[16];
               if constexpr (kDqExp == 0) dequant_chunk<kBF16, true>(v[p][c], ctx, r);
               else raw_chunk<kBF16>(v[p][c], r);
-              if constexpr (kDqExp != 2) tmem_st_x16(acol + p * 64 + c * 16, r);
-              else if (r[0] == 0x12345u && r[5] == 0x777u) tmem_st_x16(acol + p * 64 + c * 16, r);
+              const uint32_t col = acol + p * 64 + c * 16;
+              if constexpr (kDqExp != 2) tmem_st_x16(col, r);
+              else if (r[0] == 0x12345u && r[5] == 0x777u) tmem_st_x16(col, r);
             }
           }
         }
