@@ -910,6 +910,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   }
 }
 
+__global__ void debug_stamp_kernel(unsigned long long* buf) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  const unsigned long long n = atomicAdd(buf, 1ull);
+  if (n < 4095) buf[1 + n] = t;
+}
+
 // ---------------------------------------------------------------------------------------------
 // Split-K finalize: out[r][n] = act(f(sum_s part[s][r][...])), f = silu(gate) * up when gated, for
 // rows r < *row_limit. One thread per 4 outputs.
@@ -1207,6 +1214,13 @@ int w4a16_debug_trace(void* buf) {
 }
 int w4a16_debug_trace_cta(int cta) {
   return cudaMemcpyToSymbol(g_w4_trace_cta, &cta, sizeof(cta)) == cudaSuccess ? W4_OK : W4_ERR_CUDA;
+}
+
+/* Debug aid: one thread appends %globaltimer (ns) to buf[1 + n] (n = buf[0]++): stream-ordered
+ * timestamps around captured work, to see whether consecutive graph replays overlap. */
+int w4a16_debug_stamp(void* buf, cudaStream_t stream) {
+  debug_stamp_kernel<<<1, 1, 0, stream>>>(static_cast<unsigned long long*>(buf));
+  return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
 
 int w4a16_tile_rows(void) { return kTileRows; }

@@ -60,6 +60,7 @@ SIGNATURES = {
 DEBUG_SIGNATURES = {
     "w4a16_debug_trace": (_i, [_p]),
     "w4a16_debug_trace_cta": (_i, [_i]),
+    "w4a16_debug_stamp": (_i, [_p, _p]),
 }
 
 _lock = threading.Lock()
