@@ -58,11 +58,28 @@ W4_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+// How waits poll an mbarrier phase (-DW4A16_WAIT=...): 0 = try_wait (the thread may be suspended
+// until the phase completes or a system time limit), 1 = test_wait spin (never suspends),
+// 2 = try_wait with a short suspend-time hint.
+#ifndef W4A16_WAIT
+#define W4A16_WAIT 0
+#endif
+#if W4A16_WAIT == 1
+#define W4_WAIT_OP "mbarrier.test_wait.parity"
+#define W4_WAIT_HINT ""
+#elif W4A16_WAIT == 2
+#define W4_WAIT_OP "mbarrier.try_wait.parity"
+#define W4_WAIT_HINT ", 0x20"
+#else
+#define W4_WAIT_OP "mbarrier.try_wait.parity"
+#define W4_WAIT_HINT ""
+#endif
+
 W4_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P;\n\t"
       "W4_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      W4_WAIT_OP ".shared::cta.b64 P, [%0], %1" W4_WAIT_HINT ";\n\t"
       "@!P bra W4_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
@@ -97,7 +114,7 @@ W4_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P;\n\t"
       "W4_WAITC_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], %1;\n\t"
+      W4_WAIT_OP ".acquire.cluster.shared::cta.b64 P, [%0], %1" W4_WAIT_HINT ";\n\t"
       "@!P bra W4_WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
@@ -109,8 +126,8 @@ W4_DEV void mbar_wait2_cluster(uint64_t* b0, uint32_t ph0, uint64_t* b1, uint32_
   asm volatile(
       "{\n\t.reg .pred P0, P1;\n\t"
       "W4_WAIT2_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P0, [%0], %1;\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%2], %3;\n\t"
+      W4_WAIT_OP ".acquire.cluster.shared::cta.b64 P0, [%0], %1" W4_WAIT_HINT ";\n\t"
+      W4_WAIT_OP ".acquire.cluster.shared::cta.b64 P1, [%2], %3" W4_WAIT_HINT ";\n\t"
       "@!P0 bra W4_WAIT2_%=;\n\t"
       "@!P1 bra W4_WAIT2_%=;\n\t}" ::"r"(smem_u32(b0)),
       "r"(ph0), "r"(smem_u32(b1)), "r"(ph1)
@@ -123,7 +140,7 @@ W4_DEV void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P, Q;\n\t"
       "W4_WAITW_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%0], %1;\n\t"
+      W4_WAIT_OP ".acquire.cluster.shared::cta.b64 P, [%0], %1" W4_WAIT_HINT ";\n\t"
       "vote.sync.all.pred Q, P, 0xffffffff;\n\t"
       "@!Q bra.uni W4_WAITW_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
@@ -133,8 +150,8 @@ W4_DEV void mbar_wait2_warp(uint64_t* b0, uint32_t ph0, uint64_t* b1, uint32_t p
   asm volatile(
       "{\n\t.reg .pred P0, P1, P, Q;\n\t"
       "W4_WAIT2W_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P0, [%0], %1;\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%2], %3;\n\t"
+      W4_WAIT_OP ".acquire.cluster.shared::cta.b64 P0, [%0], %1" W4_WAIT_HINT ";\n\t"
+      W4_WAIT_OP ".acquire.cluster.shared::cta.b64 P1, [%2], %3" W4_WAIT_HINT ";\n\t"
       "and.pred P, P0, P1;\n\t"
       "vote.sync.all.pred Q, P, 0xffffffff;\n\t"
       "@!Q bra.uni W4_WAIT2W_%=;\n\t}" ::"r"(smem_u32(b0)),
@@ -363,6 +380,9 @@ W4_DEV uint32_t lop3_and_or(uint32_t a, uint32_t mask, uint32_t orv) {
 
 W4_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+W4_DEV void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 }  // namespace w4

@@ -28,7 +28,17 @@
 
 namespace w4 {
 
-constexpr int kNumThreads = 14 * 32;
+// Experiment (-DW4A16_DUAL=1): a 15th warp as the second MMA issuer of the prefill kernel (see kDual).
+#ifndef W4A16_DUAL
+#define W4A16_DUAL 0
+#endif
+constexpr bool kDualEnv = W4A16_DUAL != 0;
+constexpr int kNumThreads = (kDualEnv ? 15 : 14) * 32;
+constexpr int kMma2Warp = 14;
+// named barriers handing the issue turn between the two MMA issuers, one per direction (warp 1 ->
+// warp 14 and back; a single shared barrier could be completed by one warp's own arrive + sync when
+// it runs ahead). Id 1: epilogue warps.
+constexpr uint32_t kTurnBar0 = 3, kTurnBar1 = 4;
 constexpr int kDequantWarp0 = 2;
 constexpr int kNumDequantWarps = 8;  // two groups of 4 (one warp per TMEM lane quadrant) alternating stages
 constexpr int kDequantGroup = 4;
@@ -126,6 +136,14 @@ struct Cfg {
   // so this stays an experiment.
   static constexpr bool kSplitA = kSplitAEnv && !kOffset && kParts == 2;
   static constexpr int kAUnits = kSplitA ? 2 : 1;  // A-ring slots per stage
+  // Prefill experiment: two MMA warps issue alternate stages (warp 1 even, warp 14 odd), handing the
+  // turn over with a named barrier right after issuing. Measured (tools/microbench/mma_wait.cu,
+  // tools/trace_gemm.py): issuing a stage's 16 N=128 MMAs takes ~640 cycles, its two commits ~190
+  // and the next afull wait ~170-400 more, so one issuer leaves the tensor pipe idle between stages
+  // (stage period ~1420 cycles for 1024 of MMA). Two issuers cut the period to ~1325 cycles, but a
+  // sustained prefill GEMM is power-capped (sw_power_cap, SM clock 1.2-1.3 GHz): the same-box A/B
+  // gave equal wall time (the clock drops by what the cycles gain), so this stays off.
+  static constexpr bool kDual = kDualEnv && !kOffset && !kPair && !kSplitA;
   static constexpr int kACols = (kSplitA ? 1 : kParts) * (kTileK / 2);  // fp16 pairs per 32-bit column
   // TMEM budget (512 columns): A ring + accumulator ring
   // 3 A slots if two accumulator stages still fit, else 2; the gated prefill projection (56-stage
@@ -289,6 +307,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   uint64_t* accempty = accfull + C::kNumAcc;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accempty + C::kNumAcc);
   uint64_t* trbar = accempty + C::kNumAcc + 2;  // trace builds: per-stage MMA completion (8-deep ring)
+  uint64_t* trbar2 = trbar + 8;                  // trace builds: MMA warp's post-issue arrive (8-deep ring)
   int* mt_off = reinterpret_cast<int*>(bars + 256);
   uint2* tile_tab = reinterpret_cast<uint2*>(mt_off + kMaxExperts + 2);  // 8-byte aligned (odd int count + 1)
   int* n_tiles_sm = mt_off + kMaxExperts + 1;
@@ -315,6 +334,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     for (int i = 0; i < C::kNumAcc; ++i) { mbar_init(&accfull[i], 1); mbar_init(&accempty[i], C::kAccEmptyArrivals); }
 #ifdef W4A16_TRACE
     for (int i = 0; i < 8; ++i) mbar_init(&trbar[i], 1);
+    for (int i = 0; i < 8; ++i) mbar_init(&trbar2[i], 1);
 #endif
     fence_mbar_init();
   } else if (warp == 2) {
@@ -367,7 +387,16 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // offset mode: all 32 lanes also copy the stage's (C, S) sums with 8-byte cp.async and arrive on
     // the same barrier when their copies land.
 #ifdef W4A16_TRACE
-    if (!kOffset && lane == 1 && tr && !kPair) {  // MMA completion times (trace event 15)
+    if (!kOffset && lane == 2 && tr && !kPair && !C::kSplitA && !C::kDual) {  // visibility of the MMA warp's arrive (event 22)
+      uint32_t n = 0;
+      TileInfo ti;
+      for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it)
+        for (int j = stage_beg(ti); j < stage_end(ti); ++j, ++n) {
+          mbar_wait(&trbar2[n & 7], (n >> 3) & 1);
+          trace_at(tr, 22, n);
+        }
+    }
+    if (!kOffset && lane == 1 && tr && !kPair && !C::kDual) {  // MMA completion times (trace event 15)
       uint32_t n = 0;
       TileInfo ti;
       for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it)
@@ -430,11 +459,55 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (leader CTA of a pair)
+  } else if (warp == 1 || warp == kMma2Warp) {
+    // ------------------------------------------------------------ MMA issuer(s) (leader CTA of a pair)
     // whole warp runs the loop; one elected lane issues. Waiting on afull (all dequant warps of the
     // pair arrived, each after its own full barrier) also covers the stage's X tile(s).
-    if (!kPair || rank == 0) {
+    if constexpr (C::kDual) {
+      const uint32_t my = warp == 1 ? 0u : 1u;  // stage parity this warp issues
+      const uint32_t bar_in = my ? kTurnBar0 : kTurnBar1, bar_out = my ? kTurnBar1 : kTurnBar0;
+      constexpr uint32_t idesc_full = make_idesc_f16(128, kNTok, kBF16);
+      const uint32_t tb_u = __shfl_sync(0xffffffffu, tbase, 0);
+      const uint32_t xs_u = __shfl_sync(0xffffffffu, smem_u32(smem_x), 0);
+      Ring st, ar, acc;
+      uint32_t gs = 0;
+      TileInfo ti;
+      for (int it = 0; tile_at<kNTok, 1, C::kNPer>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
+        const uint32_t n_mma = min(kNTok, (ti.m_rows + 15) / 16 * 16);
+        const uint32_t idesc = (idesc_full & ~(0x3Fu << 17)) | ((n_mma >> 3) << 17);
+        const int jb = stage_beg(ti), je = stage_end(ti);
+        for (int j = jb; j < je; ++j, ++gs) {
+          if ((gs & 1u) == my) {
+            if (j == jb) mbar_wait_warp(&accempty[acc.i], acc.ph ^ 1);  // the tile's accumulator is free
+            mbar_wait_warp(&afull[ar.i], ar.ph);
+            if (gs > 0) named_bar_sync(bar_in, 64);  // the other warp has issued stage gs - 1
+            tc_fence_after();
+            trace_at(tr, 4, gs);
+            const uint32_t dcol = tb_u + acc.i * C::kAccCols;
+            const uint64_t xdesc = make_sdesc_sw128(xs_u + st.i * C::kXBytes);
+            const uint32_t acol = tb_u + kAcol0 + ar.i * C::kACols;
+            if (elect_one()) {
+              StageAsm<kNTok, (kMode == kModeNPair ? kModeGateUp : kMode), 1, false, 1>::issue(
+                  dcol, acol, xdesc, idesc, static_cast<uint32_t>(j));
+              tc_fence_before();
+            }
+            __syncwarp();
+            if (!(it == n_tiles - 1 && j == je - 1)) named_bar_arrive(bar_out, 64);  // hand the turn over
+            if (elect_one()) {
+              umma_commit(&empty[st.i]);
+              umma_commit(&aempty[ar.i]);
+              if (j == je - 1) umma_commit(&accfull[acc.i]);  // in-order pipe: covers the other warp's MMAs
+              trace_at(tr, 5, gs);
+            }
+            __syncwarp();
+            progress_at(2, gs + 1);
+          }
+          st.next(C::kNS);
+          ar.next(C::kNumA);
+        }
+        acc.next(C::kNumAcc);
+      }
+    } else if (warp == 1 && (!kPair || rank == 0)) {
       constexpr uint32_t idesc_full = make_idesc_f16(128 * C::kCG, kNTok, kBF16);
       // provably warp-uniform bases (shfl from lane 0): ptxas keeps the MMA operands in uniform registers
       const uint32_t tb_u = __shfl_sync(0xffffffffu, tbase, 0);
@@ -503,7 +576,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 dcol, acol, xdesc, idesc, static_cast<uint32_t>(j));
             trace_at(tr, 5, gs);
 #ifdef W4A16_TRACE
-            if (!kOffset && !kPair && tr) umma_commit(&trbar[gs & 7]);
+            if (!kOffset && !kPair && tr) {
+              mbar_arrive(&trbar2[gs & 7]);  // right after the MMAs: how soon do other warps see it?
+              umma_commit(&trbar[gs & 7]);
+            }
 #endif
             if constexpr (kPair) {
               umma_commit_pair(&empty[st.i]);
@@ -514,8 +590,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               umma_commit(&aempty[ar.i]);
               if constexpr (kOffset) umma_commit(&accfull[acc.i]);
             }
+            trace_at(tr, 20, gs);  // commits accepted
           }
           __syncwarp();
+          trace_at(tr, 21, gs);  // warp reconverged
           progress_at(2, gs + 1);
           st.next(C::kNS);
           ar.next(C::kNumA);
@@ -638,6 +716,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (trd) trace_at(tr, 3, gs);
+        if (lane == 0) trace_at(tr, 16 + quad, gs);  // every quad's arrival (per-SMSP skew)
         if (trd) progress_at(1, gs + 1);
         if (lane == 0) {
           if constexpr (kPair) mbar_arrive_cluster(mapa_shared(&afull[ar.i], 0));
