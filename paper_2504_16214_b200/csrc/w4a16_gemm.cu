@@ -60,11 +60,6 @@ constexpr int kSmemBudget = 225 * 1024;
 // experiment (-DW4A16_SPLITA=1): prefill k-half TMEM A units; measured slower (gate/up T=8192 3.57 vs
 // 3.43 ms), see the Cfg comment
 constexpr bool kSplitAEnv = W4A16_SPLITA != 0;
-#ifndef W4A16_DQEXP
-#define W4A16_DQEXP 0
-#endif
-// experiment (prefill dequant): 1 = store raw codes (no FP math), 2 = no TMEM stores at all
-constexpr int kDqExp = W4A16_DQEXP;
 
 struct GemmArgs {
   const uint8_t* wblocks;        // [E][NT][KT][parts * kPartBytes]
@@ -704,11 +699,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll
             for (int c = 0; c < kChunks; ++c) {
               uint32_t r[16];
-              if constexpr (kDqExp == 0) dequant_chunk<kBF16, true>(v[p][c], ctx, r);
-              else raw_chunk<kBF16>(v[p][c], r);
-              const uint32_t col = acol + p * 64 + c * 16;
-              if constexpr (kDqExp != 2) tmem_st_x16(col, r);
-              else if (r[0] == 0x12345u && r[5] == 0x777u) tmem_st_x16(col, r);
+              dequant_chunk<kBF16, true>(v[p][c], ctx, r);
+              tmem_st_x16(acol + p * 64 + c * 16, r);
             }
           }
         }
