@@ -110,14 +110,18 @@ W4_DEV uint32_t mapa_shared(const void* p, uint32_t rank) {
 W4_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// Acquire scope of the waits below: .cluster when CTA peers arrive on the barrier (cta_group::2 pairs);
+// .cta otherwise -- an acquire at cluster scope invalidates L1 (CCTL.IVALL), which ncu showed as the
+// most stall-sampled instruction of the decode GEMMs.
+#define W4_WAIT_BODY1(LABEL, SCOPE)                                                        \
+  "{\n\t.reg .pred P;\n\t" LABEL ":\n\t" W4_WAIT_OP ".acquire." SCOPE ".shared::cta.b64 P, [%0], %1" \
+  W4_WAIT_HINT ";\n\t@!P bra " LABEL ";\n\t}"
+template <bool kCluster = true>
 W4_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P;\n\t"
-      "W4_WAITC_%=:\n\t"
-      W4_WAIT_OP ".acquire.cluster.shared::cta.b64 P, [%0], %1" W4_WAIT_HINT ";\n\t"
-      "@!P bra W4_WAITC_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
+  if constexpr (kCluster)
+    asm volatile(W4_WAIT_BODY1("W4_WAITC_%=", "cluster") ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+  else
+    asm volatile(W4_WAIT_BODY1("W4_WAITA_%=", "cta") ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 // Wait for two barrier phases at once: both try_waits are in flight together, so a ready barrier
 // costs its latency once instead of once per barrier (a completed phase stays completed until the
@@ -136,27 +140,29 @@ W4_DEV void mbar_wait2_cluster(uint64_t* b0, uint32_t ph0, uint64_t* b1, uint32_
 
 // Warp-wide forms: the whole (converged) warp waits and branches on a vote, so ptxas sees uniform
 // control flow afterwards and keeps warp-uniform values in uniform registers (MMA operands).
+#define W4_WAIT_BODYW(LABEL, SCOPE)                                                               \
+  "{\n\t.reg .pred P, Q;\n\t" LABEL ":\n\t" W4_WAIT_OP ".acquire." SCOPE ".shared::cta.b64 P, [%0], %1"   \
+  W4_WAIT_HINT ";\n\tvote.sync.all.pred Q, P, 0xffffffff;\n\t@!Q bra.uni " LABEL ";\n\t}"
+#define W4_WAIT_BODY2W(LABEL, SCOPE)                                                                      \
+  "{\n\t.reg .pred P0, P1, P, Q;\n\t" LABEL ":\n\t" W4_WAIT_OP ".acquire." SCOPE                     \
+  ".shared::cta.b64 P0, [%0], %1" W4_WAIT_HINT ";\n\t" W4_WAIT_OP ".acquire." SCOPE                      \
+  ".shared::cta.b64 P1, [%2], %3" W4_WAIT_HINT ";\n\tand.pred P, P0, P1;\n\t"                          \
+  "vote.sync.all.pred Q, P, 0xffffffff;\n\t@!Q bra.uni " LABEL ";\n\t}"
+template <bool kCluster = true>
 W4_DEV void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P, Q;\n\t"
-      "W4_WAITW_%=:\n\t"
-      W4_WAIT_OP ".acquire.cluster.shared::cta.b64 P, [%0], %1" W4_WAIT_HINT ";\n\t"
-      "vote.sync.all.pred Q, P, 0xffffffff;\n\t"
-      "@!Q bra.uni W4_WAITW_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
+  if constexpr (kCluster)
+    asm volatile(W4_WAIT_BODYW("W4_WAITW_%=", "cluster") ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+  else
+    asm volatile(W4_WAIT_BODYW("W4_WAITWA_%=", "cta") ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
+template <bool kCluster = true>
 W4_DEV void mbar_wait2_warp(uint64_t* b0, uint32_t ph0, uint64_t* b1, uint32_t ph1) {
-  asm volatile(
-      "{\n\t.reg .pred P0, P1, P, Q;\n\t"
-      "W4_WAIT2W_%=:\n\t"
-      W4_WAIT_OP ".acquire.cluster.shared::cta.b64 P0, [%0], %1" W4_WAIT_HINT ";\n\t"
-      W4_WAIT_OP ".acquire.cluster.shared::cta.b64 P1, [%2], %3" W4_WAIT_HINT ";\n\t"
-      "and.pred P, P0, P1;\n\t"
-      "vote.sync.all.pred Q, P, 0xffffffff;\n\t"
-      "@!Q bra.uni W4_WAIT2W_%=;\n\t}" ::"r"(smem_u32(b0)),
-      "r"(ph0), "r"(smem_u32(b1)), "r"(ph1)
-      : "memory");
+  if constexpr (kCluster)
+    asm volatile(W4_WAIT_BODY2W("W4_WAIT2W_%=", "cluster") ::"r"(smem_u32(b0)), "r"(ph0), "r"(smem_u32(b1)),
+                 "r"(ph1) : "memory");
+  else
+    asm volatile(W4_WAIT_BODY2W("W4_WAIT2WA_%=", "cta") ::"r"(smem_u32(b0)), "r"(ph0), "r"(smem_u32(b1)),
+                 "r"(ph1) : "memory");
 }
 
 W4_DEV void cluster_sync_all() {

@@ -473,8 +473,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         const int jb = stage_beg(ti), je = stage_end(ti);
         for (int j = jb; j < je; ++j, ++gs) {
           if ((gs & 1u) == my) {
-            if (j == jb) mbar_wait_warp(&accempty[acc.i], acc.ph ^ 1);  // the tile's accumulator is free
-            mbar_wait_warp(&afull[ar.i], ar.ph);
+            if (j == jb) mbar_wait_warp<kPair>(&accempty[acc.i], acc.ph ^ 1);  // the tile's accumulator is free
+            mbar_wait_warp<kPair>(&afull[ar.i], ar.ph);
             if (gs > 0) named_bar_sync(bar_in, 64);  // the other warp has issued stage gs - 1
             tc_fence_after();
             trace_at(tr, 4, gs);
@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         const uint32_t n_mma = min(kNTok, (ti.m_rows + 16 * C::kCG - 1) / (16 * C::kCG) * (16 * C::kCG));
         const uint32_t idesc = (idesc_full & ~(0x3Fu << 17)) | ((n_mma >> 3) << 17);
         if constexpr (!kOffset) {
-          mbar_wait_warp(&accempty[acc.i], acc.ph ^ 1);
+          mbar_wait_warp<kPair>(&accempty[acc.i], acc.ph ^ 1);
           tc_fence_after();
           trace_at(tr, 6, it);
         }
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             const uint64_t xdesc = make_sdesc_sw128(xs_u + st.i * C::kXBytes);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              mbar_wait_warp(&afull[ar.i], ar.ph);
+              mbar_wait_warp<kPair>(&afull[ar.i], ar.ph);
               tc_fence_after();
               if (h == 0) trace_at(tr, 4, gs);
               const uint32_t acol = tb_u + kAcol0 + ar.i * C::kACols;
@@ -557,9 +557,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             continue;
           }
           if constexpr (kOffset)  // fresh partials per stage: accumulator slot free + A slot filled
-            mbar_wait2_warp(&accempty[acc.i], acc.ph ^ 1, &afull[ar.i], ar.ph);
+            mbar_wait2_warp<kPair>(&accempty[acc.i], acc.ph ^ 1, &afull[ar.i], ar.ph);
           else
-            mbar_wait_warp(&afull[ar.i], ar.ph);
+            mbar_wait_warp<kPair>(&afull[ar.i], ar.ph);
           tc_fence_after();
           trace_at(tr, 4, gs);
           const uint32_t dcol = tb_u + acc.i * C::kAccCols;
@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
         if constexpr (C::kSplitA) {
           // unit layout: part p's two chunks at columns p * 32 + {0, 16}
-          mbar_wait_cluster(&aempty[ar.i], ar.ph ^ 1);
+          mbar_wait_cluster<kPair>(&aempty[ar.i], ar.ph ^ 1);
           tc_fence_after();
           if (trd) trace_at(tr, 2, gs);
           const uint32_t acol = tbase + lane_off + kAcol0 + ar.i * C::kACols;
@@ -680,7 +680,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           ar.next(C::kNumA);
           continue;
         }
-        mbar_wait_cluster(&aempty[ar.i], ar.ph ^ 1);
+        mbar_wait_cluster<kPair>(&aempty[ar.i], ar.ph ^ 1);
         tc_fence_after();
         if (trd) trace_at(tr, 2, gs);
         const uint32_t acol = tbase + lane_off + kAcol0 + ar.i * C::kACols;
@@ -787,7 +787,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             const uint32_t zb = lds_u8(part + kZeroOff + (row >> 1));
             zf[p] = static_cast<float>((row & 1) ? (zb >> 4) : (zb & 15u));
           }
-          mbar_wait_cluster(&accfull[acc.i], acc.ph);
+          mbar_wait_cluster<kPair>(&accfull[acc.i], acc.ph);
           tc_fence_after();
           if (tre) trace_at(tr, 7, egs);
           const uint32_t dcol = tbase + lane_off + acc.i * C::kAccCols;
@@ -895,7 +895,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           }
         }
       } else {
-        mbar_wait_cluster(&accfull[acc.i], acc.ph);
+        mbar_wait_cluster<kPair>(&accfull[acc.i], acc.ph);
         tc_fence_after();
         if (tre) trace_at(tr, 7, it);
         const uint32_t dcol = tbase + lane_off + acc.i * C::kAccCols;
