@@ -9,6 +9,7 @@
  * (vllm fused_experts(hidden_states, w1, w2, topk_weights, topk_ids, ...)) bind it:
  *
  *   route:    w4a16_route_topk                         top-k of softmax/sigmoid router scores
+ *             w4a16_route_grouped_topk                 DeepSeek-V3/R1 grouped top-k (vLLM grouped_topk)
  *   permute:  w4a16_moe_permute                        stable counting sort of (token, slot) by expert
  *   gather:   w4a16_moe_gather                         X_perm[p] = x[token(p)]   (128-bit vectors)
  *             w4a16_moe_gather_sums                    same, plus per-group activation sums (decode)
@@ -72,6 +73,16 @@ int w4a16_dequant(const uint8_t* wblocks, int64_t num_experts, int64_t n_rows, i
  * topk_weights [T][k] fp32 (softmax or sigmoid of the selected logits, optionally renormalised). */
 int w4a16_route_topk(const float* logits, int64_t T, int64_t E, int64_t k, int scoring, int renormalize,
                      int32_t* topk_ids, float* topk_weights, cudaStream_t stream);
+
+/* DeepSeek-V3/R1 routing, vLLM grouped_topk semantics (vllm/model_executor/layers/fused_moe/router/
+ * grouped_topk_router.py:81-162): scores = softmax|sigmoid(logits); choice = scores + bias (bias [E]
+ * fp32 e_score_correction_bias, or NULL); group score = sum of the group's two best choices (bias) or
+ * its best score (no bias); keep the topk_group best of num_groups groups; topk_ids = the k best
+ * kept choices (ties -> lower id); topk_weights = their unbiased scores, renormalised if asked,
+ * times routed_scaling_factor. num_groups <= 32 must divide E. */
+int w4a16_route_grouped_topk(const float* logits, int64_t T, int64_t E, int64_t k, int64_t num_groups,
+                             int64_t topk_group, int scoring, int renormalize, const float* bias,
+                             float routed_scaling_factor, int32_t* topk_ids, float* topk_weights, cudaStream_t stream);
 
 /* Stable counting sort of the P = T*k flattened (token, slot) pairs by expert id.
  * ids outside [0, E) are dropped (pair_pos = -1). Outputs: expert_counts [E], expert_offsets [E+1],

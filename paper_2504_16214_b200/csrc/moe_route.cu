@@ -69,6 +69,122 @@ __global__ void route_topk_kernel(const float* __restrict__ logits, int T, int E
   }
 }
 
+// ------------------------------------------------------------------------------- grouped top-k
+// DeepSeek-V3/R1 routing (vLLM grouped_topk, vllm/model_executor/layers/fused_moe/router/
+// grouped_topk_router.py:81-162): scores = softmax or sigmoid of the logits; choice = scores + bias
+// (e_score_correction_bias, optional); a group's score is the sum of its two best choices (with a
+// bias) or its best score (without); the topk_group best groups stay, every other expert is masked;
+// the k best remaining choices are selected; weights are the *unbiased* scores of the selected
+// experts, optionally renormalised, times routed_scaling_factor. Ties -> lower group / expert id.
+// One warp per token; lane l holds experts l, l+32, ... as in route_topk_kernel.
+template <int kPer>
+__global__ void route_grouped_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int G, int TG,
+                                          int scoring, int renorm, const float* __restrict__ bias, float scale,
+                                          int32_t* __restrict__ ids, float* __restrict__ wts) {
+  griddep_wait();  // PDL: inputs written by the previous kernel in the stream
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= T) return;
+  const float* row = logits + static_cast<int64_t>(warp) * E;
+  const int gsize = E / G;
+  float sc[kPer], ch[kPer];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int e = lane + 32 * i;
+    sc[i] = e < E ? __ldg(row + e) : -INFINITY;
+    mx = fmaxf(mx, sc[i]);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float denom = 0.f;
+  if (scoring == W4_SCORE_SOFTMAX) {
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) denom += lane + 32 * i < E ? __expf(sc[i] - mx) : 0.f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) denom += __shfl_xor_sync(0xffffffffu, denom, o);
+  }
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const int e = lane + 32 * i;
+    if (e < E) {
+      sc[i] = scoring == W4_SCORE_SOFTMAX ? __expf(sc[i] - mx) / denom : 1.0f / (1.0f + __expf(-sc[i]));
+      ch[i] = bias ? sc[i] + __ldg(bias + e) : sc[i];
+    } else {
+      ch[i] = -INFINITY;
+    }
+  }
+  // group scores: lane g ends up holding group g's score
+  float gscore = -INFINITY;
+  for (int g = 0; g < G; ++g) {
+    float b1 = -INFINITY, b2 = -INFINITY;  // lane-local best two choices of group g
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int e = lane + 32 * i;
+      if (e < E && e / gsize == g) {
+        if (ch[i] > b1) { b2 = b1; b1 = ch[i]; } else if (ch[i] > b2) { b2 = ch[i]; }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {  // merge two sorted pairs
+      const float o1 = __shfl_xor_sync(0xffffffffu, b1, o), o2 = __shfl_xor_sync(0xffffffffu, b2, o);
+      const float n1 = fmaxf(b1, o1);
+      const float n2 = fmaxf(fminf(b1, o1), fmaxf(b2, o2));
+      b1 = n1;
+      b2 = n2;
+    }
+    const float gs = bias ? b1 + b2 : b1;
+    if (lane == g) gscore = gs;
+  }
+  // the topk_group best groups (ties -> lower group id) as a bit mask
+  uint32_t gmask = 0;
+  for (int j = 0; j < TG; ++j) {
+    float best = (lane < G && !((gmask >> lane) & 1u)) ? gscore : -INFINITY;
+    int bidx = (lane < G && !((gmask >> lane) & 1u)) ? lane : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+      if (oi != 0x7fffffff && (bidx == 0x7fffffff || ob > best || (ob == best && oi < bidx))) { best = ob; bidx = oi; }
+    }
+    gmask |= 1u << bidx;
+  }
+  // top-k over the kept experts' choices
+  float sel_sum = 0.f, my_w = 0.f;
+  int my_id = 0;
+  uint32_t taken = 0;
+  for (int j = 0; j < k; ++j) {
+    float best = -INFINITY;
+    int bidx = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int e = lane + 32 * i;
+      if (e < E && ((gmask >> (e / gsize)) & 1u) && !((taken >> i) & 1u) && (bidx == 0x7fffffff || ch[i] > best)) {
+        best = ch[i];
+        bidx = e;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+      if (oi != 0x7fffffff && (bidx == 0x7fffffff || ob > best || (ob == best && oi < bidx))) { best = ob; bidx = oi; }
+    }
+    float w = 0.f;  // the selected expert's unbiased score, from its owning lane
+#pragma unroll
+    for (int i = 0; i < kPer; ++i)
+      if (lane + 32 * i == bidx) w = sc[i];
+    w = __shfl_sync(0xffffffffu, w, bidx & 31);
+    if ((bidx & 31) == lane) taken |= 1u << (bidx >> 5);
+    sel_sum += w;
+    if (lane == j) { my_w = w; my_id = bidx; }
+  }
+  if (lane < k) {
+    ids[static_cast<int64_t>(warp) * k + lane] = my_id;
+    wts[static_cast<int64_t>(warp) * k + lane] = (renorm ? my_w / sel_sum : my_w) * scale;
+  }
+}
+
 // ---------------------------------------------------------------------------------------- permute
 // Single CTA of 1024 threads. Pass 1: histogram (smem atomics; counts are order-independent).
 // Pass 2: exclusive scan. Pass 3: walk the pairs in 1024-wide chunks; within a chunk a pair's rank
@@ -517,6 +633,33 @@ int w4a16_route_topk(const float* logits, int64_t T, int64_t E, int64_t k, int s
   else if (per <= 16) W4_ROUTE(16);
   else W4_ROUTE(32);
 #undef W4_ROUTE
+  return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
+}
+
+int w4a16_route_grouped_topk(const float* logits, int64_t T, int64_t E, int64_t k, int64_t num_groups,
+                             int64_t topk_group, int scoring, int renormalize, const float* bias,
+                             float routed_scaling_factor, int32_t* topk_ids, float* topk_weights, cudaStream_t stream) {
+  if (!logits || !topk_ids || !topk_weights) return W4_ERR_ARG;
+  if (E <= 0 || E > 1024 || k <= 0 || k > 32 || k > E) return W4_ERR_SHAPE;
+  if (num_groups <= 0 || num_groups > 32 || E % num_groups || topk_group <= 0 || topk_group > num_groups)
+    return W4_ERR_SHAPE;
+  if (topk_group * (E / num_groups) < k) return W4_ERR_SHAPE;  // fewer kept experts than k
+  if (bias && E / num_groups < 2) return W4_ERR_SHAPE;         // group score = sum of the best two
+  if (scoring != W4_SCORE_SOFTMAX && scoring != W4_SCORE_SIGMOID) return W4_ERR_ARG;
+  if (T <= 0) return W4_OK;
+  const int thr = 128;
+  const int64_t blocks = (T * 32 + thr - 1) / thr;
+  const int per = static_cast<int>((E + 31) / 32);
+#define W4_GROUTE(P)                                                                                        \
+  launch_pdl(route_grouped_topk_kernel<P>, blocks, thr, 0, stream, logits, (int)T, (int)E, (int)k, (int)num_groups, \
+             (int)topk_group, scoring, renormalize, bias, routed_scaling_factor, topk_ids, topk_weights)
+  if (per <= 1) W4_GROUTE(1);
+  else if (per <= 2) W4_GROUTE(2);
+  else if (per <= 4) W4_GROUTE(4);
+  else if (per <= 8) W4_GROUTE(8);
+  else if (per <= 16) W4_GROUTE(16);
+  else W4_GROUTE(32);
+#undef W4_GROUTE
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
 

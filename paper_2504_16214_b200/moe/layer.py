@@ -23,9 +23,19 @@ from .weights import MoEWeights
 
 
 def select_experts(router_logits: torch.Tensor, top_k: int, scoring: str = "softmax",
-                   renormalize: bool = False):
-    """-> (topk_weights fp32 [T, k], topk_ids int32 [T, k]); ties go to the lower expert id."""
-    ids, wts = ops.route_topk(router_logits.float().contiguous(), top_k, scoring, renormalize)
+                   renormalize: bool = False, num_expert_group: int = 0, topk_group: int = 0,
+                   e_score_correction_bias: torch.Tensor | None = None, routed_scaling_factor: float = 1.0):
+    """-> (topk_weights fp32 [T, k], topk_ids int32 [T, k]); ties go to the lower expert id.
+    ``num_expert_group`` > 0 selects DeepSeek-V3/R1 grouped top-k (vLLM ``grouped_topk``: groups,
+    ``topk_group`` kept groups, optional correction bias, ``routed_scaling_factor``)."""
+    logits = router_logits.float().contiguous()
+    if num_expert_group:
+        ids, wts = ops.route_grouped_topk(logits, top_k, num_expert_group, topk_group, scoring, renormalize,
+                                          e_score_correction_bias, routed_scaling_factor)
+    else:
+        ids, wts = ops.route_topk(logits, top_k, scoring, renormalize)
+        if routed_scaling_factor != 1.0:
+            wts = wts * routed_scaling_factor
     return wts, ids
 
 
@@ -154,9 +164,12 @@ def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, 
 
 def fused_moe_w4a16(x: torch.Tensor, router_logits: torch.Tensor, weights: MoEWeights, top_k: int,
                     scoring: str = "softmax", renormalize: bool = False, ep_group=None,
-                    timer: KernelTimer | None = None) -> torch.Tensor:
+                    timer: KernelTimer | None = None, num_expert_group: int = 0, topk_group: int = 0,
+                    e_score_correction_bias: torch.Tensor | None = None,
+                    routed_scaling_factor: float = 1.0) -> torch.Tensor:
     with (timer or _NOTIMER).span("route"):
-        topk_weights, topk_ids = select_experts(router_logits, top_k, scoring, renormalize)
+        topk_weights, topk_ids = select_experts(router_logits, top_k, scoring, renormalize, num_expert_group,
+                                                topk_group, e_score_correction_bias, routed_scaling_factor)
     return moe_w4a16(x, weights, topk_weights, topk_ids, ep_group=ep_group, timer=timer)
 
 

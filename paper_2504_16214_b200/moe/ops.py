@@ -77,6 +77,28 @@ def route_topk(logits: torch.Tensor, k: int, scoring: str = "softmax", renormali
     return ids, wts
 
 
+def route_grouped_topk(logits: torch.Tensor, k: int, num_groups: int, topk_group: int, scoring: str = "sigmoid",
+                       renormalize: bool = True, bias: torch.Tensor | None = None,
+                       routed_scaling_factor: float = 1.0):
+    """DeepSeek-V3/R1 grouped top-k (vLLM ``grouped_topk`` semantics, see the C header)."""
+    _need_cuda(logits)
+    if logits.dtype != torch.float32:
+        raise _lib.W4A16Error("router logits must be float32")
+    T, E = logits.shape
+    if bias is not None:
+        _need_cuda(bias)
+        bias = bias.float().contiguous()
+        if bias.numel() != E:
+            raise _lib.W4A16Error("e_score_correction_bias must have one entry per expert")
+    ids = torch.empty((T, k), dtype=torch.int32, device=logits.device)
+    wts = torch.empty((T, k), dtype=torch.float32, device=logits.device)
+    sc = {"softmax": _lib.SCORE_SOFTMAX, "sigmoid": _lib.SCORE_SIGMOID}[scoring]
+    _lib.call("w4a16_route_grouped_topk", logits.data_ptr(), T, E, k, num_groups, topk_group, sc, int(renormalize),
+              bias.data_ptr() if bias is not None else None, float(routed_scaling_factor), ids.data_ptr(),
+              wts.data_ptr(), _stream())
+    return ids, wts
+
+
 def moe_permute(topk_ids: torch.Tensor, num_experts: int, workspace: torch.Tensor | None = None):
     """-> (expert_counts [E], expert_offsets [E+1], sorted_pairs [P], pair_pos [P]) int32. Large P runs
     the multi-CTA kernel when a workspace of permute_ws_bytes(P, E) bytes is given (or allocated)."""

@@ -73,6 +73,46 @@ def test_route_topk(scoring, renorm, E, k):
     np.testing.assert_allclose(w.cpu().numpy(), rw, rtol=1e-5, atol=1e-6)
 
 
+@pytest.mark.parametrize("case", [(64, 256, 8, 8, 4, "sigmoid", True, True, 2.5),   # DeepSeek-R1
+                                  (33, 256, 8, 8, 4, "sigmoid", True, False, 1.0),
+                                  (16, 64, 6, 4, 2, "softmax", False, False, 1.0),
+                                  (200, 128, 4, 8, 3, "softmax", True, True, 1.0),
+                                  (5, 1024, 8, 32, 6, "sigmoid", True, True, 1.0),
+                                  (7, 60, 3, 3, 2, "sigmoid", False, True, 1.0)])
+def test_route_grouped_topk(case):
+    """DeepSeek-V3/R1 grouped top-k kernel == the oracle (which tests/test_oracle.py pins to vLLM)."""
+    T, E, k, G, TG, scoring, renorm, use_bias, scale = case
+    rng = np.random.default_rng(T * E + k)
+    lg = rng.standard_normal((T, E)).astype(np.float32)
+    bias = (rng.standard_normal(E) * 0.1).astype(np.float32) if use_bias else None
+    ids, w = _ops().route_grouped_topk(torch.from_numpy(lg).cuda(), k, G, TG, scoring, renorm,
+                                       torch.from_numpy(bias).cuda() if bias is not None else None, scale)
+    rid, rw = O.grouped_topk(lg, k, G, TG, scoring, renorm, bias, scale)
+    assert np.array_equal(ids.cpu().numpy(), rid)
+    np.testing.assert_allclose(w.cpu().numpy(), rw, rtol=1e-5, atol=1e-6)
+
+
+def test_fused_moe_grouped_routing_layer():
+    """The layer with DeepSeek-style routing (grouped top-k + bias + scaling) == oracle layer."""
+    from paper_2504_16214_b200.moe import fused_moe_w4a16
+    from paper_2504_16214_b200.moe.weights import MoEWeights
+    rng = np.random.default_rng(5)
+    T, E, k, H, I, dt = 24, 32, 4, 256, 256, "f16"
+    q13, z13, s13 = O.synth_awq_expert_weights(rng, E, 2 * I, H, dt)
+    q2, z2, s2 = O.synth_awq_expert_weights(rng, E, H, I, dt)
+    w = MoEWeights(_packed(q13, z13, s13, dt, True), _packed(q2, z2, s2, dt, False))
+    x = O.round_act(rng.standard_normal((T, H)).astype(np.float32) * 0.5, dt)
+    lg = rng.standard_normal((T, E)).astype(np.float32)
+    bias = (rng.standard_normal(E) * 0.1).astype(np.float32)
+    y = fused_moe_w4a16(_to_dev_act(x, dt), torch.from_numpy(lg).cuda(), w, k, "sigmoid", True,
+                        num_expert_group=4, topk_group=2, e_score_correction_bias=torch.from_numpy(bias).cuda(),
+                        routed_scaling_factor=2.5)
+    torch.cuda.synchronize()
+    rid, rw = O.grouped_topk(lg, k, 4, 2, "sigmoid", True, bias, 2.5)
+    want = O.moe_forward(x, O.dequant(q13, z13, s13, dt), O.dequant(q2, z2, s2, dt), rid, rw, dt)
+    np.testing.assert_allclose(_from_dev_act(y, dt), want, rtol=RTOL, atol=ATOL)
+
+
 # ------------------------------------------------------------------------------------------- permute
 @pytest.mark.parametrize("P,E", [(1, 4), (64 * 8, 256), (3000, 256), (5000, 7), (65536, 256), (2048, 1024),
                                  (20000, 1024), (9001, 3), (131072, 128)])

@@ -95,3 +95,33 @@ def test_group_sums_restatement():
                               for k in range(128)])
                 assert np.isclose(got[g, r, 1], xs.sum(), rtol=1e-6, atol=1e-4)
                 assert np.isclose(got[g, r, 0], (c * xs).sum(), rtol=1e-6, atol=1e-2)
+
+
+GOLD_GT = Path(__file__).resolve().parent / "golden" / "grouped_topk_vllm.npz"
+
+
+@pytest.mark.parametrize("case", ["ds_r1", "ds_r1_nobias", "softmax_g4", "softmax_bias"])
+def test_grouped_topk_matches_vllm(case):
+    """The grouped top-k restatement == vLLM 0.22's torch grouped_topk on the golden vectors
+    (tools/make_golden_grouped_topk.py; slots ordered by descending weight)."""
+    g = np.load(GOLD_GT)
+    T, E, k, G, TG, softmax, renorm, use_bias = (int(v) for v in g[f"{case}_meta"])
+    bias = g[f"{case}_bias"] if use_bias else None
+    ids, w = O.grouped_topk(g[f"{case}_logits"], k, G, TG, "softmax" if softmax else "sigmoid", bool(renorm), bias,
+                            float(g[f"{case}_scale"][0]))
+    order = np.argsort(-w, axis=1, kind="stable")
+    np.testing.assert_array_equal(np.take_along_axis(ids, order, axis=1), g[f"{case}_ids"])
+    np.testing.assert_allclose(np.take_along_axis(w, order, axis=1), g[f"{case}_weights"], rtol=1e-6, atol=1e-7)
+
+
+def test_grouped_topk_group_rule():
+    """Experts outside the kept groups are never chosen, even when their scores are the largest."""
+    lg = np.full((1, 16), -3.0, dtype=np.float32)
+    lg[0, 0] = 5.0                  # group 0 (experts 0-3): one huge expert, the rest small
+    lg[0, 4:8] = 1.0                # group 1: uniformly medium (bias-free group score = max = 1 < 5)
+    lg[0, 8:12] = [2.0, 2.0, -9, -9]
+    ids, _ = O.grouped_topk(lg, 2, 4, 1, "sigmoid", True, None)
+    assert set(ids[0].tolist()) <= {0, 1, 2, 3}
+    bias = np.zeros(16, dtype=np.float32)  # with a bias the group score is the sum of the best two
+    ids, _ = O.grouped_topk(lg, 2, 4, 1, "sigmoid", True, bias)
+    assert set(ids[0].tolist()) <= {8, 9, 10, 11}
