@@ -10,7 +10,9 @@
 //   warp 1      MMA      : one elected thread issues tcgen05.mma kind::f16, A from TMEM, B from smem
 //   warps 2-9   dequant  : ld.shared 16 B of int4 per row-thread -> LOP3/HSUB2/HMUL2 -> tcgen05.st
 //                           into a TMEM A-operand ring (lane = weight row, 2 k per 32-bit column)
-//   warps 10-13 epilogue : tcgen05.ld of the fp32 accumulator, SiLU(gate)*up when fused, store
+//   warps 10-13 epilogue : tcgen05.ld of the fp32 accumulator, SiLU(gate)*up when fused, 16-token
+//                           chunks staged in shared memory and stored with 16-byte stores
+//   (warp 14     second MMA issuer, -DW4A16_DUAL=1 experiment only)
 // The dequantised weights never touch shared memory or HBM: int4 goes HBM -> smem -> registers ->
 // TMEM -> tensor core. Barriers: smem full/empty, TMEM-A full/empty, accumulator full/empty.
 #include <cuda.h>
@@ -154,7 +156,7 @@ struct Cfg {
   static constexpr int kNumA = kSplitA ? kNumAS : kNumA_;
   static constexpr int kStageBytes = kBlk + kXBytes + kSumBytes;
   // barriers, m-tile prefix, tile table, epilogue cross-warp reduction scratch (4 warps x 16 x float2)
-  // prefill epilogue: per-warp staging of a 16-token x 32-column output block (x2 for n-pair tiles)
+  // epilogue: per-warp staging of a 16-token x 32-column output block (x2 for n-pair tiles)
   static constexpr int kEpiStageBytes = 4 * 1024 * (kNPer == 2 ? 2 : 1);  // [4 warps][...], 16 B aligned
   static constexpr int kFixed = 2048 + 4 * (kMaxExperts + 2) + 8 * kTileTab + 512 + 16 + kEpiStageBytes;
   static constexpr int kNS0 = (kSmemBudget - kFixed - 1024) / kStageBytes;
@@ -302,7 +304,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   uint64_t* accempty = accfull + C::kNumAcc;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accempty + C::kNumAcc);
   uint64_t* trbar = accempty + C::kNumAcc + 2;  // trace builds: per-stage MMA completion (8-deep ring)
-  uint64_t* trbar2 = trbar + 8;                  // trace builds: MMA warp's post-issue arrive (8-deep ring)
   int* mt_off = reinterpret_cast<int*>(bars + 256);
   uint2* tile_tab = reinterpret_cast<uint2*>(mt_off + kMaxExperts + 2);  // 8-byte aligned (odd int count + 1)
   int* n_tiles_sm = mt_off + kMaxExperts + 1;
@@ -329,7 +330,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     for (int i = 0; i < C::kNumAcc; ++i) { mbar_init(&accfull[i], 1); mbar_init(&accempty[i], C::kAccEmptyArrivals); }
 #ifdef W4A16_TRACE
     for (int i = 0; i < 8; ++i) mbar_init(&trbar[i], 1);
-    for (int i = 0; i < 8; ++i) mbar_init(&trbar2[i], 1);
 #endif
     fence_mbar_init();
   } else if (warp == 2) {
@@ -382,15 +382,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // offset mode: all 32 lanes also copy the stage's (C, S) sums with 8-byte cp.async and arrive on
     // the same barrier when their copies land.
 #ifdef W4A16_TRACE
-    if (!kOffset && lane == 2 && tr && !kPair && !C::kSplitA && !C::kDual) {  // visibility of the MMA warp's arrive (event 22)
-      uint32_t n = 0;
-      TileInfo ti;
-      for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it)
-        for (int j = stage_beg(ti); j < stage_end(ti); ++j, ++n) {
-          mbar_wait(&trbar2[n & 7], (n >> 3) & 1);
-          trace_at(tr, 22, n);
-        }
-    }
     if (!kOffset && lane == 1 && tr && !kPair && !C::kDual) {  // MMA completion times (trace event 15)
       uint32_t n = 0;
       TileInfo ti;
@@ -571,10 +562,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                 dcol, acol, xdesc, idesc, static_cast<uint32_t>(j));
             trace_at(tr, 5, gs);
 #ifdef W4A16_TRACE
-            if (!kOffset && !kPair && tr) {
-              mbar_arrive(&trbar2[gs & 7]);  // right after the MMAs: how soon do other warps see it?
-              umma_commit(&trbar[gs & 7]);
-            }
+            if (!kOffset && !kPair && tr) umma_commit(&trbar[gs & 7]);
 #endif
             if constexpr (kPair) {
               umma_commit_pair(&empty[st.i]);
@@ -767,7 +755,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         __syncwarp();  // the staging block is rewritten by the next call
       };
       if constexpr (kOffset) {
-        constexpr int kOuts = kGated ? 2 : 1;  // gate|up accumulators, else one (k-pair parts summed)
+        // gate|up, or the two n-tiles of an n-pair tile; else one (k-pair parts summed)
+        constexpr int kOuts = (kGated || C::kNPer == 2) ? 2 : 1;
         const int m_rows = ti.m_rows;
         float a[kOuts][kNTok];
 #pragma unroll
@@ -810,7 +799,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll
                 for (int p = 0; p < C::kParts; ++p) {
                   const int g = kMode == kModeKPair ? p : 0;
-                  const int o = kGated ? p : 0;
+                  const int o = (kGated || C::kNPer == 2) ? p : 0;
                   const float2 cs = csg[g];
                   float pv = __uint_as_float(r[p][0][i]);
 #pragma unroll
@@ -841,7 +830,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           for (int m = 0; m < kNTok; ++m) {
             if (m < m_rows) {
 #pragma unroll
-              for (int o = 0; o < kOuts; ++o) pbase[static_cast<int64_t>(m) * args.part_ld + o * args.ldo] = a[o][m];
+              for (int o = 0; o < kOuts; ++o)  // up half at +n_out; an n-pair's second tile at +128
+                pbase[static_cast<int64_t>(m) * args.part_ld + o * (kGated ? args.ldo : kTileRows)] = a[o][m];
             }
           }
         } else {
@@ -860,6 +850,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               hv[m] = m < m_rows ? act_bits_to_float<kBF16>(hb[i]) : 0.f;
             }
             store16_staged(m0, ro, hb, 0, 0);
+            if constexpr (C::kNPer == 2) {  // the pair's second n-tile
+              uint16_t hu[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) hu[i] = to_act_bits<kBF16>(a[kOuts - 1][m0 + i]);
+              store16_staged(m0, ro, hu, kTileRows, 1);
+            }
           }
           if constexpr (kGated && kNTok <= 16) {
             if (args.osum != nullptr) {
@@ -1215,6 +1211,15 @@ int npair_min_ntok() {
   return v;
 }
 
+// n-pair stages for the decode (offset-mode) down projection (W4A16_DECODE_NPAIR=0 disables)
+bool decode_npair_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("W4A16_DECODE_NPAIR");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 // Experiment knob: W4A16_PREFILL_PAIR=1 runs the prefill (64/128-token) kernels on CTA pairs.
 bool prefill_pairs_enabled() {
   static const bool on = [] {
@@ -1270,6 +1275,9 @@ GemmPlan plan_gemm(int64_t rows, int64_t K, int64_t num_experts, int64_t n_out, 
   pl.mode = gated ? kModeGateUp : ((kt % 2 == 0 && pl.ntok <= 64) ? kModeKPair : kModePlain);
   // prefill down projection: two n-tiles per stage share the X tile (halves the X smem traffic)
   if (!gated && !pl.offset && pl.ntok >= npair_min_ntok() && nt % 2 == 0) pl.mode = kModeNPair;
+  // decode down projection: n-pair stages too (one k-group of two n-tiles on one X tile): tiles of
+  // K/128 stages instead of K/256 k-pair stages, half the X bytes per stage
+  if (!gated && pl.offset && pl.ntok == 16 && nt % 2 == 0 && decode_npair_enabled()) pl.mode = kModeNPair;
   const int n_stages = kt / (pl.mode == kModeKPair ? 2 : 1);
   pl.splits = (pl.offset && rows < (1 << 20)) ? choose_splits(rows, num_experts, nt, n_stages, sm_count()) : 1;
   return pl;
@@ -1367,6 +1375,9 @@ int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t*
   else if (pl.mode == kModeKPair)
     rc = bf ? dispatch_ntok<kModeKPair, true>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream)
             : dispatch_ntok<kModeKPair, false>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream);
+  else if (pl.mode == kModeNPair && pl.offset)  // decode n-pair: 16-token tiles, no CTA pairs
+    rc = bf ? launch_gemm<16, kModeNPair, true, true, false>(a, x, rows, K, grid, stream)
+            : launch_gemm<16, kModeNPair, false, true, false>(a, x, rows, K, grid, stream);
   else if (pl.mode == kModeNPair)
     rc = bf ? dispatch_prefill<kModeNPair, true>(pl.ntok, a, x, rows, K, grid, stream)
             : dispatch_prefill<kModeNPair, false>(pl.ntok, a, x, rows, K, grid, stream);

@@ -224,11 +224,20 @@ def test_grouped_gemm_ring_wrap(gated, sums):
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
 
 
+@pytest.mark.parametrize("N,ntok", [(384, 16), (640, 16), (384, 32)])
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+def test_grouped_gemm_odd_ntiles_decode(N, ntok, dt):
+    """An odd number of n-tiles cannot form n-pairs: the decode down projection falls back to k-pair
+    stages (two k-groups of one n-tile per stage)."""
+    got, want = _gemm_case(dt, False, [3, 0, 17, 9], K=1024, N=N, ntok=ntok, seed=9, sums=True)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+
+
 @pytest.mark.parametrize("gated,K,N", [(True, 2048, 1024), (False, 4096, 512), (False, 1920, 256)])
 @pytest.mark.parametrize("dt", ["f16", "bf16"])
 def test_grouped_gemm_splitk(gated, K, N, dt):
     """Few tiles (1-2 experts, a few tokens): the decode GEMM splits K over CTAs into fp32 partials
-    and a finalize kernel (k-pair, gated and plain block modes)."""
+    and a finalize kernel (gated and n-pair block modes; K/128 = 15 is odd)."""
     got, want = _gemm_case(dt, gated, [2, 0, 3] if gated else [1, 2], K=K, N=N, ntok=16, seed=8, sums=True,
                            splitk=True)
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=(2 if dt == "bf16" else 1) * ATOL)

@@ -38,7 +38,7 @@ nout = N // 2 if gated else N
 xs = ops.group_sums(x) if a.ntok <= 32 else None
 for _ in range(2):
     ops.grouped_gemm(x, w.blocks, E, nout, gated, counts, off, a.ntok, xsum=xs)
-buf = torch.full((23, 4096), -1, dtype=torch.int64, device=dev)
+buf = torch.full((22, 4096), -1, dtype=torch.int64, device=dev)
 _lib.call("w4a16_debug_trace_cta", a.cta)
 _lib.call("w4a16_debug_trace", buf.data_ptr())
 torch.cuda.synchronize()
@@ -71,8 +71,6 @@ if (t[16] >= 0).sum() > 8:  # per-quad afull arrival (rows 16..19), relative to 
     q = [t[16 + i][s] for i in range(4)]
     print("  afull arrival per quad rel. to quad 0:", [round(m(q[i] - q[0]), 1) for i in range(4)],
           f" MMA ready - last arrival {m(t[4][s] - np.max(np.stack(q), axis=0)):.1f}")
-if (t[22] >= 0).sum() > 8:
-    print(f"  MMA warp arrive right after issuing -> seen by another warp {m(t[22][s] - t[5][s]):8.1f}")
 if (t[20] >= 0).sum() > 8:
     print(f"  MMA warp: issued -> commits accepted {m(t[20][s] - t[5][s]):8.1f}, -> reconverged {m(t[21][s] - t[5][s]):8.1f}, "
           f"reconverged -> next ready {m(t[4][lo + 1:hi + 1] - t[21][s]):8.1f}")
