@@ -146,7 +146,8 @@ int w4a16_pick_ntok(int64_t rows, int64_t num_experts);
  * several CTAs writing fp32 partials to ws, then summed (and SiLU*up applied) by a finalize kernel.
  * ws_bytes >= w4a16_grouped_gemm_ws_bytes(...) (0 when no split is planned); a smaller workspace
  * just disables split-K. osum (optional): also produce the output's group sums (w4a16_group_sums
- * layout) -- the next GEMM's xsum; the decode gate/up epilogue computes them in place. out_rows
+ * layout) -- the next GEMM's xsum; the decode gate/up epilogue computes them in place (gated, xsum
+ * given, 16-token tiles, no split-K; otherwise a w4a16_group_sums pass follows the GEMM). out_rows
  * (optional): row i of the result is written to out row out_rows[i] (e.g. straight back into
  * expert-parallel arrival order); not combinable with osum. */
 int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t* wblocks, int64_t num_experts,

@@ -16,6 +16,8 @@ the experts are sharded across ranks and tokens travel by all-to-all (:mod:`.ep`
 """
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import ops
@@ -58,6 +60,9 @@ class _Workspace:
 
 
 _ws = _Workspace()
+# decode: h's group sums from the gate/up epilogue instead of a separate kernel -- W4A16_FUSED_OSUM=1 / 0
+# forces it on / off; unset: by rows per expert (see moe_w4a16)
+_FUSED_OSUM = None if os.environ.get("W4A16_FUSED_OSUM", "") == "" else os.environ["W4A16_FUSED_OSUM"] != "0"
 # largest token tile that runs the offset-code (decode) GEMM; larger tiles dequantise with the scale
 _DECODE_MAX_NTOK = int(__import__("os").environ.get("W4A16_DECODE_MAX_NTOK", "16"))
 
@@ -147,12 +152,17 @@ def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, 
         return _ws.get("splitk", (b,), torch.uint8, dev) if b else None
 
     hs = _ws.get("hs", ops.sums_shape(P, I), torch.float32, dev) if decode else None
-    # h's group sums (the down GEMM's xsum): a separate small kernel -- measured slightly faster than
-    # the GEMM's fused osum epilogue (its per-tile cross-warp reduction stalls the epilogue warps)
+    gu_ws = splitk_ws(H, I, True)
+    # h's group sums (the down GEMM's xsum) from the gate/up epilogue: measured ~1 % faster than the
+    # separate kernel at <= 2 rows per expert (DS-R1 T <= 64), 3 % slower at 8 (T = 256; the epilogue's
+    # per-tile cross-warp reduction grows with the tile's rows)
+    want_fused = P <= 4 * E if _FUSED_OSUM is None else _FUSED_OSUM
+    fused_osum = decode and want_fused  # (with split-K the C entry point runs the sums pass itself)
     with tm.span("gemm_gate_up"):
         h = ops.grouped_gemm(xp, weights.w13.blocks, E, I, True, counts, offsets, nt,
-                             out=_ws.get("h", (P, I), x.dtype, dev), xsum=xs, workspace=splitk_ws(H, I, True))
-    if decode:
+                             out=_ws.get("h", (P, I), x.dtype, dev), xsum=xs, workspace=gu_ws,
+                             osum=hs if fused_osum else None)
+    if decode and not fused_osum:
         with tm.span("sums_h"):
             ops.group_sums(h, offsets[E:], out=hs)
     with tm.span("gemm_down"):
