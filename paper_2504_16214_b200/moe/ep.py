@@ -71,10 +71,15 @@ class CudaBackend:
         nt = ntok or cuda_ops.pick_ntok(x.shape[0], E)
         from .layer import _DECODE_MAX_NTOK
         decode = nt <= _DECODE_MAX_NTOK
-        xs = cuda_ops.group_sums(x) if decode else None
+        xs = hs = None
+        if decode:
+            with tm.span("sums_x"):
+                xs = cuda_ops.group_sums(x)
         with tm.span("gemm_gate_up"):
             h = cuda_ops.grouped_gemm(x, weights.w13.blocks, E, I, True, counts, offsets, nt, xsum=xs)
-        hs = cuda_ops.group_sums(h) if decode else None
+        if decode:
+            with tm.span("sums_h"):
+                hs = cuda_ops.group_sums(h)
         with tm.span("gemm_down"):
             return cuda_ops.grouped_gemm(h, weights.w2.blocks, E, H, False, counts, offsets, nt, xsum=hs,
                                          out_rows=out_rows)
@@ -92,9 +97,13 @@ def moe_w4a16_ep(x: torch.Tensor, weights, topk_weights: torch.Tensor, topk_ids:
     topk_ids = topk_ids.to(torch.int32).contiguous()
     topk_weights = topk_weights.to(torch.float32).contiguous()
 
+    from .layer import _NOTIMER
+    tm = timer or _NOTIMER
     # 1-2: group pairs by destination (global expert order) and pack rows
-    g_counts, g_offsets, sorted_pairs, pair_pos = backend.permute(topk_ids, e_global)
-    send_x = backend.gather(x.contiguous(), sorted_pairs, k, T * k)
+    with tm.span("permute"):
+        g_counts, g_offsets, sorted_pairs, pair_pos = backend.permute(topk_ids, e_global)
+    with tm.span("gather"):
+        send_x = backend.gather(x.contiguous(), sorted_pairs, k, T * k)
     # 3: counts exchange + host splits
     plan = plan_dispatch(g_counts, world, group)
     n_recv = sum(plan.recv_splits)
@@ -103,11 +112,13 @@ def moe_w4a16_ep(x: torch.Tensor, weights, topk_weights: torch.Tensor, topk_ids:
     dist.all_to_all_single(recv_x, send_x, plan.recv_splits, plan.send_splits, group=group)
     # 5: local expert order + grouped GEMMs
     if hasattr(backend, "local_order"):
-        l_counts, l_offsets, l_sorted, l_pos = backend.local_order(plan.recv_counts, n_recv)
+        with tm.span("local_order"):
+            l_counts, l_offsets, l_sorted, l_pos = backend.local_order(plan.recv_counts, n_recv)
     else:  # generic: ids of the received rows, then the stable permutation
         lid = local_expert_ids(plan.recv_counts, n_recv)
         l_counts, l_offsets, l_sorted, l_pos = backend.permute(lid, e_local)
-    xl = backend.gather(recv_x, l_sorted, 1, n_recv) if n_recv else recv_x
+    with tm.span("gather_local"):
+        xl = backend.gather(recv_x, l_sorted, 1, n_recv) if n_recv else recv_x
     # 6: the down GEMM scatters its rows straight back to arrival order; combine exchange, reduction
     if not n_recv:
         y_recv = recv_x
@@ -118,7 +129,8 @@ def moe_w4a16_ep(x: torch.Tensor, weights, topk_weights: torch.Tensor, topk_ids:
         y_recv = backend.gather(yl, l_pos, 1, n_recv)
     y_back = x.new_empty((T * k, H))
     dist.all_to_all_single(y_back, y_recv, plan.send_splits, plan.recv_splits, group=group)
-    return backend.combine(y_back, pair_pos, topk_weights)
+    with tm.span("combine"):
+        return backend.combine(y_back, pair_pos, topk_weights)
 
 
 def shard_bounds(num_experts: int, world: int, rank: int) -> tuple[int, int]:
