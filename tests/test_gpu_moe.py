@@ -444,3 +444,35 @@ def test_c_abi_moe_forward(T):
     assert lib.w4a16_moe_forward(xd.data_ptr(), T, H, I, E, k, idd.data_ptr(), wd.data_ptr(), w.w13.blocks.data_ptr(),
                                  w.w2.blocks.data_ptr(), 0, y.data_ptr(), ws.data_ptr(), wsb - 1,
                                  torch.cuda.current_stream().cuda_stream) == -6  # W4_ERR_WORKSPACE
+
+
+def test_ep_nccl_world1_layer():
+    """The expert-parallel path over NCCL (all-to-all dispatch / combine, receiver-side local order,
+    scattered down GEMM) at world size 1 == the oracle layer."""
+    import socket
+    import torch.distributed as dist
+    from paper_2504_16214_b200.moe import fused_moe_w4a16
+    from paper_2504_16214_b200.moe.weights import MoEWeights
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(41)
+        for T, dt in ((40, "f16"), (300, "bf16")):  # decode (16-token tiles) and prefill tiles
+            E, k, H, I = 16, 4, 256, 256
+            q13, z13, s13 = O.synth_awq_expert_weights(rng, E, 2 * I, H, dt)
+            q2, z2, s2 = O.synth_awq_expert_weights(rng, E, H, I, dt)
+            w = MoEWeights(_packed(q13, z13, s13, dt, True), _packed(q2, z2, s2, dt, False))
+            x = O.round_act(rng.standard_normal((T, H)).astype(np.float32) * 0.5, dt)
+            lg = rng.standard_normal((T, E)).astype(np.float32)
+            y = fused_moe_w4a16(_to_dev_act(x, dt), torch.from_numpy(lg).cuda(), w, k, "softmax", True,
+                                ep_group=dist.group.WORLD)
+            torch.cuda.synchronize()
+            rid, rw = O.route_topk(lg, k, "softmax", True)
+            want = O.moe_forward(x, O.dequant(q13, z13, s13, dt), O.dequant(q2, z2, s2, dt), rid, rw, dt)
+            np.testing.assert_allclose(_from_dev_act(y, dt), want, rtol=RTOL, atol=(2 if dt == "bf16" else 1) * ATOL)
+    finally:
+        dist.destroy_process_group()
