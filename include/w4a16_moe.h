@@ -15,6 +15,7 @@
  *             w4a16_moe_gather_sums                    same, plus per-group activation sums (decode)
  *   sums:     w4a16_group_sums                         per-(group of 128 k, row) sums of an activation
  *   GEMM:     w4a16_grouped_gemm                       per-expert X_e * W_e^T, optional fused SiLU*up
+ *             w4a16_grouped_gemm_gather                same, X rows gathered by the producer (TMA gather4)
  *   combine:  w4a16_moe_combine                        y[t] = sum_j w[t,j] * Y_perm[pos(t,j)]
  *   EP:       w4a16_ep_pack_counts / w4a16_moe_permute over received rows (NCCL all-to-all is
  *             driven by the host through torch.distributed)
@@ -154,6 +155,17 @@ int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t*
                           int64_t n_out, int gated, const int32_t* expert_counts, const int32_t* expert_offsets,
                           const float* xsum, float* osum, const int32_t* out_rows, void* out, int dtype, int ntok,
                           void* ws, int64_t ws_bytes, cudaStream_t stream);
+
+/* The gate/up GEMM with the token gather fused into its producer (replaces w4a16_moe_gather +
+ * w4a16_grouped_gemm): row i of the GEMM input is row gather_rows[i] / gather_div of x [x_rows][K]
+ * (gather_rows = sorted_pairs and gather_div = top_k for the MoE layer), loaded with TMA gather4.
+ * xsum, when given, holds the group sums of x's own rows (w4a16_group_sums over x). No out_rows, no
+ * CTA pairs. */
+int w4a16_grouped_gemm_gather(const void* x, int64_t x_rows, const int32_t* gather_rows, int gather_div, int64_t rows,
+                              int64_t K, const uint8_t* wblocks, int64_t num_experts, int64_t n_out, int gated,
+                              const int32_t* expert_counts, const int32_t* expert_offsets, const float* xsum,
+                              float* osum, void* out, int dtype, int ntok, void* ws, int64_t ws_bytes,
+                              cudaStream_t stream);
 int64_t w4a16_grouped_gemm_ws_bytes(int64_t rows, int64_t K, int64_t num_experts, int64_t n_out, int gated,
                                     int ntok);
 

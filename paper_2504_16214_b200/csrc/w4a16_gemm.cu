@@ -75,8 +75,13 @@ struct GemmArgs {
   int splits;                    // split-K factor (decode mode; 1 = none)
   float* part;                   // splits > 1: fp32 partials [splits][rows][part_ld]
   int64_t part_ld;               // (gated ? 2 : 1) * n_out
-  float2* osum;                  // gated decode: (C, S) sums of the output h [nt][sum_ld] (next GEMM's xsum)
+  float2* osum;                  // gated decode: (C, S) sums of the output h [nt][osum_ld] (next GEMM's xsum)
+  int64_t osum_ld;               // = w4a16_group_sums_ld(rows) (sum_ld follows x's rows under a fused gather)
   const int32_t* out_rows;       // optional: output row of input row i (scatter, e.g. back to EP arrival order)
+  // optional fused gather: row i of the GEMM input is row gather_rows[i] / gather_div of x (the X map
+  // then covers x itself and the producer loads rows with TMA gather4); xsum is indexed by x's rows
+  const int32_t* gather_rows;
+  int gather_div;
 };
 
 // Numeric modes.
@@ -273,6 +278,18 @@ __device__ __forceinline__ float act_bits_to_float(uint32_t b) {
   else return __half2float(__ushort_as_half(static_cast<unsigned short>(b)));
 }
 
+// TMA tile::gather4: rows r0..r3 of the 2-D map (box {64 columns, 1 row}), 64 columns from `col`, into
+// 4 consecutive 128-byte smem rows (128B swizzle by smem row, the same layout as a 2-D box load;
+// tools/microbench/tma_gather4.cu)
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, int col, int r0, int r1, int r2, int r3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+      "%6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+
 struct Ring {  // (stage, phase) iterator of an mbarrier ring
   int i = 0;
   uint32_t ph = 0;
@@ -392,8 +409,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
     }
 #endif
-    if (kOffset || lane == 0) {
+    const bool gather = args.gather_rows != nullptr;  // fused gather: all lanes issue gather4 loads
+    if (kOffset || gather || lane == 0) {
       const uint64_t pol_w = policy_evict_first();
+      // gather: this lane loads 4-row group lane % kG4 of the X tile, k halves lane / kG4 (+ 32 / kG4 ...)
+      constexpr int kG4 = (kNTok / 4 < 32) ? kNTok / 4 : 32;
+      constexpr int kHalves = 2 * C::kGroupsPerStage;
+      int src4[4] = {0, 0, 0, 0};
       Ring st;
       uint32_t pgs = 0;
       TileInfo ti;
@@ -405,6 +427,14 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         // the peer's, so the peer's X rows start at token N/2 of the tile (N = the tile's MMA N, below)
         const int x_row0 = ti.m_start + static_cast<int>(rank) *
                                             (min(kNTok, (ti.m_rows + 16 * C::kCG - 1) / (16 * C::kCG) * (16 * C::kCG)) / 2);
+        if (gather) {  // source rows of this lane's 4-row group (rows past the tile's end repeat its first)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int m = (static_cast<int>(lane) % kG4) * 4 + q;
+            const int i = ti.m_start + (m < ti.m_rows ? m : 0);
+            src4[q] = __ldg(args.gather_rows + i) / args.gather_div;
+          }
+        }
         for (int j = stage_beg(ti); j < stage_end(ti); ++j) {
           mbar_wait(&empty[st.i], st.ph ^ 1);
           if (lane == 0) {
@@ -419,11 +449,22 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               bulk_g2s_hint(smem_w + st.i * C::kBlk, wsrc + static_cast<int64_t>(j) * C::kBlk, C::kBlk, &full[st.i],
                             pol_w);
             }
-            uint8_t* xs = smem_x + st.i * C::kXBytes;
+            if (!gather) {
+              uint8_t* xs = smem_x + st.i * C::kXBytes;
 #pragma unroll
-            for (int h = 0; h < 2 * C::kGroupsPerStage; ++h)
-              tma_load_2d(xs + h * (C::kXRows * 128), &xmap, j * C::kGroupsPerStage * kTileK + h * 64,
-                          x_row0, &full[st.i]);
+              for (int h = 0; h < kHalves; ++h)
+                tma_load_2d(xs + h * (C::kXRows * 128), &xmap, j * C::kGroupsPerStage * kTileK + h * 64,
+                            x_row0, &full[st.i]);
+            }
+          }
+          if (gather) {
+            __syncwarp();  // lane 0's expect_tx is in: the gathers complete bytes on the same phase
+            uint8_t* xs = smem_x + st.i * C::kXBytes;
+            for (int op = static_cast<int>(lane); op < (kNTok / 4) * kHalves; op += 32) {
+              const int g4 = op % kG4, h = op / kG4;  // kG4 == kNTok / 4 whenever ops exceed 32 lanes
+              tma_gather4(xs + h * (C::kXRows * 128) + g4 * 512, &xmap, j * C::kGroupsPerStage * kTileK + h * 64,
+                          src4[0], src4[1], src4[2], src4[3], &full[st.i]);
+            }
           }
           if constexpr (kOffset) {
             // all 32 lanes copy and arrive every stage (fewer items than lanes: items are duplicated --
@@ -434,7 +475,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             for (int i0 = 0; i0 < (C::kSumItems > 32 ? C::kSumItems : 32); i0 += 32) {
               const int i = (i0 + lane) % C::kSumItems;
               const int g = i / kNTok, m = i % kNTok;
-              const int64_t r = ti.m_start + m < args.rows ? ti.m_start + m : 0;
+              int64_t r = ti.m_start + m < args.rows ? ti.m_start + m : 0;
+              if (gather) r = __ldg(args.gather_rows + r) / args.gather_div;  // sums of x's rows
               cp_async_8(ss + i * 8,
                          args.xsum + ((static_cast<int64_t>(j) * C::kGroupsPerStage + g) * args.sum_ld + r) * 2);
             }
@@ -884,7 +926,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                   t.x += u.x;
                   t.y += u.y;
                 }
-                args.osum[static_cast<int64_t>(ti.n_tile) * args.sum_ld + ti.m_start + lane] = t;
+                args.osum[static_cast<int64_t>(ti.n_tile) * args.osum_ld + ti.m_start + lane] = t;
               }
               named_bar_sync(1, 128);  // scratch reused by the next tile
             }
@@ -1152,7 +1194,7 @@ int launch_gemm(const GemmArgs& a, const void* x, int64_t rows, int64_t K, int g
     attr = true;
   }
   CUtensorMap map;
-  if (make_x_map(&map, x, rows, K, C::kXRows) != W4_OK) return W4_ERR_CUDA;
+  if (make_x_map(&map, x, rows, K, a.gather_rows ? 1 : C::kXRows) != W4_OK) return W4_ERR_CUDA;  // gather4: 1-row box
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kPair ? (grid & ~1) : grid);
   cfg.blockDim = dim3(kNumThreads);
@@ -1328,7 +1370,8 @@ int64_t w4a16_grouped_gemm_ws_bytes(int64_t rows, int64_t K, int64_t num_experts
   return pl.splits > 1 ? static_cast<int64_t>(pl.splits) * rows * (gated ? 2 : 1) * n_out * 4 : 0;
 }
 
-int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t* wblocks, int64_t num_experts,
+static int grouped_gemm_impl(const void* x, int64_t x_rows, const int32_t* gather_rows, int gather_div,
+                             int64_t rows, int64_t K, const uint8_t* wblocks, int64_t num_experts,
                           int64_t n_out, int gated, const int32_t* expert_counts, const int32_t* expert_offsets,
                           const float* xsum, float* osum, const int32_t* out_rows, void* out, int dtype, int ntok,
                           void* ws, int64_t ws_bytes, cudaStream_t stream) {
@@ -1353,7 +1396,10 @@ int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t*
   a.nt = static_cast<int>(n_out / kTileRows);
   a.kt = static_cast<int>(K / kTileK);
   a.xsum = xsum;
-  a.sum_ld = w4a16_group_sums_ld(rows);
+  a.sum_ld = w4a16_group_sums_ld(gather_rows ? x_rows : rows);  // xsum covers x's rows
+  a.osum_ld = w4a16_group_sums_ld(rows);
+  a.gather_rows = gather_rows;
+  a.gather_div = gather_div;
   a.rows = rows;
   a.splits = pl.splits;
   a.part = static_cast<float*>(ws);
@@ -1365,25 +1411,25 @@ int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t*
   if (out_rows && osum) return W4_ERR_ARG;  // sums of a scattered output are not supported
   // CTA pairs (cta_group::2) measured slower at decode token counts (an M=256 x N=16 MMA with 8-row B
   // halves executes ~4x slower than two M=128 ones): opt-in only (W4A16_PAIR=1)
-  const bool pair = pl.splits == 1 && a.nt % 2 == 0 && (pl.offset ? pairs_enabled() : prefill_pairs_enabled());
+  const bool pair = !gather_rows && pl.splits == 1 && a.nt % 2 == 0 && (pl.offset ? pairs_enabled() : prefill_pairs_enabled());
   const int grid = sm_count();
   const bool bf = dtype == W4_DTYPE_BF16;
   int rc;
   if (pl.mode == kModeGateUp)
-    rc = bf ? dispatch_ntok<kModeGateUp, true>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream)
-            : dispatch_ntok<kModeGateUp, false>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream);
+    rc = bf ? dispatch_ntok<kModeGateUp, true>(pl.ntok, pl.offset, pair, a, x, x_rows, K, grid, stream)
+            : dispatch_ntok<kModeGateUp, false>(pl.ntok, pl.offset, pair, a, x, x_rows, K, grid, stream);
   else if (pl.mode == kModeKPair)
-    rc = bf ? dispatch_ntok<kModeKPair, true>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream)
-            : dispatch_ntok<kModeKPair, false>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream);
+    rc = bf ? dispatch_ntok<kModeKPair, true>(pl.ntok, pl.offset, pair, a, x, x_rows, K, grid, stream)
+            : dispatch_ntok<kModeKPair, false>(pl.ntok, pl.offset, pair, a, x, x_rows, K, grid, stream);
   else if (pl.mode == kModeNPair && pl.offset)  // decode n-pair: 16-token tiles, no CTA pairs
-    rc = bf ? launch_gemm<16, kModeNPair, true, true, false>(a, x, rows, K, grid, stream)
-            : launch_gemm<16, kModeNPair, false, true, false>(a, x, rows, K, grid, stream);
+    rc = bf ? launch_gemm<16, kModeNPair, true, true, false>(a, x, x_rows, K, grid, stream)
+            : launch_gemm<16, kModeNPair, false, true, false>(a, x, x_rows, K, grid, stream);
   else if (pl.mode == kModeNPair)
-    rc = bf ? dispatch_prefill<kModeNPair, true>(pl.ntok, a, x, rows, K, grid, stream)
-            : dispatch_prefill<kModeNPair, false>(pl.ntok, a, x, rows, K, grid, stream);
+    rc = bf ? dispatch_prefill<kModeNPair, true>(pl.ntok, a, x, x_rows, K, grid, stream)
+            : dispatch_prefill<kModeNPair, false>(pl.ntok, a, x, x_rows, K, grid, stream);
   else
-    rc = bf ? dispatch_ntok<kModePlain, true>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream)
-            : dispatch_ntok<kModePlain, false>(pl.ntok, pl.offset, pair, a, x, rows, K, grid, stream);
+    rc = bf ? dispatch_ntok<kModePlain, true>(pl.ntok, pl.offset, pair, a, x, x_rows, K, grid, stream)
+            : dispatch_ntok<kModePlain, false>(pl.ntok, pl.offset, pair, a, x, x_rows, K, grid, stream);
   if (rc != W4_OK) return rc;
   if (pl.splits > 1) {
   const int thr = 128;
@@ -1401,6 +1447,24 @@ int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t*
   if (osum != nullptr && !fused_osum)
     return w4a16_group_sums(out, rows, n_out, expert_offsets + num_experts, dtype, osum, stream);
   return W4_OK;
+}
+
+int w4a16_grouped_gemm_ws(const void* x, int64_t rows, int64_t K, const uint8_t* wblocks, int64_t num_experts,
+                          int64_t n_out, int gated, const int32_t* expert_counts, const int32_t* expert_offsets,
+                          const float* xsum, float* osum, const int32_t* out_rows, void* out, int dtype, int ntok,
+                          void* ws, int64_t ws_bytes, cudaStream_t stream) {
+  return grouped_gemm_impl(x, rows, nullptr, 1, rows, K, wblocks, num_experts, n_out, gated, expert_counts,
+                           expert_offsets, xsum, osum, out_rows, out, dtype, ntok, ws, ws_bytes, stream);
+}
+
+int w4a16_grouped_gemm_gather(const void* x, int64_t x_rows, const int32_t* gather_rows, int gather_div, int64_t rows,
+                              int64_t K, const uint8_t* wblocks, int64_t num_experts, int64_t n_out, int gated,
+                              const int32_t* expert_counts, const int32_t* expert_offsets, const float* xsum,
+                              float* osum, void* out, int dtype, int ntok, void* ws, int64_t ws_bytes,
+                              cudaStream_t stream) {
+  if (!gather_rows || gather_div <= 0 || x_rows <= 0) return W4_ERR_ARG;
+  return grouped_gemm_impl(x, x_rows, gather_rows, gather_div, rows, K, wblocks, num_experts, n_out, gated,
+                           expert_counts, expert_offsets, xsum, osum, nullptr, out, dtype, ntok, ws, ws_bytes, stream);
 }
 
 int w4a16_grouped_gemm(const void* x, int64_t rows, int64_t K, const uint8_t* wblocks, int64_t num_experts,

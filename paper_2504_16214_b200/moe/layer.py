@@ -60,6 +60,10 @@ class _Workspace:
 
 
 _ws = _Workspace()
+# experiment (W4A16_FUSED_GATHER=1): the gate/up GEMM gathers x's rows itself (TMA gather4 in its
+# producer) instead of a gather kernel. Correct (bit-identical) but measured 1.5x slower at T=64 and 2.8x
+# slower gate/up at T=8192: 64 four-row gather4 requests per 49 KB stage throttle the TMA unit.
+_FUSED_GATHER = os.environ.get("W4A16_FUSED_GATHER", "0") not in ("", "0")
 # decode: h's group sums from the gate/up epilogue instead of a separate kernel -- W4A16_FUSED_OSUM=1 / 0
 # forces it on / off; unset: by rows per expert (see moe_w4a16)
 _FUSED_OSUM = None if os.environ.get("W4A16_FUSED_OSUM", "") == "" else os.environ["W4A16_FUSED_OSUM"] != "0"
@@ -140,13 +144,21 @@ def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, 
             topk_ids, E, _ws.get("perm_ws", (max(ops.permute_ws_bytes(P, E), 1),), torch.uint8, dev))
     nt = ntok or ops.pick_ntok(P, E)
     decode = nt <= _DECODE_MAX_NTOK  # offset-code GEMMs: per-group activation sums ride along with X and h
-    with tm.span("gather"):
-        xp_buf = _ws.get("xp", (P, H), x.dtype, dev)
+    if _FUSED_GATHER:  # the gate/up producer gathers x's rows itself (TMA gather4); decode sums over x
+        xp = None
         if decode:
-            xp, xs = ops.moe_gather_sums(x, sorted_pairs, k, P, offsets[E:], out=xp_buf,
-                                         sums=_ws.get("xs", ops.sums_shape(P, H), torch.float32, dev))
+            with tm.span("sums_x"):
+                xs = ops.group_sums(x, out=_ws.get("xs", ops.sums_shape(T, H), torch.float32, dev))
         else:
-            xp, xs = ops.moe_gather(x, sorted_pairs, k, P, offsets[E:], out=xp_buf), None
+            xs = None
+    else:
+        with tm.span("gather"):
+            xp_buf = _ws.get("xp", (P, H), x.dtype, dev)
+            if decode:
+                xp, xs = ops.moe_gather_sums(x, sorted_pairs, k, P, offsets[E:], out=xp_buf,
+                                             sums=_ws.get("xs", ops.sums_shape(P, H), torch.float32, dev))
+            else:
+                xp, xs = ops.moe_gather(x, sorted_pairs, k, P, offsets[E:], out=xp_buf), None
     def splitk_ws(K: int, n_out: int, gated: bool):
         b = ops.gemm_ws_bytes(P, K, E, n_out, gated, nt) if decode else 0
         return _ws.get("splitk", (b,), torch.uint8, dev) if b else None
@@ -159,9 +171,13 @@ def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, 
     want_fused = P <= 4 * E if _FUSED_OSUM is None else _FUSED_OSUM
     fused_osum = decode and want_fused  # (with split-K the C entry point runs the sums pass itself)
     with tm.span("gemm_gate_up"):
-        h = ops.grouped_gemm(xp, weights.w13.blocks, E, I, True, counts, offsets, nt,
-                             out=_ws.get("h", (P, I), x.dtype, dev), xsum=xs, workspace=gu_ws,
-                             osum=hs if fused_osum else None)
+        h_buf = _ws.get("h", (P, I), x.dtype, dev)
+        if xp is None:
+            h = ops.grouped_gemm_gather(x, sorted_pairs, k, weights.w13.blocks, E, I, True, counts, offsets, nt,
+                                        out=h_buf, xsum=xs, workspace=gu_ws, osum=hs if fused_osum else None, rows=P)
+        else:
+            h = ops.grouped_gemm(xp, weights.w13.blocks, E, I, True, counts, offsets, nt, out=h_buf, xsum=xs,
+                                 workspace=gu_ws, osum=hs if fused_osum else None)
     if decode and not fused_osum:
         with tm.span("sums_h"):
             ops.group_sums(h, offsets[E:], out=hs)

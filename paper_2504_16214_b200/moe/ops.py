@@ -219,6 +219,27 @@ def grouped_gemm(x: torch.Tensor, blocks: torch.Tensor, num_experts: int, n_out:
     return out
 
 
+def grouped_gemm_gather(x: torch.Tensor, gather_rows: torch.Tensor, gather_div: int, blocks: torch.Tensor,
+                        num_experts: int, n_out: int, gated: bool, expert_counts: torch.Tensor,
+                        expert_offsets: torch.Tensor, ntok: int = 0, out: torch.Tensor | None = None,
+                        xsum: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+                        osum: torch.Tensor | None = None, rows: int | None = None) -> torch.Tensor:
+    """grouped_gemm on the rows x[gather_rows[i] // gather_div] (i < rows) without materialising them:
+    the GEMM's producer gathers them with TMA gather4. ``xsum`` = group_sums(x) (x's own rows)."""
+    _need_cuda(x, gather_rows, blocks, expert_counts, expert_offsets)
+    if gather_rows.dtype != torch.int32:
+        raise _lib.W4A16Error("gather_rows must be int32")
+    rows = gather_rows.numel() if rows is None else rows
+    x_rows, K = x.shape
+    if out is None:
+        out = torch.empty((rows, n_out), dtype=x.dtype, device=x.device)
+    wsb = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _lib.call("w4a16_grouped_gemm_gather", x.data_ptr(), x_rows, gather_rows.data_ptr(), gather_div, rows, K,
+              blocks.data_ptr(), num_experts, n_out, int(gated), expert_counts.data_ptr(), expert_offsets.data_ptr(),
+              _ptr(xsum), _ptr(osum), out.data_ptr(), act_code(x.dtype), ntok, _ptr(workspace), wsb, _stream())
+    return out
+
+
 def gemm_ws_bytes(rows: int, K: int, num_experts: int, n_out: int, gated: bool, ntok: int = 0) -> int:
     """Split-K workspace bytes the decode-mode grouped GEMM would use (0: no split planned)."""
     return int(_lib.load().w4a16_grouped_gemm_ws_bytes(rows, K, num_experts, n_out, int(gated), ntok))

@@ -446,6 +446,31 @@ def test_c_abi_moe_forward(T):
                                  torch.cuda.current_stream().cuda_stream) == -6  # W4_ERR_WORKSPACE
 
 
+@pytest.mark.parametrize("ntok,dt", [(16, "f16"), (16, "bf16"), (32, "f16"), (64, "bf16"), (128, "f16")])
+def test_grouped_gemm_fused_gather(ntok, dt):
+    """The gate/up GEMM gathering x's rows itself (TMA gather4 in the producer) == gather kernel +
+    GEMM, bit for bit (same rows, same sums, same kernel otherwise)."""
+    ops = _ops()
+    rng = np.random.default_rng(ntok)
+    T, E, k, K, N = 150, 12, 4, 512, 256
+    q, z, s = O.synth_awq_expert_weights(rng, E, 2 * N, K, dt)
+    w = _packed(q, z, s, dt, True)
+    x = _to_dev_act(O.round_act(rng.standard_normal((T, K)).astype(np.float32) * 0.5, dt), dt)
+    ids = torch.from_numpy(np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)).cuda()
+    c, o, sp, pp = ops.moe_permute(ids, E)
+    P = T * k
+    decode = ntok == 16
+    if decode:
+        xp, xsp = ops.moe_gather_sums(x, sp, k)
+        xs = ops.group_sums(x)
+    else:
+        xp, xsp, xs = ops.moe_gather(x, sp, k, P), None, None
+    want = ops.grouped_gemm(xp, w.blocks, E, N, True, c, o, ntok, xsum=xsp)
+    got = ops.grouped_gemm_gather(x, sp, k, w.blocks, E, N, True, c, o, ntok, xsum=xs, rows=P)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+
+
 def test_ep_nccl_world1_layer():
     """The expert-parallel path over NCCL (all-to-all dispatch / combine, receiver-side local order,
     scattered down GEMM) at world size 1 == the oracle layer."""

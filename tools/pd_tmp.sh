@@ -1,3 +1,6 @@
 python -m paper_2504_16214_b200._build >/dev/null 2>&1
-W4A16_FUSED_OSUM=1 timeout 300 python -m pytest tests/test_gpu_moe.py -q -x -k "layer or graph or pipeline" 2>&1 | tail -1
-for f in 1 0 1 0; do echo "== FUSED_OSUM=$f"; W4A16_FUSED_OSUM=$f timeout 200 python tools/layer_sweep.py 2>&1 | grep '"ds"' | head -5; done
+timeout 200 python -m pytest tests/test_gpu_moe.py -q -x -k "fused_gather" 2>&1 | tail -3
+timeout 300 python -m pytest tests/test_gpu_moe.py -q -x 2>&1 | tail -1
+W4A16_FUSED_GATHER=0 timeout 300 python -m pytest tests/test_gpu_moe.py -q -x -k "layer or graph or pipeline or forward" 2>&1 | tail -1
+for fg in 1 0; do echo "== FUSED_GATHER=$fg"; W4A16_FUSED_GATHER=$fg timeout 200 python tools/layer_sweep.py --model ds --tokens 1,16,64,256,1024 2>&1 | tail -5
+W4A16_FUSED_GATHER=$fg timeout 200 python tools/gemm_sweep.py --tokens 8192 --reps 5 2>&1 | tail -1 | cut -c1-330; done
