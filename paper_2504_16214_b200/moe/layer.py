@@ -188,14 +188,35 @@ def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, 
         return ops.moe_combine(yp, pair_pos, topk_weights)
 
 
+def with_shared_experts(topk_weights: torch.Tensor, topk_ids: torch.Tensor, first_shared: int, num_shared: int,
+                        scale: float = 1.0):
+    """Append the always-active shared experts (DeepSeek-V3/R1: one) as extra routing slots of weight
+    ``scale``: the grouped GEMMs then run them next to the routed experts, and the combine adds their
+    output -- y = sum_j w_j E_{id_j}(x) + scale * sum_s Shared_s(x). Shared expert s is expert
+    ``first_shared + s`` of the packed weights."""
+    T = topk_ids.shape[0]
+    sid = torch.arange(first_shared, first_shared + num_shared, dtype=torch.int32, device=topk_ids.device)
+    ids = torch.cat([topk_ids.to(torch.int32), sid.expand(T, num_shared)], dim=1).contiguous()
+    wts = torch.cat([topk_weights.float(), topk_weights.new_full((T, num_shared), scale, dtype=torch.float32)],
+                    dim=1).contiguous()
+    return wts, ids
+
+
 def fused_moe_w4a16(x: torch.Tensor, router_logits: torch.Tensor, weights: MoEWeights, top_k: int,
                     scoring: str = "softmax", renormalize: bool = False, ep_group=None,
                     timer: KernelTimer | None = None, num_expert_group: int = 0, topk_group: int = 0,
                     e_score_correction_bias: torch.Tensor | None = None,
-                    routed_scaling_factor: float = 1.0) -> torch.Tensor:
+                    routed_scaling_factor: float = 1.0, num_shared_experts: int = 0) -> torch.Tensor:
+    """``num_shared_experts`` > 0: the last experts of ``weights`` are shared experts (always active,
+    weight 1; the router logits cover only the routed ones)."""
     with (timer or _NOTIMER).span("route"):
         topk_weights, topk_ids = select_experts(router_logits, top_k, scoring, renormalize, num_expert_group,
                                                 topk_group, e_score_correction_bias, routed_scaling_factor)
+    if num_shared_experts:
+        if ep_group is not None:
+            raise NotImplementedError("shared experts with expert parallelism (run them data-parallel)")
+        topk_weights, topk_ids = with_shared_experts(topk_weights, topk_ids, weights.num_experts - num_shared_experts,
+                                                     num_shared_experts)
     return moe_w4a16(x, weights, topk_weights, topk_ids, ep_group=ep_group, timer=timer)
 
 
@@ -207,24 +228,26 @@ class FusedMoEGraph:
 
     def __init__(self, weights: MoEWeights, tokens: int, top_k: int, scoring: str = "softmax",
                  renormalize: bool = False, dtype: torch.dtype = torch.float16, device=None,
-                 x: torch.Tensor | None = None, router_logits: torch.Tensor | None = None):
+                 x: torch.Tensor | None = None, router_logits: torch.Tensor | None = None,
+                 num_shared_experts: int = 0):
         dev = torch.device(device) if device is not None else weights.w13.blocks.device
         self.x = torch.zeros((tokens, weights.hidden), dtype=dtype, device=dev)
-        self.logits = torch.randn((tokens, weights.num_experts), device=dev)
+        self.logits = torch.randn((tokens, weights.num_experts - num_shared_experts), device=dev)
         if x is not None:  # warm up / capture on the caller's first inputs (same routing as served)
             self.x.copy_(x)
         if router_logits is not None:
             self.logits.copy_(router_logits)
         args = (weights, top_k, scoring, renormalize)
+        kw = {"num_shared_experts": num_shared_experts}
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side):  # warm-up: kernel attributes, workspace growth, first launches
             for _ in range(2):
-                fused_moe_w4a16(self.x, self.logits, *args)
+                fused_moe_w4a16(self.x, self.logits, *args, **kw)
         torch.cuda.current_stream(dev).wait_stream(side)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            self.y = fused_moe_w4a16(self.x, self.logits, *args)
+            self.y = fused_moe_w4a16(self.x, self.logits, *args, **kw)
         self._keep = dict(_ws.buf)  # the graph reads/writes these exact buffers: keep them alive
 
     def __call__(self, x: torch.Tensor | None = None, router_logits: torch.Tensor | None = None) -> torch.Tensor:

@@ -446,6 +446,39 @@ def test_c_abi_moe_forward(T):
                                  torch.cuda.current_stream().cuda_stream) == -6  # W4_ERR_WORKSPACE
 
 
+@pytest.mark.parametrize("T,dt", [(20, "f16"), (300, "bf16")])
+def test_fused_moe_shared_expert(T, dt):
+    """DeepSeek-style shared expert (always active, weight 1) packed as the last expert: the layer ==
+    routed oracle layer + the shared expert's MLP on every token; also through the CUDA graph."""
+    from paper_2504_16214_b200.moe import FusedMoEGraph, fused_moe_w4a16
+    from paper_2504_16214_b200.moe.weights import MoEWeights
+    rng = np.random.default_rng(T)
+    E, k, H, I = 16, 4, 256, 256  # 16 routed + 1 shared
+    q13, z13, s13 = O.synth_awq_expert_weights(rng, E + 1, 2 * I, H, dt)
+    q2, z2, s2 = O.synth_awq_expert_weights(rng, E + 1, H, I, dt)
+    w = MoEWeights(_packed(q13, z13, s13, dt, True), _packed(q2, z2, s2, dt, False))
+    x = O.round_act(rng.standard_normal((T, H)).astype(np.float32) * 0.5, dt)
+    lg = rng.standard_normal((T, E)).astype(np.float32)
+    y = fused_moe_w4a16(_to_dev_act(x, dt), torch.from_numpy(lg).cuda(), w, k, "sigmoid", True, num_expert_group=4,
+                        topk_group=2, routed_scaling_factor=2.5, num_shared_experts=1)
+    torch.cuda.synchronize()
+    rid, rw = O.grouped_topk(lg, k, 4, 2, "sigmoid", True, None, 2.5)
+    ids = np.concatenate([rid, np.full((T, 1), E, np.int32)], axis=1)
+    wts = np.concatenate([rw, np.ones((T, 1), np.float32)], axis=1)
+    want = O.moe_forward(x, O.dequant(q13, z13, s13, dt), O.dequant(q2, z2, s2, dt), ids, wts, dt)
+    tol = (2 if dt == "bf16" else 1) * ATOL
+    np.testing.assert_allclose(_from_dev_act(y, dt), want, rtol=RTOL, atol=tol)
+    if dt == "f16":  # graph replay of the same layer (softmax routing here)
+        g = FusedMoEGraph(w, T, k, "softmax", True, torch.float16, num_shared_experts=1)
+        y2 = g(_to_dev_act(x, dt), torch.from_numpy(lg).cuda())
+        torch.cuda.synchronize()
+        rid, rw = O.route_topk(lg, k, "softmax", True)
+        ids = np.concatenate([rid, np.full((T, 1), E, np.int32)], axis=1)
+        wts = np.concatenate([rw, np.ones((T, 1), np.float32)], axis=1)
+        want2 = O.moe_forward(x, O.dequant(q13, z13, s13, dt), O.dequant(q2, z2, s2, dt), ids, wts, dt)
+        np.testing.assert_allclose(_from_dev_act(y2, dt), want2, rtol=RTOL, atol=tol)
+
+
 @pytest.mark.parametrize("ntok,dt", [(16, "f16"), (16, "bf16"), (32, "f16"), (64, "bf16"), (128, "f16")])
 def test_grouped_gemm_fused_gather(ntok, dt):
     """The gate/up GEMM gathering x's rows itself (TMA gather4 in the producer) == gather kernel +
