@@ -10,6 +10,7 @@
  *
  *   route:    w4a16_route_topk                         top-k of softmax/sigmoid router scores
  *             w4a16_route_grouped_topk                 DeepSeek-V3/R1 grouped top-k (vLLM grouped_topk)
+ *             w4a16_route_permute                      route_topk + moe_permute in one CTA (small batches)
  *   permute:  w4a16_moe_permute                        stable counting sort of (token, slot) by expert
  *   gather:   w4a16_moe_gather                         X_perm[p] = x[token(p)]   (128-bit vectors)
  *             w4a16_moe_gather_sums                    same, plus per-group activation sums (decode)
@@ -74,6 +75,12 @@ int w4a16_dequant(const uint8_t* wblocks, int64_t num_experts, int64_t n_rows, i
  * topk_weights [T][k] fp32 (softmax or sigmoid of the selected logits, optionally renormalised). */
 int w4a16_route_topk(const float* logits, int64_t T, int64_t E, int64_t k, int scoring, int renormalize,
                      int32_t* topk_ids, float* topk_weights, cudaStream_t stream);
+
+/* w4a16_route_topk + w4a16_moe_permute of its ids in one single-CTA kernel (small batches: one launch
+ * and one kernel boundary fewer before the GEMMs). Same outputs as the two calls. T * k <= 2^20. */
+int w4a16_route_permute(const float* logits, int64_t T, int64_t E, int64_t k, int scoring, int renormalize,
+                        int32_t* topk_ids, float* topk_weights, int32_t* expert_counts, int32_t* expert_offsets,
+                        int32_t* sorted_pairs, int32_t* pair_pos, cudaStream_t stream);
 
 /* DeepSeek-V3/R1 routing, vLLM grouped_topk semantics (vllm/model_executor/layers/fused_moe/router/
  * grouped_topk_router.py:81-162): scores = softmax|sigmoid(logits); choice = scores + bias (bias [E]

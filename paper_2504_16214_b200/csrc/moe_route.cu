@@ -16,13 +16,12 @@ namespace w4 {
 // ---------------------------------------------------------------------------------------- top-k
 // One warp per token; lane l holds logits l, l+32, ... (kPer per lane = power of two >= E/32, padded
 // with -inf). Selection compares raw logits (softmax / sigmoid are monotone), ties -> lower expert id.
+// Routes token `tok` (one warp): ids / wts rows of length k.
 template <int kPer>
-__global__ void route_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int scoring, int renorm,
-                                  int32_t* __restrict__ ids, float* __restrict__ wts) {
-  griddep_wait();  // PDL: inputs written by the previous kernel in the stream
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= T) return;
+__device__ __forceinline__ void route_token(const float* __restrict__ logits, int tok, int E, int k, int scoring,
+                                            int renorm, int32_t* __restrict__ ids, float* __restrict__ wts,
+                                            int lane) {
+  const int warp = tok;
   const float* row = logits + static_cast<int64_t>(warp) * E;
   float v[kPer];
   float mx = -INFINITY;
@@ -67,6 +66,15 @@ __global__ void route_topk_kernel(const float* __restrict__ logits, int T, int E
     ids[static_cast<int64_t>(warp) * k + lane] = my_id;
     wts[static_cast<int64_t>(warp) * k + lane] = renorm ? my_w / sel_sum : my_w;
   }
+}
+
+template <int kPer>
+__global__ void route_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int scoring, int renorm,
+                                  int32_t* __restrict__ ids, float* __restrict__ wts) {
+  griddep_wait();  // PDL: inputs written by the previous kernel in the stream
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (warp >= T) return;
+  route_token<kPer>(logits, warp, E, k, scoring, renorm, ids, wts, threadIdx.x & 31);
 }
 
 // ------------------------------------------------------------------------------- grouped top-k
@@ -193,11 +201,9 @@ __global__ void route_grouped_topk_kernel(const float* __restrict__ logits, int 
 constexpr int kPermThreads = 1024;
 constexpr int kPermWarps = kPermThreads / 32;
 
-__global__ void __launch_bounds__(kPermThreads, 1)
-    moe_permute_kernel(const int32_t* __restrict__ ids, int P, int E, int32_t* __restrict__ counts,
-                       int32_t* __restrict__ offsets, int32_t* __restrict__ sorted_pairs,
-                       int32_t* __restrict__ pair_pos) {
-  griddep_wait();  // PDL: inputs written by the previous kernel in the stream
+__device__ __forceinline__ void permute_block(const int32_t* __restrict__ ids, int P, int E,
+                                              int32_t* __restrict__ counts, int32_t* __restrict__ offsets,
+                                              int32_t* __restrict__ sorted_pairs, int32_t* __restrict__ pair_pos) {
   extern __shared__ int sm[];
   int* cnt = sm;                     // [E]
   int* base = cnt + E;               // [E]
@@ -261,6 +267,30 @@ __global__ void __launch_bounds__(kPermThreads, 1)
     }
     __syncthreads();
   }
+}
+
+__global__ void __launch_bounds__(kPermThreads, 1)
+    moe_permute_kernel(const int32_t* __restrict__ ids, int P, int E, int32_t* __restrict__ counts,
+                       int32_t* __restrict__ offsets, int32_t* __restrict__ sorted_pairs,
+                       int32_t* __restrict__ pair_pos) {
+  griddep_wait();  // PDL: inputs written by the previous kernel in the stream
+  permute_block(ids, P, E, counts, offsets, sorted_pairs, pair_pos);
+}
+
+// Routing and the permutation in one CTA (small batches): the 32 warps route the tokens, then the
+// block permutes the ids it just wrote (block-scope visibility after __syncthreads). One launch and
+// one kernel boundary fewer on the decode critical path.
+template <int kPer>
+__global__ void __launch_bounds__(kPermThreads, 1)
+    route_permute_kernel(const float* __restrict__ logits, int T, int E, int k, int scoring, int renorm,
+                         int32_t* __restrict__ ids, float* __restrict__ wts, int32_t* __restrict__ counts,
+                         int32_t* __restrict__ offsets, int32_t* __restrict__ sorted_pairs,
+                         int32_t* __restrict__ pair_pos) {
+  griddep_wait();  // PDL: inputs written by the previous kernel in the stream
+  const int warp = threadIdx.x >> 5;
+  for (int t = warp; t < T; t += kPermWarps) route_token<kPer>(logits, t, E, k, scoring, renorm, ids, wts, threadIdx.x & 31);
+  __syncthreads();
+  permute_block(ids, T * k, E, counts, offsets, sorted_pairs, pair_pos);
 }
 
 // ---------------------------------------------------------------------------------------- permute (multi-CTA)
@@ -633,6 +663,38 @@ int w4a16_route_topk(const float* logits, int64_t T, int64_t E, int64_t k, int s
   else if (per <= 16) W4_ROUTE(16);
   else W4_ROUTE(32);
 #undef W4_ROUTE
+  return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
+}
+
+int w4a16_route_permute(const float* logits, int64_t T, int64_t E, int64_t k, int scoring, int renormalize,
+                        int32_t* topk_ids, float* topk_weights, int32_t* expert_counts, int32_t* expert_offsets,
+                        int32_t* sorted_pairs, int32_t* pair_pos, cudaStream_t stream) {
+  if (!logits || !topk_ids || !topk_weights || !expert_counts || !expert_offsets || !sorted_pairs || !pair_pos)
+    return W4_ERR_ARG;
+  if (E <= 0 || E > 1024 || k <= 0 || k > 32 || k > E) return W4_ERR_SHAPE;
+  if (T < 0 || T * k > (int64_t(1) << 20)) return W4_ERR_SHAPE;
+  if (scoring != W4_SCORE_SOFTMAX && scoring != W4_SCORE_SIGMOID) return W4_ERR_ARG;
+  const size_t smem = sizeof(int) * (2 * E + kPermWarps * E);
+  const int per = static_cast<int>((E + 31) / 32);
+#define W4_RPERM(P)                                                                                         \
+  do {                                                                                                      \
+    static bool attr = false;                                                                               \
+    if (!attr) {                                                                                            \
+      if (cudaFuncSetAttribute(route_permute_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                               sizeof(int) * (2 * 1024 + kPermWarps * 1024)) != cudaSuccess)                \
+        return W4_ERR_CUDA;                                                                                 \
+      attr = true;                                                                                          \
+    }                                                                                                       \
+    launch_pdl(route_permute_kernel<P>, 1, kPermThreads, smem, stream, logits, (int)T, (int)E, (int)k, scoring, \
+               renormalize, topk_ids, topk_weights, expert_counts, expert_offsets, sorted_pairs, pair_pos);  \
+  } while (0)
+  if (per <= 1) W4_RPERM(1);
+  else if (per <= 2) W4_RPERM(2);
+  else if (per <= 4) W4_RPERM(4);
+  else if (per <= 8) W4_RPERM(8);
+  else if (per <= 16) W4_RPERM(16);
+  else W4_RPERM(32);
+#undef W4_RPERM
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
 

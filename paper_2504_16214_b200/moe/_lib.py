@@ -40,6 +40,7 @@ SIGNATURES = {
     "w4a16_dequant": (_i, [_p, _i64, _i64, _i64, _i, _i, _p, _p]),
     "w4a16_route_topk": (_i, [_p, _i64, _i64, _i64, _i, _i, _p, _p, _p]),
     "w4a16_route_grouped_topk": (_i, [_p, _i64, _i64, _i64, _i64, _i64, _i, _i, _p, C.c_float, _p, _p, _p]),
+    "w4a16_route_permute": (_i, [_p, _i64, _i64, _i64, _i, _i, _p, _p, _p, _p, _p, _p, _p]),
     "w4a16_moe_permute": (_i, [_p, _i64, _i64, _p, _p, _p, _p, _p]),
     "w4a16_moe_permute_ws": (_i, [_p, _i64, _i64, _p, _p, _p, _p, _p, _i64, _p]),
     "w4a16_moe_permute_ws_bytes": (_i64, [_i64, _i64]),

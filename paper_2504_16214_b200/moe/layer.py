@@ -60,6 +60,10 @@ class _Workspace:
 
 
 _ws = _Workspace()
+# fused route + permute (one CTA) up to this many (token, slot) pairs; 0 disables. Measured: ~1 us faster
+# for DS-R1 T=1 (8 pairs), a wash at T=16 and slower from T=64 on (one CTA routes every token, where
+# the separate routing kernel spreads tokens over SMs), so only the smallest batches use it.
+_ROUTE_PERMUTE_MAX_PAIRS = int(os.environ.get("W4A16_ROUTE_PERMUTE_MAX_PAIRS", "64"))
 # experiment (W4A16_FUSED_GATHER=1): the gate/up GEMM gathers x's rows itself (TMA gather4 in its
 # producer) instead of a gather kernel. Correct (bit-identical) but measured 1.5x slower at T=64 and 2.8x
 # slower gate/up at T=8192: 64 four-row gather4 requests per 49 KB stage throttle the TMA unit.
@@ -119,7 +123,7 @@ _NOTIMER = _NoTimer()
 
 
 def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, topk_ids: torch.Tensor,
-              ep_group=None, ntok: int = 0, timer: KernelTimer | None = None) -> torch.Tensor:
+              ep_group=None, ntok: int = 0, timer: KernelTimer | None = None, perm=None) -> torch.Tensor:
     """y[t] = sum_j topk_weights[t, j] * Expert_{topk_ids[t, j]}(x[t]) for the W4A16 SwiGLU experts.
 
     ``x`` [T, H] fp16/bf16 on CUDA; ``topk_ids`` int32 [T, k]; ``topk_weights`` fp32 [T, k]."""
@@ -139,9 +143,12 @@ def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, 
     E, I = weights.num_experts, weights.inter
     P = T * k
     dev = x.device
-    with tm.span("permute"):
-        counts, offsets, sorted_pairs, pair_pos = ops.moe_permute(
-            topk_ids, E, _ws.get("perm_ws", (max(ops.permute_ws_bytes(P, E), 1),), torch.uint8, dev))
+    if perm is not None:  # (counts, offsets, sorted_pairs, pair_pos) already computed with the routing
+        counts, offsets, sorted_pairs, pair_pos = perm
+    else:
+        with tm.span("permute"):
+            counts, offsets, sorted_pairs, pair_pos = ops.moe_permute(
+                topk_ids, E, _ws.get("perm_ws", (max(ops.permute_ws_bytes(P, E), 1),), torch.uint8, dev))
     nt = ntok or ops.pick_ntok(P, E)
     decode = nt <= _DECODE_MAX_NTOK  # offset-code GEMMs: per-group activation sums ride along with X and h
     if _FUSED_GATHER:  # the gate/up producer gathers x's rows itself (TMA gather4); decode sums over x
@@ -209,6 +216,14 @@ def fused_moe_w4a16(x: torch.Tensor, router_logits: torch.Tensor, weights: MoEWe
                     routed_scaling_factor: float = 1.0, num_shared_experts: int = 0) -> torch.Tensor:
     """``num_shared_experts`` > 0: the last experts of ``weights`` are shared experts (always active,
     weight 1; the router logits cover only the routed ones)."""
+    T = router_logits.shape[0]
+    if (ep_group is None and not num_expert_group and not num_shared_experts and routed_scaling_factor == 1.0
+            and T * top_k <= _ROUTE_PERMUTE_MAX_PAIRS):
+        # small batch: routing and the permutation in one single-CTA kernel
+        with (timer or _NOTIMER).span("route_permute"):
+            ids, wts, counts, offsets, sp, pp = ops.route_permute(router_logits.float().contiguous(), top_k, scoring,
+                                                                  renormalize)
+        return moe_w4a16(x, weights, wts, ids, timer=timer, perm=(counts, offsets, sp, pp))
     with (timer or _NOTIMER).span("route"):
         topk_weights, topk_ids = select_experts(router_logits, top_k, scoring, renormalize, num_expert_group,
                                                 topk_group, e_score_correction_bias, routed_scaling_factor)

@@ -77,6 +77,26 @@ def route_topk(logits: torch.Tensor, k: int, scoring: str = "softmax", renormali
     return ids, wts
 
 
+def route_permute(logits: torch.Tensor, k: int, scoring: str = "softmax", renormalize: bool = False):
+    """route_topk + moe_permute of its ids in one single-CTA kernel (small batches).
+    -> (ids, weights, expert_counts, expert_offsets, sorted_pairs, pair_pos)."""
+    _need_cuda(logits)
+    if logits.dtype != torch.float32:
+        raise _lib.W4A16Error("router logits must be float32")
+    T, E = logits.shape
+    dev = logits.device
+    ids = torch.empty((T, k), dtype=torch.int32, device=dev)
+    wts = torch.empty((T, k), dtype=torch.float32, device=dev)
+    counts = torch.empty(E, dtype=torch.int32, device=dev)
+    offsets = torch.empty(E + 1, dtype=torch.int32, device=dev)
+    sp = torch.empty(T * k, dtype=torch.int32, device=dev)
+    pp = torch.empty(T * k, dtype=torch.int32, device=dev)
+    sc = {"softmax": _lib.SCORE_SOFTMAX, "sigmoid": _lib.SCORE_SIGMOID}[scoring]
+    _lib.call("w4a16_route_permute", logits.data_ptr(), T, E, k, sc, int(renormalize), ids.data_ptr(), wts.data_ptr(),
+              counts.data_ptr(), offsets.data_ptr(), sp.data_ptr(), pp.data_ptr(), _stream())
+    return ids, wts, counts, offsets, sp, pp
+
+
 def route_grouped_topk(logits: torch.Tensor, k: int, num_groups: int, topk_group: int, scoring: str = "sigmoid",
                        renormalize: bool = True, bias: torch.Tensor | None = None,
                        routed_scaling_factor: float = 1.0):

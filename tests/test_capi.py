@@ -18,7 +18,7 @@ def _declared():
 
 def test_header_declares_the_path():
     d = _declared()
-    for fn in ("w4a16_grouped_gemm", "w4a16_route_topk", "w4a16_route_grouped_topk", "w4a16_moe_permute", "w4a16_moe_gather",
+    for fn in ("w4a16_grouped_gemm", "w4a16_route_topk", "w4a16_route_grouped_topk", "w4a16_route_permute", "w4a16_moe_permute", "w4a16_moe_gather",
                "w4a16_moe_combine", "w4a16_repack_awq", "w4a16_dequant", "w4a16_moe_forward"):
         assert fn in d
 

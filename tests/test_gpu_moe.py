@@ -113,6 +113,21 @@ def test_fused_moe_grouped_routing_layer():
     np.testing.assert_allclose(_from_dev_act(y, dt), want, rtol=RTOL, atol=ATOL)
 
 
+@pytest.mark.parametrize("T,E,k,scoring", [(1, 256, 8, "softmax"), (64, 256, 8, "softmax"), (37, 128, 8, "sigmoid"),
+                                           (200, 8, 2, "softmax"), (512, 256, 8, "softmax"), (3, 1024, 4, "sigmoid")])
+def test_route_permute_fused(T, E, k, scoring):
+    """Routing + permutation in one CTA == route_topk then moe_permute, bit for bit."""
+    ops = _ops()
+    rng = np.random.default_rng(T * 3 + E)
+    lg = torch.from_numpy(rng.standard_normal((T, E)).astype(np.float32)).cuda()
+    ids, w, c, o, sp, pp = ops.route_permute(lg, k, scoring, True)
+    ids2, w2 = ops.route_topk(lg, k, scoring, True)
+    c2, o2, sp2, pp2 = ops.moe_permute(ids2, E)
+    torch.cuda.synchronize()
+    assert torch.equal(ids, ids2) and torch.equal(w, w2)
+    assert torch.equal(c, c2) and torch.equal(o, o2) and torch.equal(sp, sp2) and torch.equal(pp, pp2)
+
+
 # ------------------------------------------------------------------------------------------- permute
 @pytest.mark.parametrize("P,E", [(1, 4), (64 * 8, 256), (3000, 256), (5000, 7), (65536, 256), (2048, 1024),
                                  (20000, 1024), (9001, 3), (131072, 128)])
