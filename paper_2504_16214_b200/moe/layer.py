@@ -167,8 +167,9 @@ def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, 
             else:
                 xp, xs = ops.moe_gather(x, sorted_pairs, k, P, offsets[E:], out=xp_buf), None
     def splitk_ws(K: int, n_out: int, gated: bool):
+        # one buffer per GEMM: a captured graph keeps _ws's buffers alive, so neither may be reallocated
         b = ops.gemm_ws_bytes(P, K, E, n_out, gated, nt) if decode else 0
-        return _ws.get("splitk", (b,), torch.uint8, dev) if b else None
+        return _ws.get("splitk_gu" if gated else "splitk_dn", (b,), torch.uint8, dev) if b else None
 
     hs = _ws.get("hs", ops.sums_shape(P, I), torch.float32, dev) if decode else None
     gu_ws = splitk_ws(H, I, True)
