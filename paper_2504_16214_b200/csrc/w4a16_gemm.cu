@@ -1238,6 +1238,7 @@ int dispatch_ntok(int ntok, bool offset, bool pair, const GemmArgs& a, const voi
 
 template <int kMode, bool kBF16>
 int dispatch_prefill(int ntok, const GemmArgs& a, const void* x, int64_t rows, int64_t K, int grid, cudaStream_t st) {
+  if (ntok == 32) return launch_gemm<32, kMode, kBF16, false, false>(a, x, rows, K, grid, st);
   if (ntok == 64) return launch_gemm<64, kMode, kBF16, false, false>(a, x, rows, K, grid, st);
   if (ntok == 128) return launch_gemm<128, kMode, kBF16, false, false>(a, x, rows, K, grid, st);
   return W4_ERR_ARG;
@@ -1316,7 +1317,7 @@ GemmPlan plan_gemm(int64_t rows, int64_t K, int64_t num_experts, int64_t n_out, 
   // (64 KB for a k-pair -> only 2 smem stages), so 128-token tiles use one group per stage
   pl.mode = gated ? kModeGateUp : ((kt % 2 == 0 && pl.ntok <= 64) ? kModeKPair : kModePlain);
   // prefill down projection: two n-tiles per stage share the X tile (halves the X smem traffic)
-  if (!gated && !pl.offset && pl.ntok >= npair_min_ntok() && nt % 2 == 0) pl.mode = kModeNPair;
+  if (!gated && !pl.offset && pl.ntok >= 32 && pl.ntok >= npair_min_ntok() && nt % 2 == 0) pl.mode = kModeNPair;
   // decode down projection: n-pair stages too (one k-group of two n-tiles on one X tile): tiles of
   // K/128 stages instead of K/256 k-pair stages, half the X bytes per stage
   if (!gated && pl.offset && pl.ntok == 16 && nt % 2 == 0 && decode_npair_enabled()) pl.mode = kModeNPair;
