@@ -7,6 +7,7 @@
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
 #include <cstdint>
+#include <cstdlib>
 #include "ptx.cuh"
 #include "launch.cuh"
 #include "w4a16_moe.h"
@@ -749,7 +750,13 @@ int64_t w4a16_moe_permute_ws_bytes(int64_t P, int64_t E) {
 int w4a16_moe_permute_ws(const int32_t* topk_ids, int64_t P, int64_t E, int32_t* expert_counts,
                          int32_t* expert_offsets, int32_t* sorted_pairs, int32_t* pair_pos, void* ws,
                          int64_t ws_bytes, cudaStream_t stream) {
-  if (!ws || ws_bytes < w4a16_moe_permute_ws_bytes(P, E) || P <= 2 * kChunk)
+  // largest P for the one-CTA kernel (W4A16_PERMUTE_SINGLE_MAX overrides). Measured in a graph
+  // (tools/perm_probe.py): one CTA 8.3 us vs 9.9 at P = 2048, 14.0 vs 10.1 at P = 4096.
+  static const int64_t single_max = [] {
+    const char* e = getenv("W4A16_PERMUTE_SINGLE_MAX");
+    return e ? static_cast<int64_t>(atoll(e)) : static_cast<int64_t>(kChunk);
+  }();
+  if (!ws || ws_bytes < w4a16_moe_permute_ws_bytes(P, E) || P <= single_max)
     return w4a16_moe_permute(topk_ids, P, E, expert_counts, expert_offsets, sorted_pairs, pair_pos, stream);
   if (!topk_ids || !expert_counts || !expert_offsets || !sorted_pairs || !pair_pos) return W4_ERR_ARG;
   if (E <= 0 || E > 1024 || P > (int64_t(1) << 30)) return W4_ERR_SHAPE;
