@@ -647,10 +647,10 @@ extern "C" {
 
 int w4a16_route_topk(const float* logits, int64_t T, int64_t E, int64_t k, int scoring, int renormalize,
                      int32_t* topk_ids, float* topk_weights, cudaStream_t stream) {
-  if (!logits || !topk_ids || !topk_weights) return W4_ERR_ARG;
   if (E <= 0 || E > 1024 || k <= 0 || k > 32 || k > E) return W4_ERR_SHAPE;
   if (scoring != W4_SCORE_SOFTMAX && scoring != W4_SCORE_SIGMOID) return W4_ERR_ARG;
-  if (T <= 0) return W4_OK;
+  if (T <= 0) return W4_OK;  // empty batch: nothing to read or write (pointers may be null)
+  if (!logits || !topk_ids || !topk_weights) return W4_ERR_ARG;
   const int thr = 128;
   const int64_t blocks = (T * 32 + thr - 1) / thr;
   const int per = static_cast<int>((E + 31) / 32);
@@ -670,7 +670,8 @@ int w4a16_route_topk(const float* logits, int64_t T, int64_t E, int64_t k, int s
 int w4a16_route_permute(const float* logits, int64_t T, int64_t E, int64_t k, int scoring, int renormalize,
                         int32_t* topk_ids, float* topk_weights, int32_t* expert_counts, int32_t* expert_offsets,
                         int32_t* sorted_pairs, int32_t* pair_pos, cudaStream_t stream) {
-  if (!logits || !topk_ids || !topk_weights || !expert_counts || !expert_offsets || !sorted_pairs || !pair_pos)
+  if (!expert_counts || !expert_offsets ||
+      (T > 0 && (!logits || !topk_ids || !topk_weights || !sorted_pairs || !pair_pos)))
     return W4_ERR_ARG;
   if (E <= 0 || E > 1024 || k <= 0 || k > 32 || k > E) return W4_ERR_SHAPE;
   if (T < 0 || T * k > (int64_t(1) << 20)) return W4_ERR_SHAPE;
@@ -702,7 +703,7 @@ int w4a16_route_permute(const float* logits, int64_t T, int64_t E, int64_t k, in
 int w4a16_route_grouped_topk(const float* logits, int64_t T, int64_t E, int64_t k, int64_t num_groups,
                              int64_t topk_group, int scoring, int renormalize, const float* bias,
                              float routed_scaling_factor, int32_t* topk_ids, float* topk_weights, cudaStream_t stream) {
-  if (!logits || !topk_ids || !topk_weights) return W4_ERR_ARG;
+  if (T > 0 && (!logits || !topk_ids || !topk_weights)) return W4_ERR_ARG;
   if (E <= 0 || E > 1024 || k <= 0 || k > 32 || k > E) return W4_ERR_SHAPE;
   if (num_groups <= 0 || num_groups > 32 || E % num_groups || topk_group <= 0 || topk_group > num_groups)
     return W4_ERR_SHAPE;
@@ -728,7 +729,8 @@ int w4a16_route_grouped_topk(const float* logits, int64_t T, int64_t E, int64_t 
 
 int w4a16_moe_permute(const int32_t* topk_ids, int64_t P, int64_t E, int32_t* expert_counts,
                       int32_t* expert_offsets, int32_t* sorted_pairs, int32_t* pair_pos, cudaStream_t stream) {
-  if (!topk_ids || !expert_counts || !expert_offsets || !sorted_pairs || !pair_pos) return W4_ERR_ARG;
+  // P == 0: no pair is read or written (those pointers may be null); counts / offsets are still zeroed
+  if (!expert_counts || !expert_offsets || (P > 0 && (!topk_ids || !sorted_pairs || !pair_pos))) return W4_ERR_ARG;
   if (E <= 0 || E > 1024 || P < 0 || P > (int64_t(1) << 30)) return W4_ERR_SHAPE;
   const size_t smem = sizeof(int) * (2 * E + kPermWarps * E);
   static bool attr = false;

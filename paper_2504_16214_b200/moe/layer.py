@@ -132,6 +132,8 @@ def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, 
         return moe_w4a16_ep(x, weights, topk_weights, topk_ids, ep_group, ntok=ntok, timer=timer)
     tm = timer or _NOTIMER
     T, H = x.shape
+    if T == 0:  # empty batch (single GPU): nothing to launch
+        return x.new_empty((0, H))
     if H != weights.hidden:
         raise ValueError(f"hidden size {H} != packed weights' {weights.hidden}")
     if x.dtype != weights.w13.dtype:
@@ -218,6 +220,8 @@ def fused_moe_w4a16(x: torch.Tensor, router_logits: torch.Tensor, weights: MoEWe
     """``num_shared_experts`` > 0: the last experts of ``weights`` are shared experts (always active,
     weight 1; the router logits cover only the routed ones)."""
     T = router_logits.shape[0]
+    if T == 0 and ep_group is None:  # (EP ranks with no tokens still join the exchanges)
+        return x.new_empty((0, x.shape[1]))
     if (ep_group is None and not num_expert_group and not num_shared_experts and routed_scaling_factor == 1.0
             and T * top_k <= _ROUTE_PERMUTE_MAX_PAIRS):
         # small batch: routing and the permutation in one single-CTA kernel

@@ -314,6 +314,28 @@ def test_dense_w4a16_linear_llama_shape(M):
 
 
 # ------------------------------------------------------------------------------------------- layer
+@pytest.mark.parametrize("T,E,k", [(0, 8, 2), (7, 1, 1), (33, 4, 4), (5, 1024, 8)])
+def test_moe_layer_edge_shapes(T, E, k):
+    """Edge shapes: an empty batch, a single expert with top-1, every token on every expert (k = E),
+    and the largest expert count (1024, most experts empty)."""
+    from paper_2504_16214_b200.moe import fused_moe_w4a16
+    from paper_2504_16214_b200.moe.weights import MoEWeights
+    rng = np.random.default_rng(E + k)
+    H, I, dt = 128, 128, "f16"
+    q13, z13, s13 = O.synth_awq_expert_weights(rng, E, 2 * I, H, dt)
+    q2, z2, s2 = O.synth_awq_expert_weights(rng, E, H, I, dt)
+    w = MoEWeights(_packed(q13, z13, s13, dt, True), _packed(q2, z2, s2, dt, False))
+    x = O.round_act(rng.standard_normal((T, H)).astype(np.float32) * 0.5, dt)
+    lg = rng.standard_normal((T, E)).astype(np.float32)
+    y = fused_moe_w4a16(_to_dev_act(x, dt), torch.from_numpy(lg).cuda(), w, k, "softmax", True)
+    torch.cuda.synchronize()
+    assert tuple(y.shape) == (T, H)
+    if T:
+        ids, wts = O.route_topk(lg, k, "softmax", True)
+        want = O.moe_forward(x, O.dequant(q13, z13, s13, dt), O.dequant(q2, z2, s2, dt), ids, wts, dt)
+        np.testing.assert_allclose(_from_dev_act(y, dt), want, rtol=RTOL, atol=ATOL)
+
+
 @pytest.mark.parametrize("dt", ["f16", "bf16"])
 @pytest.mark.parametrize("T,E,k,H,I", [(1, 8, 2, 256, 384), (24, 16, 4, 512, 256), (130, 8, 2, 256, 256),
                                        (64, 32, 8, 256, 128)])
@@ -549,3 +571,19 @@ def test_ep_nccl_world1_layer():
             np.testing.assert_allclose(_from_dev_act(y, dt), want, rtol=RTOL, atol=(2 if dt == "bf16" else 1) * ATOL)
     finally:
         dist.destroy_process_group()
+
+
+def test_empty_inputs_c_abi():
+    """Empty batches through the routing / permutation entry points: OK without touching the (null)
+    pair pointers; the permutation still zeroes the expert counts and offsets."""
+    ops = _ops()
+    E = 16
+    lg = torch.empty((0, E), dtype=torch.float32, device="cuda")
+    ids, w = ops.route_topk(lg, 4)
+    assert ids.shape == (0, 4)
+    c, o, sp, pp = ops.moe_permute(torch.empty((0, 4), dtype=torch.int32, device="cuda"), E)
+    torch.cuda.synchronize()
+    assert int(c.sum()) == 0 and int(o.abs().sum()) == 0
+    ids, w, c, o, sp, pp = ops.route_permute(lg, 4)
+    torch.cuda.synchronize()
+    assert int(c.sum()) == 0 and int(o.abs().sum()) == 0
