@@ -233,10 +233,16 @@ def fused_moe_w4a16(x: torch.Tensor, router_logits: torch.Tensor, weights: MoEWe
         topk_weights, topk_ids = select_experts(router_logits, top_k, scoring, renormalize, num_expert_group,
                                                 topk_group, e_score_correction_bias, routed_scaling_factor)
     if num_shared_experts:
+        first = weights.num_experts - num_shared_experts
         if ep_group is not None:
-            raise NotImplementedError("shared experts with expert parallelism (run them data-parallel)")
-        topk_weights, topk_ids = with_shared_experts(topk_weights, topk_ids, weights.num_experts - num_shared_experts,
-                                                     num_shared_experts)
+            # expert parallel: the routed shard goes through the exchange, the (replicated) shared
+            # experts run data-parallel on this rank's own tokens
+            y = moe_w4a16(x, weights.slice_experts(0, first), topk_weights, topk_ids, ep_group=ep_group, timer=timer)
+            T = x.shape[0]
+            sw, sid = with_shared_experts(topk_weights[:, :0], topk_ids[:, :0], 0, num_shared_experts)
+            return y.add_(moe_w4a16(x, weights.slice_experts(first, weights.num_experts), sw, sid, timer=timer)) \
+                if T else y
+        topk_weights, topk_ids = with_shared_experts(topk_weights, topk_ids, first, num_shared_experts)
     return moe_w4a16(x, weights, topk_weights, topk_ids, ep_group=ep_group, timer=timer)
 
 

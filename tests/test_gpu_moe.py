@@ -569,6 +569,22 @@ def test_ep_nccl_world1_layer():
             rid, rw = O.route_topk(lg, k, "softmax", True)
             want = O.moe_forward(x, O.dequant(q13, z13, s13, dt), O.dequant(q2, z2, s2, dt), rid, rw, dt)
             np.testing.assert_allclose(_from_dev_act(y, dt), want, rtol=RTOL, atol=(2 if dt == "bf16" else 1) * ATOL)
+        # a shared expert (packed last): routed experts through the exchange, the shared one locally
+        T, E, k, H, I, dt = 24, 8, 2, 256, 256, "f16"
+        q13, z13, s13 = O.synth_awq_expert_weights(rng, E + 1, 2 * I, H, dt)
+        q2, z2, s2 = O.synth_awq_expert_weights(rng, E + 1, H, I, dt)
+        w = MoEWeights(_packed(q13, z13, s13, dt, True), _packed(q2, z2, s2, dt, False))
+        x = O.round_act(rng.standard_normal((T, H)).astype(np.float32) * 0.5, dt)
+        lg = rng.standard_normal((T, E)).astype(np.float32)
+        y = fused_moe_w4a16(_to_dev_act(x, dt), torch.from_numpy(lg).cuda(), w, k, "softmax", True,
+                            ep_group=dist.group.WORLD, num_shared_experts=1)
+        torch.cuda.synchronize()
+        rid, rw = O.route_topk(lg, k, "softmax", True)
+        ids = np.concatenate([rid, np.full((T, 1), E, np.int32)], axis=1)
+        wts = np.concatenate([rw, np.ones((T, 1), np.float32)], axis=1)
+        want = O.moe_forward(x, O.dequant(q13, z13, s13, dt), O.dequant(q2, z2, s2, dt), ids, wts, dt)
+        # the EP sum adds two rounded partial outputs (routed + shared): one extra rounding
+        np.testing.assert_allclose(_from_dev_act(y, dt), want, rtol=RTOL, atol=2 * ATOL)
     finally:
         dist.destroy_process_group()
 
