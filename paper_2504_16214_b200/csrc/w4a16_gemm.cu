@@ -959,6 +959,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             store16_staged(cb * 16, ro, hb, 0, 0);
             if (tre) trace_at(tr, 14, it * 32 + cb * 2 + 1);
           } else if constexpr (C::kNPer == 2) {  // second accumulator = the next n-tile's columns
+            if (tre) trace_at(tr, 14, it * 32 + cb * 2);
             uint16_t hu[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
@@ -967,6 +968,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             }
             store16_staged(cb * 16, ro, hb, 0, 0);
             store16_staged(cb * 16, ro, hu, kTileRows, 1);
+            if (tre) trace_at(tr, 14, it * 32 + cb * 2 + 1);
           } else {
 #pragma unroll
             for (int i = 0; i < 16; ++i) hb[i] = to_act_bits<kBF16>(__uint_as_float(g[i]));
