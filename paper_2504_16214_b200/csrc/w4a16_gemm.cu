@@ -796,6 +796,30 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
         __syncwarp();  // the staging block is rewritten by the next call
       };
+      // both n-tiles of an n-pair chunk: one round of shared-memory staging (two buffers), so the two
+      // outputs' store latencies overlap instead of adding up
+      auto store16x2_staged = [&](int m0, int64_t ro, const uint16_t (&hb)[16], const uint16_t (&hu)[16]) {
+        const uint32_t sa = smem_u32(my_stage), sb = sa + 1024;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(sa + i * 64 + lane * 2), "h"(hb[i]) : "memory");
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(sb + i * 64 + lane * 2), "h"(hu[i]) : "memory");
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int sgi = static_cast<int>(lane) + 32 * j;
+          const int t = sgi >> 2, q = sgi & 3;
+          const int64_t o = __shfl_sync(0xffffffffu, ro, t);
+          const uint4 v0 = lds128(sa + t * 64 + q * 16);
+          const uint4 v1 = lds128(sb + t * 64 + q * 16);
+          if (m0 + t < ti.m_rows) {
+            *reinterpret_cast<uint4*>(ocol - lane + o + q * 8) = v0;
+            *reinterpret_cast<uint4*>(ocol - lane + o + kTileRows + q * 8) = v1;
+          }
+        }
+        __syncwarp();
+      };
       if constexpr (kOffset) {
         // gate|up, or the two n-tiles of an n-pair tile; else one (k-pair parts summed)
         constexpr int kOuts = (kGated || C::kNPer == 2) ? 2 : 1;
@@ -966,8 +990,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               hb[i] = to_act_bits<kBF16>(__uint_as_float(g[i]));
               hu[i] = to_act_bits<kBF16>(__uint_as_float(u[i]));
             }
-            store16_staged(cb * 16, ro, hb, 0, 0);
-            store16_staged(cb * 16, ro, hu, kTileRows, 1);
+            store16x2_staged(cb * 16, ro, hb, hu);
             if (tre) trace_at(tr, 14, it * 32 + cb * 2 + 1);
           } else {
 #pragma unroll
