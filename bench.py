@@ -331,7 +331,7 @@ def other_configs(dev, hbm_peak: float, tc_peak: float):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--tokens", type=int, default=64, help="tokens per rank (decode batch)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
