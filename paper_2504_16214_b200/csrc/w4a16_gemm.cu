@@ -298,7 +298,9 @@ struct Ring {  // (stage, phase) iterator of an mbarrier ring
   }
 };
 
-template <int kNTok, int kMode, bool kBF16, bool kOffset, bool kPair>
+// kGather: the fused-gather variant (X rows gathered by the producer, w4a16_grouped_gemm_gather); a
+// separate instantiation so the regular kernels carry none of its code
+template <int kNTok, int kMode, bool kBF16, bool kOffset, bool kPair, bool kGather = false>
 __global__ void __launch_bounds__(kNumThreads, 1)
     w4a16_moe_gemm_kernel(const GemmArgs args, const __grid_constant__ CUtensorMap xmap) {
   using C = Cfg<kNTok, kMode, kOffset, kPair>;
@@ -409,7 +411,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
     }
 #endif
-    const bool gather = args.gather_rows != nullptr;  // fused gather: all lanes issue gather4 loads
+    constexpr bool gather = kGather;  // fused gather: all lanes issue gather4 loads
     if (kOffset || gather || lane == 0) {
       const uint64_t pol_w = policy_evict_first();
       // gather: this lane loads 4-row group lane % kG4 of the X tile, k halves lane / kG4 (+ 32 / kG4 ...)
@@ -1208,10 +1210,10 @@ int sm_count() {
   return n;
 }
 
-template <int kNTok, int kMode, bool kBF16, bool kOffset, bool kPair>
+template <int kNTok, int kMode, bool kBF16, bool kOffset, bool kPair, bool kGather = false>
 int launch_gemm(const GemmArgs& a, const void* x, int64_t rows, int64_t K, int grid, cudaStream_t st) {
   using C = Cfg<kNTok, kMode, kOffset, kPair>;
-  auto kern = w4a16_moe_gemm_kernel<kNTok, kMode, kBF16, kOffset, kPair>;
+  auto kern = w4a16_moe_gemm_kernel<kNTok, kMode, kBF16, kOffset, kPair, kGather>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
@@ -1257,6 +1259,20 @@ int dispatch_ntok(int ntok, bool offset, bool pair, const GemmArgs& a, const voi
     case 32: return launch_gemm<32, kMode, kBF16, false, false>(a, x, rows, K, grid, st);
     case 64: return launch_gemm<64, kMode, kBF16, false, false>(a, x, rows, K, grid, st);
     case 128: return launch_gemm<128, kMode, kBF16, false, false>(a, x, rows, K, grid, st);
+    default: return W4_ERR_ARG;
+  }
+}
+
+// fused-gather gate/up kernels (decode 16-token offset mode, or the prefill token tiles)
+template <bool kBF16>
+int dispatch_gather(int ntok, bool offset, const GemmArgs& a, const void* x, int64_t rows, int64_t K, int grid,
+                    cudaStream_t st) {
+  if (offset && ntok == 16) return launch_gemm<16, kModeGateUp, kBF16, true, false, true>(a, x, rows, K, grid, st);
+  switch (ntok) {
+    case 16: return launch_gemm<16, kModeGateUp, kBF16, false, false, true>(a, x, rows, K, grid, st);
+    case 32: return launch_gemm<32, kModeGateUp, kBF16, false, false, true>(a, x, rows, K, grid, st);
+    case 64: return launch_gemm<64, kModeGateUp, kBF16, false, false, true>(a, x, rows, K, grid, st);
+    case 128: return launch_gemm<128, kModeGateUp, kBF16, false, false, true>(a, x, rows, K, grid, st);
     default: return W4_ERR_ARG;
   }
 }
@@ -1441,7 +1457,11 @@ static int grouped_gemm_impl(const void* x, int64_t x_rows, const int32_t* gathe
   const int grid = sm_count();
   const bool bf = dtype == W4_DTYPE_BF16;
   int rc;
-  if (pl.mode == kModeGateUp)
+  if (gather_rows) {  // fused gather: gate/up projection only
+    if (pl.mode != kModeGateUp) return W4_ERR_ARG;
+    rc = bf ? dispatch_gather<true>(pl.ntok, pl.offset, a, x, x_rows, K, grid, stream)
+            : dispatch_gather<false>(pl.ntok, pl.offset, a, x, x_rows, K, grid, stream);
+  } else if (pl.mode == kModeGateUp)
     rc = bf ? dispatch_ntok<kModeGateUp, true>(pl.ntok, pl.offset, pair, a, x, x_rows, K, grid, stream)
             : dispatch_ntok<kModeGateUp, false>(pl.ntok, pl.offset, pair, a, x, x_rows, K, grid, stream);
   else if (pl.mode == kModeKPair)
