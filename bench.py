@@ -468,7 +468,40 @@ def main():
     # = this rank's touched W13 blocks + X_perm read + H write.
     per_rank_touched = int(touched[lo:hi].sum().item()) if world > 1 else e_touched
     k_bytes = per_rank_touched * w_bytes(2 * I_DS, H_DS) + T_job * K_DS // world * (H_DS + I_DS) * 2
-    k_ms = timer.mean_ms("gemm_gate_up")
+    k_ms_step = timer.mean_ms("gemm_gate_up")  # inside eager steps (events around every kernel)
+    k_ms = k_ms_step
+    if group is None:
+        # the same launch on the step's own inputs, replayed back to back from a CUDA graph (CUDA events
+        # on its stream): the kernel's own duration, without the eager pass's per-kernel event gaps
+        from paper_2504_16214_b200.moe import ops as _ops
+        from paper_2504_16214_b200.moe import select_experts as _sel
+        _w, _ids = _sel(lg, K_DS, "softmax", True)
+        _c, _o, _sp, _pp = _ops.moe_permute(_ids, E_DS)
+        _P = T * K_DS
+        _xp, _xs = _ops.moe_gather_sums(x, _sp, K_DS, _P, _o[E_DS:])
+        _h = torch.empty((_P, I_DS), dtype=tdt, device=dev)
+        # the step's launch computes h's group sums in its epilogue at <= 4 rows per expert (layer rule)
+        _hs = torch.empty(_ops.sums_shape(_P, I_DS), dtype=torch.float32, device=dev) if _P <= 4 * E_DS else None
+
+        def _gu():
+            _ops.grouped_gemm(_xp, weights.w13.blocks, E_DS, I_DS, True, _c, _o, 0, out=_h, xsum=_xs, osum=_hs)
+        for _ in range(3):
+            _gu()
+        torch.cuda.synchronize()
+        _g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(_g):
+            for _ in range(10):
+                _gu()
+        _g.replay()
+        torch.cuda.synchronize()
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record()
+        for _ in range(3):
+            _g.replay()
+        b_.record()
+        torch.cuda.synchronize()
+        k_ms = a_.elapsed_time(b_) / 30
+        del _g
     k_gbs = k_bytes / (k_ms * 1e-3) / 1e9 if k_ms > 0 else 0.0
     traffic = None
     prof = ROOT / "profiles" / "traffic.json"
@@ -568,6 +601,10 @@ def main():
                          "achieved": round(k_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
                          "frac": round(k_gbs / hbm_peak, 4), "traffic": traffic,
                          "algorithmic_bytes_per_launch": k_bytes, "ms_per_launch": round(k_ms, 4),
+                         "ms_per_launch_in_eager_step": round(k_ms_step, 4),
+                         "timing": ("CUDA events around 30 back-to-back graph replays of the step's gate/up "
+                                    "launch on its own inputs" if group is None else
+                                    "CUDA events around the launch inside eager EP steps"),
                          "peak_source": peak_src},
             "e2e": e2e,
             "latency_ms_per_step": round(latency_ms, 4),
