@@ -56,7 +56,8 @@ def peaks():
 
 
 class ClockSampler:
-    """SM clock + throttle reasons sampled through NVML every 5 ms during the timed region."""
+    """SM clock + throttle reasons sampled through NVML every 0.5 ms during the timed region (a
+    50-step decode region lasts ~50 ms)."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
@@ -90,7 +91,7 @@ class ClockSampler:
                 self.samples.append((mhz, rs))
             except Exception as e:
                 self.err = repr(e)
-            self._stop.wait(0.005)
+            self._stop.wait(0.0005)
 
     def __exit__(self, *exc):
         self._stop.set()
@@ -107,52 +108,97 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------------------------- CPU
-def cpu_oracle_sample(T: int, dtype: str = "f16", budget_s: float = 12.0, seed: int = 0):
-    """Time the numpy oracle (oracle/moe_oracle.py) on a bounded sample of the DS-R1 layer: the
-    first routed experts of a T-token batch, processed one expert at a time until ``budget_s`` of
-    CPU work; returns the algorithmic bytes/s of the processed experts."""
+def bench_inputs(T: int, rank: int, tdt):
+    """The step's synthetic inputs (host, CPU generator seeded by rank): x ~ N(0,1)*0.5, logits ~ N(0,1)."""
+    import torch
+    g = torch.Generator(device="cpu")
+    g.manual_seed(rank)
+    x = (torch.randn((T, H_DS), generator=g) * 0.5).to(tdt)
+    lg = torch.randn((T, E_DS), generator=g)
+    return x, lg
+
+
+def bench_config(T: int, world: int, e_touched: int) -> dict:
+    """One config dict for both arms (the driver compares them key by key)."""
+    return {"workload": f"deepseek_r1_moe_layer_T{T}", "E": E_DS, "topk": K_DS, "hidden": H_DS, "moe_inter": I_DS,
+            "tokens_per_rank": T, "tokens_job": T * world, "group_size": 128, "parallelism": f"ep{world}",
+            "experts_touched": e_touched, "l2": "no flush: 5.9 GB of packed weights per step >> 126 MB L2",
+            "bytes_per_step": layer_bytes(e_touched, T * world, H_DS, I_DS, K_DS),
+            "flops_per_step": layer_flops(T * world, K_DS, H_DS, I_DS)}
+
+
+def _cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+_REF_WEIGHTS: list = []
+
+
+def cpu_oracle_check(x, lg, weights_seed: int, dtype: str, budget_s: float, gpu_masked=None):
+    """The CPU baseline AND the output check of the timed step, on one bounded sample.
+
+    The numpy oracle (oracle/moe_oracle.py) processes the step's routed experts one at a time, in a
+    seeded random order, until ``budget_s`` of CPU work: dequantise W13 / W2 (regenerated from the
+    bench weights' per-expert seeds), SwiGLU, down projection. Its rate (algorithmic bytes of the
+    processed experts / CPU seconds) is ``cpu_baseline.value``. ``gpu_masked(w)`` runs the GPU layer
+    on the same inputs with the routing weights of unprocessed experts zeroed; its output must equal
+    the oracle's restricted to the processed experts (rtol = atol = 1e-2)."""
     import numpy as np
+    import torch
     sys.path.insert(0, str(ROOT / "oracle"))
     import moe_oracle as O
-    rng = np.random.default_rng(seed)
-    x = O.round_act(rng.standard_normal((T, H_DS)).astype(np.float32) * 0.5, dtype)
-    lg = rng.standard_normal((T, E_DS)).astype(np.float32)
-    ids, wts = O.route_topk(lg, K_DS, "softmax", True)
-    counts, offsets, sorted_pairs, _ = O.moe_permute(ids, E_DS)
-    xp = x[sorted_pairs // K_DS]
-    touched = [e for e in range(E_DS) if counts[e] > 0]
-    done_bytes, done_flops, n_exp, elapsed = 0, 0, 0, 0.0
-    for e in touched:
-        q13, z13, s13 = O.synth_awq_expert_weights(rng, 1, 2 * I_DS, H_DS, dtype)
-        q2, z2, s2 = O.synth_awq_expert_weights(rng, 1, H_DS, I_DS, dtype)
+    xf = x.float().numpy()
+    ids, wts = O.route_topk(lg.numpy(), K_DS, "softmax", True)
+    counts, offsets, sorted_pairs, pair_pos = O.moe_permute(ids, E_DS)
+    xp = xf[sorted_pairs // K_DS]
+    yp = np.zeros((xp.shape[0], H_DS), np.float32)
+    order = np.random.default_rng(0).permutation(np.nonzero(counts)[0])
+    done, elapsed, done_bytes, done_flops = [], 0.0, 0, 0
+    regen = None
+    if gpu_masked is not None:
+        from paper_2504_16214_b200.moe.weights import random_awq_expert
+        tdt = torch.float16 if dtype == "f16" else torch.bfloat16
+
+        def regen(seed, e, N, K):
+            qw, sc, qz = random_awq_expert(seed, e, N, K, tdt, "cuda")
+            return O.from_awq(qw.cpu().numpy(), sc.float().cpu().numpy(), qz.cpu().numpy())
+    rng = np.random.default_rng(1)
+    for e in order:
+        if regen is not None:  # the bench's own weights (untimed regeneration)
+            w13 = regen(2 * weights_seed, int(e), 2 * I_DS, H_DS)
+            w2 = regen(2 * weights_seed + 1, int(e), H_DS, I_DS)
+        else:  # reference arm (no GPU): same shapes, oracle-generated codes (cached across steps)
+            if len(_REF_WEIGHTS) <= len(done):
+                _REF_WEIGHTS.append((tuple(a[0] for a in O.synth_awq_expert_weights(rng, 1, 2 * I_DS, H_DS, dtype)),
+                                     tuple(a[0] for a in O.synth_awq_expert_weights(rng, 1, H_DS, I_DS, dtype))))
+            w13, w2 = _REF_WEIGHTS[len(done)]
         a, b = int(offsets[e]), int(offsets[e] + counts[e])
         t0 = time.perf_counter()
-        w13 = O.dequant(q13[0], z13[0], s13[0], dtype)
-        acc = xp[a:b] @ w13.T
-        h = O.round_act(O.silu(acc[:, :I_DS]) * acc[:, I_DS:], dtype)
-        w2 = O.dequant(q2[0], z2[0], s2[0], dtype)
-        O.round_act(h @ w2.T, dtype)
+        yp[a:b] = O.expert_rows(xp[a:b], *w13, *w2, dtype)
         elapsed += time.perf_counter() - t0
-        n_exp += 1
+        done.append(int(e))
         done_bytes += w_bytes(2 * I_DS, H_DS) + w_bytes(H_DS, I_DS) + 4 * (b - a) * H_DS
         done_flops += 6 * (b - a) * H_DS * I_DS
         if elapsed >= budget_s:
             break
-    try:
-        import numpy.__config__ as npc  # noqa: F401
-        cores = len(os.sched_getaffinity(0))
-    except Exception:
-        cores = os.cpu_count() or 1
-    return {
-        "value": round(done_bytes / elapsed / 1e9, 3),
-        "unit": "GB/s",
-        "cores": cores,
-        "kind": "port",
-        "sample": (f"numpy oracle (oracle/moe_oracle.py, expert-at-a-time dequant + fp32 GEMM), "
-                   f"{n_exp} of {len(touched)} routed experts of the DeepSeek-R1 layer at T={T}, "
-                   f"{elapsed:.1f} s of CPU work; threads = BLAS default over {cores} host cores"),
-        "tflops": round(done_flops / elapsed / 1e12, 6),
-    }
+    out = {
+        "value": round(done_bytes / elapsed / 1e9, 4), "unit": "GB/s", "cores": _cores(), "kind": "port",
+        "sample": (f"numpy oracle (oracle/moe_oracle.py: per-expert dequant + fp32 GEMMs), {len(done)} of "
+                   f"{len(order)} routed experts of the DeepSeek-R1 layer at T={xf.shape[0]}, {elapsed:.1f} s of "
+                   f"CPU work; BLAS threads over {_cores()} host cores"),
+        "tflops": round(done_flops / elapsed / 1e12, 6)}
+    if gpu_masked is not None:
+        w_mask = np.where(np.isin(ids, done), wts, 0.0).astype(np.float32)
+        want = O.combine(yp, pair_pos, w_mask, dtype)
+        got = gpu_masked(torch.from_numpy(w_mask), torch.from_numpy(ids)).float().cpu().numpy()
+        diff = np.abs(got - want)
+        out["check"] = {"experts_checked": len(done), "max_abs_diff": float(diff.max()),
+                        "max_rel_diff": float((diff / (np.abs(want) + 1e-2)).max()),
+                        "within_rtol_atol_1e-2": bool(np.allclose(got, want, rtol=1e-2, atol=1e-2))}
+    return out
 
 
 SYNTH_PROGRAMS = {  # SURVEY.md Appendix A: P0 fixture, P1 decode CTA tile, P2 prefill CTA tile
@@ -196,37 +242,109 @@ def synth_baseline(repeats: int = 1):
         if len(reports) == 2:
             row["reports_identical"] = reports["ours"] == reports["reference"]
         out[key] = row
-    return {"cores_used": 1, "cores_available": len(os.sched_getaffinity(0)), "programs": out}
+    res = {"cores_used": 1, "cores_available": _cores(), "programs": out}
+    if not (ref_path / "tilesynth").is_dir():
+        res["reference"] = ("not timed on this host: the reference tilesynth lives only in baseline/_ref "
+                            "(git-ignored install from /root/reference); the committed goldens in "
+                            "tests/golden/tilesynth pin report identity instead")
+    return res
 
 
 def run_reference(args):
+    """``--impl reference``: the CPU oracle port of the numeric path (the reference, Hexcute's
+    ``tilesynth``, contains no MoE arithmetic -- DESIGN.md 5) on the host's cores, same config,
+    metric and unit as our arm; each step is a bounded sample of the layer's experts."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    vals = []
-    cb = None
+    import torch
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import moe_oracle as O
+    world = args.gpus
+    tdt = torch.float16 if args.dtype == "f16" else torch.bfloat16
+    touched = set()
+    for r in range(world):  # the job's experts touched: every rank's routing (same inputs as our arm)
+        _, lg_r = bench_inputs(args.tokens, r, tdt)
+        touched |= set(O.route_topk(lg_r.numpy(), K_DS, "softmax", True)[0].ravel().tolist())
+    x, lg = bench_inputs(args.tokens, 0, tdt)
+    per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
     for _ in range(args.warmup):
-        cpu_oracle_sample(args.tokens, budget_s=2.0)
+        cpu_oracle_check(x, lg, 0, args.dtype, budget_s=per_step)
+    vals, cb, t_all = [], None, 0.0
     for _ in range(args.steps):
-        cb = cpu_oracle_sample(args.tokens, budget_s=max(2.0, 20.0 / max(1, args.steps)))
+        t0 = time.perf_counter()
+        cb = cpu_oracle_check(x, lg, 0, args.dtype, budget_s=per_step)
+        t_all += time.perf_counter() - t0
         vals.append(cb["value"])
     v = statistics.median(vals)
+    cfg = bench_config(args.tokens, world, len(touched))
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f16", "data": "synthetic",
-        "config": {"workload": f"deepseek_r1_moe_layer_T{args.tokens}", "E": E_DS, "topk": K_DS, "hidden": H_DS,
-                   "moe_inter": I_DS, "tokens_per_rank": args.tokens, "group_size": 128},
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        # wall time per step of the bounded CPU sample (the rate `value` is over the processed experts)
+        "ms_per_step": round(1e3 * t_all / max(1, args.steps), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+        "config": cfg,
         "cpu_baseline": {**cb, "value": v},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": ("the reference (tilesynth) has no MoE kernel: this arm is the CPU oracle port of the "
-                 "numeric path (DESIGN.md §Oracle)"),
+                 "numeric path (DESIGN.md 5), timed on a bounded per-step sample of the layer's experts"),
     }
     print(json.dumps(line))
     return 0
 
 
+def _spawn_ranks(args) -> int:
+    """``--gpus N`` (N > 1) outside torchrun: relaunch this script under torch.distributed.run, one
+    rank per GPU on this node (rendezvous on 127.0.0.1)."""
+    import socket
+    import subprocess
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def run_dry(args) -> int:
+    """``--dry-run``: the multi-rank plumbing without a GPU (gloo on CPU): rendezvous, the EP count
+    exchange of the dispatch plan, barrier + max-over-ranks timing, rank 0's JSON line."""
+    import torch
+    import torch.distributed as dist
+    from paper_2504_16214_b200.moe.ep import plan_dispatch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    e_local = E_DS // world
+    _, lg = bench_inputs(args.tokens, rank, torch.float16)
+    ids = torch.topk(lg, K_DS, dim=1).indices
+    counts = torch.bincount(ids.flatten(), minlength=E_DS).to(torch.int32)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        plan = plan_dispatch(counts, world)
+    dist.barrier()
+    t = torch.tensor([time.perf_counter() - t0])
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    recv = torch.tensor([sum(plan.recv_splits)])
+    dist.all_reduce(recv)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": round(1e3 * float(t) / args.steps, 4),
+                          "dry_run": True, "backend": "gloo (CPU)", "experts_per_rank": e_local,
+                          "rows_exchanged_per_step": int(recv), "higher_is_better": True, "scaling": "weak"}))
+    dist.destroy_process_group()
+    return 0
+
+
 # --------------------------------------------------------------------------------------------- GPU
+def _columns(rows: list) -> dict:
+    """[{k: v}, ...] -> {k: [v, ...]}: the same numbers in a shorter JSON line."""
+    return {k: [r.get(k) for r in rows] for k in rows[0]} if rows else {}
+
+
 def _graph_ms(fn, reps: int = 10) -> float:
     """Device ms per call of fn captured once in a CUDA graph (warm-up, capture, timed replays)."""
     import torch
@@ -281,7 +399,7 @@ def other_configs(dev, hbm_peak: float, tc_peak: float):
         by, fl = w_bytes(14336, 4096) + 2 * M * (4096 + 14336), 2 * M * 4096 * 14336
         rows.append({"M": M, "ms": round(ms, 4), "GB/s": round(by / ms / 1e6, 1), "TFLOP/s": round(fl / ms / 1e9, 2),
                      "hbm_frac": round(by / ms / 1e6 / hbm_peak, 4), "tc_frac": round(fl / ms / 1e9 / tc_peak, 4)})
-    out["llama3_8b_dense_K4096_N14336"] = rows
+    out["llama3_8b_dense_K4096_N14336"] = _columns(rows)
     del w
     # configs 3 and 5: MoE layers
     for name, (E, k, H, I), Ts, zipf in (
@@ -322,7 +440,7 @@ def other_configs(dev, hbm_peak: float, tc_peak: float):
                          "TFLOP/s": round(fl / ms / 1e9, 2), "hbm_frac": round(by / ms / 1e6 / hbm_peak, 4),
                          "tc_frac": round(fl / ms / 1e9 / tc_peak, 4)})
             del gr
-        out[name] = rows
+        out[name] = _columns(rows)
         del wm
         torch.cuda.empty_cache()
     return out
@@ -341,9 +459,15 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of a CUDA graph")
     ap.add_argument("--ep", action="store_true",
                     help="run the expert-parallel path (NCCL process group, all-to-all) even on one GPU")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU: exercise the N-rank launch, count exchange and timing plumbing over gloo")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return _spawn_ranks(args)
+    if args.dry_run:
+        return run_dry(args)
 
     import torch
     import torch.distributed as dist
@@ -368,11 +492,13 @@ def main():
     tdt = torch.float16 if args.dtype == "f16" else torch.bfloat16
     T = args.tokens
     lo, hi = shard_bounds(E_DS, world, rank)
-    weights = random_moe_weights(hi - lo, H_DS, I_DS, tdt, device=dev, seed=1234 + rank)
+    w_seed = 1234 + rank
+    weights = random_moe_weights(hi - lo, H_DS, I_DS, tdt, device=dev, seed=w_seed)
     g = torch.Generator(device="cpu")
-    g.manual_seed(rank)
-    x_host = (torch.randn((T, H_DS), generator=g) * 0.5).to(tdt).pin_memory()
-    lg_host = torch.randn((T, E_DS), generator=g).pin_memory()
+    g.manual_seed(1000 + rank)  # (sweep / other inputs)
+    x_cpu, lg_cpu = bench_inputs(T, rank, tdt)
+    x_host = x_cpu.pin_memory()
+    lg_host = lg_cpu.pin_memory()
     x = x_host.to(dev)
     lg = lg_host.to(dev)
 
@@ -503,10 +629,13 @@ def main():
         k_ms = a_.elapsed_time(b_) / 30
         del _g
     k_gbs = k_bytes / (k_ms * 1e-3) / 1e9 if k_ms > 0 else 0.0
-    traffic = None
+    traffic, traffic_src = None, None
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
-        traffic = json.loads(prof.read_text()).get(f"gemm_gate_up_T{T}")
+        tj = json.loads(prof.read_text())
+        traffic = tj.get(f"gemm_gate_up_T{T}")
+        traffic_src = (f"NOT measured by this run: dram__bytes_read.sum + dram__bytes_write.sum of this launch "
+                       f"from one ncu --set full capture ({tj.get('source', 'profiles/traffic.json')})")
     launches_per_step = timer.count() // args.steps
 
     # ---- end to end through the public API with host buffers (H2D inputs, D2H output)
@@ -581,25 +710,33 @@ def main():
 
     cpu = None
     synth = None
+    graph_eq = None
+    if world == 1 and graphed is not None:  # the graph the bench times == the eager kernels, bit for bit
+        yg = graphed(x, lg).clone()
+        graph_eq = bool(torch.equal(yg, step()))
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_oracle_sample(T, args.dtype)
+        from paper_2504_16214_b200.moe import moe_w4a16 as _moe, select_experts as _sel2
+
+        def gpu_masked(w_mask, ids_oracle):
+            _, ids_gpu = _sel2(lg, K_DS, "softmax", True)
+            if not torch.equal(ids_gpu.cpu(), ids_oracle):
+                raise AssertionError("GPU routing ids differ from the oracle's")
+            return _moe(x, weights, w_mask.to(dev), ids_gpu)
+        cpu = cpu_oracle_check(x_cpu, lg_cpu, w_seed, args.dtype, 12.0, gpu_masked)
         synth = synth_baseline()
 
     if rank == 0:
+        check = cpu.pop("check", None) if cpu else None
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": f"deepseek_r1_moe_layer_T{T}", "E": E_DS, "topk": K_DS, "hidden": H_DS,
-                       "moe_inter": I_DS, "tokens_per_rank": T, "tokens_job": T_job, "group_size": 128,
-                       "parallelism": f"ep{world}", "experts_touched": e_touched,
-                       "l2": "no flush: 5.9 GB of packed weights per step >> 126 MB L2",
-                       "bytes_per_step": job_bytes, "flops_per_step": job_flops},
+            "config": bench_config(T, world, e_touched),
             "tflops": round(tflops, 3),
             "hbm_frac": round(value / hbm_peak, 4),
             "roofline": {"bound": "hbm", "kernel": "w4a16_moe_gemm_kernel (gate/up, fused SiLU*up)",
                          "achieved": round(k_gbs, 1), "peak": hbm_peak, "unit": "GB/s",
-                         "frac": round(k_gbs / hbm_peak, 4), "traffic": traffic,
+                         "frac": round(k_gbs / hbm_peak, 4), "traffic": traffic, "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": k_bytes, "ms_per_launch": round(k_ms, 4),
                          "ms_per_launch_in_eager_step": round(k_ms_step, 4),
                          "timing": ("CUDA events around 30 back-to-back graph replays of the step's gate/up "
@@ -607,16 +744,18 @@ def main():
                                     "CUDA events around the launch inside eager EP steps"),
                          "peak_source": peak_src},
             "e2e": e2e,
-            "latency_ms_per_step": round(latency_ms, 4),
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": launches_per_step * args.steps,
+            "check": {**(check or {}), "graph_equals_eager": graph_eq},
+            "latency_ms_per_step": round(latency_ms, 4),
             "kernel_ms": {n: round(timer.mean_ms(n), 4) for n in timer.events},
-            "sweep": sweep,
             "other_configs": configs,
             "layout_synthesis_cpu": synth,
+            # last, so a truncated tail of the line still shows the DeepSeek-R1 decode .. prefill sweep
+            "sweep_ds_r1": _columns(sweep),
         }
-        print(json.dumps(line))
+        print(json.dumps(line, separators=(",", ":")))
     if group is not None:
         dist.destroy_process_group()
     return 0

@@ -18,8 +18,8 @@
  *   GEMM:     w4a16_grouped_gemm                       per-expert X_e * W_e^T, optional fused SiLU*up
  *             w4a16_grouped_gemm_gather                same, X rows gathered by the producer (TMA gather4)
  *   combine:  w4a16_moe_combine                        y[t] = sum_j w[t,j] * Y_perm[pos(t,j)]
- *   EP:       w4a16_ep_pack_counts / w4a16_moe_permute over received rows (NCCL all-to-all is
- *             driven by the host through torch.distributed)
+ *   EP:       w4a16_ep_local_order                     receiver-side local-expert order of the rows an
+ *                                                      all-to-all delivered (grouped by source rank)
  *   weights:  w4a16_repack_awq, w4a16_dequant (test/oracle aid), w4a16_packed_bytes
  *   driver:   w4a16_moe_forward                        the whole layer, one call, caller workspace
  *

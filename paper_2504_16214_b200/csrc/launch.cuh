@@ -3,6 +3,7 @@
 // descriptor prefetch) overlap the tail of the previous kernel in the stream; the kernel executes
 // griddep_wait() before it reads anything the previous kernel wrote. W4A16_NO_PDL=1 disables it.
 #pragma once
+#include <atomic>
 #include <cstdlib>
 #include <cuda_runtime.h>
 
@@ -16,6 +17,20 @@ inline bool pdl_enabled() {
     return !(e && atoi(e) != 0);
   }();
   return on;
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device property of a kernel: `done` holds one
+// bit per device ordinal (< 64) for which it has been set. Setting it twice is harmless, so the racy
+// first use from two threads only costs a repeated (cheap) call.
+template <typename Kern>
+bool ensure_smem_attr(Kern kernel, int bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  const unsigned long long bit = dev < 64 ? 1ull << dev : 0ull;
+  if (bit && (done.load(std::memory_order_relaxed) & bit)) return true;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+  if (bit) done.fetch_or(bit, std::memory_order_relaxed);
+  return true;
 }
 
 template <typename Kern, typename... Args>

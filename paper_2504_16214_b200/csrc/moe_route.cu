@@ -680,13 +680,9 @@ int w4a16_route_permute(const float* logits, int64_t T, int64_t E, int64_t k, in
   const int per = static_cast<int>((E + 31) / 32);
 #define W4_RPERM(P)                                                                                         \
   do {                                                                                                      \
-    static bool attr = false;                                                                               \
-    if (!attr) {                                                                                            \
-      if (cudaFuncSetAttribute(route_permute_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
-                               sizeof(int) * (2 * 1024 + kPermWarps * 1024)) != cudaSuccess)                \
-        return W4_ERR_CUDA;                                                                                 \
-      attr = true;                                                                                          \
-    }                                                                                                       \
+    static std::atomic<unsigned long long> attr{0};                                                         \
+    if (!ensure_smem_attr(route_permute_kernel<P>, sizeof(int) * (2 * 1024 + kPermWarps * 1024), attr))     \
+      return W4_ERR_CUDA;                                                                                   \
     launch_pdl(route_permute_kernel<P>, 1, kPermThreads, smem, stream, logits, (int)T, (int)E, (int)k, scoring, \
                renormalize, topk_ids, topk_weights, expert_counts, expert_offsets, sorted_pairs, pair_pos);  \
   } while (0)
@@ -733,13 +729,8 @@ int w4a16_moe_permute(const int32_t* topk_ids, int64_t P, int64_t E, int32_t* ex
   if (!expert_counts || !expert_offsets || (P > 0 && (!topk_ids || !sorted_pairs || !pair_pos))) return W4_ERR_ARG;
   if (E <= 0 || E > 1024 || P < 0 || P > (int64_t(1) << 30)) return W4_ERR_SHAPE;
   const size_t smem = sizeof(int) * (2 * E + kPermWarps * E);
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(moe_permute_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             sizeof(int) * (2 * 1024 + kPermWarps * 1024)) != cudaSuccess)
-      return W4_ERR_CUDA;
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  if (!ensure_smem_attr(moe_permute_kernel, sizeof(int) * (2 * 1024 + kPermWarps * 1024), attr)) return W4_ERR_CUDA;
   launch_pdl(moe_permute_kernel, 1, kPermThreads, smem, stream, topk_ids, (int)P, (int)E, expert_counts, expert_offsets,
                                                          sorted_pairs, pair_pos);
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
@@ -764,13 +755,8 @@ int w4a16_moe_permute_ws(const int32_t* topk_ids, int64_t P, int64_t E, int32_t*
   if (E <= 0 || E > 1024 || P > (int64_t(1) << 30)) return W4_ERR_SHAPE;
   const int nb = static_cast<int>((P + kChunk - 1) / kChunk);
   int32_t* w = static_cast<int32_t*>(ws);
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(permute_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             sizeof(int) * (1024 + kPermWarps * 1024)) != cudaSuccess)
-      return W4_ERR_CUDA;
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  if (!ensure_smem_attr(permute_scatter_kernel, sizeof(int) * (1024 + kPermWarps * 1024), attr)) return W4_ERR_CUDA;
   launch_pdl(permute_hist_kernel, nb, 512, sizeof(int) * E, stream, topk_ids, (int)P, (int)E, w);
   launch_pdl(permute_scan_kernel, 1, 1024, 0, stream, nb, (int)E, w, expert_counts, expert_offsets);
   launch_pdl(permute_scatter_kernel, nb, kPermThreads, sizeof(int) * (E + kPermWarps * E), stream, 

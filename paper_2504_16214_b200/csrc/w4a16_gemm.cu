@@ -235,19 +235,20 @@ __device__ __forceinline__ bool get_tile(int t, const int* mt_off, const GemmArg
   return true;
 }
 
-// Packed tile: w0 = e | (m_rows - 1) << 10 | n_tile << 17, w1 = m_start | split << 20 (split-K
-// launches have rows < 2^20; without split-K split is 0 and m_start uses all 32 bits).
+// Packed tile: w0 = e | (m_rows - 1) << 10 | n_tile << 17, w1 = m_start | split << 20. Only split-K
+// launches (rows < 2^20, enforced by plan_gemm) pack a split; otherwise split is 0 and unpack_tile
+// reads m_start from all 32 bits, so row counts >= 2^20 stay exact.
 __device__ __forceinline__ uint2 pack_tile(const TileInfo& ti) {
   return make_uint2(static_cast<uint32_t>(ti.e) | static_cast<uint32_t>(ti.m_rows - 1) << 10 |
                         static_cast<uint32_t>(ti.n_tile) << 17,
                     static_cast<uint32_t>(ti.m_start) | static_cast<uint32_t>(ti.split) << 20);
 }
-__device__ __forceinline__ void unpack_tile(uint2 p, TileInfo& ti) {
+__device__ __forceinline__ void unpack_tile(uint2 p, TileInfo& ti, bool split_k) {
   ti.e = p.x & 1023u;
   ti.m_rows = static_cast<int>((p.x >> 10) & 127u) + 1;
   ti.n_tile = static_cast<int>(p.x >> 17);
-  ti.m_start = static_cast<int>(p.y & 0xFFFFFu);
-  ti.split = static_cast<int>(p.y >> 20);
+  ti.m_start = static_cast<int>(split_k ? (p.y & 0xFFFFFu) : p.y);
+  ti.split = split_k ? static_cast<int>(p.y >> 20) : 0;
 }
 
 // The CTA's i-th tile (t = tile0 + i * tstride): from the smem table when i < kTileTab, else searched.
@@ -256,7 +257,7 @@ __device__ __forceinline__ bool tile_at(int i, int n_tiles, int tile0, int tstri
                                         const GemmArgs& a, uint32_t rank, TileInfo& ti) {
   if (i >= n_tiles) return false;
   if (i < kTileTab) {
-    unpack_tile(tab[i], ti);
+    unpack_tile(tab[i], ti, a.splits > 1);
     return true;
   }
   return get_tile<kNTok, kNSplit, kNPer>(tile0 + i * tstride, mt_off, a, rank, ti);
@@ -1198,15 +1199,20 @@ int make_x_map(CUtensorMap* map, const void* x, int64_t rows, int64_t K, int box
   return r == CUDA_SUCCESS ? W4_OK : W4_ERR_CUDA;
 }
 
+// SM count of the current device (cached per device ordinal; the persistent grid is one CTA per SM)
 int sm_count() {
-  static int n = 0;
-  if (!n && getenv("W4A16_GRID")) n = atoi(getenv("W4A16_GRID"));  // debug: persistent grid override
-  if (!n) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) !=
-                                                  cudaSuccess || n <= 0)
-      n = 148;  // no device (planning queries on a build host): B200
+  static const int forced = getenv("W4A16_GRID") ? atoi(getenv("W4A16_GRID")) : 0;  // debug override
+  if (forced > 0) return forced;
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;  // no device (planning on a build host): B200
+  if (dev < 64) {
+    const int c = cache[dev].load(std::memory_order_relaxed);
+    if (c > 0) return c;
   }
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) return 148;
+  if (dev < 64) cache[dev].store(n, std::memory_order_relaxed);
   return n;
 }
 
@@ -1214,12 +1220,8 @@ template <int kNTok, int kMode, bool kBF16, bool kOffset, bool kPair, bool kGath
 int launch_gemm(const GemmArgs& a, const void* x, int64_t rows, int64_t K, int grid, cudaStream_t st) {
   using C = Cfg<kNTok, kMode, kOffset, kPair>;
   auto kern = w4a16_moe_gemm_kernel<kNTok, kMode, kBF16, kOffset, kPair, kGather>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes) != cudaSuccess)
-      return W4_ERR_CUDA;
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  if (!ensure_smem_attr(kern, C::kSmemBytes, attr)) return W4_ERR_CUDA;
   CUtensorMap map;
   if (make_x_map(&map, x, rows, K, a.gather_rows ? 1 : C::kXRows) != W4_OK) return W4_ERR_CUDA;  // gather4: 1-row box
   cudaLaunchConfig_t cfg = {};

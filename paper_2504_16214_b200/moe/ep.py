@@ -103,7 +103,9 @@ def moe_w4a16_ep(x: torch.Tensor, weights, topk_weights: torch.Tensor, topk_ids:
     with tm.span("permute"):
         g_counts, g_offsets, sorted_pairs, pair_pos = backend.permute(topk_ids, e_global)
     with tm.span("gather"):
-        send_x = backend.gather(x.contiguous(), sorted_pairs, k, T * k)
+        # row_limit = the number of valid pairs (ids < 0 or >= e_global are dropped by the permutation
+        # and leave the tail of sorted_pairs unwritten): the gather never reads those entries
+        send_x = backend.gather(x.contiguous(), sorted_pairs, k, T * k, g_offsets[e_global:])
     # 3: counts exchange + host splits
     plan = plan_dispatch(g_counts, world, group)
     n_recv = sum(plan.recv_splits)
@@ -131,6 +133,15 @@ def moe_w4a16_ep(x: torch.Tensor, weights, topk_weights: torch.Tensor, topk_ids:
     dist.all_to_all_single(y_back, y_recv, plan.send_splits, plan.recv_splits, group=group)
     with tm.span("combine"):
         return backend.combine(y_back, pair_pos, topk_weights)
+
+
+def shard_with_shared(weights, num_shared: int, world: int, rank: int):
+    """Full packed weights laid out [routed experts | shared experts] -> (this rank's contiguous
+    routed shard, the shared experts), the two pieces ``fused_moe_w4a16(..., ep_group=...,
+    shared_weights=...)`` takes. The shared experts are replicated on every rank."""
+    routed = weights.num_experts - num_shared
+    lo, hi = shard_bounds(routed, world, rank)
+    return weights.slice_experts(lo, hi), weights.slice_experts(routed, weights.num_experts)
 
 
 def shard_bounds(num_experts: int, world: int, rank: int) -> tuple[int, int]:

@@ -16,7 +16,9 @@ the experts are sharded across ranks and tokens travel by all-to-all (:mod:`.ep`
 """
 from __future__ import annotations
 
+import contextlib
 import os
+import threading
 
 import torch
 
@@ -42,24 +44,53 @@ def select_experts(router_logits: torch.Tensor, top_k: int, scoring: str = "soft
 
 
 class _Workspace:
-    """Grow-only per-device scratch so steady-state calls allocate nothing."""
+    """Grow-only scratch so steady-state calls allocate nothing. Buffers are keyed by (device,
+    stream): two layer calls in flight on different streams never share intermediates. A captured
+    FusedMoEGraph owns a private instance (see :func:`_use_workspace`), so its replays cannot collide
+    with eager calls or with other graphs either."""
 
-    def __init__(self):
+    def __init__(self, per_stream: bool = True):
         self.buf: dict[tuple, torch.Tensor] = {}
+        self.per_stream = per_stream
 
     def get(self, name: str, shape, dtype, device) -> torch.Tensor:
         n = 1
         for s in shape:
             n *= s
-        key = (name, dtype, str(device))
+        dev = torch.device(device)
+        key = (name, dtype, str(dev), torch.cuda.current_stream(dev).cuda_stream if self.per_stream else 0)
         t = self.buf.get(key)
         if t is None or t.numel() < n:
-            t = torch.empty(max(n, 1), dtype=dtype, device=device)
+            t = torch.empty(max(n, 1), dtype=dtype, device=dev)
             self.buf[key] = t
         return t[:n].view(*shape)
 
 
-_ws = _Workspace()
+_default_ws = _Workspace()
+_active = threading.local()
+
+
+class _WsProxy:
+    """The workspace of the current thread: a graph's private one while it is warmed up / captured,
+    else the process default (keyed by stream)."""
+
+    def get(self, *a):
+        return (getattr(_active, "ws", None) or _default_ws).get(*a)
+
+
+_ws = _WsProxy()
+
+
+@contextlib.contextmanager
+def _use_workspace(ws: _Workspace):
+    prev = getattr(_active, "ws", None)
+    _active.ws = ws
+    try:
+        yield ws
+    finally:
+        _active.ws = prev
+
+
 # fused route + permute (one CTA) up to this many (token, slot) pairs; 0 disables. Measured: ~1 us faster
 # for DS-R1 T=1 (8 pairs), a wash at T=16 and slower from T=64 on (one CTA routes every token, where
 # the separate routing kernel spreads tokens over SMs), so only the smallest batches use it.
@@ -216,9 +247,23 @@ def fused_moe_w4a16(x: torch.Tensor, router_logits: torch.Tensor, weights: MoEWe
                     scoring: str = "softmax", renormalize: bool = False, ep_group=None,
                     timer: KernelTimer | None = None, num_expert_group: int = 0, topk_group: int = 0,
                     e_score_correction_bias: torch.Tensor | None = None,
-                    routed_scaling_factor: float = 1.0, num_shared_experts: int = 0) -> torch.Tensor:
-    """``num_shared_experts`` > 0: the last experts of ``weights`` are shared experts (always active,
-    weight 1; the router logits cover only the routed ones)."""
+                    routed_scaling_factor: float = 1.0, num_shared_experts: int = 0,
+                    shared_weights: MoEWeights | None = None) -> torch.Tensor:
+    """Shared experts (always active, weight 1; the router logits cover only the routed experts):
+
+    * ``shared_weights`` given: they are those experts (``num_shared_experts`` defaults to their
+      count) and ``weights`` holds only routed experts -- the full set on one GPU, this rank's
+      contiguous shard (:func:`~.ep.shard_bounds`) under ``ep_group``;
+    * else ``num_shared_experts`` > 0 on one GPU: the last experts of ``weights`` are the shared ones.
+      Under ``ep_group`` this needs ``shared_weights`` (a routed shard plus a shared tail cannot be
+      told apart from a larger shard; :func:`~.ep.shard_with_shared` builds both pieces)."""
+    if shared_weights is not None:
+        num_shared_experts = num_shared_experts or shared_weights.num_experts
+        if num_shared_experts != shared_weights.num_experts:
+            raise ValueError(f"num_shared_experts={num_shared_experts} but shared_weights holds "
+                             f"{shared_weights.num_experts}")
+    elif num_shared_experts and ep_group is not None:
+        raise ValueError("expert parallel with shared experts: pass shared_weights= (see ep.shard_with_shared)")
     T = router_logits.shape[0]
     if T == 0 and ep_group is None:  # (EP ranks with no tokens still join the exchanges)
         return x.new_empty((0, x.shape[1]))
@@ -232,18 +277,35 @@ def fused_moe_w4a16(x: torch.Tensor, router_logits: torch.Tensor, weights: MoEWe
     with (timer or _NOTIMER).span("route"):
         topk_weights, topk_ids = select_experts(router_logits, top_k, scoring, renormalize, num_expert_group,
                                                 topk_group, e_score_correction_bias, routed_scaling_factor)
-    if num_shared_experts:
-        first = weights.num_experts - num_shared_experts
-        if ep_group is not None:
-            # expert parallel: the routed shard goes through the exchange, the (replicated) shared
-            # experts run data-parallel on this rank's own tokens
-            y = moe_w4a16(x, weights.slice_experts(0, first), topk_weights, topk_ids, ep_group=ep_group, timer=timer)
-            T = x.shape[0]
-            sw, sid = with_shared_experts(topk_weights[:, :0], topk_ids[:, :0], 0, num_shared_experts)
-            return y.add_(moe_w4a16(x, weights.slice_experts(first, weights.num_experts), sw, sid, timer=timer)) \
-                if T else y
-        topk_weights, topk_ids = with_shared_experts(topk_weights, topk_ids, first, num_shared_experts)
-    return moe_w4a16(x, weights, topk_weights, topk_ids, ep_group=ep_group, timer=timer)
+    if not num_shared_experts:
+        return moe_w4a16(x, weights, topk_weights, topk_ids, ep_group=ep_group, timer=timer)
+    if ep_group is not None:
+        # expert parallel: the routed shard goes through the exchange, the (replicated) shared experts
+        # run data-parallel on this rank's own tokens
+        y = moe_w4a16(x, weights, topk_weights, topk_ids, ep_group=ep_group, timer=timer)
+        if not x.shape[0]:
+            return y
+        sw, sid = with_shared_experts(topk_weights[:, :0], topk_ids[:, :0], 0, num_shared_experts)
+        return y.add_(moe_w4a16(x, shared_weights, sw, sid, timer=timer))
+    if shared_weights is not None:  # one GPU: run routed + shared in the same grouped GEMMs
+        weights = concat_experts(weights, shared_weights)
+    first = weights.num_experts - num_shared_experts
+    topk_weights, topk_ids = with_shared_experts(topk_weights, topk_ids, first, num_shared_experts)
+    return moe_w4a16(x, weights, topk_weights, topk_ids, timer=timer)
+
+
+_CONCAT_CACHE: dict = {}
+
+
+def concat_experts(a: MoEWeights, b: MoEWeights) -> MoEWeights:
+    """[a's experts | b's experts] as one MoEWeights (one copy, cached per (a, b) buffer pair)."""
+    key = (a.w13.blocks.data_ptr(), a.w2.blocks.data_ptr(), b.w13.blocks.data_ptr(), b.w2.blocks.data_ptr(),
+           a.num_experts, b.num_experts)
+    hit = _CONCAT_CACHE.get(key)
+    if hit is None:
+        hit = a.concat(b)
+        _CONCAT_CACHE[key] = hit
+    return hit
 
 
 class FusedMoEGraph:
@@ -255,8 +317,11 @@ class FusedMoEGraph:
     def __init__(self, weights: MoEWeights, tokens: int, top_k: int, scoring: str = "softmax",
                  renormalize: bool = False, dtype: torch.dtype = torch.float16, device=None,
                  x: torch.Tensor | None = None, router_logits: torch.Tensor | None = None,
-                 num_shared_experts: int = 0):
+                 num_shared_experts: int = 0, workspace: _Workspace | None = None):
+        """``workspace``: the graph's private intermediates (default: its own). Graphs that share one
+        must be replayed in stream order (FusedMoEPipeline's two slots do)."""
         dev = torch.device(device) if device is not None else weights.w13.blocks.device
+        self.workspace = workspace or _Workspace(per_stream=False)
         self.x = torch.zeros((tokens, weights.hidden), dtype=dtype, device=dev)
         self.logits = torch.randn((tokens, weights.num_experts - num_shared_experts), device=dev)
         if x is not None:  # warm up / capture on the caller's first inputs (same routing as served)
@@ -267,14 +332,14 @@ class FusedMoEGraph:
         kw = {"num_shared_experts": num_shared_experts}
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream(dev))
-        with torch.cuda.stream(side):  # warm-up: kernel attributes, workspace growth, first launches
-            for _ in range(2):
-                fused_moe_w4a16(self.x, self.logits, *args, **kw)
-        torch.cuda.current_stream(dev).wait_stream(side)
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
-            self.y = fused_moe_w4a16(self.x, self.logits, *args, **kw)
-        self._keep = dict(_ws.buf)  # the graph reads/writes these exact buffers: keep them alive
+        with _use_workspace(self.workspace):
+            with torch.cuda.stream(side):  # warm-up: kernel attributes, workspace growth, first launches
+                for _ in range(2):
+                    fused_moe_w4a16(self.x, self.logits, *args, **kw)
+            torch.cuda.current_stream(dev).wait_stream(side)
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph):
+                self.y = fused_moe_w4a16(self.x, self.logits, *args, **kw)
 
     def __call__(self, x: torch.Tensor | None = None, router_logits: torch.Tensor | None = None) -> torch.Tensor:
         if x is not None:
@@ -303,8 +368,9 @@ class FusedMoEPipeline:
                  renormalize: bool = False, dtype: torch.dtype = torch.float16, device=None,
                  x: torch.Tensor | None = None, router_logits: torch.Tensor | None = None):
         self.dev = torch.device(device) if device is not None else weights.w13.blocks.device
-        self.slots = [FusedMoEGraph(weights, tokens, top_k, scoring, renormalize, dtype, self.dev, x, router_logits)
-                      for _ in range(2)]
+        ws = _Workspace(per_stream=False)  # shared by both slots: their replays are serialised on one stream
+        self.slots = [FusedMoEGraph(weights, tokens, top_k, scoring, renormalize, dtype, self.dev, x, router_logits,
+                                    workspace=ws) for _ in range(2)]
         self.h2d = torch.cuda.Stream(device=self.dev)
         self.d2h = torch.cuda.Stream(device=self.dev)
         self.i = 0

@@ -38,6 +38,13 @@ class PackedW4:
         return PackedW4(self.blocks[start * per:stop * per], stop - start, self.n_rows, self.K, self.parts,
                         self.dtype)
 
+    def concat(self, other: "PackedW4") -> "PackedW4":
+        """[self's experts | other's experts] (a copy; shapes and dtype must agree)."""
+        if (self.n_rows, self.K, self.parts, self.dtype) != (other.n_rows, other.K, other.parts, other.dtype):
+            raise ValueError("concat of packed weights with different shapes / dtype")
+        return PackedW4(torch.cat([self.blocks, other.blocks]), self.num_experts + other.num_experts, self.n_rows,
+                        self.K, self.parts, self.dtype)
+
 
 @dataclass(frozen=True)
 class MoEWeights:
@@ -58,6 +65,9 @@ class MoEWeights:
 
     def slice_experts(self, start: int, stop: int) -> "MoEWeights":
         return MoEWeights(self.w13.slice_experts(start, stop), self.w2.slice_experts(start, stop))
+
+    def concat(self, other: "MoEWeights") -> "MoEWeights":
+        return MoEWeights(self.w13.concat(other.w13), self.w2.concat(other.w2))
 
 
 def pack_awq(qweight: torch.Tensor, scales: torch.Tensor, qzeros: torch.Tensor, gated: bool,
@@ -81,13 +91,38 @@ def pack_moe_awq(w13_qweight, w13_scales, w13_qzeros, w2_qweight, w2_scales, w2_
                       pack_awq(w2_qweight, w2_scales, w2_qzeros, False, group_size))
 
 
-def random_packed(E: int, N: int, K: int, gated: bool, dtype: torch.dtype, generator: torch.Generator,
-                  device="cuda", chunk: int = 16) -> PackedW4:
-    """Synthetic AWQ weights generated on the device in expert chunks (q, z ~ U{0..15} from random
-    bytes; scales ~ U(0.5, 1.5) * 2^-7) and packed straight into one buffer."""
+def _expert_seed(seed: int, e: int, N: int, K: int) -> int:
+    return (seed * 1_000_003 + e * 7919 + N * 131 + K) & 0x7FFF_FFFF_FFFF
+
+
+def random_awq_expert(seed: int, e: int, N: int, K: int, dtype: torch.dtype, device="cuda"):
+    """The synthetic AWQ tensors of expert ``e`` of a ``random_packed(..., generator=seed)`` projection
+    (qweight [K, N/8] int32, scales [K/128, N], qzeros [K/128, N/8] int32): q, z ~ U{0..15} from random
+    bytes, scales ~ U(0.5, 1.5) * 2^-7. Each expert has its own seed, so a checker can regenerate any
+    sampled expert without the others."""
+    g = torch.Generator(device=device)
+    g.manual_seed(_expert_seed(seed, e, N, K))
+    qw = torch.randint(0, 256, (K, N // 2), generator=g, device=device, dtype=torch.uint8).view(torch.int32)
+    qz = torch.randint(0, 256, (K // 128, N // 2), generator=g, device=device, dtype=torch.uint8).view(torch.int32)
+    sc = ((torch.rand((K // 128, N), generator=g, device=device) + 0.5) * (2.0 ** -7)).to(dtype)
+    return qw, sc, qz
+
+
+def random_packed(E: int, N: int, K: int, gated: bool, dtype: torch.dtype, generator, device="cuda",
+                  chunk: int = 16) -> PackedW4:
+    """Synthetic AWQ weights generated on the device and packed straight into one buffer.
+    ``generator``: an int seed (per-expert streams, see :func:`random_awq_expert`) or a
+    torch.Generator (expert chunks drawn from it in order)."""
+    from . import _lib
     parts = 2 if gated else 1
     per = ops.packed_bytes(1, N, K)
     blocks = torch.empty(E * per, dtype=torch.uint8, device=device)
+    if isinstance(generator, int):
+        for e in range(E):
+            qw, sc, qz = random_awq_expert(generator, e, N, K, dtype, device)
+            _lib.call("w4a16_repack_awq", qw.data_ptr(), sc.data_ptr(), qz.data_ptr(), 1, K, N, parts, 128,
+                      blocks[e * per:(e + 1) * per].data_ptr(), ops._stream())
+        return PackedW4(blocks, E, N, K, parts, dtype)
     for e0 in range(0, E, chunk):
         n = min(chunk, E - e0)
         qw = torch.randint(0, 256, (n, K, N // 2), generator=generator, device=device,
@@ -96,7 +131,6 @@ def random_packed(E: int, N: int, K: int, gated: bool, dtype: torch.dtype, gener
                            dtype=torch.uint8).view(torch.int32)
         sc = ((torch.rand((n, K // 128, N), generator=generator, device=device) + 0.5) * (2.0 ** -7)).to(dtype)
         out = blocks[e0 * per:(e0 + n) * per]
-        from . import _lib
         _lib.call("w4a16_repack_awq", qw.data_ptr(), sc.data_ptr(), qz.data_ptr(), n, K, N, parts, 128,
                   out.data_ptr(), ops._stream())
         del qw, qz, sc
@@ -104,8 +138,8 @@ def random_packed(E: int, N: int, K: int, gated: bool, dtype: torch.dtype, gener
 
 
 def random_moe_weights(E: int, H: int, I: int, dtype: torch.dtype, device="cuda", seed: int = 0) -> MoEWeights:
-    """Synthetic packed MoE weights of the named shapes (benchmarks at full size)."""
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
-    return MoEWeights(random_packed(E, 2 * I, H, True, dtype, g, device),
-                      random_packed(E, H, I, False, dtype, g, device))
+    """Synthetic packed MoE weights of the named shapes (benchmarks at full size). Expert e's AWQ
+    tensors are ``random_awq_expert(2 * seed, e, 2 * I, H)`` (w13) and
+    ``random_awq_expert(2 * seed + 1, e, H, I)`` (w2)."""
+    return MoEWeights(random_packed(E, 2 * I, H, True, dtype, 2 * seed, device),
+                      random_packed(E, H, I, False, dtype, 2 * seed + 1, device))

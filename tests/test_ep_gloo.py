@@ -38,7 +38,9 @@ class CpuBackend:
         return (torch.from_numpy(c), torch.from_numpy(o), torch.from_numpy(sp), torch.from_numpy(pp))
 
     @staticmethod
-    def gather(x, sorted_pairs, topk, rows):
+    def gather(x, sorted_pairs, topk, rows, row_limit=None):
+        if row_limit is not None:
+            rows = min(rows, int(row_limit[0]))
         idx = sorted_pairs[:rows].long() // topk
         return x[idx].clone()
 
@@ -109,3 +111,27 @@ def test_local_expert_ids_and_plan_shapes():
     from paper_2504_16214_b200.moe.ep import local_expert_ids
     rc = torch.tensor([[2, 0, 1], [0, 3, 1]], dtype=torch.int32)
     assert local_expert_ids(rc).tolist() == [0, 0, 2, 1, 1, 1, 2]
+
+
+def test_shard_with_shared_layout():
+    """[routed | shared] packed weights -> (this rank's routed shard, the replicated shared experts)."""
+    from paper_2504_16214_b200.moe.ep import shard_with_shared
+    from paper_2504_16214_b200.moe.weights import MoEWeights, PackedW4
+    per13, per2 = 10, 6
+    E, S, world = 8, 1, 4
+    full = MoEWeights(PackedW4(torch.arange((E + S) * per13), E + S, 256, 128, 2, torch.float16),
+                      PackedW4(torch.arange((E + S) * per2), E + S, 128, 128, 1, torch.float16))
+    for rank in range(world):
+        routed, shared = shard_with_shared(full, S, world, rank)
+        assert routed.num_experts == 2 and shared.num_experts == 1
+        assert routed.w13.blocks.tolist() == list(range(2 * rank * per13, (2 * rank + 2) * per13))
+        assert shared.w2.blocks.tolist() == list(range(E * per2, (E + S) * per2))
+
+
+def test_ep_shared_experts_need_explicit_weights():
+    from paper_2504_16214_b200.moe import fused_moe_w4a16
+    from paper_2504_16214_b200.moe.weights import MoEWeights, PackedW4
+    w = MoEWeights(PackedW4(torch.zeros(4), 2, 256, 128, 2, torch.float16),
+                   PackedW4(torch.zeros(4), 2, 128, 128, 1, torch.float16))
+    with pytest.raises(ValueError, match="shared_weights"):
+        fused_moe_w4a16(torch.zeros(2, 128), torch.zeros(2, 1), w, 1, ep_group=object(), num_shared_experts=1)

@@ -576,8 +576,10 @@ def test_ep_nccl_world1_layer():
         w = MoEWeights(_packed(q13, z13, s13, dt, True), _packed(q2, z2, s2, dt, False))
         x = O.round_act(rng.standard_normal((T, H)).astype(np.float32) * 0.5, dt)
         lg = rng.standard_normal((T, E)).astype(np.float32)
-        y = fused_moe_w4a16(_to_dev_act(x, dt), torch.from_numpy(lg).cuda(), w, k, "softmax", True,
-                            ep_group=dist.group.WORLD, num_shared_experts=1)
+        from paper_2504_16214_b200.moe.ep import shard_with_shared
+        routed, shared = shard_with_shared(w, 1, dist.get_world_size(), dist.get_rank())
+        y = fused_moe_w4a16(_to_dev_act(x, dt), torch.from_numpy(lg).cuda(), routed, k, "softmax", True,
+                            ep_group=dist.group.WORLD, shared_weights=shared)
         torch.cuda.synchronize()
         rid, rw = O.route_topk(lg, k, "softmax", True)
         ids = np.concatenate([rid, np.full((T, 1), E, np.int32)], axis=1)
