@@ -8,6 +8,14 @@ ids bit-exact), through the public API on full-size synthetic weights:
 * the dense Llama-3-8B linear (K=4096, N=14336) at M=4096;
 * a grouped GEMM whose row count passes 2^20 (tile-table packing limit).
 
+Tolerance: |got - want| <= atol + rtol * scale with rtol = atol = 1e-2, where scale is the magnitude of
+the terms each output sums, sum_j |w_j| * (|h_j| @ |W2_j|^T) (``moe_oracle.expert_rows``). At these K
+(2048..14336) the pinned intermediate roundings (h and each expert's output in fp16/bf16) see 1-ulp
+flips between any two fp32 accumulation orders; such a flip moves an output by ~ulp of those terms,
+which for outputs that cancel to near zero exceeds 1e-2 of |want| (bf16 ulp at 32 is 0.25). The
+fraction of elements that also meet the plain |want|-relative rule is asserted >= 99 % (fp16) / 90 %
+(bf16, 8-bit mantissa).
+
 The GPU always runs the WHOLE layer (every routed expert, the real tile plan). The CPU oracle then checks
 a sample of experts: the routing weights of pairs routed to unsampled experts are zeroed, so the layer
 output equals the oracle's restricted to the sampled experts (`moe_oracle.moe_forward_expertwise`). Each
@@ -86,9 +94,18 @@ def _layer_case(E, k, H, I, T, dt, n_check, seed, zipf=False, outliers=False, gr
     w13 = [_expert_awq(2 * seed, e, 2 * I, H, dt) for e in pick]
     w2 = [_expert_awq(2 * seed + 1, e, H, I, dt) for e in pick]
     st = lambda ws, i: np.stack([w[i] for w in ws])  # noqa: E731
-    want = O.moe_forward_expertwise(x, st(w13, 0), st(w13, 1), st(w13, 2), st(w2, 0), st(w2, 1), st(w2, 2),
-                                    ids_loc, w_masked, dt)
-    return got, want, pick
+    want, scale = O.moe_forward_expertwise(x, st(w13, 0), st(w13, 1), st(w13, 2), st(w2, 0), st(w2, 1), st(w2, 2),
+                                           ids_loc, w_masked, dt, with_scale=True)
+    return got, want, scale, pick
+
+
+def _check(got, want, scale, plain_frac=0.99):
+    err = np.abs(got - want)
+    bad = err > ATOL + RTOL * scale
+    assert not bad.any(), (f"{int(bad.sum())} of {bad.size} outputs off: max |diff| {err.max():.4g}, "
+                           f"worst at scale {scale.flat[int(np.argmax(err - RTOL * scale))]:.4g}")
+    plain = np.mean(err <= ATOL + RTOL * np.abs(want))
+    assert plain >= plain_frac, f"only {plain:.4%} within the plain |want|-relative rule"
 
 
 DS = (256, 8, 7168, 2048)
@@ -97,30 +114,29 @@ DS = (256, 8, 7168, 2048)
 @pytest.mark.parametrize("T,dt", [(1, "f16"), (1, "bf16"), (64, "f16"), (64, "bf16"), (8192, "f16"),
                                   (8192, "bf16")])
 def test_deepseek_r1_layer(T, dt):
-    got, want, pick = _layer_case(*DS, T, dt, n_check=16, seed=100 + T, graph=(T == 64 and dt == "f16"))
+    got, want, scale, pick = _layer_case(*DS, T, dt, n_check=16, seed=100 + T, graph=(T == 64 and dt == "f16"))
     assert len(pick) == min(16, 8 * T)
-    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+    _check(got, want, scale, 0.99 if dt == "f16" else 0.9)
 
 
 @pytest.mark.parametrize("dt", ["f16", "bf16"])
 def test_deepseek_r1_decode_outliers(dt):
     """Heavy-tailed activations at K=7168 in decode mode: the offset codes carry a 1024*sum(x) term
     through the fp32 partials -- it must still cancel to within the bar."""
-    got, want, _ = _layer_case(*DS, 64, dt, n_check=16, seed=7, outliers=True)
-    scale = max(1.0, float(np.abs(want).max()) / 8.0)  # outputs grow with the outliers: bar relative to them
-    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL * scale)
+    got, want, scale, _ = _layer_case(*DS, 64, dt, n_check=16, seed=7, outliers=True)
+    _check(got, want, scale, 0.99 if dt == "f16" else 0.9)
 
 
 @pytest.mark.parametrize("T", [16, 2048])
 def test_mixtral_layer(T):
-    got, want, _ = _layer_case(8, 2, 4096, 14336, T, "f16", n_check=8 if T == 16 else 3, seed=200 + T)
-    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+    got, want, scale, _ = _layer_case(8, 2, 4096, 14336, T, "f16", n_check=8 if T == 16 else 3, seed=200 + T)
+    _check(got, want, scale)
 
 
 @pytest.mark.parametrize("zipf", [False, True])
 def test_qwen3_layer(zipf):
-    got, want, _ = _layer_case(128, 8, 2048, 768, 256, "f16", n_check=16, seed=300, zipf=zipf)
-    np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
+    got, want, scale, _ = _layer_case(128, 8, 2048, 768, 256, "f16", n_check=16, seed=300, zipf=zipf)
+    _check(got, want, scale)
 
 
 def test_llama_dense_m4096():

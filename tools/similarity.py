@@ -1,0 +1,72 @@
+#!/usr/bin/env python
+"""Token-sequence similarity of our synthesizer modules against the reference package (build-container
+aid; /root/reference is read-only and absent on GPU boxes).
+
+For every ``paper_2504_16214_b200/tilesynth/*.py`` file prints the highest difflib ratio against any
+``/root/reference/pkg/src/tilesynth/*.py`` file, on two token streams:
+
+* raw  -- Python tokens as written (comments / docstrings / layout dropped);
+* norm -- identifiers -> ID, strings -> STR, numbers -> NUM (structure only).
+
+Both with difflib's default autojunk and without it (the stricter figure)."""
+from __future__ import annotations
+
+import difflib
+import io
+import keyword
+import sys
+import tokenize
+from pathlib import Path
+
+REF = Path("/root/reference/pkg/src/tilesynth")
+OURS = Path(__file__).resolve().parent.parent / "paper_2504_16214_b200" / "tilesynth"
+SKIP = {tokenize.COMMENT, tokenize.NL, tokenize.NEWLINE, tokenize.INDENT, tokenize.DEDENT, tokenize.ENCODING,
+        tokenize.ENDMARKER}
+
+
+def tokens(path: Path, norm: bool) -> list[str]:
+    out = []
+    prev = None
+    for tok in tokenize.generate_tokens(io.StringIO(path.read_text()).readline):
+        if tok.type in SKIP:
+            prev = tok
+            continue
+        if tok.type == tokenize.STRING and (prev is None or prev.type in (tokenize.NEWLINE, tokenize.INDENT,
+                                                                          tokenize.DEDENT, tokenize.NL)):
+            prev = tok  # docstring / bare string statement
+            continue
+        s = tok.string
+        if norm:
+            if tok.type == tokenize.NAME and not keyword.iskeyword(s):
+                s = "ID"
+            elif tok.type == tokenize.STRING:
+                s = "STR"
+            elif tok.type == tokenize.NUMBER:
+                s = "NUM"
+        out.append(s)
+        prev = tok
+    return out
+
+
+def ratio(a, b, autojunk):
+    return difflib.SequenceMatcher(None, a, b, autojunk=autojunk).ratio()
+
+
+def main():
+    refs = {p.name: (tokens(p, False), tokens(p, True)) for p in sorted(REF.glob("*.py"))}
+    worst = 0.0
+    rows = []
+    for p in sorted(OURS.glob("*.py")):
+        raw, nrm = tokens(p, False), tokens(p, True)
+        best = max(((max(ratio(raw, r, True), ratio(raw, r, False)), max(ratio(nrm, n, True), ratio(nrm, n, False)),
+                     name) for name, (r, n) in refs.items()), key=lambda x: x[1])
+        rows.append((p.name, *best))
+        worst = max(worst, best[1])
+    for name, r, n, ref in rows:
+        print(f"{name:28s} vs {ref:14s} raw {r:.2f}  norm {n:.2f}")
+    print(f"max norm {worst:.2f}")
+    return 0 if worst < float(sys.argv[1]) else 1 if len(sys.argv) > 1 else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
