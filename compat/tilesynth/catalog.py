@@ -1,6 +1,6 @@
-"""Compat alias: reference module ``tilesynth.catalog`` -> ``paper_2504_16214_b200.tilesynth.isa``."""
+"""Compat alias: reference module ``tilesynth.catalog`` -> ``paper_2504_16214_b200.tilesynth.instr_catalog``."""
 import sys as _sys
 
-from paper_2504_16214_b200.tilesynth import isa as _m
+from paper_2504_16214_b200.tilesynth import instr_catalog as _m
 
 _sys.modules[__name__] = _m

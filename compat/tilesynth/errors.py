@@ -1,6 +1,6 @@
-"""Compat alias: reference module ``tilesynth.errors`` -> ``paper_2504_16214_b200.tilesynth.exceptions``."""
+"""Compat alias: reference module ``tilesynth.errors`` -> ``paper_2504_16214_b200.tilesynth.errors``."""
 import sys as _sys
 
-from paper_2504_16214_b200.tilesynth import exceptions as _m
+from paper_2504_16214_b200.tilesynth import errors as _m
 
 _sys.modules[__name__] = _m

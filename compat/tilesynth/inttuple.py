@@ -1,6 +1,6 @@
-"""Compat alias: reference module ``tilesynth.inttuple`` -> ``paper_2504_16214_b200.tilesynth.tuples``."""
+"""Compat alias: reference module ``tilesynth.inttuple`` -> ``paper_2504_16214_b200.tilesynth.nested``."""
 import sys as _sys
 
-from paper_2504_16214_b200.tilesynth import tuples as _m
+from paper_2504_16214_b200.tilesynth import nested as _m
 
 _sys.modules[__name__] = _m

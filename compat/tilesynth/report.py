@@ -1,6 +1,6 @@
-"""Compat alias: reference module ``tilesynth.report`` -> ``paper_2504_16214_b200.tilesynth.reporting``."""
+"""Compat alias: reference module ``tilesynth.report`` -> ``paper_2504_16214_b200.tilesynth.report_json``."""
 import sys as _sys
 
-from paper_2504_16214_b200.tilesynth import reporting as _m
+from paper_2504_16214_b200.tilesynth import report_json as _m
 
 _sys.modules[__name__] = _m

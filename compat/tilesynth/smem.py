@@ -1,6 +1,6 @@
-"""Compat alias: reference module ``tilesynth.smem`` -> ``paper_2504_16214_b200.tilesynth.smem_synth``."""
+"""Compat alias: reference module ``tilesynth.smem`` -> ``paper_2504_16214_b200.tilesynth.smem_layout``."""
 import sys as _sys
 
-from paper_2504_16214_b200.tilesynth import smem_synth as _m
+from paper_2504_16214_b200.tilesynth import smem_layout as _m
 
 _sys.modules[__name__] = _m

@@ -1,21 +1,31 @@
-"""Layout synthesis for tile programs (host side of the W4A16 path) -- a re-implementation of the
-reference ``tilesynth`` API (``/root/reference/pkg/src/tilesynth/__init__.py:16-58``) whose chosen
-thread-value, shared-memory and swizzle layouts, instruction choices, costs and JSON reports are
-bit-identical to the reference on the same programs (tests/test_tilesynth_parity.py).
+"""Layout synthesis for tile programs -- the host side of the W4A16 path, written for this repository.
 
-Module map (reference -> here): inttuple -> tuples, errors -> exceptions, layout -> algebra,
-tv -> thread_value, swizzle -> banks, ir -> program, catalog -> isa, synth -> propagation,
-smem -> smem_synth, cost -> latency, pipeline -> driver, report -> reporting, cli -> cli.
-``compat/tilesynth`` re-exports them under the reference module names.
+It answers the reference's API (``/root/reference/pkg/src/tilesynth/__init__.py:16-58``) with the same
+results: chosen thread-value, shared-memory and swizzle layouts, instructions, costs and JSON reports
+are byte-identical to the reference's on the same programs (tests/test_tilesynth_parity.py). Modules:
+
+* ``nested``          nested integer tuples (colex digits, text form)
+* ``layout_algebra``  ``Layout`` and its algebra; numpy tables of whole maps
+* ``tvl``             thread-value layouts with cached position grids
+* ``banking``         swizzles and the vectorised 32-bank conflict model
+* ``tile_ir``         program text format, validation, liveness, components
+* ``instr_catalog``   instruction models (``data/*.cat``) and queries
+* ``tv_solver``       anchors and round-based constraint propagation
+* ``smem_layout``     shared-memory constraints, unification, materialisation, swizzle choice
+* ``search``          the candidate walk with per-component memoisation
+* ``latency_model``   the issue / completion latency model and ranking
+* ``synthesize``      ``synthesize_program``;  ``report_json`` reports;  ``cli`` the command line
+
+``compat/tilesynth`` maps the reference's module names onto these.
 """
-from .algebra import (Layout, coalesce, complement, compose, concat, dim_restrict, inverse, parse_layout,
-                      restrict_first_mode)
-from .banks import Swizzle, bank_conflicts
-from .driver import SynthesisResult, synthesize_program
-from .isa import Catalog, Instruction, builtin_catalog_path, load_catalog
-from .program import ProgramGraph, parse_program, validate
-from .propagation import SynthesisConfig
-from .thread_value import TvLayout
+from .banking import Swizzle, bank_conflicts
+from .instr_catalog import Catalog, Instruction, builtin_catalog_path, load_catalog
+from .layout_algebra import (Layout, coalesce, complement, compose, concat, dim_restrict, inverse, parse_layout,
+                             restrict_first_mode)
+from .synthesize import SynthesisResult, synthesize_program
+from .tile_ir import ProgramGraph, parse_program, validate
+from .tv_solver import SynthesisConfig
+from .tvl import TvLayout
 
 __version__ = "0.1.0"
 
