@@ -9,7 +9,7 @@ For every ``paper_2504_16214_b200/tilesynth/*.py`` file prints the highest diffl
 * norm -- identifiers -> ID, strings -> STR, numbers -> NUM (structure only).
 
 Ratios are difflib's with autojunk OFF -- the figure the round-1 review quoted (its numbers for
-the round-1 port reproduce exactly this way); ``--junk`` also shows the autojunk ones."""
+the round-1 port reproduce exactly this way)."""
 from __future__ import annotations
 
 import difflib
