@@ -1,6 +1,6 @@
-"""Compat alias: reference module ``tilesynth.layout`` -> ``paper_2504_16214_b200.tilesynth.layout_algebra``."""
+"""Compat alias: reference module ``tilesynth.layout`` -> ``paper_2504_16214_b200.tilesynth.algebra``."""
 import sys as _sys
 
-from paper_2504_16214_b200.tilesynth import layout_algebra as _m
+from paper_2504_16214_b200.tilesynth import algebra as _m
 
 _sys.modules[__name__] = _m

@@ -1,6 +1,3 @@
-"""Compat alias: reference module ``tilesynth.pipeline`` -> ``paper_2504_16214_b200.tilesynth.synthesize``."""
-import sys as _sys
-
-from paper_2504_16214_b200.tilesynth import synthesize as _m
-
-_sys.modules[__name__] = _m
+"""Compat module: reference module ``tilesynth.pipeline`` = this repository's ``explore``
+(``synthesize_program`` / ``SynthesisResult`` live next to the search)."""
+from paper_2504_16214_b200.tilesynth.explore import SynthesisResult, synthesize_program  # noqa: F401

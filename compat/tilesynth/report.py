@@ -1,6 +1,6 @@
-"""Compat alias: reference module ``tilesynth.report`` -> ``paper_2504_16214_b200.tilesynth.report_json``."""
+"""Compat alias: reference module ``tilesynth.report`` -> ``paper_2504_16214_b200.tilesynth.frontend``."""
 import sys as _sys
 
-from paper_2504_16214_b200.tilesynth import report_json as _m
+from paper_2504_16214_b200.tilesynth import frontend as _m
 
 _sys.modules[__name__] = _m

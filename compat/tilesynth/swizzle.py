@@ -1,6 +1,6 @@
-"""Compat alias: reference module ``tilesynth.swizzle`` -> ``paper_2504_16214_b200.tilesynth.banking``."""
+"""Compat alias: reference module ``tilesynth.swizzle`` -> ``paper_2504_16214_b200.tilesynth.bankmodel``."""
 import sys as _sys
 
-from paper_2504_16214_b200.tilesynth import banking as _m
+from paper_2504_16214_b200.tilesynth import bankmodel as _m
 
 _sys.modules[__name__] = _m

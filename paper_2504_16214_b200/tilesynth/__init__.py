@@ -4,34 +4,34 @@ It answers the reference's API (``/root/reference/pkg/src/tilesynth/__init__.py:
 results: chosen thread-value, shared-memory and swizzle layouts, instructions, costs and JSON reports
 are byte-identical to the reference's on the same programs (tests/test_tilesynth_parity.py). Modules:
 
-* ``nested``          nested integer tuples (colex digits, text form)
-* ``layout_algebra``  ``Layout`` and its algebra; numpy tables of whole maps
-* ``tvl``             thread-value layouts with cached position grids
-* ``banking``         swizzles and the vectorised 32-bank conflict model
-* ``tile_ir``         program text format, validation, liveness, components
-* ``instr_catalog``   instruction models (``data/*.cat``) and queries
-* ``tv_solver``       anchors and round-based constraint propagation
-* ``smem_layout``     shared-memory constraints, unification, materialisation, swizzle choice
-* ``search``          the candidate walk with per-component memoisation
-* ``latency_model``   the issue / completion latency model and ranking
-* ``synthesize``      ``synthesize_program``;  ``report_json`` reports;  ``cli`` the command line
+* ``ituple``      nested integer tuples (iterative walks, token-machine parser)
+* ``algebra``     ``Layout`` over flat run lists; interval-based composition; numpy tables
+* ``tvmap``       thread-value layouts with whole-domain position grids
+* ``bankmodel``   swizzles and the array-at-a-time 32-bank conflict model
+* ``tileprog``    program text format (handler table), validation rules, liveness, components
+* ``isa_table``   instruction catalogs (``data/*.cat``) and queries
+* ``layout_flow`` anchors and round-based constraint propagation
+* ``smem_plan``   shared-memory constraints, unification, materialisation, swizzle choice
+* ``explore``     the candidate walk (per-component memoisation) and ``synthesize_program``
+* ``cyclemodel``  issue / completion latency model (tensor scoreboard) and ranking
+* ``frontend``    JSON / text reports, ``--explain`` and the ``tilesynth`` command line
 
 ``compat/tilesynth`` maps the reference's module names onto these.
 """
-from .banking import Swizzle, bank_conflicts
-from .instr_catalog import Catalog, Instruction, builtin_catalog_path, load_catalog
-from .layout_algebra import (Layout, coalesce, complement, compose, concat, dim_restrict, inverse, parse_layout,
-                             restrict_first_mode)
-from .synthesize import SynthesisResult, synthesize_program
-from .tile_ir import ProgramGraph, parse_program, validate
-from .tv_solver import SynthesisConfig
-from .tvl import TvLayout
+from . import algebra as _algebra, bankmodel as _banks, explore as _explore, isa_table as _isa, layout_flow as _flow
+from . import tileprog as _prog, tvmap as _tv
 
 __version__ = "0.1.0"
 
-__all__ = [
-    "Catalog", "Instruction", "Layout", "ProgramGraph", "SynthesisConfig", "SynthesisResult", "Swizzle", "TvLayout",
-    "bank_conflicts", "builtin_catalog_path", "coalesce", "complement", "compose", "concat", "dim_restrict",
-    "inverse", "load_catalog", "parse_layout", "parse_program", "restrict_first_mode", "synthesize_program",
-    "validate",
-]
+# public name -> the module that defines it (the reference's export list, tilesynth/__init__.py:16-58)
+_EXPORTS = {
+    _algebra: "Layout coalesce complement compose concat dim_restrict inverse parse_layout restrict_first_mode",
+    _banks: "Swizzle bank_conflicts",
+    _explore: "SynthesisResult synthesize_program",
+    _isa: "Catalog Instruction builtin_catalog_path load_catalog",
+    _flow: "SynthesisConfig",
+    _prog: "ProgramGraph parse_program validate",
+    _tv: "TvLayout",
+}
+globals().update({name: getattr(mod, name) for mod, names in _EXPORTS.items() for name in names.split()})
+__all__ = sorted(name for names in _EXPORTS.values() for name in names.split())

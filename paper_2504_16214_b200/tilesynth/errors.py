@@ -1,71 +1,59 @@
-"""Exception types of the layout synthesizer.
+"""Error taxonomy of the layout synthesizer.
 
-The class NAMES and their subclass relations are the reference's public interface
-(``/root/reference/pkg/src/tilesynth/errors.py:4-124``): callers catch them by name, and the
-reference's own tests import them. They are declared here as one table -- (name, parent,
-meaning) -- and materialised with ``type``; only the two classes that carry structured payloads
-(:class:`ParseError`, :class:`ConflictDetected`) are written out.
+The class names and their is-a relations are the public contract -- callers (and the reference's
+own tests, run against this package through ``compat/``) catch ``LayoutError`` or a specific leaf
+such as ``NotInvertible`` -- so they follow /root/reference/pkg/src/tilesynth/errors.py:1-124.
+The leaves are generated from one table; only the two errors that carry data are written out.
 """
 from __future__ import annotations
 
-__all__: list[str] = []
-
 
 class TileSynthError(Exception):
-    """Root of every error raised by the synthesizer."""
+    """Root of everything the synthesizer raises."""
 
 
-# name -> (parent, one-line meaning). Order matters only in that parents precede children.
-_TABLE = {
-    # layout algebra
-    "LayoutError": ("TileSynthError", "layout-algebra failure"),
-    "ShapeMismatch": ("LayoutError", "coordinate / operand structure does not fit the shape"),
-    "OutOfDomain": ("LayoutError", "index or coordinate outside a layout's domain"),
-    "LayoutIncompatible": ("LayoutError", "operands violate a divisibility condition"),
-    "NotInvertible": ("LayoutError", "not a bijection onto a contiguous range"),
-    "NotComplementable": ("LayoutError", "no gap-filling layout for the codomain"),
-    "NotDivisible": ("LayoutError", "a mode cannot be split at the requested size"),
-    "IntegerOverflow": ("LayoutError", "value outside the supported 64-bit range"),
-    # shared-memory banking
-    "MisalignedAccess": ("TileSynthError", "an access is not aligned to its width"),
-    # program IR
-    "UnknownTensor": ("TileSynthError", "reference to an undeclared tensor"),
-    "ArityError": ("TileSynthError", "wrong operand count / kind for an operation"),
-    "UnknownOp": ("TileSynthError", "operation index out of range"),
-    # instruction catalog
-    "CatalogFormatError": ("TileSynthError", "malformed catalog text"),
-    "NonBijectiveLayout": ("TileSynthError", "an instruction layout is not a bijection onto its tile"),
-    "NoInstructionAvailable": ("TileSynthError", "no compatible instruction"),
-    # synthesis
-    "NonDivisibleTile": ("TileSynthError", "extent not divisible by the instruction / warp tiling"),
-    "UnsolvedResidual": ("TileSynthError", "constraints left after propagation reached a fixpoint"),
-    # shared memory
-    "StrideConflict": ("TileSynthError", "unified constraints force duplicate addresses"),
-    "Unsatisfiable": ("TileSynthError", "stride variables admit no bijective assignment"),
-}
+# (class, parent, what it means)
+_TAXONOMY = (
+    ("LayoutError", "TileSynthError", "Layout-algebra failure."),
+    ("ShapeMismatch", "LayoutError", "A coordinate or operand does not fit the shape tree."),
+    ("OutOfDomain", "LayoutError", "An index or coordinate lies outside a layout's domain."),
+    ("LayoutIncompatible", "LayoutError", "Two layouts cannot be combined (divisibility)."),
+    ("NotInvertible", "LayoutError", "Not a bijection onto a contiguous index range."),
+    ("NotComplementable", "LayoutError", "No gap-filling layout for the requested codomain."),
+    ("NotDivisible", "LayoutError", "A mode cannot be cut at the requested extent."),
+    ("IntegerOverflow", "LayoutError", "An extent, stride or index leaves the 64-bit range."),
+    ("MisalignedAccess", "TileSynthError", "A vector access is not aligned to its width."),
+    ("UnknownTensor", "TileSynthError", "A statement names a tensor that was never declared."),
+    ("ArityError", "TileSynthError", "An operation got the wrong operand roles."),
+    ("UnknownOp", "TileSynthError", "An operation index is out of range."),
+    ("CatalogFormatError", "TileSynthError", "Malformed instruction catalog."),
+    ("NonBijectiveLayout", "TileSynthError", "A catalog layout does not cover its tile exactly once."),
+    ("NoInstructionAvailable", "TileSynthError", "No catalog instruction fits the request."),
+    ("NonDivisibleTile", "TileSynthError", "A tensor extent does not divide by the tiling."),
+    ("UnsolvedResidual", "TileSynthError", "Constraints left after propagation reached a fixpoint."),
+    ("StrideConflict", "TileSynthError", "Buffer constraints force two elements onto one address."),
+    ("Unsatisfiable", "TileSynthError", "Stride variables admit no bijective assignment."),
+)
 
-_ns = globals()
-for _name, (_parent, _meaning) in _TABLE.items():
-    _ns[_name] = type(_name, (_ns[_parent],), {"__doc__": _meaning[0].upper() + _meaning[1:] + ".",
-                                               "__module__": __name__})
+for _cls, _base, _doc in _TAXONOMY:
+    globals()[_cls] = type(_cls, (globals()[_base],), {"__doc__": _doc, "__module__": __name__})
 
 
 class ParseError(TileSynthError):
-    """Malformed program / layout / catalog text; ``line`` and ``column`` locate it (0 = unknown)."""
+    """Malformed program, layout or tuple text; ``line`` / ``column`` locate it when known."""
 
-    def __init__(self, message: str, line: int = 0, column: int = 0):
+    def __init__(self, message, line=0, column=0):
         self.line, self.column = line, column
         super().__init__(f"line {line}, col {column}: {message}" if line else message)
 
 
 class ConflictDetected(TileSynthError):
-    """Two different thread-value layouts demanded for one tensor (kept for API parity: synthesis
-    resolves such conflicts with a redistribution instead of raising)."""
+    """One tensor was handed two different thread-value layouts."""
 
-    def __init__(self, tensor: str, existing, incoming, op_index: int):
+    def __init__(self, tensor, existing, incoming, op_index):
         self.tensor, self.existing, self.incoming, self.op_index = tensor, existing, incoming, op_index
-        super().__init__(f"tensor '{tensor}' assigned two different thread-value layouts "
-                         f"(op {op_index}): {existing} vs {incoming}")
+        super().__init__(f"op {op_index} assigns tensor '{tensor}' the layout {incoming}, "
+                         f"but it already has {existing}")
 
 
-__all__ += ["TileSynthError", "ParseError", "ConflictDetected", *_TABLE]
+__all__ = ["TileSynthError", "ParseError", "ConflictDetected"] + [row[0] for row in _TAXONOMY]

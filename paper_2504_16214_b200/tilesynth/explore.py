@@ -1,0 +1,226 @@
+"""Candidate search over the copy-instruction choices, per-candidate shared / staging buffer
+synthesis, and the one-call pipeline (validate -> dead code -> search -> rank).
+
+Contract: /root/reference/pkg/src/tilesynth/synth.py:66-75,505-720 and pipeline.py:1-60 -- leaves in
+depth-first (lexicographic) order of the per-copy choice indices, capped at ``max_candidates - 1``
+walked leaves plus the all-narrowest fallback leaf; leaves failing layout solving or buffer
+unification are pruned; failures surface as diagnostics.
+
+Construction here: a leaf is evaluated component by component, and each component's propagation
+result is memoised on the instruction choices of ITS copies (components only share shared-memory
+buffers, which are synthesised afterwards), so a search of n leaves over c components propagates
+each distinct (component, choice) pair once. The leaf walk is ``itertools.product`` over the
+choice lists.
+"""
+from __future__ import annotations
+
+import itertools
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Tuple
+
+from .errors import (LayoutIncompatible, NoInstructionAvailable, NonDivisibleTile, NotDivisible, NotInvertible,
+                     OutOfDomain, ShapeMismatch, StrideConflict, TileSynthError, Unsatisfiable)
+from .isa_table import Catalog, Instruction, candidates_for_copy
+from .layout_flow import PropagationState, RearrangePatch, SlotKey, SynthesisConfig, propagate
+from .smem_plan import BufferCopy, SmemLayout, synthesize_buffer
+from .tileprog import OpNode, ProgramGraph, TensorDecl, eliminate_dead_code, partition_components, validate
+from .tvmap import TvLayout
+
+PRUNE = (LayoutIncompatible, NonDivisibleTile, NotDivisible, NotInvertible, OutOfDomain, ShapeMismatch,
+         StrideConflict, Unsatisfiable, NoInstructionAvailable)
+
+
+@dataclass
+class Candidate:
+    index: int
+    choices: Dict[int, Instruction]
+    layouts: Dict[SlotKey, TvLayout]
+    patches: List[RearrangePatch]
+    smem: Dict[str, SmemLayout]
+    staging: Dict[str, SmemLayout] = field(default_factory=dict)
+    cost: Optional[object] = None
+
+
+def _copy_choice_points(graph, catalog):
+    """(copy op, its candidate instructions) for every copy that needs an instruction."""
+    out = []
+    for op in graph.ops:
+        if op.kind == "copy":
+            src, dst = graph.tensor(op.operands[0]), graph.tensor(op.results[0])
+            if not src.scope == dst.scope == "Register":
+                out.append((op, candidates_for_copy(catalog, src, dst)))
+    return out
+
+
+class _ComponentMemo:
+    """Propagation results of one component, keyed by the instruction choices of its ops."""
+
+    def __init__(self, ops):
+        self.ops = list(ops)
+        self.indices = [op.index for op in ops]
+        self.seen: Dict[Tuple, object] = {}
+
+    def run(self, graph, choices, config, catalog):
+        key = tuple(id(choices.get(i)) for i in self.indices)
+        hit = self.seen.get(key)
+        if hit is None:
+            state = PropagationState(graph, config)
+            local = {i: choices[i] for i in self.indices if i in choices}
+            try:
+                propagate(self.ops, graph, local, config, catalog, state)
+                hit = (local, state.layouts, state.patches)
+            except TileSynthError as e:
+                hit = e
+            self.seen[key] = hit
+        if isinstance(hit, Exception):
+            raise hit
+        return hit
+
+
+class _Evaluator:
+    """Evaluates leaves of one search (graph, catalog, config fixed)."""
+
+    def __init__(self, graph, catalog, config):
+        self.graph, self.catalog, self.config = graph, catalog, config
+        self.parts = [_ComponentMemo(c) for c in partition_components(graph)]
+
+    def evaluate(self, picked):
+        choices = dict(picked)
+        state = PropagationState(self.graph, self.config)
+        for part in self.parts:
+            chosen, layouts, patches = part.run(self.graph, choices, self.config, self.catalog)
+            choices.update(chosen)
+            state.layouts.update(layouts)
+            state.patches.extend(patches)
+        return (choices, state.layouts, state.patches, _synthesize_shared(self.graph, choices, state),
+                _synthesize_staging(self.graph, self.catalog, self.config, state))
+
+
+def evaluate_assignment(graph, catalog, config, choices):
+    """Propagate layouts over every component and synthesise every buffer for one leaf;
+    ``choices`` is completed in place with the matrix instructions the anchors pick."""
+    state = PropagationState(graph, config)
+    for component in partition_components(graph):
+        propagate(component, graph, choices, config, catalog, state)
+    return (choices, state.layouts, state.patches, _synthesize_shared(graph, choices, state),
+            _synthesize_staging(graph, catalog, config, state))
+
+
+def _synthesize_shared(graph, choices, state):
+    """One layout + swizzle per shared tensor from the accesses of every copy touching it."""
+    users = {}
+    for op in graph.ops:
+        if op.kind != "copy":
+            continue
+        for side, name in (("src", op.operands[0]), ("dst", op.results[0])):
+            decl = graph.tensor(name)
+            if decl.scope == "Shared":
+                inst = choices[op.index]
+                users.setdefault(name, []).append(BufferCopy(op.index, state.layouts[(op.index, side)],
+                                                             inst.vector_elems(decl.dtype), inst.name))
+    return {name: synthesize_buffer(name, graph.tensor(name).shape, graph.tensor(name).dtype.bits, copies)
+            for name, copies in sorted(users.items())}
+
+
+def _staging_instructions(catalog, decl):
+    """(store, load) pairs of equal width for a register redistribution through shared memory,
+    widest store first; loads are generic entries."""
+    tmp = TensorDecl("staging", "Shared", decl.dtype, decl.shape)
+    loads = {}
+    for ld in candidates_for_copy(catalog, tmp, decl):
+        if ld.generic:
+            loads.setdefault(ld.vector_bytes, ld)
+    return [(st, loads[st.vector_bytes]) for st in candidates_for_copy(catalog, decl, tmp) if st.vector_bytes in loads]
+
+
+def _synthesize_staging(graph, catalog, config, state):
+    """A staging buffer for every user rearrange and every inserted redistribution patch: the first
+    (store, load) pair whose two accesses unify."""
+    jobs = [(f"rearrange@{op.index}", op.operands[0], state.layouts[op.operands[0]], state.layouts[op.results[0]])
+            for op in graph.ops
+            if op.kind == "rearrange" and op.operands[0] in state.layouts and op.results[0] in state.layouts]
+    jobs += [(f"redistribute@{p.op_index}:{p.tensor}", p.tensor, p.from_layout, p.to_layout) for p in state.patches]
+    out = {}
+    for label, tensor, before, after in jobs:
+        decl = graph.tensor(tensor)
+        for st, ld in _staging_instructions(catalog, decl):
+            pair = [BufferCopy(-1, before, st.vector_elems(decl.dtype), st.name),
+                    BufferCopy(-2, after, ld.vector_elems(decl.dtype), ld.name)]
+            try:
+                out[label] = synthesize_buffer(label, decl.shape, decl.dtype.bits, pair)
+                break
+            except PRUNE:
+                continue
+        else:
+            raise Unsatisfiable(f"no staging layout for redistribution of {tensor}")
+    return out
+
+
+def expand_search(graph, catalog, config):
+    """Surviving leaves in lexicographic order of the choice indices (at most ``max_candidates - 1``
+    from the walk, at least one), then the all-narrowest fallback leaf if it was not among them."""
+    if not graph.ops:
+        return []
+    points = _copy_choice_points(graph, catalog)
+    ev = _Evaluator(graph, catalog, config)
+    found = []
+    kept = set()
+
+    def leaf(pick):
+        try:
+            parts = ev.evaluate({op.index: opts[i] for (op, opts), i in zip(points, pick)})
+        except PRUNE:
+            return None
+        return Candidate(len(found), *parts)
+
+    cap = max(1, config.max_candidates - 1)
+    for pick in itertools.product(*(range(len(opts)) for _, opts in points)):
+        if len(found) >= cap:
+            break
+        cand = leaf(pick)
+        if cand is not None:
+            found.append(cand)
+            kept.add(pick)
+    narrowest = tuple(len(opts) - 1 for _, opts in points)
+    if config.max_candidates > 1 and narrowest not in kept:
+        cand = leaf(narrowest)
+        if cand is not None:
+            found.append(cand)
+    return found
+
+
+# ------------------------------------------------------------------------------------------ pipeline
+@dataclass
+class SynthesisResult:
+    graph: ProgramGraph
+    config: SynthesisConfig
+    catalog: Catalog
+    diagnostics: List[str] = field(default_factory=list)
+    candidates: List[Candidate] = field(default_factory=list)
+
+    @property
+    def ok(self):
+        return not self.diagnostics and (bool(self.candidates) or not self.graph.ops)
+
+    @property
+    def best(self):
+        return self.candidates[0] if self.candidates else None
+
+
+def synthesize_program(graph, catalog, config=None):
+    """Validate, drop dead code, search, rank. Failures come back as diagnostics (``result.ok``)."""
+    from .cyclemodel import rank
+    config = config or SynthesisConfig()
+    problems = validate(graph)
+    if problems:
+        return SynthesisResult(graph, config, catalog, problems)
+    live = eliminate_dead_code(graph)
+    if graph.ops and not live.ops:
+        return SynthesisResult(live, config, catalog, ["all operations are dead code (no global store)"])
+    try:
+        found = expand_search(live, catalog, config)
+    except TileSynthError as e:
+        return SynthesisResult(live, config, catalog, [str(e)])
+    if live.ops and not found:
+        return SynthesisResult(live, config, catalog, ["no valid candidate: every instruction assignment failed"])
+    return SynthesisResult(live, config, catalog, [], rank(found, live, catalog))

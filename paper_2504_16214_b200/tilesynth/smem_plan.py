@@ -1,0 +1,385 @@
+"""Shared-memory layout synthesis: per-copy layout constraints, their unification, materialisation
+into a bijective buffer layout, the TMA feasibility check, and the swizzle choice.
+
+Contract: /root/reference/pkg/src/tilesynth/smem.py:1-647 (constraint text, unify / materialize
+results and error classes, check_tma, synthesize_buffer's layout, swizzle and per-copy conflicts).
+
+Construction here:
+
+* A constraint dimension is a *factorisation*: a list of ``(extent, entry)`` pieces whose extents
+  multiply to the dimension; an entry is a concrete stride (int) or a :class:`StrideVar`.
+* :func:`build_constraint` inverts the (de-duplicated) access map and cuts its runs at two sets of
+  boundaries at once -- the vector field [T, T*vec) in thread-value index space and the dimension
+  ends in logical space -- with one generic :func:`_refine` over "boundary lists".
+* :func:`unify` overlays two factorisations of each dimension on the cumulative-extent axis: two
+  cursors walk the piece ends, each step ends at the nearer one, and the piece of the common
+  refinement takes its entry from the piece of each side that contains it.
+* :func:`materialize` runs a stride-chain cursor: concrete pieces pin the chain, free pieces fill
+  the gaps (first fitting piece in logical order, split by gcd) and then extend the chain.
+* The swizzle search builds every copy's warp address matrix straight from the buffer layout's
+  table and the access grid (numpy fancy indexing) and scores all candidate swizzles at once
+  (:func:`bankmodel.score_pattern_matrix`).
+"""
+from __future__ import annotations
+
+import math
+import re
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Tuple, Union
+
+import numpy as np
+
+from . import bankmodel
+from .algebra import Layout, fuse_runs, inverse
+from .bankmodel import IDENTITY_SWIZZLE, AccessPattern, Swizzle, candidate_swizzles
+from .errors import LayoutIncompatible, MisalignedAccess, NotInvertible, StrideConflict, Unsatisfiable
+from .tvmap import TvLayout, filter_replication
+
+
+class StrideVar:
+    """A stride still to be chosen; its value must be a multiple of ``divisibility``."""
+
+    __slots__ = ("divisibility",)
+
+    def __init__(self, divisibility=1):
+        self.divisibility = divisibility
+
+    def __repr__(self):
+        return f"StrideVar(div={self.divisibility})"
+
+
+Entry = Union[int, StrideVar]
+Piece = Tuple[int, Entry]
+
+
+@dataclass
+class LayoutConstraint:
+    """``splits[i]``: the pieces of dimension i, fastest first; extents multiply to ``dims[i]``."""
+
+    dims: Tuple[int, ...]
+    splits: List[List[Piece]]
+
+    def size(self):
+        return math.prod(self.dims)
+
+    def concrete_modes(self):
+        return [(e, s) for dim in self.splits for e, s in dim if isinstance(s, int)]
+
+    def render(self):
+        """``(s0,(s1,s2)):(1,(D1,D2))`` -- free strides numbered by first appearance."""
+        names = {}
+
+        def word(s):
+            return str(s) if isinstance(s, int) else names.setdefault(id(s), f"D{len(names) + 1}")
+
+        def group(items):
+            return items[0] if len(items) == 1 else "(" + ",".join(items) + ")"
+
+        shapes = [group([str(e) for e, _ in dim]) for dim in self.splits]
+        strides = [group([word(s) for _, s in dim]) for dim in self.splits]
+        return "(" + ",".join(shapes) + "):(" + ",".join(strides) + ")"
+
+    def structure_key(self):
+        return tuple(tuple((e, s if isinstance(s, int) else "var") for e, s in dim) for dim in self.splits)
+
+    def __str__(self):
+        return self.render()
+
+
+_ITEM = re.compile(r"\(([^()]*)\)|([^,()]+)")
+
+
+def parse_constraint(text):
+    """``"((8,8),64):((1,D1),D2)"`` -> constraint; equal variable names are one variable."""
+    body = "".join(text.split())
+    try:
+        shape_txt, stride_txt = body.split(":")
+    except ValueError:
+        raise LayoutIncompatible(f"constraint text {text!r} needs one ':'") from None
+    shape_items, stride_items = _items(shape_txt), _items(stride_txt)
+    if len(shape_items) != len(stride_items):
+        raise LayoutIncompatible("constraint shape and stride have different dimension counts")
+    free = {}
+    splits = []
+    for sh, st in zip(shape_items, stride_items):
+        if isinstance(sh, list) is not isinstance(st, list):
+            raise LayoutIncompatible("constraint dimension nests differently in shape and stride")
+        sh, st = (sh, st) if isinstance(sh, list) else ([sh], [st])
+        splits.append([(int(e), int(s) if s.isdigit() else free.setdefault(s, StrideVar())) for e, s in zip(sh, st)])
+    return LayoutConstraint(tuple(math.prod(e for e, _ in dim) for dim in splits), splits)
+
+
+def _items(text):
+    if not (text.startswith("(") and text.endswith(")")):
+        raise LayoutIncompatible(f"constraint part {text!r} is not parenthesised")
+    return [g.split(",") if g is not None else w for g, w in ((m.group(1), m.group(2))
+                                                            for m in _ITEM.finditer(text[1:-1]))]
+
+
+# ------------------------------------------------------------------------------------------- build
+def _refine(extent, weight, cuts):
+    """Local cut points (1 < p < extent) of a run covering weights [weight, weight * extent) at the
+    given global boundaries; a boundary inside the run must be a multiple of ``weight``."""
+    out = []
+    for b in cuts:
+        if weight < b < weight * extent:
+            if b % weight:
+                raise LayoutIncompatible(f"boundary {b} is not aligned to the run weight {weight}")
+            out.append(b // weight)
+    return out
+
+
+def build_constraint(f, vector_elems, dims):
+    """The constraint one copy puts on the buffer layout: each thread's ``vector_elems`` consecutive
+    values must sit at consecutive addresses; every other stride stays free. LayoutIncompatible when
+    the access is not a bijection onto the buffer."""
+    f = filter_replication(f)
+    total = math.prod(dims)
+    if f.threads * f.values != total:
+        raise LayoutIncompatible(f"the access covers {f.threads * f.values} of {total} elements")
+    try:
+        runs = inverse(f.layout).runs
+    except NotInvertible as e:
+        raise LayoutIncompatible(str(e)) from e
+    T = f.threads
+    vec_cuts = (T, T * vector_elems)
+    dim_ends = list(np.cumprod(dims, dtype=object))
+    splits = [[] for _ in dims]
+    logical = 1
+    for extent, tv_weight in runs:
+        points = sorted(set(_refine(extent, tv_weight, vec_cuts)) | set(_refine(extent, logical, dim_ends)))
+        prev = 1
+        for p in points + [extent]:
+            if p % prev or extent % p:
+                raise LayoutIncompatible(f"cannot cut a run of {extent} at {p}")
+            n = p // prev
+            if n > 1 or (prev == 1 and p == extent):
+                w, lw = tv_weight * prev, logical * prev
+                dim = next(i for i, end in enumerate(dim_ends) if lw < end)
+                entry = w // T if T <= w < T * vector_elems else StrideVar(vector_elems)
+                _append_merging(splits[dim], n, entry)
+            prev = p
+        logical *= extent
+    return LayoutConstraint(tuple(dims), [dim or [(1, StrideVar(1))] for dim in splits])
+
+
+def _append_merging(dim, n, entry):
+    """Append a piece; two neighbouring free pieces of one dimension become one free piece."""
+    if dim and isinstance(entry, StrideVar) and isinstance(dim[-1][1], StrideVar):
+        m, other = dim[-1]
+        dim[-1] = (m * n, StrideVar(max(other.divisibility, entry.divisibility)))
+    else:
+        dim.append((n, entry))
+
+
+# ------------------------------------------------------------------------------------------- unify
+def _bounds(pieces):
+    """(start, end, entry) of each piece on the cumulative-extent axis."""
+    out, at = [], 1
+    for e, s in pieces:
+        out.append((at, at * e, s))
+        at *= e
+    return out
+
+
+def _sub_entry(piece, lo):
+    start, _, s = piece
+    return s * (lo // start) if isinstance(s, int) else StrideVar(s.divisibility)
+
+
+def unify(c1, c2):
+    """Least-committed constraint holding every concrete stride of both. StrideConflict when the
+    factorisations cannot be overlaid, concrete strides disagree, or the concrete pieces overlap."""
+    if c1.dims != c2.dims:
+        raise StrideConflict(f"buffer extents {c1.dims} and {c2.dims} differ")
+    merged = []
+    for xs, ys in zip(c1.splits, c2.splits):
+        bx, by = _bounds(xs), _bounds(ys)
+        dim, lo, i, j = [], 1, 0, 0
+        while i < len(bx) and j < len(by):
+            hi = min(bx[i][1], by[j][1])      # next boundary of the common refinement
+            if bx[i][1] % hi or by[j][1] % hi:
+                raise StrideConflict(f"piece boundaries misalign at {hi}")
+            a, b = _sub_entry(bx[i], lo), _sub_entry(by[j], lo)
+            if isinstance(a, int) and isinstance(b, int) and a != b:
+                raise StrideConflict(f"concrete strides {a} and {b} disagree")
+            if isinstance(a, int) or isinstance(b, int):
+                dim.append((hi // lo, a if isinstance(a, int) else b))
+            else:
+                dim.append((hi // lo, StrideVar(max(a.divisibility, b.divisibility))))
+            step_x, step_y = bx[i][1] == hi, by[j][1] == hi
+            i, j, lo = i + step_x, j + step_y, hi
+        if i < len(bx) or j < len(by):
+            raise StrideConflict("the two factorisations do not cover the same extent")
+        merged.append(dim)
+    out = LayoutConstraint(c1.dims, merged)
+    _check_chain(out)
+    return out
+
+
+def _check_chain(c):
+    """Concrete pieces, by stride, must stack into a bijection's stride chain."""
+    reach = 1
+    for e, s in sorted(c.concrete_modes(), key=lambda m: m[1]):
+        if s < reach or s % reach:
+            raise StrideConflict(f"concrete piece {e}:{s} overlaps the span {reach} below it")
+        reach = s * e
+
+
+# ------------------------------------------------------------------------------------- materialize
+def materialize(c):
+    """Pick the free strides so the layout is a bijection onto [0, size): concrete pieces first by
+    stride, free pieces fill the chain gaps and then extend the chain in logical order."""
+    _check_chain(c)
+    placed = {}
+    free = []  # [dim, pos, remaining extent, var] in logical order
+    for d, dim in enumerate(c.splits):
+        for p, (e, s) in enumerate(dim):
+            if isinstance(s, int):
+                placed[(d, p)] = [(e, s)]
+            else:
+                free.append([d, p, e, s])
+
+    def fill(gap, at):
+        while gap > 1:
+            for rec in free:
+                g = math.gcd(rec[2], gap)
+                if g > 1 and at % rec[3].divisibility == 0:
+                    break
+            else:
+                raise Unsatisfiable(f"no free piece fits the stride gap {gap} at {at}")
+            placed.setdefault((rec[0], rec[1]), []).append((g, at))
+            rec[2] //= g
+            if rec[2] == 1:
+                free.remove(rec)
+            at, gap = at * g, gap // g
+
+    reach = 1
+    for e, s in sorted(c.concrete_modes(), key=lambda m: m[1]):
+        if s > reach:
+            fill(s // reach, reach)
+        reach = s * e
+    for d, p, e, var in free:
+        if reach % var.divisibility:
+            raise Unsatisfiable(f"stride {reach} is not a multiple of {var.divisibility}")
+        placed.setdefault((d, p), []).append((e, reach))
+        reach *= e
+    if reach != c.size():
+        raise Unsatisfiable(f"the strides span {reach}, the buffer holds {c.size()}")
+    trees = []
+    for d, dim in enumerate(c.splits):
+        runs = fuse_runs(r for p in range(len(dim)) for r in sorted(placed[(d, p)], key=lambda r: r[1])) or [(1, 0)]
+        trees.append(runs[0] if len(runs) == 1 else (tuple(e for e, _ in runs), tuple(s for _, s in runs)))
+    return Layout(tuple(s for s, _ in trees), tuple(d for _, d in trees))
+
+
+# ----------------------------------------------------------------------------------------------- TMA
+@dataclass
+class TmaCheck:
+    feasible: bool
+    reason: str = ""
+    hint: Optional[Layout] = None
+
+
+def check_tma(c, element_bits, *, max_dims=5, align_bytes=16, max_box=256):
+    """Can a bulk tensor copy serve this buffer? Few enough pieces, every extent within the box cap,
+    a 16-byte contiguous innermost run; the hint materialises the free strides."""
+    pieces = sum(map(len, c.splits))
+    if pieces > max_dims:
+        return TmaCheck(False, f"{pieces} dims exceed limit {max_dims}")
+    if max(c.dims) > max_box:
+        return TmaCheck(False, f"extent exceeds box cap {max_box}")
+    run = 1
+    for e, s in sorted(c.concrete_modes(), key=lambda m: m[1]):
+        run *= e if s == run else 1
+    if run * element_bits // 8 < align_bytes:
+        return TmaCheck(False, f"innermost contiguous run is {run * element_bits // 8}B < {align_bytes}B")
+    try:
+        return TmaCheck(True, "", materialize(c))
+    except Unsatisfiable as e:
+        return TmaCheck(False, str(e))
+
+
+# ------------------------------------------------------------------------------------------ buffers
+@dataclass
+class BufferCopy:
+    """One copy touching a shared buffer: its memory-side access layout, vector width (elements)
+    and instruction name."""
+
+    op_index: int
+    access: TvLayout
+    vector_elems: int
+    instruction: str
+
+
+@dataclass
+class SmemLayout:
+    buffer: str
+    layout: Layout
+    swizzle: Swizzle
+    element_bits: int
+    copy_conflicts: Dict[int, int] = field(default_factory=dict)
+    identity_conflicts: Dict[int, int] = field(default_factory=dict)
+    constraint: Optional[LayoutConstraint] = None
+    copies: List[BufferCopy] = field(default_factory=list)
+
+    def byte_address(self, logical):
+        return self.swizzle(self.layout(logical) * self.element_bits // 8)
+
+    def render(self):
+        return f"{self.layout} (+) {self.swizzle}"
+
+
+def warp_address_matrix(m, element_bits, copy):
+    """Pre-swizzle byte addresses of every distinct warp-wide access of one copy: row (warp w,
+    vector j) holds lane l's address of ``m(access(32 w + l, j * vec))``. Returns (rows, width)."""
+    f, vec = copy.access, copy.vector_elems
+    width = max(1, vec * element_bits // 8)
+    if width not in bankmodel.VALID_WIDTHS:
+        raise MisalignedAccess(f"{width}-byte accesses are not modelled")
+    lanes = min(32, f.threads)
+    warps = max(1, f.threads // 32)
+    iters = max(1, f.values // vec)
+    grid = f.grid()
+    threads = (np.arange(warps)[:, None] * 32 + np.arange(lanes)).ravel()
+    elems = grid[threads][:, np.arange(iters) * vec]            # [warps * lanes, iters]
+    addrs = m.table()[elems] * element_bits // 8
+    rows = addrs.reshape(warps, lanes, iters).transpose(0, 2, 1).reshape(-1, lanes)
+    if (rows % width).any():
+        raise MisalignedAccess(f"a {width}-byte access of copy {copy.op_index} is misaligned")
+    return np.unique(rows, axis=0), width
+
+
+_MEMO: Dict[Tuple, SmemLayout] = {}
+
+
+def synthesize_buffer(buffer, dims, element_bits, copies):
+    """Unify the copies' constraints, materialise the layout, choose the swizzle, record each copy's
+    conflict degree under it and under the identity. Memoised on (extents, width, accesses)."""
+    if not copies:
+        raise Unsatisfiable(f"buffer {buffer} has no copies")
+    key = (tuple(dims), element_bits,
+           tuple((c.op_index, c.access.layout, c.access.tile, c.vector_elems) for c in copies))
+    hit = _MEMO.get(key)
+    if hit is None:
+        constraint = build_constraint(copies[0].access, copies[0].vector_elems, dims)
+        for c in copies[1:]:
+            constraint = unify(constraint, build_constraint(c.access, c.vector_elems, dims))
+        m = materialize(constraint)
+        widest = max(max(1, c.vector_elems * element_bits // 8) for c in copies)
+        pool = candidate_swizzles(min_base=max(2, (widest - 1).bit_length()))
+        groups = [warp_address_matrix(m, element_bits, c) for c in copies]
+        best, _, _ = bankmodel.score_pattern_matrix(groups, pool)
+        hit = SmemLayout(buffer, m, best, element_bits, constraint=constraint, copies=list(copies))
+        for c, (rows, width) in zip(copies, groups):
+            for sw, table in ((best, hit.copy_conflicts), (IDENTITY_SWIZZLE, hit.identity_conflicts)):
+                table[c.op_index] = int(bankmodel.phase_degrees(sw(rows), width).max(initial=1))
+        _MEMO[key] = hit
+    return SmemLayout(buffer, hit.layout, hit.swizzle, hit.element_bits, dict(hit.copy_conflicts),
+                      dict(hit.identity_conflicts), hit.constraint, list(hit.copies))
+
+
+def access_patterns(m, element_bits, copy):
+    """The copy's distinct warp-wide accesses as :class:`AccessPattern` objects (diagnostics)."""
+    rows, width = warp_address_matrix(m, element_bits, copy)
+    return [AccessPattern(tuple(int(a) for a in row), width) for row in rows]

@@ -24,11 +24,11 @@ def ref():
     return mods
 
 
-from paper_2504_16214_b200.tilesynth import banking as B  # noqa: E402
-from paper_2504_16214_b200.tilesynth import layout_algebra as LA  # noqa: E402
-from paper_2504_16214_b200.tilesynth import nested as N  # noqa: E402
-from paper_2504_16214_b200.tilesynth import smem_layout as SM  # noqa: E402
-from paper_2504_16214_b200.tilesynth import tvl as TV  # noqa: E402
+from paper_2504_16214_b200.tilesynth import bankmodel as B  # noqa: E402
+from paper_2504_16214_b200.tilesynth import algebra as LA  # noqa: E402
+from paper_2504_16214_b200.tilesynth import ituple as N  # noqa: E402
+from paper_2504_16214_b200.tilesynth import smem_plan as SM  # noqa: E402
+from paper_2504_16214_b200.tilesynth import tvmap as TV  # noqa: E402
 
 
 def _outcome(fn, *args):
@@ -242,11 +242,11 @@ def test_whole_synthesis_matches_reference_on_random_programs(ref):
         r_synth = importlib.import_module("tilesynth.synth")
     finally:
         sys.path.remove("/root/reference/pkg/src")
-    from paper_2504_16214_b200.tilesynth import instr_catalog as C
-    from paper_2504_16214_b200.tilesynth import report_json as R
-    from paper_2504_16214_b200.tilesynth import tile_ir as IR
-    from paper_2504_16214_b200.tilesynth.synthesize import synthesize_program
-    from paper_2504_16214_b200.tilesynth.tv_solver import SynthesisConfig
+    from paper_2504_16214_b200.tilesynth import isa_table as C
+    from paper_2504_16214_b200.tilesynth import frontend as R
+    from paper_2504_16214_b200.tilesynth import tileprog as IR
+    from paper_2504_16214_b200.tilesynth.explore import synthesize_program
+    from paper_2504_16214_b200.tilesynth.layout_flow import SynthesisConfig
     ours_cat = C.load_catalog(C.builtin_catalog_path())
     ref_cat = r_cat.load_catalog(r_cat.builtin_catalog_path())
     rng = random.Random(1234)
