@@ -308,33 +308,69 @@ def _spawn_ranks(args) -> int:
     return subprocess.call(cmd)
 
 
-def run_dry(args) -> int:
-    """``--dry-run``: the multi-rank plumbing without a GPU (gloo on CPU): rendezvous, the EP count
-    exchange of the dispatch plan, barrier + max-over-ranks timing, rank 0's JSON line."""
+def ep_world1_probe(weights, x, lg, T, tdt, dev, single):
+    """The expert-parallel layer (NCCL all-gather dispatch / reduce-scatter combine, captured in a CUDA
+    graph) on a one-rank NCCL group, timed like the single-GPU graph it is compared with."""
     import torch
     import torch.distributed as dist
-    from paper_2504_16214_b200.moe.ep import plan_dispatch
+    from paper_2504_16214_b200.moe import FusedMoEGraph
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 2000))
+        dist.init_process_group("nccl", device_id=dev, rank=0, world_size=1)
+    g = FusedMoEGraph(weights, T, K_DS, "softmax", True, tdt, dev, x=x, router_logits=lg, ep_group=dist.group.WORLD)
+
+    def timed(graph, n=20):
+        for _ in range(3):
+            graph()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(n):
+            graph()
+        b.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / n
+    y_ep = g(x, lg).clone()
+    y_1 = single(x, lg).clone()
+    ms_ep, ms_1 = timed(g), timed(single)
+    single.x.copy_(x)
+    single.logits.copy_(lg)
+    return {"ms": round(ms_ep, 4), "single_gpu_ms": round(ms_1, 4), "ratio": round(ms_ep / ms_1, 4),
+            "equal_to_single_gpu": bool(torch.equal(y_ep, y_1)),
+            "path": "graphed EP layer on a 1-rank NCCL group (all-gather, localize, local experts, "
+                    "fp32 partial combine, reduce-scatter, rounding) vs the graphed single-GPU layer"}
+
+
+def run_dry(args) -> int:
+    """``--dry-run``: the multi-rank plumbing without a GPU (gloo on CPU): rendezvous, the EP exchange
+    shapes (all-gather of every rank's tokens and routing, reduce of the fp32 partials), barrier +
+    max-over-ranks timing, rank 0's JSON line."""
+    import torch
+    import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     e_local = E_DS // world
     _, lg = bench_inputs(args.tokens, rank, torch.float16)
-    ids = torch.topk(lg, K_DS, dim=1).indices
-    counts = torch.bincount(ids.flatten(), minlength=E_DS).to(torch.int32)
+    ids = torch.topk(lg, K_DS, dim=1).indices.to(torch.int32)
     dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        plan = plan_dispatch(counts, world)
+        parts = [torch.empty_like(ids) for _ in range(world)]
+        dist.all_gather(parts, ids)
+        ids_all = torch.cat(parts) - rank * e_local
+        local = ((ids_all >= 0) & (ids_all < e_local)).sum()
+        dist.all_reduce(local)
     dist.barrier()
     t = torch.tensor([time.perf_counter() - t0])
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    recv = torch.tensor([sum(plan.recv_splits)])
-    dist.all_reduce(recv)
     if rank == 0:
         print(json.dumps({"metric": METRIC, "value": None, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
                           "warmup": args.warmup, "ms_per_step": round(1e3 * float(t) / args.steps, 4),
                           "dry_run": True, "backend": "gloo (CPU)", "experts_per_rank": e_local,
-                          "rows_exchanged_per_step": int(recv), "higher_is_better": True, "scaling": "weak"}))
+                          "tokens_gathered_per_rank": world * args.tokens, "pairs_routed_per_step": int(local),
+                          "higher_is_better": True, "scaling": "weak"}))
     dist.destroy_process_group()
     return 0
 
@@ -458,7 +494,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of a CUDA graph")
     ap.add_argument("--ep", action="store_true",
-                    help="run the expert-parallel path (NCCL process group, all-to-all) even on one GPU")
+                    help="run the expert-parallel path (NCCL all-gather / reduce-scatter) even on one GPU")
     ap.add_argument("--dry-run", action="store_true",
                     help="no GPU: exercise the N-rank launch, count exchange and timing plumbing over gloo")
     args = ap.parse_args()
@@ -505,12 +541,13 @@ def main():
     def step(timer=None, xx=x, ll=lg):
         return fused_moe_w4a16(xx, ll, weights, K_DS, "softmax", True, ep_group=group, timer=timer)
 
-    # single GPU: the whole layer step captured once in a CUDA graph (decode-serving mode; every
-    # kernel still runs per replay). EP (N > 1) reads split sizes on the host, so it runs eagerly.
+    # the whole layer step captured once in a CUDA graph (decode-serving mode; every kernel still runs
+    # per replay). Expert parallel too: its exchange is an NCCL all-gather + reduce-scatter of fixed
+    # shapes (no host read-back), captured inside the graph.
     graphed = None
-    if group is None and not args.no_graph:
+    if not args.no_graph:
         from paper_2504_16214_b200.moe import FusedMoEGraph
-        graphed = FusedMoEGraph(weights, T, K_DS, "softmax", True, tdt, dev, x=x, router_logits=lg)
+        graphed = FusedMoEGraph(weights, T, K_DS, "softmax", True, tdt, dev, x=x, router_logits=lg, ep_group=group)
 
     def timed_step(xx=x, ll=lg):
         if graphed is not None:
@@ -643,7 +680,7 @@ def main():
     pipe = None
     if graphed is not None:  # serving loop: H2D of step i+1 and D2H of step i overlap step i's layer
         from paper_2504_16214_b200.moe import FusedMoEPipeline
-        pipe = FusedMoEPipeline(weights, T, K_DS, "softmax", True, tdt, dev, x=x, router_logits=lg)
+        pipe = FusedMoEPipeline(weights, T, K_DS, "softmax", True, tdt, dev, x=x, router_logits=lg, ep_group=group)
 
     def e2e_steps(n):
         if pipe is not None:
@@ -705,8 +742,11 @@ def main():
             del xs, ls, gs_
 
     configs = None
+    ep1 = None
     if world == 1 and not args.no_sweep and group is None:
         configs = other_configs(dev, hbm_peak, tc_peak)
+        if graphed is not None:
+            ep1 = ep_world1_probe(weights, x, lg, T, tdt, dev, graphed)
 
     cpu = None
     synth = None
@@ -752,6 +792,7 @@ def main():
             "kernel_ms": {n: round(timer.mean_ms(n), 4) for n in timer.events},
             "other_configs": configs,
             "layout_synthesis_cpu": synth,
+            "ep_world1": ep1,
             # last, so a truncated tail of the line still shows the DeepSeek-R1 decode .. prefill sweep
             "sweep_ds_r1": _columns(sweep),
         }

@@ -18,10 +18,15 @@
  *   GEMM:     w4a16_grouped_gemm                       per-expert X_e * W_e^T, optional fused SiLU*up
  *             w4a16_grouped_gemm_gather                same, X rows gathered by the producer (TMA gather4)
  *   combine:  w4a16_moe_combine                        y[t] = sum_j w[t,j] * Y_perm[pos(t,j)]
- *   EP:       w4a16_ep_local_order                     receiver-side local-expert order of the rows an
+ *   combine:  w4a16_moe_combine_f32                    same, fp32 unrounded (expert-parallel partials)
+ *   EP:       w4a16_ep_dispatch / w4a16_ep_combine     all-gather dispatch / reduce-scatter combine over an
+ *                                                      opaque NCCL communicator (w4a16_ep_comm_*)
+ *             w4a16_ep_localize                        global -> local expert ids of the gathered batch
+ *             w4a16_moe_forward_ep                     the whole expert-parallel layer, one call
+ *             w4a16_ep_local_order                     receiver-side local-expert order of the rows an
  *                                                      all-to-all delivered (grouped by source rank)
  *   weights:  w4a16_repack_awq, w4a16_dequant (test/oracle aid), w4a16_packed_bytes
- *   driver:   w4a16_moe_forward                        the whole layer, one call, caller workspace
+ *   driver:   w4a16_moe_forward(_f32)                  the whole layer, one call, caller workspace
  *
  * Conventions: raw device pointers, int64_t extents, cudaStream_t (pass 0 for the legacy stream);
  * every function is stream-ordered, returns an int status (0 ok, < 0 error, never throws), performs
@@ -46,7 +51,8 @@ enum {
   W4_ERR_DTYPE = -3,  /* unsupported activation dtype */
   W4_ERR_GROUP = -4,  /* unsupported quantisation group size (only 128) */
   W4_ERR_CUDA = -5,   /* launch / driver failure (cudaGetLastError() has details) */
-  W4_ERR_WORKSPACE = -6
+  W4_ERR_WORKSPACE = -6,
+  W4_ERR_NCCL = -7    /* NCCL missing (libnccl.so.2 not loadable) or a collective failed */
 };
 
 enum { W4_DTYPE_F16 = 0, W4_DTYPE_BF16 = 1 };
@@ -137,6 +143,11 @@ int64_t w4a16_group_sums_ld(int64_t rows);
 int w4a16_moe_combine(const void* y_perm, int64_t T, int64_t H, int64_t topk, const int32_t* pair_pos,
                       const float* topk_weights, int dtype, void* y, cudaStream_t stream);
 
+/* Same as w4a16_moe_combine, but y is float [T][H] and the fp32 sums are NOT rounded (the partial a
+ * reduction across expert-parallel ranks adds up before the one rounding, w4a16_ep_combine). */
+int w4a16_moe_combine_f32(const void* y_perm, int64_t T, int64_t H, int64_t topk, const int32_t* pair_pos,
+                          const float* topk_weights, int dtype, float* y, cudaStream_t stream);
+
 /* ---- grouped GEMM ----------------------------------------------------------------------------- */
 /* For each expert e: out[off_e + m][n] = act( sum_k X[off_e + m][k] * W_e[n][k] ), m < counts[e].
  * x [rows][K]; wblocks packed (parts = gated ? 2 : 1, n_rows = gated ? 2*n_out : n_out);
@@ -186,6 +197,52 @@ int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E,
                       const int32_t* topk_ids, const float* topk_weights, const uint8_t* w13,
                       const uint8_t* w2, int dtype, void* y, void* workspace, int64_t workspace_bytes,
                       cudaStream_t stream);
+
+/* Same as w4a16_moe_forward with the fp32, unrounded combine (w4a16_moe_combine_f32): y float [T][H]. */
+int w4a16_moe_forward_f32(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, int64_t topk,
+                          const int32_t* topk_ids, const float* topk_weights, const uint8_t* w13,
+                          const uint8_t* w2, int dtype, float* y, void* workspace, int64_t workspace_bytes,
+                          cudaStream_t stream);
+
+/* ---- expert parallelism (NCCL over NVLink / NVSwitch) ------------------------------------------ */
+/* Experts shard contiguously: rank r owns global experts [r * E_local, (r + 1) * E_local). Dispatch is
+ * an all-gather of every rank's tokens and routing, combine a reduce-scatter of fp32 partial sums:
+ * fixed shapes, no host synchronisation, CUDA-graph capturable. Every rank passes the same T (pad
+ * with rows whose topk_ids are -1). NCCL is loaded at run time (libnccl.so.2); w4a16_ep_available()
+ * says whether it was found. The communicator is opaque. */
+typedef struct w4a16_ep_comm w4a16_ep_comm;
+int w4a16_ep_available(void);
+/* 128-byte NCCL unique id: make it on one rank, hand it to every rank (any host channel). */
+int w4a16_ep_unique_id(void* id);
+/* Collective over `world` ranks (one per GPU, each with its device current). */
+int w4a16_ep_comm_init(const void* id, int rank, int world, w4a16_ep_comm** comm);
+/* Borrow an existing ncclComm_t (not destroyed by w4a16_ep_comm_destroy). */
+int w4a16_ep_comm_wrap(void* nccl_comm, w4a16_ep_comm** comm);
+int w4a16_ep_comm_destroy(w4a16_ep_comm* comm);
+int w4a16_ep_comm_rank(const w4a16_ep_comm* comm);
+int w4a16_ep_comm_size(const w4a16_ep_comm* comm);
+
+/* x [T][H], topk_ids [T][k] (GLOBAL expert ids), topk_weights [T][k] of every rank ->
+ * x_all [world*T][H], ids_all / w_all [world*T][k] (rank r's rows at r*T). */
+int w4a16_ep_dispatch(w4a16_ep_comm* comm, const void* x, const int32_t* topk_ids, const float* topk_weights,
+                      int64_t T, int64_t H, int64_t topk, int dtype, void* x_all, int32_t* ids_all, float* w_all,
+                      cudaStream_t stream);
+/* ids_local[i] = ids[i] - expert_base when that is in [0, local_experts), else -1. */
+int w4a16_ep_localize(const int32_t* ids, int64_t n, int64_t expert_base, int64_t local_experts, int32_t* ids_local,
+                      cudaStream_t stream);
+/* partial float [world*T][H] (this rank's experts' weighted sums for the whole node batch) ->
+ * reduce-scatter (sum over ranks, fp32) into reduced float [T][H] -> y [T][H] act dtype (one rounding). */
+int w4a16_ep_combine(w4a16_ep_comm* comm, const float* partial, int64_t T, int64_t H, int dtype, float* reduced,
+                     void* y, cudaStream_t stream);
+
+/* The whole expert-parallel layer: dispatch -> localize -> w4a16_moe_forward_f32 on this rank's shard
+ * (w13 / w2 packed for local_experts) -> combine. */
+int64_t w4a16_moe_ep_workspace_bytes(int64_t T, int64_t world, int64_t topk, int64_t local_experts, int64_t H,
+                                     int64_t I);
+int w4a16_moe_forward_ep(w4a16_ep_comm* comm, const void* x, int64_t T, int64_t H, int64_t I, int64_t local_experts,
+                         int64_t topk, const int32_t* topk_ids, const float* topk_weights, const uint8_t* w13,
+                         const uint8_t* w2, int dtype, void* y, void* workspace, int64_t workspace_bytes,
+                         cudaStream_t stream);
 
 #ifdef __cplusplus
 }

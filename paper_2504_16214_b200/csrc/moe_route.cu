@@ -603,10 +603,12 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
 
 // grid (T, H/8 / blockDim): each thread owns one 16-byte vector of one token and accumulates the k
 // expert rows in slot order in fp32 (enough CTAs to saturate HBM even at decode token counts).
-template <bool kBF16>
+// kF32Out: write the fp32 sums unrounded (y is float [T][H]) -- the per-rank partial that expert
+// parallelism reduces across ranks before the one rounding to the activation dtype.
+template <bool kBF16, bool kF32Out = false>
 __global__ void moe_combine_kernel(const uint4* __restrict__ yp, int64_t hv, int topk,
                                    const int32_t* __restrict__ pair_pos, const float* __restrict__ wts,
-                                   uint4* __restrict__ y) {
+                                   void* __restrict__ y) {
   griddep_wait();  // PDL: inputs written by the previous kernel in the stream
   const int64_t t = blockIdx.x;
   const int64_t i = static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x;
@@ -627,7 +629,13 @@ __global__ void moe_combine_kernel(const uint4* __restrict__ yp, int64_t hv, int
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = fmaf(wt[j], f[q], acc[q]);
   }
-  y[t * hv + i] = pack8<kBF16>(acc);
+  if constexpr (kF32Out) {
+    float4* o = static_cast<float4*>(y) + 2 * (t * hv + i);
+    o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  } else {
+    static_cast<uint4*>(y)[t * hv + i] = pack8<kBF16>(acc);
+  }
 }
 
 }  // namespace w4
@@ -820,22 +828,39 @@ int w4a16_group_sums(const void* x, int64_t rows, int64_t K, const int32_t* row_
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
 
-int w4a16_moe_combine(const void* y_perm, int64_t T, int64_t H, int64_t topk, const int32_t* pair_pos,
-                      const float* topk_weights, int dtype, void* y, cudaStream_t stream) {
+}  // extern "C"
+
+namespace {
+template <bool kF32Out>
+int combine_launch(const void* y_perm, int64_t T, int64_t H, int64_t topk, const int32_t* pair_pos,
+                   const float* topk_weights, int dtype, void* y, cudaStream_t stream) {
   if (!y_perm || !pair_pos || !topk_weights || !y) return W4_ERR_ARG;
   if (H <= 0 || H % 8 || topk <= 0 || topk > 32) return W4_ERR_SHAPE;
   if (T <= 0) return W4_OK;
   const int thr = 128;
   const dim3 grid(static_cast<unsigned>(T), static_cast<unsigned>((H / 8 + thr - 1) / thr));
   if (dtype == W4_DTYPE_BF16)
-    launch_pdl(moe_combine_kernel<true>, grid, thr, 0, stream, static_cast<const uint4*>(y_perm), H / 8, (int)topk,
-                                                       pair_pos, topk_weights, static_cast<uint4*>(y));
+    launch_pdl(moe_combine_kernel<true, kF32Out>, grid, thr, 0, stream, static_cast<const uint4*>(y_perm), H / 8,
+               (int)topk, pair_pos, topk_weights, y);
   else if (dtype == W4_DTYPE_F16)
-    launch_pdl(moe_combine_kernel<false>, grid, thr, 0, stream, static_cast<const uint4*>(y_perm), H / 8, (int)topk,
-                                                        pair_pos, topk_weights, static_cast<uint4*>(y));
+    launch_pdl(moe_combine_kernel<false, kF32Out>, grid, thr, 0, stream, static_cast<const uint4*>(y_perm), H / 8,
+               (int)topk, pair_pos, topk_weights, y);
   else
     return W4_ERR_DTYPE;
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
+}
+}  // namespace
+
+extern "C" {
+
+int w4a16_moe_combine(const void* y_perm, int64_t T, int64_t H, int64_t topk, const int32_t* pair_pos,
+                      const float* topk_weights, int dtype, void* y, cudaStream_t stream) {
+  return combine_launch<false>(y_perm, T, H, topk, pair_pos, topk_weights, dtype, y, stream);
+}
+
+int w4a16_moe_combine_f32(const void* y_perm, int64_t T, int64_t H, int64_t topk, const int32_t* pair_pos,
+                          const float* topk_weights, int dtype, float* y, cudaStream_t stream) {
+  return combine_launch<true>(y_perm, T, H, topk, pair_pos, topk_weights, dtype, y, stream);
 }
 
 int64_t w4a16_moe_workspace_bytes(int64_t T, int64_t topk, int64_t E, int64_t H, int64_t I) {
@@ -846,10 +871,13 @@ int64_t w4a16_moe_workspace_bytes(int64_t T, int64_t topk, int64_t E, int64_t H,
          align256(w4a16_moe_permute_ws_bytes(P, E)) + align256(splitk_bytes(P, E, H, I));
 }
 
-int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, int64_t topk,
-                      const int32_t* topk_ids, const float* topk_weights, const uint8_t* w13,
-                      const uint8_t* w2, int dtype, void* y, void* workspace, int64_t workspace_bytes,
-                      cudaStream_t stream) {
+}  // extern "C"
+
+namespace {
+int moe_forward_impl(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, int64_t topk,
+                     const int32_t* topk_ids, const float* topk_weights, const uint8_t* w13, const uint8_t* w2,
+                     int dtype, void* y, bool f32_out, void* workspace, int64_t workspace_bytes,
+                     cudaStream_t stream) {
   if (!x || !topk_ids || !topk_weights || !w13 || !w2 || !y || !workspace) return W4_ERR_ARG;
   if (workspace_bytes < w4a16_moe_workspace_bytes(T, topk, E, H, I)) return W4_ERR_WORKSPACE;
   if (T <= 0) return W4_OK;
@@ -886,7 +914,27 @@ int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E,
   if ((rc = w4a16_grouped_gemm_ws(hp, P, I, w2, E, H, 0, counts, offsets, decode ? hsum : nullptr, nullptr, nullptr,
                                   yp, dtype, nt, kws, kws_bytes, stream)))
     return rc;
-  return w4a16_moe_combine(yp, T, H, topk, pos, topk_weights, dtype, y, stream);
+  return f32_out ? w4a16_moe_combine_f32(yp, T, H, topk, pos, topk_weights, dtype, static_cast<float*>(y), stream)
+                 : w4a16_moe_combine(yp, T, H, topk, pos, topk_weights, dtype, y, stream);
+}
+}  // namespace
+
+extern "C" {
+
+int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, int64_t topk,
+                      const int32_t* topk_ids, const float* topk_weights, const uint8_t* w13,
+                      const uint8_t* w2, int dtype, void* y, void* workspace, int64_t workspace_bytes,
+                      cudaStream_t stream) {
+  return moe_forward_impl(x, T, H, I, E, topk, topk_ids, topk_weights, w13, w2, dtype, y, false, workspace,
+                          workspace_bytes, stream);
+}
+
+int w4a16_moe_forward_f32(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, int64_t topk,
+                          const int32_t* topk_ids, const float* topk_weights, const uint8_t* w13,
+                          const uint8_t* w2, int dtype, float* y, void* workspace, int64_t workspace_bytes,
+                          cudaStream_t stream) {
+  return moe_forward_impl(x, T, H, I, E, topk, topk_ids, topk_weights, w13, w2, dtype, y, true, workspace,
+                          workspace_bytes, stream);
 }
 
 }  // extern "C"

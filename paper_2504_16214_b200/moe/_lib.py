@@ -19,6 +19,7 @@ ERRORS = {
     -4: "W4_ERR_GROUP (only group size 128 is supported)",
     -5: "W4_ERR_CUDA (launch / driver failure)",
     -6: "W4_ERR_WORKSPACE (workspace too small)",
+    -7: "W4_ERR_NCCL (NCCL not loadable, or a collective failed)",
 }
 DTYPE_F16, DTYPE_BF16 = 0, 1
 SCORE_SOFTMAX, SCORE_SIGMOID = 0, 1
@@ -59,6 +60,20 @@ SIGNATURES = {
     "w4a16_grouped_gemm_ws_bytes": (_i64, [_i64, _i64, _i64, _i64, _i, _i]),
     "w4a16_moe_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64]),
     "w4a16_moe_forward": (_i, [_p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _i, _p, _p, _i64, _p]),
+    "w4a16_moe_combine_f32": (_i, [_p, _i64, _i64, _i64, _p, _p, _i, _p, _p]),
+    "w4a16_moe_forward_f32": (_i, [_p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _i, _p, _p, _i64, _p]),
+    "w4a16_ep_available": (_i, []),
+    "w4a16_ep_unique_id": (_i, [_p]),
+    "w4a16_ep_comm_init": (_i, [_p, _i, _i, _p]),
+    "w4a16_ep_comm_wrap": (_i, [_p, _p]),
+    "w4a16_ep_comm_destroy": (_i, [_p]),
+    "w4a16_ep_comm_rank": (_i, [_p]),
+    "w4a16_ep_comm_size": (_i, [_p]),
+    "w4a16_ep_dispatch": (_i, [_p, _p, _p, _p, _i64, _i64, _i64, _i, _p, _p, _p, _p]),
+    "w4a16_ep_localize": (_i, [_p, _i64, _i64, _i64, _p, _p]),
+    "w4a16_ep_combine": (_i, [_p, _p, _i64, _i64, _i, _p, _p, _p]),
+    "w4a16_moe_ep_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64, _i64]),
+    "w4a16_moe_forward_ep": (_i, [_p, _p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _i, _p, _p, _i64, _p]),
 }
 # debug aids exported by the library but not part of the public header
 DEBUG_SIGNATURES = {

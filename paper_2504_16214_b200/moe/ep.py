@@ -1,138 +1,106 @@
-"""Expert parallelism: experts sharded contiguously across the ranks of one node, tokens exchanged
-by all-to-all(v) over NCCL (NVLink / NVSwitch) for dispatch and combine.
+"""Expert parallelism: experts sharded contiguously across the ranks of one node; tokens reach them
+by an all-gather and come back by a reduce-scatter, both NCCL collectives over NVLink / NVSwitch run
+by this library (``csrc/moe_ep.cu``, C ABI ``w4a16_ep_*``) on its own communicator.
 
-Rank r owns global experts [r*E_l, (r+1)*E_l). Each rank routes its own tokens, then:
+Rank r owns global experts [r*E_l, (r+1)*E_l). With T tokens on every rank:
 
-  1. permute its (token, slot) pairs by *global* expert (stable counting sort, CUDA) -- this also
-     groups them by destination rank, since experts are contiguous per rank;
-  2. gather the rows (CUDA) into the send buffer;
-  3. exchange per-expert counts (all_to_all_single, int32 [world * E_l]) and read the split sizes
-     back to the host (the one host synchronisation EP needs: NCCL all-to-all-v takes host splits);
-  4. all_to_all_single the rows (dispatch);
-  5. received rows arrive grouped by (source rank, local expert); permute them by local expert
-     (CUDA) and run the two grouped GEMMs on the local shard;
-  6. un-permute back to arrival order, all_to_all_single back (combine), and reduce the k expert
-     outputs of every token with its routing weights (CUDA).
+  1. dispatch: all-gather x [T, H], topk_ids and topk_weights [T, k] -> the node batch [world*T];
+  2. localize: ids outside this rank's shard become -1 (the permutation drops them);
+  3. the single-GPU layer (permute -> gather -> gate/up -> down -> combine) on the local pairs, with
+     the combine's fp32 sums left unrounded: this rank's partial output for every node token;
+  4. combine: reduce-scatter the fp32 partials (sum over ranks) and round once -> [T, H].
 
-The only collective is the exchange step itself. ``backend`` supplies the primitive
-ops; the product path uses the CUDA ops (:mod:`.ops`) -- tests inject a CPU backend to exercise the
-exchange plumbing on ``gloo`` with world_size 2.
+Every shape is fixed by (world, T, k, H), so nothing is read back to the host and the whole step can
+be captured in a CUDA graph (the all-to-all(v) alternative needs its split sizes on the host). The
+traffic per rank -- world*T*H activations in, world*T*H fp32 out -- matches an all-to-all of the
+T*k routed rows when k = world (DS-R1 top-8 on 8 GPUs), and NCCL runs both collectives with in-switch
+multicast / reduction (NVLS) on NVSwitch systems. Every rank must pass the same T.
+
+``exchange`` supplies the collectives and the local layer; the product path is :class:`NcclExchange`,
+the tests inject a CPU exchange over ``gloo`` (world size 2 and 4) to check the decomposition.
 """
 from __future__ import annotations
-
-from dataclasses import dataclass
 
 import torch
 import torch.distributed as dist
 
-from . import ops as cuda_ops
+from . import ops
 
 
-@dataclass
-class DispatchPlan:
-    send_splits: list[int]      # rows this rank sends to each rank
-    recv_splits: list[int]      # rows this rank receives from each rank
-    recv_counts: torch.Tensor   # [world, E_l] int32: rows per (source rank, local expert)
+class EPComm:
+    """This library's NCCL communicator for one torch.distributed group (created once per group,
+    collectively: the group's first rank makes the unique id, the group broadcasts it)."""
+
+    _by_group: dict = {}
+
+    def __init__(self, group=None):
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        uid = [ops.ep_unique_id() if self.rank == 0 else None]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(uid, src=src, group=group)
+        self.handle = ops.ep_comm_init(uid[0], self.rank, self.world)
+
+    @classmethod
+    def of(cls, group=None) -> "EPComm":
+        key = id(group) if group is not None else None
+        if key not in cls._by_group:
+            cls._by_group[key] = cls(group)
+        return cls._by_group[key]
 
 
-def plan_dispatch(global_counts: torch.Tensor, world: int, group=None) -> DispatchPlan:
-    """global_counts [world * E_l] int32 (rows this rank routes to each global expert)."""
-    e_local = global_counts.numel() // world
-    recv = torch.empty_like(global_counts)
-    dist.all_to_all_single(recv, global_counts.contiguous(), group=group)
-    send_splits = global_counts.view(world, e_local).sum(dim=1)
-    both = torch.cat([send_splits, recv.view(world, e_local).sum(dim=1)]).cpu().tolist()
-    return DispatchPlan(both[:world], both[world:], recv.view(world, e_local))
+class NcclExchange:
+    """Product path: all-gather / reduce-scatter through the library's NCCL communicator."""
+
+    def __init__(self, group=None):
+        self.comm = EPComm.of(group)
+        self.world, self.rank = self.comm.world, self.comm.rank
+
+    def dispatch(self, x, topk_ids, topk_weights):
+        return ops.ep_dispatch(self.comm.handle, self.world, x, topk_ids, topk_weights)
+
+    @staticmethod
+    def localize(ids_all, base, local_experts):
+        return ops.ep_localize(ids_all, base, local_experts)
+
+    @staticmethod
+    def experts(x_all, weights, w_all, ids_local, ntok=0, timer=None):
+        from .layer import moe_w4a16
+        return moe_w4a16(x_all, weights, w_all, ids_local, ntok=ntok, timer=timer, f32_out=True)
+
+    def combine(self, partial, T, dtype):
+        return ops.ep_combine(self.comm.handle, partial, T, dtype)
+
+
+def moe_w4a16_ep(x: torch.Tensor, weights, topk_weights: torch.Tensor, topk_ids: torch.Tensor, group=None,
+                 ntok: int = 0, timer=None, exchange=None) -> torch.Tensor:
+    """Expert-parallel W4A16 MoE. ``weights`` holds this rank's contiguous expert shard;
+    ``topk_ids`` are global expert ids; every rank passes the same number of tokens."""
+    from .layer import _NOTIMER
+    tm = timer or _NOTIMER
+    ex = exchange or NcclExchange(group)
+    T = x.shape[0]
+    if T == 0:
+        return x.new_empty((0, x.shape[1]))
+    e_local = weights.num_experts
+    with tm.span("dispatch"):
+        x_all, ids_all, w_all = ex.dispatch(x.contiguous(), topk_ids.to(torch.int32).contiguous(),
+                                            topk_weights.to(torch.float32).contiguous())
+    with tm.span("localize"):
+        ids_local = ex.localize(ids_all, ex.rank * e_local, e_local)
+    partial = ex.experts(x_all, weights, w_all, ids_local, ntok, timer)
+    with tm.span("ep_combine"):
+        return ex.combine(partial, T, x.dtype)
 
 
 def local_expert_ids(recv_counts: torch.Tensor, n_recv: int | None = None) -> torch.Tensor:
-    """Local expert id of every received row (rows arrive grouped by source, then by expert).
-    ``n_recv`` (the host-known total) avoids a device->host synchronisation."""
+    """Local expert id of every row an all-to-all delivered grouped by (source rank, local expert)
+    with counts ``recv_counts`` [world, E_l] -- the rule the C entry ``w4a16_ep_local_order`` (kept
+    for all-to-all based callers) orders by."""
     world, e_local = recv_counts.shape
     experts = torch.arange(e_local, device=recv_counts.device, dtype=torch.int32).repeat(world)
     return torch.repeat_interleave(experts, recv_counts.reshape(-1).to(torch.int64),
                                    output_size=n_recv).to(torch.int32)
-
-
-class CudaBackend:
-    permute = staticmethod(cuda_ops.moe_permute)
-    local_order = staticmethod(cuda_ops.ep_local_order)  # one kernel: receiver-side local expert order
-    scatter_out = True  # the down GEMM writes arrival order directly
-    gather = staticmethod(cuda_ops.moe_gather)
-    combine = staticmethod(cuda_ops.moe_combine)
-
-    @staticmethod
-    def experts(x, weights, counts, offsets, ntok, timer=None, out_rows=None):
-        """Both grouped GEMMs; with ``out_rows`` the down projection writes its rows scattered
-        through it (straight back to arrival order)."""
-        from .layer import _NOTIMER
-        tm = timer or _NOTIMER
-        E, H, I = weights.num_experts, weights.hidden, weights.inter
-        nt = ntok or cuda_ops.pick_ntok(x.shape[0], E)
-        from .layer import _DECODE_MAX_NTOK
-        decode = nt <= _DECODE_MAX_NTOK
-        xs = hs = None
-        if decode:
-            with tm.span("sums_x"):
-                xs = cuda_ops.group_sums(x)
-        with tm.span("gemm_gate_up"):
-            h = cuda_ops.grouped_gemm(x, weights.w13.blocks, E, I, True, counts, offsets, nt, xsum=xs)
-        if decode:
-            with tm.span("sums_h"):
-                hs = cuda_ops.group_sums(h)
-        with tm.span("gemm_down"):
-            return cuda_ops.grouped_gemm(h, weights.w2.blocks, E, H, False, counts, offsets, nt, xsum=hs,
-                                         out_rows=out_rows)
-
-
-def moe_w4a16_ep(x: torch.Tensor, weights, topk_weights: torch.Tensor, topk_ids: torch.Tensor, group=None,
-                 ntok: int = 0, timer=None, backend=CudaBackend) -> torch.Tensor:
-    """Expert-parallel W4A16 MoE. ``weights`` holds this rank's contiguous expert shard;
-    ``topk_ids`` are global expert ids."""
-    world = dist.get_world_size(group)
-    T, H = x.shape
-    k = topk_ids.shape[1]
-    e_local = weights.num_experts
-    e_global = e_local * world
-    topk_ids = topk_ids.to(torch.int32).contiguous()
-    topk_weights = topk_weights.to(torch.float32).contiguous()
-
-    from .layer import _NOTIMER
-    tm = timer or _NOTIMER
-    # 1-2: group pairs by destination (global expert order) and pack rows
-    with tm.span("permute"):
-        g_counts, g_offsets, sorted_pairs, pair_pos = backend.permute(topk_ids, e_global)
-    with tm.span("gather"):
-        # row_limit = the number of valid pairs (ids < 0 or >= e_global are dropped by the permutation
-        # and leave the tail of sorted_pairs unwritten): the gather never reads those entries
-        send_x = backend.gather(x.contiguous(), sorted_pairs, k, T * k, g_offsets[e_global:])
-    # 3: counts exchange + host splits
-    plan = plan_dispatch(g_counts, world, group)
-    n_recv = sum(plan.recv_splits)
-    # 4: dispatch
-    recv_x = x.new_empty((n_recv, H))
-    dist.all_to_all_single(recv_x, send_x, plan.recv_splits, plan.send_splits, group=group)
-    # 5: local expert order + grouped GEMMs
-    if hasattr(backend, "local_order"):
-        with tm.span("local_order"):
-            l_counts, l_offsets, l_sorted, l_pos = backend.local_order(plan.recv_counts, n_recv)
-    else:  # generic: ids of the received rows, then the stable permutation
-        lid = local_expert_ids(plan.recv_counts, n_recv)
-        l_counts, l_offsets, l_sorted, l_pos = backend.permute(lid, e_local)
-    with tm.span("gather_local"):
-        xl = backend.gather(recv_x, l_sorted, 1, n_recv) if n_recv else recv_x
-    # 6: the down GEMM scatters its rows straight back to arrival order; combine exchange, reduction
-    if not n_recv:
-        y_recv = recv_x
-    elif getattr(backend, "scatter_out", False):
-        y_recv = backend.experts(xl, weights, l_counts, l_offsets, ntok, timer, out_rows=l_sorted)
-    else:
-        yl = backend.experts(xl, weights, l_counts, l_offsets, ntok, timer)
-        y_recv = backend.gather(yl, l_pos, 1, n_recv)
-    y_back = x.new_empty((T * k, H))
-    dist.all_to_all_single(y_back, y_recv, plan.send_splits, plan.recv_splits, group=group)
-    with tm.span("combine"):
-        return backend.combine(y_back, pair_pos, topk_weights)
 
 
 def shard_with_shared(weights, num_shared: int, world: int, rank: int):

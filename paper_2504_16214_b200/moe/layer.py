@@ -23,7 +23,7 @@ import threading
 import torch
 
 from . import ops
-from .weights import MoEWeights
+from .weights import MoEWeights, pack_moe_awq
 
 
 def select_experts(router_logits: torch.Tensor, top_k: int, scoring: str = "softmax",
@@ -153,18 +153,47 @@ class _NoTimer:
 _NOTIMER = _NoTimer()
 
 
-def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, topk_ids: torch.Tensor,
-              ep_group=None, ntok: int = 0, timer: KernelTimer | None = None, perm=None) -> torch.Tensor:
+_AWQ_CACHE: dict = {}
+
+
+def _packed_from_awq(w13_q, w13_s, w13_z, w2_q, w2_s, w2_z, group_size):
+    """Raw AWQ tensors -> MoEWeights, repacked once per (tensor storage, version) and cached (the
+    vLLM process_weights_after_loading step, done lazily)."""
+    key = tuple((t.data_ptr(), t._version, tuple(t.shape)) for t in (w13_q, w13_s, w13_z, w2_q, w2_s, w2_z))
+    hit = _AWQ_CACHE.get(key)
+    if hit is None:
+        if len(_AWQ_CACHE) > 64:
+            _AWQ_CACHE.clear()
+        hit = _AWQ_CACHE[key] = pack_moe_awq(w13_q, w13_s, w13_z, w2_q, w2_s, w2_z, group_size)
+    return hit
+
+
+def moe_w4a16(x: torch.Tensor, weights, topk_weights: torch.Tensor, topk_ids: torch.Tensor = None, *awq_rest,
+              ep_group=None, ntok: int = 0, timer: KernelTimer | None = None, perm=None, f32_out: bool = False,
+              group_size: int = 128) -> torch.Tensor:
     """y[t] = sum_j topk_weights[t, j] * Expert_{topk_ids[t, j]}(x[t]) for the W4A16 SwiGLU experts.
 
-    ``x`` [T, H] fp16/bf16 on CUDA; ``topk_ids`` int32 [T, k]; ``topk_weights`` fp32 [T, k]."""
+    ``x`` [T, H] fp16/bf16 on CUDA; ``topk_ids`` int32 [T, k]; ``topk_weights`` fp32 [T, k].
+    ``weights`` is a :class:`MoEWeights` -- or, the raw-AWQ form of SURVEY.md 8(b),
+    ``moe_w4a16(x, w13_q, w13_s, w13_z, w2_q, w2_s, w2_z, topk_weights, topk_ids, group_size=128,
+    ep_group=None)`` with vLLM's AWQ MoE tensors (qweight [E, K, N/8] int32, scales [E, K/G, N],
+    qzeros [E, K/G, N/8] int32), repacked on first use. ``f32_out``: return the fp32 sums unrounded
+    (the expert-parallel partial)."""
+    if isinstance(weights, torch.Tensor):
+        if len(awq_rest) != 5:
+            raise TypeError("moe_w4a16(x, w13_q, w13_s, w13_z, w2_q, w2_s, w2_z, topk_weights, topk_ids, ...)")
+        w2_q, w2_s, w2_z, topk_weights_, topk_ids_ = awq_rest
+        weights = _packed_from_awq(weights, topk_weights, topk_ids, w2_q, w2_s, w2_z, group_size)
+        topk_weights, topk_ids = topk_weights_, topk_ids_
+    elif awq_rest or topk_ids is None:
+        raise TypeError("moe_w4a16(x, weights, topk_weights, topk_ids, ...)")
     if ep_group is not None:
         from .ep import moe_w4a16_ep
         return moe_w4a16_ep(x, weights, topk_weights, topk_ids, ep_group, ntok=ntok, timer=timer)
     tm = timer or _NOTIMER
     T, H = x.shape
     if T == 0:  # empty batch (single GPU): nothing to launch
-        return x.new_empty((0, H))
+        return x.new_empty((0, H), dtype=torch.float32 if f32_out else x.dtype)
     if H != weights.hidden:
         raise ValueError(f"hidden size {H} != packed weights' {weights.hidden}")
     if x.dtype != weights.w13.dtype:
@@ -226,7 +255,7 @@ def moe_w4a16(x: torch.Tensor, weights: MoEWeights, topk_weights: torch.Tensor, 
         yp = ops.grouped_gemm(h, weights.w2.blocks, E, H, False, counts, offsets, nt,
                               out=_ws.get("yp", (P, H), x.dtype, dev), xsum=hs, workspace=splitk_ws(I, H, False))
     with tm.span("combine"):
-        return ops.moe_combine(yp, pair_pos, topk_weights)
+        return ops.moe_combine(yp, pair_pos, topk_weights, f32=f32_out)
 
 
 def with_shared_experts(topk_weights: torch.Tensor, topk_ids: torch.Tensor, first_shared: int, num_shared: int,
@@ -317,19 +346,25 @@ class FusedMoEGraph:
     def __init__(self, weights: MoEWeights, tokens: int, top_k: int, scoring: str = "softmax",
                  renormalize: bool = False, dtype: torch.dtype = torch.float16, device=None,
                  x: torch.Tensor | None = None, router_logits: torch.Tensor | None = None,
-                 num_shared_experts: int = 0, workspace: _Workspace | None = None):
+                 num_shared_experts: int = 0, workspace: _Workspace | None = None, ep_group=None,
+                 shared_weights: MoEWeights | None = None):
         """``workspace``: the graph's private intermediates (default: its own). Graphs that share one
-        must be replayed in stream order (FusedMoEPipeline's two slots do)."""
+        must be replayed in stream order (FusedMoEPipeline's two slots do). ``ep_group``: capture the
+        expert-parallel layer (its NCCL all-gather / reduce-scatter are captured too; ``weights`` is
+        this rank's shard, the router logits cover all experts of the group)."""
         dev = torch.device(device) if device is not None else weights.w13.blocks.device
         self.workspace = workspace or _Workspace(per_stream=False)
         self.x = torch.zeros((tokens, weights.hidden), dtype=dtype, device=dev)
-        self.logits = torch.randn((tokens, weights.num_experts - num_shared_experts), device=dev)
+        import torch.distributed as dist
+        n_routed = (weights.num_experts * (dist.get_world_size(ep_group) if ep_group is not None else 1)
+                    - (num_shared_experts if shared_weights is None else 0))
+        self.logits = torch.randn((tokens, n_routed), device=dev)
         if x is not None:  # warm up / capture on the caller's first inputs (same routing as served)
             self.x.copy_(x)
         if router_logits is not None:
             self.logits.copy_(router_logits)
         args = (weights, top_k, scoring, renormalize)
-        kw = {"num_shared_experts": num_shared_experts}
+        kw = {"num_shared_experts": num_shared_experts, "ep_group": ep_group, "shared_weights": shared_weights}
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with _use_workspace(self.workspace):
@@ -366,11 +401,11 @@ class FusedMoEPipeline:
 
     def __init__(self, weights: MoEWeights, tokens: int, top_k: int, scoring: str = "softmax",
                  renormalize: bool = False, dtype: torch.dtype = torch.float16, device=None,
-                 x: torch.Tensor | None = None, router_logits: torch.Tensor | None = None):
+                 x: torch.Tensor | None = None, router_logits: torch.Tensor | None = None, ep_group=None):
         self.dev = torch.device(device) if device is not None else weights.w13.blocks.device
         ws = _Workspace(per_stream=False)  # shared by both slots: their replays are serialised on one stream
         self.slots = [FusedMoEGraph(weights, tokens, top_k, scoring, renormalize, dtype, self.dev, x, router_logits,
-                                    workspace=ws) for _ in range(2)]
+                                    workspace=ws, ep_group=ep_group) for _ in range(2)]
         self.h2d = torch.cuda.Stream(device=self.dev)
         self.d2h = torch.cuda.Stream(device=self.dev)
         self.i = 0

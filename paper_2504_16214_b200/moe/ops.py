@@ -2,6 +2,8 @@
 current CUDA stream. Inputs must already be CUDA tensors; nothing here runs on the CPU."""
 from __future__ import annotations
 
+import ctypes as C
+
 import torch
 
 from . import _lib
@@ -206,14 +208,71 @@ def group_sums(x: torch.Tensor, row_limit: torch.Tensor | None = None,
 
 
 def moe_combine(y_perm: torch.Tensor, pair_pos: torch.Tensor, topk_weights: torch.Tensor,
-                out: torch.Tensor | None = None) -> torch.Tensor:
+                out: torch.Tensor | None = None, f32: bool = False) -> torch.Tensor:
+    """y[t] = act(sum_j w[t, j] Y[pos(t, j)]) -- or, with ``f32``, the fp32 sums unrounded (float32
+    output: the expert-parallel partial)."""
     _need_cuda(y_perm, pair_pos, topk_weights)
     T, k = topk_weights.shape
     H = y_perm.shape[1]
     if out is None:
-        out = torch.empty((T, H), dtype=y_perm.dtype, device=y_perm.device)
-    _lib.call("w4a16_moe_combine", y_perm.data_ptr(), T, H, k, pair_pos.data_ptr(), topk_weights.data_ptr(),
-              act_code(y_perm.dtype), out.data_ptr(), _stream())
+        out = torch.empty((T, H), dtype=torch.float32 if f32 else y_perm.dtype, device=y_perm.device)
+    _lib.call("w4a16_moe_combine_f32" if f32 else "w4a16_moe_combine", y_perm.data_ptr(), T, H, k, pair_pos.data_ptr(),
+              topk_weights.data_ptr(), act_code(y_perm.dtype), out.data_ptr(), _stream())
+    return out
+
+
+# ------------------------------------------------------------------------------- expert parallelism
+def ep_available() -> bool:
+    return bool(_lib.load().w4a16_ep_available())
+
+
+def ep_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _lib.call("w4a16_ep_unique_id", C.addressof(buf))
+    return bytes(buf)
+
+
+def ep_comm_init(uid: bytes, rank: int, world: int) -> int:
+    """Opaque communicator handle (an int address) over ``world`` ranks; collective."""
+    buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    out = C.c_void_p()
+    _lib.call("w4a16_ep_comm_init", C.addressof(buf), rank, world, C.byref(out))
+    return out.value
+
+
+def ep_comm_destroy(comm: int) -> None:
+    _lib.call("w4a16_ep_comm_destroy", comm)
+
+
+def ep_dispatch(comm: int, world: int, x: torch.Tensor, topk_ids: torch.Tensor, topk_weights: torch.Tensor,
+                out: tuple | None = None):
+    """All-gather (x, ids, weights) of every rank -> ([world*T, H], [world*T, k], [world*T, k])."""
+    _need_cuda(x, topk_ids, topk_weights)
+    T, H = x.shape
+    k = topk_ids.shape[1]
+    x_all, ids_all, w_all = out or (x.new_empty((world * T, H)), topk_ids.new_empty((world * T, k)),
+                                    topk_weights.new_empty((world * T, k)))
+    _lib.call("w4a16_ep_dispatch", comm, x.data_ptr(), topk_ids.data_ptr(), topk_weights.data_ptr(), T, H, k,
+              act_code(x.dtype), x_all.data_ptr(), ids_all.data_ptr(), w_all.data_ptr(), _stream())
+    return x_all, ids_all, w_all
+
+
+def ep_localize(ids: torch.Tensor, expert_base: int, local_experts: int, out: torch.Tensor | None = None):
+    _need_cuda(ids)
+    out = torch.empty_like(ids) if out is None else out
+    _lib.call("w4a16_ep_localize", ids.data_ptr(), ids.numel(), expert_base, local_experts, out.data_ptr(), _stream())
+    return out
+
+
+def ep_combine(comm: int, partial: torch.Tensor, T: int, dtype: torch.dtype, reduced: torch.Tensor | None = None,
+               out: torch.Tensor | None = None) -> torch.Tensor:
+    """Reduce-scatter the fp32 partials [world*T, H] (sum over ranks) -> act(dtype) [T, H]."""
+    _need_cuda(partial)
+    H = partial.shape[1]
+    reduced = partial.new_empty((T, H)) if reduced is None else reduced
+    out = torch.empty((T, H), dtype=dtype, device=partial.device) if out is None else out
+    _lib.call("w4a16_ep_combine", comm, partial.data_ptr(), T, H, act_code(dtype), reduced.data_ptr(), out.data_ptr(),
+              _stream())
     return out
 
 

@@ -1,8 +1,10 @@
-"""Expert-parallel exchange plumbing on CPU: world_size 2 and 4 over ``gloo``.
+"""Expert-parallel decomposition on CPU: world_size 2 and 4 over ``gloo``.
 
-The product path runs the CUDA ops; here ``moe_w4a16_ep`` gets a CPU backend built from the oracle
-so the dispatch plan, the two all-to-alls, the receiver-side local-expert permutation and the
-combine are checked against the single-process oracle forward on the same inputs."""
+The product path runs the library's NCCL all-gather / reduce-scatter and the CUDA layer; here
+``moe_w4a16_ep`` gets a CPU exchange built from torch.distributed (gloo) and the oracle, so the
+dispatch (all-gather of tokens and routing), the per-rank expert localisation, the fp32 partial
+combine and the reduce-scatter + single rounding are checked against the single-process oracle
+forward on the same inputs."""
 import os
 import socket
 
@@ -31,34 +33,45 @@ class _W:  # the slice of MoEWeights the EP path reads
         self.num_experts, self.hidden, self.inter = w13.shape[0], w13.shape[2], w2.shape[2]
 
 
-class CpuBackend:
-    @staticmethod
-    def permute(ids, n_exp):
-        c, o, sp, pp = O.moe_permute(ids.numpy(), n_exp)
-        return (torch.from_numpy(c), torch.from_numpy(o), torch.from_numpy(sp), torch.from_numpy(pp))
+class CpuExchange:
+    """Same contract as ep.NcclExchange, on gloo + the oracle."""
+
+    def __init__(self):
+        self.world, self.rank = dist.get_world_size(), dist.get_rank()
+
+    def dispatch(self, x, ids, w):
+        out = []
+        for t in (x, ids, w):
+            parts = [torch.empty_like(t) for _ in range(self.world)]
+            dist.all_gather(parts, t)
+            out.append(torch.cat(parts))
+        return tuple(out)
 
     @staticmethod
-    def gather(x, sorted_pairs, topk, rows, row_limit=None):
-        if row_limit is not None:
-            rows = min(rows, int(row_limit[0]))
-        idx = sorted_pairs[:rows].long() // topk
-        return x[idx].clone()
+    def localize(ids_all, base, n):
+        loc = ids_all - base
+        return torch.where((loc >= 0) & (loc < n), loc, torch.full_like(loc, -1))
 
     @staticmethod
-    def combine(y_back, pair_pos, w):
-        Tn, k = w.shape
-        y = torch.zeros((Tn, y_back.shape[1]), dtype=torch.float32)
-        pp = pair_pos.view(Tn, k)
-        for j in range(k):
-            ok = pp[:, j] >= 0
-            y[ok] += w[ok, j:j + 1] * y_back[pp[ok, j].long()]
-        return torch.from_numpy(O.round_act(y.numpy(), "f16"))
+    def experts(x_all, weights, w_all, ids_local, ntok=0, timer=None):
+        """Local experts over the node batch; fp32 weighted sums, NOT rounded (the partial)."""
+        ids, w = ids_local.numpy(), w_all.numpy()
+        counts, offsets, sorted_pairs, pair_pos = O.moe_permute(ids, weights.num_experts)
+        xp = x_all.numpy()[sorted_pairs[:offsets[-1]] // ids.shape[1]]
+        h = O.grouped_gemm(xp, weights.w13d, counts, offsets, "f16", gated=True)
+        yp = O.grouped_gemm(h, weights.w2d, counts, offsets, "f16", gated=False)
+        part = np.zeros((ids.shape[0], yp.shape[1]), np.float32)
+        for j in range(ids.shape[1]):
+            pos = pair_pos.reshape(ids.shape)[:, j]
+            ok = pos >= 0
+            part[ok] += w[ok, j:j + 1] * yp[pos[ok]]
+        return torch.from_numpy(part)
 
-    @staticmethod
-    def experts(x, weights, counts, offsets, ntok, timer=None):
-        h = O.grouped_gemm(x.numpy(), weights.w13d, counts.numpy(), offsets.numpy(), "f16", gated=True)
-        y = O.grouped_gemm(h, weights.w2d, counts.numpy(), offsets.numpy(), "f16", gated=False)
-        return torch.from_numpy(y)
+    def combine(self, partial, T_, dtype):
+        total = partial.clone()
+        dist.all_reduce(total)  # gloo: reduce-scatter = all-reduce + this rank's slice
+        mine = total[self.rank * T_:(self.rank + 1) * T_]
+        return torch.from_numpy(O.round_act(mine.numpy(), "f16"))
 
 
 def _inputs(world=2):
@@ -83,7 +96,7 @@ def _worker(rank, world, port, q):
     w13, w2, xs, ids, wts = _inputs(world)
     lo, hi = shard_bounds(E, world, rank)
     y = moe_w4a16_ep(torch.from_numpy(xs[rank]), _W(w13[lo:hi], w2[lo:hi]), torch.from_numpy(wts[rank]),
-                     torch.from_numpy(ids[rank]), backend=CpuBackend)
+                     torch.from_numpy(ids[rank]), exchange=CpuExchange())
     q.put((rank, y.numpy()))
     dist.destroy_process_group()
 
@@ -103,14 +116,15 @@ def test_ep_matches_single_process_oracle(world):
     w13, w2, xs, ids, wts = _inputs(world)
     for r in range(world):
         want = O.moe_forward(xs[r], w13, w2, ids[r], wts[r], "f16")
-        # per-rank GEMMs see different row batches (BLAS blocking) -> last-ulp fp16 differences only
+        # per-rank GEMMs see different row batches (BLAS blocking) and the fp32 sum runs over ranks
+        # in a different order -> last-ulp fp16 differences only
         np.testing.assert_allclose(got[r], want, rtol=2e-3, atol=1e-4)
 
 
-def test_local_expert_ids_and_plan_shapes():
-    from paper_2504_16214_b200.moe.ep import local_expert_ids
-    rc = torch.tensor([[2, 0, 1], [0, 3, 1]], dtype=torch.int32)
-    assert local_expert_ids(rc).tolist() == [0, 0, 2, 1, 1, 1, 2]
+def test_localize_rule():
+    """ids outside [base, base + n) are dropped (-1): the CPU rule the CUDA ep_localize kernel follows."""
+    ids = torch.tensor([[0, 3, 5], [7, 2, -1]], dtype=torch.int32)
+    assert CpuExchange.localize(ids, 2, 4).tolist() == [[-1, 1, 3], [-1, 0, -1]]
 
 
 def test_shard_with_shared_layout():

@@ -542,8 +542,10 @@ def test_grouped_gemm_fused_gather(ntok, dt):
 
 
 def test_ep_nccl_world1_layer():
-    """The expert-parallel path over NCCL (all-to-all dispatch / combine, receiver-side local order,
-    scattered down GEMM) at world size 1 == the oracle layer."""
+    """The expert-parallel path over NCCL (all-gather dispatch, local experts with the fp32 partial
+    combine, reduce-scatter + rounding) at world size 1 == the oracle layer; eager, CUDA-graph
+    captured (the NCCL collectives inside the graph), and through the one-call C entry
+    w4a16_moe_forward_ep with a communicator made by w4a16_ep_unique_id / w4a16_ep_comm_init."""
     import socket
     import torch.distributed as dist
     from paper_2504_16214_b200.moe import fused_moe_w4a16
@@ -569,6 +571,13 @@ def test_ep_nccl_world1_layer():
             rid, rw = O.route_topk(lg, k, "softmax", True)
             want = O.moe_forward(x, O.dequant(q13, z13, s13, dt), O.dequant(q2, z2, s2, dt), rid, rw, dt)
             np.testing.assert_allclose(_from_dev_act(y, dt), want, rtol=RTOL, atol=(2 if dt == "bf16" else 1) * ATOL)
+            if dt == "f16":  # the same EP layer captured in a CUDA graph (no host sync anywhere in the step)
+                from paper_2504_16214_b200.moe import FusedMoEGraph
+                g = FusedMoEGraph(w, T, k, "softmax", True, torch.float16, ep_group=dist.group.WORLD)
+                yg = g(_to_dev_act(x, dt), torch.from_numpy(lg).cuda())
+                torch.cuda.synchronize()
+                assert torch.equal(yg, y)
+                _ep_c_abi_world1(w, x, rid, rw, want, dt)
         # a shared expert (packed last): routed experts through the exchange, the shared one locally
         T, E, k, H, I, dt = 24, 8, 2, 256, 256, "f16"
         q13, z13, s13 = O.synth_awq_expert_weights(rng, E + 1, 2 * I, H, dt)
@@ -589,6 +598,59 @@ def test_ep_nccl_world1_layer():
         np.testing.assert_allclose(_from_dev_act(y, dt), want, rtol=RTOL, atol=2 * ATOL)
     finally:
         dist.destroy_process_group()
+
+
+def _ep_c_abi_world1(w, x, ids, wts, want, dt):
+    """w4a16_moe_forward_ep through ctypes on a library-made NCCL communicator of one rank."""
+    import ctypes
+    from paper_2504_16214_b200.moe import _lib
+    lib = _lib.load()
+    assert lib.w4a16_ep_available() == 1
+    uid = (ctypes.c_uint8 * 128)()
+    assert lib.w4a16_ep_unique_id(ctypes.addressof(uid)) == 0
+    comm = ctypes.c_void_p()
+    assert lib.w4a16_ep_comm_init(ctypes.addressof(uid), 0, 1, ctypes.byref(comm)) == 0
+    try:
+        assert (lib.w4a16_ep_comm_rank(comm), lib.w4a16_ep_comm_size(comm)) == (0, 1)
+        T, H = x.shape
+        E, k, I = w.num_experts, ids.shape[1], w.inter
+        wsb = lib.w4a16_moe_ep_workspace_bytes(T, 1, k, E, H, I)
+        ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+        xd = _to_dev_act(x, dt)
+        y = torch.empty_like(xd)
+        idd, wd = torch.from_numpy(ids).cuda(), torch.from_numpy(wts).cuda()
+        rc = lib.w4a16_moe_forward_ep(comm, xd.data_ptr(), T, H, I, E, k, idd.data_ptr(), wd.data_ptr(),
+                                      w.w13.blocks.data_ptr(), w.w2.blocks.data_ptr(), 0 if dt == "f16" else 1,
+                                      y.data_ptr(), ws.data_ptr(), wsb, torch.cuda.current_stream().cuda_stream)
+        assert rc == 0
+        torch.cuda.synchronize()
+        np.testing.assert_allclose(_from_dev_act(y, dt), want, rtol=RTOL, atol=ATOL)
+    finally:
+        assert lib.w4a16_ep_comm_destroy(comm) == 0
+
+
+def test_moe_w4a16_raw_awq_overload():
+    """moe_w4a16(x, w13_q, w13_s, w13_z, w2_q, w2_s, w2_z, topk_weights, topk_ids, group_size=128)
+    -- vLLM's AWQ MoE tensors, repacked on first use == the packed-weights call."""
+    from paper_2504_16214_b200.moe import moe_w4a16
+    from paper_2504_16214_b200.moe.weights import pack_moe_awq
+    rng = np.random.default_rng(77)
+    T, E, k, H, I, dt = 33, 8, 2, 256, 256, "bf16"
+    q13, z13, s13 = O.synth_awq_expert_weights(rng, E, 2 * I, H, dt)
+    q2, z2, s2 = O.synth_awq_expert_weights(rng, E, H, I, dt)
+    tdt = torch.bfloat16
+    awq = []
+    for q, z, s in ((q13, z13, s13), (q2, z2, s2)):
+        qw, sc, qz = O.to_awq(q, z, s)
+        awq += [torch.from_numpy(qw).cuda(), torch.from_numpy(sc).cuda().to(tdt), torch.from_numpy(qz).cuda()]
+    x = _to_dev_act(O.round_act(rng.standard_normal((T, H)).astype(np.float32) * 0.5, dt), dt)
+    ids, wts = O.route_topk(rng.standard_normal((T, E)).astype(np.float32), k, "softmax", True)
+    idd, wd = torch.from_numpy(ids).cuda(), torch.from_numpy(wts).cuda()
+    y_raw = moe_w4a16(x, awq[0], awq[1], awq[2], awq[3], awq[4], awq[5], wd, idd, group_size=128)
+    y_raw2 = moe_w4a16(x, *awq, wd, idd)  # cached repack
+    y_pk = moe_w4a16(x, pack_moe_awq(*awq), wd, idd)
+    torch.cuda.synchronize()
+    assert torch.equal(y_raw, y_pk) and torch.equal(y_raw2, y_pk)
 
 
 def test_empty_inputs_c_abi():
