@@ -77,6 +77,9 @@ def _candidate_section(result, cand):
 
 
 def build_report(result, all_candidates=False):
+    """The report dict. A catalog with TMA entries (sm100) adds ``best.buffers[name].tma``: whether
+    the bulk tensor engine can serve the buffer (smem_plan.check_tma on its unified constraint);
+    catalogs without them (sm80) produce the reference's schema unchanged."""
     g = result.graph
     out = {
         "version": SCHEMA_VERSION,
@@ -90,6 +93,9 @@ def build_report(result, all_candidates=False):
     }
     if result.best is not None:
         out["best"] = _candidate_section(result, result.best)
+        from .repack import tma_plan
+        for name, entry in tma_plan(result).items():
+            out["best"]["buffers"][name]["tma"] = entry
     if all_candidates:
         out["all"] = [_candidate_section(result, c) for c in result.candidates]
     return out
