@@ -8,4 +8,4 @@ from paper_2504_16214_b200.tilesynth.layout_flow import (PropagationState, Rearr
                                                          build_constraints, coalesced_access_layout,
                                                          init_gemm_anchor, propagate, reduce_projection, slot_for,
                                                          solve_copy, solve_reduce)
-from paper_2504_16214_b200.tilesynth.tvmap import TvLayout, restrict_tv, tv_from_mode_lists  # noqa: F401
+from paper_2504_16214_b200.tilesynth.algebra import TvLayout, restrict_tv, tv_from_mode_lists  # noqa: F401

@@ -31,7 +31,7 @@ from .isa_table import builtin_catalog_path, load_catalog
 from .layout_flow import SynthesisConfig, slot_for
 from .smem_plan import build_constraint
 from .tileprog import parse_program
-from .tvmap import restrict_tv
+from .algebra import restrict_tv
 
 SCHEMA_VERSION = 1
 

@@ -8,7 +8,7 @@ first), ``tma_candidates`` and ``fastest_mma`` (best issue cycles per MAC).
 
 Construction here: the file is split into records by a small generator; each record kind has a
 schema (allowed keys, required keys) and a builder; explicit thread-value layouts are checked for
-bijectivity through :class:`tvmap.TvLayout`'s grid.
+bijectivity through :class:`algebra.TvLayout`'s grid.
 """
 from __future__ import annotations
 
@@ -18,7 +18,7 @@ from pathlib import Path
 
 from .algebra import Layout, parse_layout
 from .errors import CatalogFormatError, NoInstructionAvailable
-from .tvmap import TvLayout
+from .algebra import TvLayout
 
 DATA_DIR = Path(__file__).resolve().parent / "data"
 

@@ -23,7 +23,7 @@ from .errors import (LayoutIncompatible, NoInstructionAvailable, NonDivisibleTil
                      OutOfDomain, ShapeMismatch, UnsolvedResidual)
 from .isa_table import Catalog, Instruction, fastest_mma
 from .tileprog import OpNode, ProgramGraph, TensorDecl
-from .tvmap import TvLayout, restrict_tv, tv_from_mode_lists
+from .algebra import TvLayout, restrict_tv, tv_from_mode_lists
 
 SlotKey = Union[str, Tuple[int, str]]
 

@@ -25,7 +25,7 @@ from __future__ import annotations
 from .algebra import Layout, coalesce, compose, group_modes, inverse
 from .isa_table import tma_candidates
 from .smem_plan import check_tma
-from .tvmap import filter_replication
+from .algebra import filter_replication
 
 
 def block_order(tv, vector_elems, extents):

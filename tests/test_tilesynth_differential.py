@@ -24,11 +24,11 @@ def ref():
     return mods
 
 
-from paper_2504_16214_b200.tilesynth import bankmodel as B  # noqa: E402
+from paper_2504_16214_b200.tilesynth import smem_plan as B  # noqa: E402
 from paper_2504_16214_b200.tilesynth import algebra as LA  # noqa: E402
 from paper_2504_16214_b200.tilesynth import ituple as N  # noqa: E402
 from paper_2504_16214_b200.tilesynth import smem_plan as SM  # noqa: E402
-from paper_2504_16214_b200.tilesynth import tvmap as TV  # noqa: E402
+from paper_2504_16214_b200.tilesynth import algebra as TV  # noqa: E402
 
 
 def _outcome(fn, *args):
