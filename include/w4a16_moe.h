@@ -198,10 +198,12 @@ int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E,
                       const uint8_t* w2, int dtype, void* y, void* workspace, int64_t workspace_bytes,
                       cudaStream_t stream);
 
-/* Same as w4a16_moe_forward with the fp32, unrounded combine (w4a16_moe_combine_f32): y float [T][H]. */
+/* Same as w4a16_moe_forward with the fp32, unrounded combine (w4a16_moe_combine_f32): y float [T][H].
+ * ntok: the GEMMs' token tile (0 = pick from T * topk / E; expert parallelism passes the tile for the
+ * pairs it expects to be local, most ids being -1). */
 int w4a16_moe_forward_f32(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, int64_t topk,
                           const int32_t* topk_ids, const float* topk_weights, const uint8_t* w13,
-                          const uint8_t* w2, int dtype, float* y, void* workspace, int64_t workspace_bytes,
+                          const uint8_t* w2, int dtype, float* y, int ntok, void* workspace, int64_t workspace_bytes,
                           cudaStream_t stream);
 
 /* ---- expert parallelism (NCCL over NVLink / NVSwitch) ------------------------------------------ */

@@ -220,11 +220,20 @@ int w4a16_ep_combine(w4a16_ep_comm* comm, const float* partial, int64_t T, int64
   return cudaGetLastError() == cudaSuccess ? W4_OK : W4_ERR_CUDA;
 }
 
+// Token tile of the local GEMMs: sized for the pairs expected on this rank (1/world of the node's
+// pairs under uniform routing), not for the node batch -- most gathered ids are other ranks' (-1).
+int ep_ntok(int64_t T, int64_t world, int64_t topk, int64_t local_experts) {
+  return w4a16_pick_ntok(T * topk, local_experts);  // (T * world * topk) / world local pairs
+}
+
 int64_t w4a16_moe_ep_workspace_bytes(int64_t T, int64_t world, int64_t topk, int64_t local_experts, int64_t H,
                                      int64_t I) {
-  const int64_t Tg = T * world;
+  const int64_t Tg = T * world, P = Tg * topk;
+  const int nt = ep_ntok(T, world, topk, local_experts);
+  const int64_t a = w4a16_grouped_gemm_ws_bytes(P, H, local_experts, I, 1, nt);
+  const int64_t b = w4a16_grouped_gemm_ws_bytes(P, I, local_experts, H, 0, nt);
   return align256(2 * Tg * H) + 3 * align256(4 * Tg * topk) + align256(4 * Tg * H) + align256(4 * T * H) +
-         align256(w4a16_moe_workspace_bytes(Tg, topk, local_experts, H, I));
+         align256(w4a16_moe_workspace_bytes(Tg, topk, local_experts, H, I)) + align256(a > b ? a : b);
 }
 
 int w4a16_moe_forward_ep(w4a16_ep_comm* comm, const void* x, int64_t T, int64_t H, int64_t I, int64_t local_experts,
@@ -249,8 +258,8 @@ int w4a16_moe_forward_ep(w4a16_ep_comm* comm, const void* x, int64_t T, int64_t 
     return rc;
   if ((rc = w4a16_ep_localize(ids_all, Tg * topk, comm->rank * local_experts, local_experts, ids_loc, stream)))
     return rc;
-  if ((rc = w4a16_moe_forward_f32(x_all, Tg, H, I, local_experts, topk, ids_loc, w_all, w13, w2, dtype, partial, ws,
-                                  rest, stream)))
+  if ((rc = w4a16_moe_forward_f32(x_all, Tg, H, I, local_experts, topk, ids_loc, w_all, w13, w2, dtype, partial,
+                                  ep_ntok(T, comm->world, topk, local_experts), ws, rest, stream)))
     return rc;
   return w4a16_ep_combine(comm, partial, T, H, dtype, reduced, y, stream);
 }

@@ -874,9 +874,11 @@ int64_t w4a16_moe_workspace_bytes(int64_t T, int64_t topk, int64_t E, int64_t H,
 }  // extern "C"
 
 namespace {
+// ntok: the token tile (0 = w4a16_pick_ntok(T * topk, E)); the split-K workspace is whatever the caller's
+// workspace holds past the fixed buffers
 int moe_forward_impl(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, int64_t topk,
                      const int32_t* topk_ids, const float* topk_weights, const uint8_t* w13, const uint8_t* w2,
-                     int dtype, void* y, bool f32_out, void* workspace, int64_t workspace_bytes,
+                     int dtype, void* y, bool f32_out, int ntok, void* workspace, int64_t workspace_bytes,
                      cudaStream_t stream) {
   if (!x || !topk_ids || !topk_weights || !w13 || !w2 || !y || !workspace) return W4_ERR_ARG;
   if (workspace_bytes < w4a16_moe_workspace_bytes(T, topk, E, H, I)) return W4_ERR_WORKSPACE;
@@ -896,12 +898,12 @@ int moe_forward_impl(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, 
   float* hsum = reinterpret_cast<float*>(ws); ws += align256(8 * ld * (I / 128));
   void* pws = ws; ws += align256(w4a16_moe_permute_ws_bytes(P, E));
   void* kws = ws;
-  const int64_t kws_bytes = splitk_bytes(P, E, H, I);
+  const int64_t kws_bytes = workspace_bytes - (ws - static_cast<uint8_t*>(workspace));
   int rc;
   if ((rc = w4a16_moe_permute_ws(topk_ids, P, E, counts, offsets, sorted, pos, pws,
                                  w4a16_moe_permute_ws_bytes(P, E), stream)))
     return rc;
-  const int nt = w4a16_pick_ntok(P, E);
+  const int nt = ntok > 0 ? ntok : w4a16_pick_ntok(P, E);
   const bool decode = nt <= 16;  // offset-code GEMMs (16-token tiles) need the per-group activation sums
   if (decode) {
     if ((rc = w4a16_moe_gather_sums(x, H, topk, sorted, P, offsets + E, xp, dtype, xsum, stream))) return rc;
@@ -925,15 +927,15 @@ int w4a16_moe_forward(const void* x, int64_t T, int64_t H, int64_t I, int64_t E,
                       const int32_t* topk_ids, const float* topk_weights, const uint8_t* w13,
                       const uint8_t* w2, int dtype, void* y, void* workspace, int64_t workspace_bytes,
                       cudaStream_t stream) {
-  return moe_forward_impl(x, T, H, I, E, topk, topk_ids, topk_weights, w13, w2, dtype, y, false, workspace,
+  return moe_forward_impl(x, T, H, I, E, topk, topk_ids, topk_weights, w13, w2, dtype, y, false, 0, workspace,
                           workspace_bytes, stream);
 }
 
 int w4a16_moe_forward_f32(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, int64_t topk,
                           const int32_t* topk_ids, const float* topk_weights, const uint8_t* w13,
-                          const uint8_t* w2, int dtype, float* y, void* workspace, int64_t workspace_bytes,
+                          const uint8_t* w2, int dtype, float* y, int ntok, void* workspace, int64_t workspace_bytes,
                           cudaStream_t stream) {
-  return moe_forward_impl(x, T, H, I, E, topk, topk_ids, topk_weights, w13, w2, dtype, y, true, workspace,
+  return moe_forward_impl(x, T, H, I, E, topk, topk_ids, topk_weights, w13, w2, dtype, y, true, ntok, workspace,
                           workspace_bytes, stream);
 }
 

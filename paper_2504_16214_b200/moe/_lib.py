@@ -61,7 +61,7 @@ SIGNATURES = {
     "w4a16_moe_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64]),
     "w4a16_moe_forward": (_i, [_p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _i, _p, _p, _i64, _p]),
     "w4a16_moe_combine_f32": (_i, [_p, _i64, _i64, _i64, _p, _p, _i, _p, _p]),
-    "w4a16_moe_forward_f32": (_i, [_p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _i, _p, _p, _i64, _p]),
+    "w4a16_moe_forward_f32": (_i, [_p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _i, _p, _i, _p, _i64, _p]),
     "w4a16_ep_available": (_i, []),
     "w4a16_ep_unique_id": (_i, [_p]),
     "w4a16_ep_comm_init": (_i, [_p, _i, _i, _p]),

@@ -63,10 +63,12 @@ class NcclExchange:
     def localize(ids_all, base, local_experts):
         return ops.ep_localize(ids_all, base, local_experts)
 
-    @staticmethod
-    def experts(x_all, weights, w_all, ids_local, ntok=0, timer=None):
+    def experts(self, x_all, weights, w_all, ids_local, ntok=0, timer=None):
+        """The local layer over the node batch; the token tile is sized for the pairs expected on
+        this rank (1/world of them under uniform routing -- the rest are other ranks' ids, -1)."""
         from .layer import moe_w4a16
-        return moe_w4a16(x_all, weights, w_all, ids_local, ntok=ntok, timer=timer, f32_out=True)
+        nt = ntok or ops.pick_ntok(ids_local.numel() // self.world, weights.num_experts)
+        return moe_w4a16(x_all, weights, w_all, ids_local, ntok=nt, timer=timer, f32_out=True)
 
     def combine(self, partial, T, dtype):
         return ops.ep_combine(self.comm.handle, partial, T, dtype)
