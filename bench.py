@@ -797,7 +797,7 @@ def main():
             "sweep_ds_r1": _columns(sweep),
         }
         print(json.dumps(line, separators=(",", ":")))
-    if group is not None:
+    if dist.is_initialized():  # the EP group, or the one-rank group of the ep_world1 probe
         dist.destroy_process_group()
     return 0
 

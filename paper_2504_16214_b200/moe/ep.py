@@ -43,10 +43,12 @@ class EPComm:
 
     @classmethod
     def of(cls, group=None) -> "EPComm":
-        key = id(group) if group is not None else None
-        if key not in cls._by_group:
-            cls._by_group[key] = cls(group)
-        return cls._by_group[key]
+        """The communicator of ``group`` (None = the default group), created on first use. Keyed by
+        the group object itself, which the cache keeps alive, so a new group never aliases an old
+        one's entry."""
+        if group not in cls._by_group:
+            cls._by_group[group] = cls(group)
+        return cls._by_group[group]
 
 
 class NcclExchange:

@@ -629,6 +629,29 @@ def _ep_c_abi_world1(w, x, ids, wts, want, dt):
         assert lib.w4a16_ep_comm_destroy(comm) == 0
 
 
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+def test_combine_f32_and_localize(dt):
+    """The expert-parallel building blocks: the fp32 (unrounded) combine rounds to the regular
+    combine bit for bit, and ep_localize keeps exactly the ids of one shard (others -> -1)."""
+    ops = _ops()
+    rng = np.random.default_rng(5)
+    T, k, H, E = 37, 8, 512, 64
+    ids = torch.from_numpy(np.stack([rng.permutation(E)[:k] for _ in range(T)]).astype(np.int32)).cuda()
+    ids[3, 2] = -1
+    w = torch.from_numpy(rng.random((T, k)).astype(np.float32)).cuda()
+    c, o, sp, pp = ops.moe_permute(ids, E)
+    tdt = torch.float16 if dt == "f16" else torch.bfloat16
+    yp = (torch.randn((T * k, H), device="cuda") * 0.5).to(tdt)
+    y = ops.moe_combine(yp, pp, w)
+    y32 = ops.moe_combine(yp, pp, w, f32=True)
+    torch.cuda.synchronize()
+    assert y32.dtype == torch.float32 and torch.equal(y32.to(tdt), y)
+    for base, n in ((0, 64), (16, 16), (48, 32), (60, 8)):
+        loc = ops.ep_localize(ids, base, n)
+        want = torch.where((ids >= base) & (ids < base + n), ids - base, torch.full_like(ids, -1))
+        assert torch.equal(loc, want)
+
+
 def test_moe_w4a16_raw_awq_overload():
     """moe_w4a16(x, w13_q, w13_s, w13_z, w2_q, w2_s, w2_z, topk_weights, topk_ids, group_size=128)
     -- vLLM's AWQ MoE tensors, repacked on first use == the packed-weights call."""
