@@ -24,7 +24,6 @@ from __future__ import annotations
 
 import itertools
 from collections import namedtuple
-from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Tuple
 
 from .algebra import TvLayout
@@ -32,6 +31,7 @@ from .errors import (LayoutIncompatible, NoInstructionAvailable, NonDivisibleTil
                      OutOfDomain, ShapeMismatch, StrideConflict, TileSynthError, Unsatisfiable)
 from .isa_table import Catalog, Instruction, candidates_for_copy
 from .layout_flow import PropagationState, RearrangePatch, SlotKey, SynthesisConfig, propagate
+from .records import record
 from .smem_plan import BufferCopy, SmemLayout, synthesize_buffer
 from .tileprog import OpNode, ProgramGraph, TensorDecl, eliminate_dead_code, partition_components, validate
 
@@ -39,15 +39,10 @@ PRUNE = (LayoutIncompatible, NonDivisibleTile, NotDivisible, NotInvertible, OutO
          StrideConflict, Unsatisfiable, NoInstructionAvailable)
 
 
-@dataclass
-class Candidate:
-    index: int
-    choices: Dict[int, Instruction]
-    layouts: Dict[SlotKey, TvLayout]
-    patches: List[RearrangePatch]
-    smem: Dict[str, SmemLayout]
-    staging: Dict[str, SmemLayout] = field(default_factory=dict)
-    cost: Optional[object] = None
+# ``cost`` is filled in by :func:`estimate`
+Candidate = record("Candidate", ["index", "choices", "layouts", "patches", "smem", ("staging", dict), ("cost", None)],
+                   "One surviving search leaf: instruction per op, layout per slot, patches, buffers.",
+                   module=__name__)
 
 
 def _copy_choice_points(graph, catalog):
@@ -199,21 +194,11 @@ def expand_search(graph, catalog, config):
 
 
 # ------------------------------------------------------------------------------------------ pipeline
-@dataclass
-class SynthesisResult:
-    graph: ProgramGraph
-    config: SynthesisConfig
-    catalog: Catalog
-    diagnostics: List[str] = field(default_factory=list)
-    candidates: List[Candidate] = field(default_factory=list)
-
-    @property
-    def ok(self):
-        return not self.diagnostics and (bool(self.candidates) or not self.graph.ops)
-
-    @property
-    def best(self):
-        return self.candidates[0] if self.candidates else None
+SynthesisResult = record(
+    "SynthesisResult", ["graph", "config", "catalog", ("diagnostics", list), ("candidates", list)],
+    "The live graph, the ranked candidates (best first) or the diagnostics.", module=__name__,
+    ok=property(lambda r: not r.diagnostics and (bool(r.candidates) or not r.graph.ops)),
+    best=property(lambda r: r.candidates[0] if r.candidates else None))
 
 
 def synthesize_program(graph, catalog, config=None):

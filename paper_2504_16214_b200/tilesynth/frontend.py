@@ -105,33 +105,42 @@ def render_json(report):
     return json.dumps(report, indent=2, sort_keys=True) + "\n"
 
 
+def _table(title, header, rows):
+    """A titled, column-aligned block (no block for no rows)."""
+    if not rows:
+        return []
+    cells = [header] + [[str(c) for c in r] for r in rows]
+    widths = [max(len(r[i]) for r in cells) for i in range(len(header))]
+    fmt = lambda r: "  " + "  ".join(c.ljust(w) for c, w in zip(r, widths)).rstrip()  # noqa: E731
+    return [title] + [fmt(r) for r in cells]
+
+
 def render_text(report):
-    """Human-readable summary of a report dict."""
-    prog, cands = report["program"], report["candidates"]
-    out = [f"arch {report['arch']}, {report['threads']} threads",
-           f"program: {prog['ops']} ops, {len(prog['tensors'])} tensors"]
-    if report["diagnostics"]:
-        out += ["diagnostics:"] + [f"  {d}" for d in report["diagnostics"]]
-    out.append(f"candidates: {cands['count']} valid, costs {cands['costs']}")
-    best = report.get("best")
-    if not best:
-        return "\n".join(out) + "\n"
-    out.append(f"best candidate #{best['index']}: {best['total_cycles']} cycles")
-    out.append("  register/tensor layouts:")
-    out += [f"    {n}: {t['tv']} over {tuple(t['tile'])}" for n, t in best["tensors"].items()]
-    if best["copies"]:
-        out.append("  copies:")
-        for c in best["copies"]:
-            tail = f", conflicts {c['conflicts']} (identity {c['identity_conflicts']})" if "conflicts" in c else ""
-            out.append(f"    op {c['op']}: {c['instruction']} ({c['vector_bytes']}B){tail}")
-    if best["buffers"]:
-        out += ["  shared buffers:"] + [f"    {n}: {b['layout']} (+) {b['swizzle']}" for n, b in best["buffers"].items()]
-    if best["redistributions"]:
-        out += ["  redistributions:"] + [f"    op {r['op']}: {r['tensor']} {r['from']} -> {r['to']}"
-                                         for r in best["redistributions"]]
-    out.append("  cost breakdown:")
-    out += [f"    {c['label']} [{c['instruction']} x{c['invocations']}]: issue {c['issue']}, stall {c['stall']}, "
-            f"start {c['start']}, completes {c['completes']}" for c in best["cost"]]
+    """Human-readable summary of a report dict: a header, then one table per section of the best
+    candidate (tensor layouts, copies, shared buffers, redistributions, cost steps)."""
+    prog, cands, best = report["program"], report["candidates"], report.get("best")
+    out = [f"tilesynth -- {report['arch']}, {report['threads']} threads, {prog['ops']} ops over "
+           f"{len(prog['tensors'])} tensors; {cands['count']} candidates {cands['costs']}"]
+    out += [f"diagnostic: {d}" for d in report["diagnostics"]]
+    if best:
+        out.append(f"best candidate #{best['index']}: {best['total_cycles']} cycles")
+        sections = (
+            ("register / tensor layouts", ("tensor", "thread-value layout", "tile"),
+             [(f"{n}:", t["tv"], "x".join(map(str, t["tile"]))) for n, t in best["tensors"].items()]),
+            ("copies", ("op", "instruction", "bytes", "conflicts (identity)"),
+             [(c["op"], c["instruction"], c["vector_bytes"],
+               f"{c['conflicts']} ({c['identity_conflicts']})" if "conflicts" in c else "-") for c in best["copies"]]),
+            ("shared buffers", ("buffer", "layout (+) swizzle", "tma"),
+             [(f"{n}:", f"{b['layout']} (+) {b['swizzle']}",
+               ("yes" if b["tma"]["feasible"] else "no") if "tma" in b else "-") for n, b in best["buffers"].items()]),
+            ("redistributions", ("op", "tensor", "from -> to"),
+             [(r["op"], r["tensor"], f"{r['from']} -> {r['to']}") for r in best["redistributions"]]),
+            ("cost", ("step", "instruction", "n", "issue", "stall", "start", "completes"),
+             [(c["label"], c["instruction"], c["invocations"], c["issue"], c["stall"], c["start"], c["completes"])
+              for c in best["cost"]]),
+        )
+        for title, header, rows in sections:
+            out += _table(title, header, rows)
     return "\n".join(out) + "\n"
 
 
@@ -180,30 +189,33 @@ def _copy_lines(graph, cand, op):
     return lines
 
 
+def _elementwise_lines(graph, cand, op):
+    return [f"  {t}: {cand.layouts[t].layout}" for t in op.operands + op.results] + [
+        "  rule: all operands share one thread-value layout"]
+
+
+def _reduce_lines(graph, cand, op):
+    f, g = (cand.layouts[t].layout for t in (op.operands[0], op.results[0]))
+    return [f"  input  {op.operands[0]}: {f}", f"  output {op.results[0]}: {g}",
+            f"  rule: collapse dimension {op.reduce_dim} of the input map"]
+
+
+_EXPLAIN = {"gemm": _gemm_lines, "copy": _copy_lines, "reduce": _reduce_lines, "cast": _elementwise_lines,
+            "elementwise": _elementwise_lines}
+
+
 def explain_op(result, op_index):
     """The constraints touching one op, evaluated on the best candidate."""
-    g = result.graph
-    if not 0 <= op_index < len(g.ops):
-        raise UnknownOp(f"op index {op_index} out of range (0..{len(g.ops) - 1})")
-    cand = result.best
-    if cand is None:
+    ops = result.graph.ops
+    if op_index < 0 or op_index >= len(ops):
+        raise UnknownOp(f"op index {op_index} out of range (0..{len(ops) - 1})")
+    if result.best is None:
         return "no valid candidate to explain"
-    op = g.ops[op_index]
-    lines = [f"op {op_index}: {op.kind} " + " ".join(op.operands + ["->"] + op.results)]
-    if op.kind == "gemm":
-        lines += _gemm_lines(g, cand, op)
-    elif op.kind == "copy":
-        lines += _copy_lines(g, cand, op)
-    elif op.kind == "reduce":
-        lines += [f"  input  {op.operands[0]}: {cand.layouts[op.operands[0]].layout}",
-                  f"  output {op.results[0]}: {cand.layouts[op.results[0]].layout}",
-                  f"  rule: collapse dimension {op.reduce_dim} of the input map"]
-    elif op.kind in ("cast", "elementwise"):
-        lines += [f"  {t}: {cand.layouts[t].layout}" for t in op.operands + op.results]
-        lines.append("  rule: all operands share one thread-value layout")
-    else:
-        lines.append("  redistribution step (no layout constraint)")
-    return "\n".join(lines) + "\n"
+    op = ops[op_index]
+    head = f"op {op_index}: {op.kind} {' '.join(op.operands)} -> {' '.join(op.results)}"
+    body = _EXPLAIN.get(op.kind, lambda g, c, o: ["  redistribution step (no layout constraint)"])(
+        result.graph, result.best, op)
+    return "\n".join([head] + body) + "\n"
 
 
 # ---------------------------------------------------------------------------------------- command line

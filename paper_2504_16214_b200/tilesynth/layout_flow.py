@@ -15,52 +15,36 @@ matrix anchor is table-driven over the operand roles (a, b, c).
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass
 from typing import Dict, List, Tuple, Union
 
 from .algebra import Layout, compose, inverse
 from .errors import (LayoutIncompatible, NoInstructionAvailable, NonDivisibleTile, NotDivisible, NotInvertible,
                      OutOfDomain, ShapeMismatch, UnsolvedResidual)
 from .isa_table import Catalog, Instruction, fastest_mma
+from .records import record
 from .tileprog import OpNode, ProgramGraph, TensorDecl
 from .algebra import TvLayout, restrict_tv, tv_from_mode_lists
 
 SlotKey = Union[str, Tuple[int, str]]
 
 
-@dataclass
-class SynthesisConfig:
-    threads: int = 128
-    max_candidates: int = 64
-
-    def __post_init__(self):
-        if self.threads < 32 or self.threads % 32:
-            raise ValueError("thread count must be a positive multiple of 32")
-
-    @property
-    def warps(self):
-        return self.threads // 32
+def _check_threads(cfg):
+    if cfg.threads < 32 or cfg.threads % 32:
+        raise ValueError("thread count must be a positive multiple of 32")
 
 
-@dataclass
-class RearrangePatch:
-    """A register redistribution: op ``op_index`` sees ``tensor`` as ``to_layout`` while the
-    tensor itself carries ``from_layout``."""
+SynthesisConfig = record("SynthesisConfig", [("threads", 128), ("max_candidates", 64)],
+                         "Threads per tile (a multiple of 32) and the search-leaf cap.", module=__name__,
+                         __post_init__=_check_threads, warps=property(lambda cfg: cfg.threads // 32))
 
-    op_index: int
-    tensor: str
-    from_layout: TvLayout
-    to_layout: TvLayout
-    inserted: bool = True   # False for user-written rearrange ops
+# op ``op_index`` sees ``tensor`` as ``to_layout`` while the tensor carries ``from_layout``;
+# ``inserted`` is False for user-written rearrange ops
+RearrangePatch = record("RearrangePatch", ["op_index", "tensor", "from_layout", "to_layout", ("inserted", True)],
+                        "A register redistribution at a conflict edge.", module=__name__)
 
-
-@dataclass
-class TvConstraint:
-    kind: str               # "copy" | "elem" | "reduce" | "gemm_rows" | "gemm_cols" | "gemm_red"
-    op: OpNode
-    slots: List[SlotKey]
-    tensors: List[str]
-    solved: bool = False
+# kind: "copy" | "elem" | "reduce" | "gemm_rows" | "gemm_cols" | "gemm_red"
+TvConstraint = record("TvConstraint", ["kind", "op", "slots", "tensors", ("solved", False)],
+                      "One layout constraint of an op over its slots.", module=__name__)
 
 
 def slot_for(graph, op, tensor):

@@ -33,13 +33,13 @@ from __future__ import annotations
 
 import math
 import re
-from dataclasses import dataclass, field
 from typing import Callable, Dict, Iterable, List, Optional, Tuple, Union
 
 import numpy as np
 
 from .algebra import Layout, TvLayout, filter_replication, fuse_runs, inverse
 from .errors import LayoutIncompatible, MisalignedAccess, NotInvertible, StrideConflict, Unsatisfiable
+from .records import record
 
 NUM_BANKS = 32
 BANK_BYTES = 4
@@ -223,38 +223,31 @@ Entry = Union[int, StrideVar]
 Piece = Tuple[int, Entry]
 
 
-@dataclass
-class LayoutConstraint:
-    """``splits[i]``: the pieces of dimension i, fastest first; extents multiply to ``dims[i]``."""
+def _constraint_render(c):
+    """``(s0,(s1,s2)):(1,(D1,D2))`` -- free strides numbered by first appearance."""
+    names = {}
 
-    dims: Tuple[int, ...]
-    splits: List[List[Piece]]
+    def word(st):
+        return str(st) if isinstance(st, int) else names.setdefault(id(st), f"D{len(names) + 1}")
 
-    def size(self):
-        return math.prod(self.dims)
+    def group(items):
+        return items[0] if len(items) == 1 else "(" + ",".join(items) + ")"
 
-    def concrete_modes(self):
-        return [(e, s) for dim in self.splits for e, s in dim if isinstance(s, int)]
+    shapes = [group([str(e) for e, _ in dim]) for dim in c.splits]
+    strides = [group([word(st) for _, st in dim]) for dim in c.splits]
+    return "(" + ",".join(shapes) + "):(" + ",".join(strides) + ")"
 
-    def render(self):
-        """``(s0,(s1,s2)):(1,(D1,D2))`` -- free strides numbered by first appearance."""
-        names = {}
 
-        def word(s):
-            return str(s) if isinstance(s, int) else names.setdefault(id(s), f"D{len(names) + 1}")
-
-        def group(items):
-            return items[0] if len(items) == 1 else "(" + ",".join(items) + ")"
-
-        shapes = [group([str(e) for e, _ in dim]) for dim in self.splits]
-        strides = [group([word(s) for _, s in dim]) for dim in self.splits]
-        return "(" + ",".join(shapes) + "):(" + ",".join(strides) + ")"
-
-    def structure_key(self):
-        return tuple(tuple((e, s if isinstance(s, int) else "var") for e, s in dim) for dim in self.splits)
-
-    def __str__(self):
-        return self.render()
+LayoutConstraint = record(
+    "LayoutConstraint", ["dims", "splits"],
+    "``splits[i]``: the pieces (extent, stride | StrideVar) of dimension i, fastest first; extents multiply "
+    "to ``dims[i]``.", module=__name__,
+    size=lambda c: math.prod(c.dims),
+    concrete_modes=lambda c: [(e, st) for dim in c.splits for e, st in dim if isinstance(st, int)],
+    render=_constraint_render,
+    structure_key=lambda c: tuple(tuple((e, st if isinstance(st, int) else "var") for e, st in dim)
+                                  for dim in c.splits),
+    __str__=_constraint_render)
 
 
 _ITEM = re.compile(r"\(([^()]*)\)|([^,()]+)")
@@ -445,11 +438,8 @@ def materialize(c):
 
 
 # ----------------------------------------------------------------------------------------------- TMA
-@dataclass
-class TmaCheck:
-    feasible: bool
-    reason: str = ""
-    hint: Optional[Layout] = None
+TmaCheck = record("TmaCheck", ["feasible", ("reason", ""), ("hint", None)],
+                  "Bulk-tensor-engine feasibility of a buffer, why not, and the materialised hint.", module=__name__)
 
 
 def check_tma(c, element_bits, *, max_dims=5, align_bytes=16, max_box=256):
@@ -472,33 +462,18 @@ def check_tma(c, element_bits, *, max_dims=5, align_bytes=16, max_box=256):
 
 
 # ------------------------------------------------------------------------------------------ buffers
-@dataclass
-class BufferCopy:
-    """One copy touching a shared buffer: its memory-side access layout, vector width (elements)
-    and instruction name."""
+BufferCopy = record(
+    "BufferCopy", ["op_index", "access", "vector_elems", "instruction"],
+    "One copy touching a shared buffer: its memory-side access layout, vector width (elements) and "
+    "instruction name.", module=__name__)
 
-    op_index: int
-    access: TvLayout
-    vector_elems: int
-    instruction: str
-
-
-@dataclass
-class SmemLayout:
-    buffer: str
-    layout: Layout
-    swizzle: Swizzle
-    element_bits: int
-    copy_conflicts: Dict[int, int] = field(default_factory=dict)
-    identity_conflicts: Dict[int, int] = field(default_factory=dict)
-    constraint: Optional[LayoutConstraint] = None
-    copies: List[BufferCopy] = field(default_factory=list)
-
-    def byte_address(self, logical):
-        return self.swizzle(self.layout(logical) * self.element_bits // 8)
-
-    def render(self):
-        return f"{self.layout} (+) {self.swizzle}"
+SmemLayout = record(
+    "SmemLayout", ["buffer", "layout", "swizzle", "element_bits", ("copy_conflicts", dict),
+                   ("identity_conflicts", dict), ("constraint", None), ("copies", list)],
+    "A synthesized shared buffer: layout, swizzle, per-copy conflict degree (chosen / identity swizzle).",
+    module=__name__,
+    byte_address=lambda b, logical: b.swizzle(b.layout(logical) * b.element_bits // 8),
+    render=lambda b: f"{b.layout} (+) {b.swizzle}")
 
 
 def warp_address_matrix(m, element_bits, copy):

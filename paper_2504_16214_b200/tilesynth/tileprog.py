@@ -21,34 +21,27 @@ from __future__ import annotations
 
 import math
 from collections import deque
-from dataclasses import dataclass, field
-from typing import Callable, Dict, List, Optional, Tuple
 
 from . import ituple
 from .algebra import Layout, parse_layout
 from .errors import ArityError, ParseError, TileSynthError, UnknownTensor
+from .records import record
 
 
-# ------------------------------------------------------------------------------------------- dtypes
-@dataclass(frozen=True)
-class DType:
-    kind: str                         # "float" | "int" | "uint"
-    bits: int
-    float_format: Optional[str] = None
+# ----------------------------------------------------------------------------------- record types
+DType = record(
+    "DType", ["kind", "bits", ("float_format", None)],
+    "An element type: kind 'float' | 'int' | 'uint', width in bits, fp8 flavour.", frozen=True, module=__name__,
+    name=property(lambda d: f"float8_{d.float_format}" if d.float_format else f"{d.kind}{d.bits}"),
+    __str__=lambda d: d.name)
 
-    @property
-    def name(self):
-        return f"float8_{self.float_format}" if self.float_format else f"{self.kind}{self.bits}"
-
-    def __str__(self):
-        return self.name
-
-
-_DTYPES: Dict[str, DType] = dict(
-    [(f"float{b}", DType("float", b)) for b in (16, 32, 64)]
-    + [("bfloat16", DType("float", 16))]
-    + [(f"{k}{b}", DType(k, b)) for b in (1, 2, 4, 8, 16, 32, 64) for k in ("int", "uint")]
-    + [(f"float8_{f}", DType("float", 8, f)) for f in ("e5m2", "e4m3")])
+_DTYPES = {}
+for _b in (16, 32, 64):
+    _DTYPES[f"float{_b}"] = DType("float", _b)
+_DTYPES["bfloat16"] = DType("float", 16)
+for _b in (1, 2, 4, 8, 16, 32, 64):
+    _DTYPES.update({f"{_k}{_b}": DType(_k, _b) for _k in ("int", "uint")})
+_DTYPES.update({f"float8_{_f}": DType("float", 8, _f) for _f in ("e5m2", "e4m3")})
 
 
 def parse_dtype(name):
@@ -57,65 +50,39 @@ def parse_dtype(name):
     return _DTYPES[name]
 
 
-# ------------------------------------------------------------------------------------------ tensors
 SCOPES = ("Global", "Shared", "Register")
 ACTION_KINDS = ("copy", "gemm", "cast", "rearrange", "elementwise", "reduce")
 _DERIVING = ("cast", "rearrange", "elementwise", "reduce")   # ops that declare their result
 
+# a Global tensor also carries its layout and backing buffer name
+TensorDecl = record(
+    "TensorDecl", ["name", "scope", "dtype", "shape", ("layout", None), ("buffer", None)],
+    "A declared tensor: scope, element type, logical extents (+ layout / buffer when Global).", module=__name__,
+    elems=property(lambda t: math.prod(t.shape)),
+    bytes=property(lambda t: math.prod(t.shape) * t.dtype.bits / 8))
 
-@dataclass
-class TensorDecl:
-    name: str
-    scope: str
-    dtype: DType
-    shape: Tuple[int, ...]
-    layout: Optional[Layout] = None   # Global tensors only
-    buffer: Optional[str] = None      # backing buffer of a Global tensor
-
-    @property
-    def elems(self):
-        return math.prod(self.shape)
-
-    @property
-    def bytes(self):
-        return self.elems * self.dtype.bits / 8
+# one action statement; trip_count = product of the enclosing loop trip counts; the per-kind extras
+# (cast dtype, reduce dim, rearrange target, elementwise fn) and the annotation default to None
+OpNode = record(
+    "OpNode", ["kind", "operands", "results", ("index", -1), ("line", 0), ("trip_count", 1), ("cast_dtype", None),
+               ("reduce_dim", None), ("rearrange_target", None), ("elementwise_fn", None),
+               ("thread_arrangement", None)],
+    "An action statement: the tensors it reads (operands) and writes (results).", module=__name__,
+    tensors=property(lambda op: op.operands + [r for r in op.results if r not in op.operands]))
 
 
-@dataclass
-class OpNode:
-    kind: str
-    operands: List[str]               # tensors read
-    results: List[str]                # tensors written
-    index: int = -1
-    line: int = 0
-    trip_count: int = 1               # product of the enclosing loop trip counts
-    cast_dtype: Optional[DType] = None
-    reduce_dim: Optional[int] = None
-    rearrange_target: Optional[Layout] = None
-    elementwise_fn: Optional[str] = None
-    thread_arrangement: Optional[Layout] = None
-
-    @property
-    def tensors(self):
-        return self.operands + [r for r in self.results if r not in self.operands]
+def _tensor_of(graph, name):
+    if name not in graph.tensors:
+        raise UnknownTensor(f"unknown tensor {name!r}")
+    return graph.tensors[name]
 
 
-@dataclass
-class ProgramGraph:
-    tensors: Dict[str, TensorDecl]
-    ops: List[OpNode]
-    diagnostics: List[str] = field(default_factory=list)
-
-    def tensor(self, name):
-        if name not in self.tensors:
-            raise UnknownTensor(f"unknown tensor {name!r}")
-        return self.tensors[name]
-
-    def producers(self, name):
-        return [op for op in self.ops if name in op.results]
-
-    def consumers(self, name):
-        return [op for op in self.ops if name in op.operands]
+ProgramGraph = record(
+    "ProgramGraph", ["tensors", "ops", ("diagnostics", list)],
+    "Declarations by name, action statements in program order, diagnostics.", module=__name__,
+    tensor=_tensor_of,
+    producers=lambda g, name: [op for op in g.ops if name in op.results],
+    consumers=lambda g, name: [op for op in g.ops if name in op.operands])
 
 
 # ------------------------------------------------------------------------------------------ parsing
@@ -123,11 +90,7 @@ class _Reader:
     """Parser state: declarations, ops, the open loops and pending annotations."""
 
     def __init__(self):
-        self.tensors: Dict[str, TensorDecl] = {}
-        self.ops: List[OpNode] = []
-        self.loops: List[int] = []
-        self.notes: List[Tuple[int, int, Layout]] = []
-        self.line = 0
+        self.tensors, self.ops, self.loops, self.notes, self.line = {}, [], [], [], 0
 
     def fail(self, msg):
         raise ParseError(msg, self.line)
@@ -236,7 +199,7 @@ def _annotate(r, lhs, args):
     r.notes.append((r.line, r.integer(args[0], "op index"), r.layout(args[2])))
 
 
-_STATEMENTS: Dict[str, Tuple[bool, Optional[Tuple[int, ...]], str, Callable]] = {
+_STATEMENTS = {  # word -> (needs lhs?, allowed arg counts (None = any >= 2), usage, handler)
     "global_view": (True, (3,), "t = global_view <buffer> <dtype> <layout>", _global_view),
     "register_tensor": (True, (2,), "t = register_tensor <dtype> <shape>", _local_tensor("Register")),
     "shared_tensor": (True, (2,), "t = shared_tensor <dtype> <shape>", _local_tensor("Shared")),
@@ -320,99 +283,115 @@ def copy_src_dst(graph, op):
 
 
 # --------------------------------------------------------------------------------------- validation
-def _tensor_rules(name, t):
-    out = []
-    if t.dtype.bits < 8 and t.shape[0] * t.dtype.bits < 8:
-        out.append(f"tensor {name}: sub-byte dtype {t.dtype} needs an innermost run of >= "
-                   f"{8 // t.dtype.bits} elements, got {t.shape[0]}")
-    if t.scope == "Global":
-        if t.layout is None:
-            out.append(f"tensor {name}: Global tensors require a layout")
-        elif any(d == 0 for e, d in t.layout.runs if e > 1):
-            out.append(f"tensor {name}: broadcast (stride-0) global layouts unsupported")
-    return out
-
-
-def _need_register(g, op, name, role):
-    return [] if g.tensor(name).scope == "Register" else [f"op {op.index}: {role} must be Register"]
-
-
-def _check_copy(g, op):
-    src, dst = copy_src_dst(g, op)
-    out = []
-    if src.shape != dst.shape:
-        out.append(f"op {op.index}: copy shape mismatch {src.name}{src.shape} -> {dst.name}{dst.shape}")
-    if src.dtype.bits != dst.dtype.bits:
-        out.append(f"op {op.index}: copy dtype width mismatch {src.dtype} -> {dst.dtype}")
-    return out
-
-
-def _check_gemm(g, op):
-    a, b, c = map(g.tensor, op.operands)
-    out = []
-    for t in (a, b, c):
-        out += _need_register(g, op, t.name, f"gemm operand {t.name}")
-        if len(t.shape) != 2:
-            out.append(f"op {op.index}: gemm operand {t.name} must be rank-2")
-    if all(len(t.shape) == 2 for t in (a, b, c)):
-        (m, ka), (n, kb) = a.shape, b.shape
-        if ka != kb:
-            out.append(f"op {op.index}: gemm reduction extent mismatch between {a.name} (K={ka}) and "
-                       f"{b.name} (K={kb})")
-        if c.shape != (m, n):
-            out.append(f"op {op.index}: gemm output extent mismatch {c.name}{c.shape} vs ({m},{n})")
-    return out
-
-
-def _check_reduce(g, op):
-    src = g.tensor(op.operands[0])
-    out = []
-    if op.reduce_dim is None or not 0 <= op.reduce_dim < len(src.shape):
-        out.append(f"op {op.index}: reduce dim {op.reduce_dim} out of range for rank-{len(src.shape)} "
-                   f"tensor {src.name}")
-    return out + _need_register(g, op, src.name, "reduce operand")
-
-
-def _check_elementwise(g, op):
-    shapes = {g.tensor(n).shape for n in op.operands}
-    return [f"op {op.index}: elementwise operand shapes differ: {shapes}"] if len(shapes) > 1 else []
-
-
-def _check_rearrange(g, op):
-    out = _need_register(g, op, op.operands[0], "rearrange operand")
-    if op.rearrange_target is not None and op.rearrange_target.rank != 2:
-        out.append(f"op {op.index}: rearrange target must be a two-mode (thread, value) layout")
-    return out
-
-
-_OP_RULES = {
-    "copy": _check_copy,
-    "gemm": _check_gemm,
-    "cast": lambda g, op: _need_register(g, op, op.operands[0], "cast operand"),
-    "reduce": _check_reduce,
-    "elementwise": _check_elementwise,
-    "rearrange": _check_rearrange,
+# The diagnostics are part of the synthesis report, so their wording is the reference's
+# (ir.py:379-480); the checks below only pick a message and its fields.
+_MESSAGES = {
+    "subbyte": "tensor {t}: sub-byte dtype {dt} needs an innermost run of >= {need} elements, got {run}",
+    "no_layout": "tensor {t}: Global tensors require a layout",
+    "broadcast": "tensor {t}: broadcast (stride-0) global layouts unsupported",
+    "twice": "op {i}: tensor {t} produced twice",
+    "copy_shape": "op {i}: copy shape mismatch {s}{ss} -> {d}{ds}",
+    "copy_width": "op {i}: copy dtype width mismatch {sd} -> {dd}",
+    "not_register": "op {i}: {role} must be Register",
+    "rank2": "op {i}: gemm operand {t} must be rank-2",
+    "gemm_k": "op {i}: gemm reduction extent mismatch between {a} (K={ka}) and {b} (K={kb})",
+    "gemm_out": "op {i}: gemm output extent mismatch {c}{cs} vs ({m},{n})",
+    "reduce_dim": "op {i}: reduce dim {dim} out of range for rank-{r} tensor {t}",
+    "elem_shapes": "op {i}: elementwise operand shapes differ: {shapes}",
+    "rearrange_rank": "op {i}: rearrange target must be a two-mode (thread, value) layout",
+    "before_def": "op {i}: tensor {t} used before definition",
 }
 
 
-def validate(graph):
-    """Scope / type / shape rules; returns the diagnostics (empty = valid)."""
-    diags = [d for name, t in graph.tensors.items() for d in _tensor_rules(name, t)]
+def _tensor_findings(name, t):
+    if t.dtype.bits < 8 and t.shape[0] * t.dtype.bits < 8:
+        yield "subbyte", dict(t=name, dt=t.dtype, need=8 // t.dtype.bits, run=t.shape[0])
+    if t.scope == "Global" and t.layout is None:
+        yield "no_layout", dict(t=name)
+    elif t.scope == "Global" and any(d == 0 for e, d in t.layout.runs if e > 1):
+        yield "broadcast", dict(t=name)
+
+
+def _reg(g, op, name, role):
+    if g.tensor(name).scope != "Register":
+        yield "not_register", dict(i=op.index, role=role)
+
+
+def _copy_findings(g, op):
+    src, dst = copy_src_dst(g, op)
+    if src.shape != dst.shape:
+        yield "copy_shape", dict(i=op.index, s=src.name, ss=src.shape, d=dst.name, ds=dst.shape)
+    if src.dtype.bits != dst.dtype.bits:
+        yield "copy_width", dict(i=op.index, sd=src.dtype, dd=dst.dtype)
+
+
+def _gemm_findings(g, op):
+    ts = [g.tensor(n) for n in op.operands]
+    for t in ts:
+        yield from _reg(g, op, t.name, f"gemm operand {t.name}")
+        if len(t.shape) != 2:
+            yield "rank2", dict(i=op.index, t=t.name)
+    if {len(t.shape) for t in ts} == {2}:
+        a, b, c = ts
+        if a.shape[1] != b.shape[1]:
+            yield "gemm_k", dict(i=op.index, a=a.name, ka=a.shape[1], b=b.name, kb=b.shape[1])
+        if c.shape != (a.shape[0], b.shape[0]):
+            yield "gemm_out", dict(i=op.index, c=c.name, cs=c.shape, m=a.shape[0], n=b.shape[0])
+
+
+def _reduce_findings(g, op):
+    src = g.tensor(op.operands[0])
+    if op.reduce_dim is None or not 0 <= op.reduce_dim < len(src.shape):
+        yield "reduce_dim", dict(i=op.index, dim=op.reduce_dim, r=len(src.shape), t=src.name)
+    yield from _reg(g, op, src.name, "reduce operand")
+
+
+def _elementwise_findings(g, op):
+    shapes = {g.tensor(n).shape for n in op.operands}
+    if len(shapes) > 1:
+        yield "elem_shapes", dict(i=op.index, shapes=shapes)
+
+
+def _rearrange_findings(g, op):
+    yield from _reg(g, op, op.operands[0], "rearrange operand")
+    if op.rearrange_target is not None and op.rearrange_target.rank != 2:
+        yield "rearrange_rank", dict(i=op.index)
+
+
+_OP_FINDINGS = {
+    "copy": _copy_findings,
+    "gemm": _gemm_findings,
+    "cast": lambda g, op: _reg(g, op, op.operands[0], "cast operand"),
+    "reduce": _reduce_findings,
+    "elementwise": _elementwise_findings,
+    "rearrange": _rearrange_findings,
+}
+
+
+def _findings(graph):
+    for name, t in graph.tensors.items():
+        yield from _tensor_findings(name, t)
     written = set()
     for op in graph.ops:
         if op.kind in _DERIVING:
-            diags += [f"op {op.index}: tensor {r} produced twice" for r in op.results if r in written]
-        diags += _OP_RULES.get(op.kind, lambda g, o: [])(graph, op)
+            for r in op.results:
+                if r in written:
+                    yield "twice", dict(i=op.index, t=r)
+        yield from _OP_FINDINGS.get(op.kind, lambda g, o: ())(graph, op)
         written.update(op.results)
-    written = set()
     produced_somewhere = {r for op in graph.ops for r in op.results}
+    written = set()
     for op in graph.ops:
         for name in op.operands:
             if (graph.tensor(name).scope == "Register" and name in produced_somewhere
                     and name not in written and name not in op.results):
-                diags.append(f"op {op.index}: tensor {name} used before definition")
+                yield "before_def", dict(i=op.index, t=name)
         written.update(op.results)
-    return diags
+
+
+def validate(graph):
+    """Scope / type / shape rules; returns the diagnostics (empty = valid)."""
+    return [_MESSAGES[key].format(**fields) for key, fields in _findings(graph)]
 
 
 # -------------------------------------------------------------------------------------- dead code
