@@ -690,3 +690,28 @@ def test_empty_inputs_c_abi():
     ids, w, c, o, sp, pp = ops.route_permute(lg, 4)
     torch.cuda.synchronize()
     assert int(c.sum()) == 0 and int(o.abs().sum()) == 0
+
+
+def test_against_vllm_kernels_golden():
+    """The B200 path vs vLLM 0.22's own kernels on the same inputs (tests/golden/vllm_moe.npz from
+    tools/make_golden_vllm.py): routing ids bit-exact with its CUDA topk_softmax / topk_sigmoid, the
+    W4A16 layer within rtol / atol 1e-2 of its moe_wna16 Triton fused_experts."""
+    from pathlib import Path
+    from paper_2504_16214_b200.moe import moe_w4a16
+    from paper_2504_16214_b200.moe.weights import MoEWeights
+    d = np.load(Path(__file__).resolve().parent / "golden" / "vllm_moe.npz")
+    ops = _ops()
+    for ci in range(6):
+        T, E, k, soft, rn = (int(v) for v in d[f"route{ci}_meta"])
+        ids, w = ops.route_topk(torch.from_numpy(d[f"route{ci}_logits"]).cuda(), k, "softmax" if soft else "sigmoid",
+                                bool(rn))
+        assert np.array_equal(ids.cpu().numpy(), d[f"route{ci}_ids"])
+        np.testing.assert_allclose(w.cpu().numpy(), d[f"route{ci}_w"], rtol=2e-6, atol=2e-7)
+    for li in range(2):
+        T, E, k, H, I, f16 = (int(v) for v in d[f"layer{li}_meta"])
+        dt = "f16" if f16 else "bf16"
+        g = lambda n: d[f"layer{li}_{n}"]  # noqa: E731
+        wts = MoEWeights(_packed(g("q13"), g("z13"), g("s13"), dt, True), _packed(g("q2"), g("z2"), g("s2"), dt, False))
+        y = moe_w4a16(_to_dev_act(g("x"), dt), wts, torch.from_numpy(g("w")).cuda(), torch.from_numpy(g("ids")).cuda())
+        torch.cuda.synchronize()
+        np.testing.assert_allclose(_from_dev_act(y, dt), g("y"), rtol=RTOL, atol=ATOL)

@@ -125,3 +125,30 @@ def test_grouped_topk_group_rule():
     bias = np.zeros(16, dtype=np.float32)  # with a bias the group score is the sum of the best two
     ids, _ = O.grouped_topk(lg, 2, 4, 1, "sigmoid", True, bias)
     assert set(ids[0].tolist()) <= {8, 9, 10, 11}
+
+
+GOLD_VLLM = Path(__file__).resolve().parent / "golden" / "vllm_moe.npz"  # tools/make_golden_vllm.py (GPU)
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_route_topk_matches_vllm_kernel(case):
+    """Softmax / sigmoid top-k == vLLM 0.22's CUDA topk_softmax / topk_sigmoid (the fused_topk of its
+    FusedMoE): ids bit-exact (ties and an all-equal row included), weights to fp32 rounding."""
+    d = np.load(GOLD_VLLM)
+    T, E, k, soft, rn = (int(v) for v in d[f"route{case}_meta"])
+    ids, w = O.route_topk(d[f"route{case}_logits"], k, "softmax" if soft else "sigmoid", bool(rn))
+    assert np.array_equal(ids, d[f"route{case}_ids"])
+    np.testing.assert_allclose(w, d[f"route{case}_w"], rtol=2e-6, atol=2e-7)
+
+
+@pytest.mark.parametrize("layer", range(2))
+def test_moe_forward_matches_vllm_w4a16_moe(layer):
+    """The oracle's W4A16 MoE layer (dequant to the activation dtype, SwiGLU, h and the expert outputs
+    rounded to it, fp32 combine) == vLLM 0.22's fused_experts with int4_w4a16 (its moe_wna16 Triton
+    path for AWQ) on the same weights and routing, within rtol / atol 1e-2 (fp16 and bf16)."""
+    d = np.load(GOLD_VLLM)
+    T, E, k, H, I, f16 = (int(v) for v in d[f"layer{layer}_meta"])
+    g = lambda n: d[f"layer{layer}_{n}"]  # noqa: E731
+    want = O.moe_forward_expertwise(g("x"), g("q13"), g("z13"), g("s13"), g("q2"), g("z2"), g("s2"), g("ids"),
+                                    g("w"), "f16" if f16 else "bf16")
+    np.testing.assert_allclose(want, g("y"), rtol=1e-2, atol=1e-2)
