@@ -82,6 +82,7 @@ struct GemmArgs {
   // then covers x itself and the producer loads rows with TMA gather4); xsum is indexed by x's rows
   const int32_t* gather_rows;
   int gather_div;
+  int direct_rows;               // offset-mode tiles with <= this many real tokens store unstaged (<= kDirectRows)
 };
 
 // Numeric modes.
@@ -104,6 +105,7 @@ constexpr int kModeGateUp = 1;  // part 0 = gate rows, part 1 = up rows, same k-
 constexpr int kModeKPair = 2;   // parts = two consecutive k-groups of the same rows (down proj.)
 constexpr int kModeNPair = 3;   // parts = one k-group of two adjacent n-tiles sharing the X tile (prefill)
 constexpr int kEpiChunk = 4;    // offset-mode epilogue token granularity
+constexpr int kDirectRows = 4;  // max of GemmArgs::direct_rows (W4A16_DIRECT_ROWS overrides the default 4; 0 = off)
 
 // kPair: a CTA pair (cluster of 2 on one TPC) runs tcgen05.mma.cta_group::2 -- M = 256 weight rows
 // (each CTA dequantises its own 128-row n-tile into its own TMEM), N = kNTok tokens with each CTA
@@ -905,6 +907,27 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           }
         } else {
           float hv[kNTok];  // the stored (rounded) outputs, for the fused sums below
+          if (m_rows <= args.direct_rows) {
+            // few real tokens (decode: ~2 rows per expert at DS-R1 T=64): compute only those and store
+            // them straight from registers -- a warp writes 32 consecutive rows (64 B) per token --
+            // instead of 16 tokens' SiLU plus the shared-memory staging round (the tile-end epilogue
+            // delays the next tile's first folds, and through them its MMAs)
+#pragma unroll
+            for (int m = 0; m < kNTok; ++m) hv[m] = 0.f;
+#pragma unroll
+            for (int m = 0; m < kDirectRows; ++m) {
+              if (m < m_rows) {  // warp-uniform
+                float v;
+                if constexpr (kGated) v = silu_f(a[0][m]) * a[1][m];
+                else v = a[0][m];
+                const uint16_t b = to_act_bits<kBF16>(v);
+                hv[m] = act_bits_to_float<kBF16>(b);
+                uint16_t* dst = ocol + orow(m);
+                *dst = b;
+                if constexpr (C::kNPer == 2) dst[kTileRows] = to_act_bits<kBF16>(a[kOuts - 1][m]);
+              }
+            }
+          } else {
 #pragma unroll
           for (int m0 = 0; m0 < kNTok; m0 += 16) {
             const int64_t ro = row_off16(m0);
@@ -925,6 +948,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               for (int i = 0; i < 16; ++i) hu[i] = to_act_bits<kBF16>(a[kOuts - 1][m0 + i]);
               store16_staged(m0, ro, hu, kTileRows, 1);
             }
+          }
           }
           if constexpr (kGated && kNTok <= 16) {
             if (args.osum != nullptr) {
@@ -1446,6 +1470,12 @@ static int grouped_gemm_impl(const void* x, int64_t x_rows, const int32_t* gathe
   a.gather_div = gather_div;
   a.rows = rows;
   a.splits = pl.splits;
+  static const int direct_rows = [] {
+    const char* e = getenv("W4A16_DIRECT_ROWS");
+    const int v = e ? atoi(e) : kDirectRows;
+    return v < 0 ? 0 : (v > kDirectRows ? kDirectRows : v);
+  }();
+  a.direct_rows = direct_rows;
   a.part = static_cast<float*>(ws);
   a.part_ld = (gated ? 2 : 1) * n_out;
   // the decode gate/up epilogue writes the output's group sums itself; otherwise a sums pass follows
