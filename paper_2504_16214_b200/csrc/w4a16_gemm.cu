@@ -121,7 +121,8 @@ struct Cfg {
   static constexpr int kGroupsPerStage = kMode == kModeKPair ? 2 : 1;
   static constexpr int kBlk = kParts * kPartBytes;
   static constexpr int kXBytes = kGroupsPerStage * kXRows * kTileK * 2;  // X tile, 64-wide 128B-swizzle atoms
-  static constexpr int kSumBytes = kOffset ? kGroupsPerStage * kNTok * 8 : 0;  // (C, S) fp32 per group/token
+  // (C, S) fp32 per group/token, padded to one 8-byte slot per producer lane (see the sums copy)
+  static constexpr int kSumBytes = kOffset ? (kGroupsPerStage * kNTok > 32 ? kGroupsPerStage * kNTok : 32) * 8 : 0;
   // offset mode: each part's 128-k partial is split over kKSplit independent accumulators (k halves)
   // so a stage issues kParts * kKSplit interleaved MMA chains -- a dependent chain of small-N MMAs is
   // bound by the accumulate latency, not by the tensor pipe
@@ -474,7 +475,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           if constexpr (kOffset) {
             // all 32 lanes copy and arrive every stage (fewer items than lanes: items are duplicated --
             // a lane arriving .noinc without its own cp.async in flight was observed never to fire);
-            // rows past the end read row 0 of the group (never used)
+            // every lane writes its own slot (duplicates land in the padding past the items, so no two
+            // lanes write one address -- racecheck-clean); rows past the end read row 0 of the group
+            // (never used)
             uint8_t* ss = smem_s + st.i * C::kSumBytes;
 #pragma unroll
             for (int i0 = 0; i0 < (C::kSumItems > 32 ? C::kSumItems : 32); i0 += 32) {
@@ -482,7 +485,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               const int g = i / kNTok, m = i % kNTok;
               int64_t r = ti.m_start + m < args.rows ? ti.m_start + m : 0;
               if (gather) r = __ldg(args.gather_rows + r) / args.gather_div;  // sums of x's rows
-              cp_async_8(ss + i * 8,
+              cp_async_8(ss + (i0 + lane) * 8,
                          args.xsum + ((static_cast<int64_t>(j) * C::kGroupsPerStage + g) * args.sum_ld + r) * 2);
             }
             cp_async_arrive_noinc(&full[st.i]);
