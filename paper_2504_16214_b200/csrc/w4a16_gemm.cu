@@ -1359,6 +1359,9 @@ namespace {
 // stages). Minimise waves x (stages per unit + per-unit overhead) over S, from an upper estimate
 // of the tile count (touched experts <= min(E, rows)).
 int choose_splits(int64_t rows, int64_t num_experts, int nt, int n_stages, int grid) {
+  // (Measured alternatives, tools/gpu_splits2.sh: the expected touched-expert count instead of this upper
+  // estimate, without the early exit, gained 1.6-3.5 % at DS-R1 T = 2 / 4 but lost 1-6 % at T = 1 / 8 and
+  // Qwen3 T = 16; kept as is.)
   const int64_t tiles = std::min<int64_t>(num_experts, rows) * nt;
   if (tiles >= 2 * grid || n_stages < 4) return 1;
   double best = 1e30;
@@ -1393,6 +1396,11 @@ GemmPlan plan_gemm(int64_t rows, int64_t K, int64_t num_experts, int64_t n_out, 
   if (!gated && pl.offset && pl.ntok == 16 && nt % 2 == 0 && decode_npair_enabled()) pl.mode = kModeNPair;
   const int n_stages = kt / (pl.mode == kModeKPair ? 2 : 1);
   pl.splits = (pl.offset && rows < (1 << 20)) ? choose_splits(rows, num_experts, nt, n_stages, sm_count()) : 1;
+  // experiment: W4A16_SPLITS_GU / W4A16_SPLITS_DN force the decode split-K factor of gate/up / down launches
+  static const int force_gu = getenv("W4A16_SPLITS_GU") ? atoi(getenv("W4A16_SPLITS_GU")) : 0;
+  static const int force_dn = getenv("W4A16_SPLITS_DN") ? atoi(getenv("W4A16_SPLITS_DN")) : 0;
+  const int force = gated ? force_gu : force_dn;
+  if (pl.offset && rows < (1 << 20) && force > 0) pl.splits = std::min(force, n_stages);
   return pl;
 }
 }  // namespace
