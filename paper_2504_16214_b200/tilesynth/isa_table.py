@@ -144,58 +144,73 @@ def _tile(text):
     return tuple(map(int, body[1:-1].split(",")))
 
 
-def _build(kind, name, rec, arch):
-    def need(key):
-        if key not in rec:
-            raise CatalogFormatError(f"instruction {name}: missing key {key!r}")
-        return rec[key]
+class _Record:
+    """One catalog record being turned into an :class:`Instruction`; every complaint names it."""
 
-    issue, completion = int(need("issue")), int(need("completion"))
-    if min(issue, completion) < 1:
-        raise CatalogFormatError(f"instruction {name}: cycles must be >= 1")
-    stray = sorted(set(rec) - _SCHEMA[kind])
-    if stray:
-        raise CatalogFormatError(f"instruction {name}: unknown keys {stray}")
-    spec = dict(name=name, category=kind, issue_cycles=issue, completion_cycles=completion, arch=arch)
-    if kind == "alu":
-        return Instruction(**spec)
-    spec["threads"] = int(rec.get("threads", "32"))
-    if kind == "mma":
-        shape, types = tuple(map(int, need("mnk").split())), need("dtypes").split()
-        if len(shape) != 3 or len(types) != 3:
-            raise CatalogFormatError(f"instruction {name}: mnk and dtypes take three values each")
-        spec.update(mnk=shape, **dict(zip(("dtype_a", "dtype_b", "dtype_c"), types)))
-        spec.update((k, parse_layout(need(k))) for k in ("tv_a", "tv_b", "tv_c"))
-        inst = Instruction(**spec)
-        checked = zip(("tv_a", "tv_b", "tv_c"), inst.mma_layouts())
-    else:
-        scopes = need("scopes").split()
-        if len(scopes) != 2 or not set(scopes) <= _SCOPE_NAMES:
-            raise CatalogFormatError(f"instruction {name}: bad scopes {scopes}")
-        spec.update(src_scope=scopes[0], dst_scope=scopes[1], vector_bytes=int(need("vector_bytes")),
-                    generic="generic" in rec, tma="tma" in rec, element_bits=int(rec.get("element_bits", "0")))
-        if spec["vector_bytes"] not in (1, 2, 4, 8, 16):
-            raise CatalogFormatError(f"instruction {name}: vector_bytes must be one of 1,2,4,8,16")
-        spec.update((k, conv(rec[k])) for k, conv in (("tile", _tile), ("tv_src", parse_layout),
-                                                      ("tv_dst", parse_layout)) if k in rec)
-        inst = Instruction(**spec)
-        checked = ()
-        if not (inst.generic or inst.tma):
-            if inst.tv_src is None or inst.tv_dst is None or not inst.tile:
-                raise CatalogFormatError(f"instruction {name}: explicit entries need tile, tv_src, tv_dst")
-            checked = tuple(zip(("tv_src", "tv_dst"), inst.copy_layouts(None)))
-    for label, tv in checked:
-        tv.check_bijective(f"{name}.{label}")
-        if kind == "copy" and tv.threads != inst.threads:
-            raise CatalogFormatError(f"instruction {name}: thread mode size != threads field")
-    return inst
+    def __init__(self, kind, name, fields, arch):
+        self.kind, self.name, self.fields, self.arch = kind, name, fields, arch
+
+    def reject(self, why):
+        raise CatalogFormatError(f"instruction {self.name}: {why}")
+
+    def need(self, key):
+        return self.fields[key] if key in self.fields else self.reject(f"missing key {key!r}")
+
+    def ensure(self, ok, why):
+        if not ok:
+            self.reject(why)
+
+    def build(self):
+        issue, completion = int(self.need("issue")), int(self.need("completion"))
+        self.ensure(min(issue, completion) >= 1, "cycles must be >= 1")
+        stray = sorted(set(self.fields) - _SCHEMA[self.kind])
+        self.ensure(not stray, f"unknown keys {stray}")
+        spec = dict(name=self.name, category=self.kind, issue_cycles=issue, completion_cycles=completion,
+                    arch=self.arch)
+        if self.kind != "alu":
+            spec["threads"] = int(self.fields.get("threads", "32"))
+        inst = Instruction(**spec, **getattr(self, "_" + self.kind)())
+        for label, tv in self._explicit_layouts(inst):
+            tv.check_bijective(f"{self.name}.{label}")
+            self.ensure(self.kind == "mma" or tv.threads == inst.threads, "thread mode size != threads field")
+        return inst
+
+    def _alu(self):
+        return {}
+
+    def _mma(self):
+        shape, types = tuple(map(int, self.need("mnk").split())), self.need("dtypes").split()
+        self.ensure(len(shape) == 3 and len(types) == 3, "mnk and dtypes take three values each")
+        out = dict(mnk=shape, dtype_a=types[0], dtype_b=types[1], dtype_c=types[2])
+        out.update((k, parse_layout(self.need(k))) for k in ("tv_a", "tv_b", "tv_c"))
+        return out
+
+    def _copy(self):
+        scopes = self.need("scopes").split()
+        self.ensure(len(scopes) == 2 and set(scopes) <= _SCOPE_NAMES, f"bad scopes {scopes}")
+        width = int(self.need("vector_bytes"))
+        self.ensure(width in (1, 2, 4, 8, 16), "vector_bytes must be one of 1,2,4,8,16")
+        out = dict(src_scope=scopes[0], dst_scope=scopes[1], vector_bytes=width, generic="generic" in self.fields,
+                   tma="tma" in self.fields, element_bits=int(self.fields.get("element_bits", "0")))
+        convert = {"tile": _tile, "tv_src": parse_layout, "tv_dst": parse_layout}
+        out.update((k, conv(self.fields[k])) for k, conv in convert.items() if k in self.fields)
+        return out
+
+    def _explicit_layouts(self, inst):
+        if self.kind == "mma":
+            return zip(("tv_a", "tv_b", "tv_c"), inst.mma_layouts())
+        if self.kind == "alu" or inst.generic or inst.tma:
+            return ()
+        self.ensure(inst.tv_src is not None and inst.tv_dst is not None and inst.tile,
+                    "explicit entries need tile, tv_src, tv_dst")
+        return zip(("tv_src", "tv_dst"), inst.copy_layouts(None))
 
 
 def load_catalog(path):
     """Load and validate a catalog file (unknown keys rejected, explicit layouts must be bijections
     onto their tiles, names unique)."""
     header = {}
-    insts = [_build(kind, name, fields, str(header.get("arch") or ""))
+    insts = [_Record(kind, name, fields, str(header.get("arch") or "")).build()
              for kind, name, fields in _records(Path(path).read_text(), header)]
     if "arch" not in header or not insts:
         raise CatalogFormatError("catalog needs a header and at least one instruction")
@@ -210,28 +225,31 @@ def builtin_catalog_path(arch="sm80"):
 
 
 # ------------------------------------------------------------------------------------------ queries
+def _pick(cat, category, **want):
+    """Catalog entries of ``category`` whose attributes equal ``want`` (in catalog order)."""
+    return [i for i in cat.instructions
+            if i.category == category and all(getattr(i, k) == v for k, v in want.items())]
+
+
 def candidates_for_copy(cat, src, dst):
     """Instructions able to move ``src`` -> ``dst`` (widest vector first, then by name; the last is
     the scalar fallback). A register-to-register move needs none: []."""
     if src.scope == dst.scope == "Register":
         return []
-    fits = sorted((i for i in cat.instructions
-                   if i.category == "copy" and not i.tma and (i.src_scope, i.dst_scope) == (src.scope, dst.scope)
-                   and i.supports_dtype(src.dtype)), key=lambda i: (-i.vector_bytes, i.name))
+    fits = [i for i in _pick(cat, "copy", tma=False, src_scope=src.scope, dst_scope=dst.scope)
+            if i.supports_dtype(src.dtype)]
     if not fits:
         raise NoInstructionAvailable(f"no copy instruction for {src.scope}->{dst.scope} {src.dtype}")
-    return fits
+    return sorted(fits, key=lambda i: (-i.vector_bytes, i.name))
 
 
 def tma_candidates(cat, src, dst):
-    return [i for i in cat.instructions
-            if i.category == "copy" and i.tma and (i.src_scope, i.dst_scope) == (src.scope, dst.scope)]
+    return _pick(cat, "copy", tma=True, src_scope=src.scope, dst_scope=dst.scope)
 
 
 def fastest_mma(cat, a_dtype, b_dtype, c_dtype):
     """The matching matrix instruction with the fewest issue cycles per MAC (then by name)."""
-    want = (a_dtype.name, b_dtype.name, c_dtype.name)
-    fits = [i for i in cat.instructions if i.category == "mma" and (i.dtype_a, i.dtype_b, i.dtype_c) == want]
+    fits = _pick(cat, "mma", dtype_a=a_dtype.name, dtype_b=b_dtype.name, dtype_c=c_dtype.name)
     if not fits:
         raise NoInstructionAvailable(f"no matrix instruction for {a_dtype} x {b_dtype} -> {c_dtype}")
     return min(fits, key=lambda i: (i.issue_cycles / i.macs(), i.name))

@@ -31,6 +31,7 @@ swizzle search is one numpy pass (:func:`score_pattern_matrix`) instead of a Pyt
 """
 from __future__ import annotations
 
+import dataclasses
 import math
 import re
 from typing import Callable, Dict, Iterable, List, Optional, Tuple, Union
@@ -391,50 +392,71 @@ def _check_chain(c):
 
 
 # ------------------------------------------------------------------------------------- materialize
+class _StrideChain:
+    """The address chain of a buffer being materialised: a cursor ``reach`` (the span covered so
+    far), the free pieces still to place (logical order, mutable remaining extents) and the strides
+    given to every (dimension, piece) slot."""
+
+    def __init__(self, c):
+        self.c = c
+        self.reach = 1
+        self.slots = {}
+        self.free = []
+        for d, dim in enumerate(c.splits):
+            for p, (e, s) in enumerate(dim):
+                if isinstance(s, int):
+                    self.slots[(d, p)] = [(e, s)]
+                else:
+                    self.free.append([d, p, e, s])
+
+    def give(self, rec, extent, stride):
+        self.slots.setdefault((rec[0], rec[1]), []).append((extent, stride))
+
+    def close_gap(self, upto):
+        """Free pieces (first fitting one in logical order, cut by gcd) until the chain reaches the
+        next concrete stride ``upto``."""
+        gap, at = upto // self.reach, self.reach
+        while gap > 1:
+            rec = next((r for r in self.free if math.gcd(r[2], gap) > 1 and at % r[3].divisibility == 0), None)
+            if rec is None:
+                raise Unsatisfiable(f"no free piece fits the stride gap {gap} at {at}")
+            g = math.gcd(rec[2], gap)
+            self.give(rec, g, at)
+            rec[2] //= g
+            if rec[2] == 1:
+                self.free.remove(rec)
+            at, gap = at * g, gap // g
+
+    def extend(self):
+        """The remaining free pieces, in logical order, on top of the chain."""
+        for rec in self.free:
+            if self.reach % rec[3].divisibility:
+                raise Unsatisfiable(f"stride {self.reach} is not a multiple of {rec[3].divisibility}")
+            self.give(rec, rec[2], self.reach)
+            self.reach *= rec[2]
+
+    def layout(self):
+        dims = []
+        for d, dim in enumerate(self.c.splits):
+            runs = fuse_runs(r for p in range(len(dim)) for r in sorted(self.slots[(d, p)], key=lambda r: r[1]))
+            runs = runs or [(1, 0)]
+            dims.append(runs[0] if len(runs) == 1 else (tuple(e for e, _ in runs), tuple(st for _, st in runs)))
+        return Layout(tuple(x for x, _ in dims), tuple(y for _, y in dims))
+
+
 def materialize(c):
     """Pick the free strides so the layout is a bijection onto [0, size): concrete pieces first by
     stride, free pieces fill the chain gaps and then extend the chain in logical order."""
     _check_chain(c)
-    placed = {}
-    free = []  # [dim, pos, remaining extent, var] in logical order
-    for d, dim in enumerate(c.splits):
-        for p, (e, s) in enumerate(dim):
-            if isinstance(s, int):
-                placed[(d, p)] = [(e, s)]
-            else:
-                free.append([d, p, e, s])
-
-    def fill(gap, at):
-        while gap > 1:
-            for rec in free:
-                g = math.gcd(rec[2], gap)
-                if g > 1 and at % rec[3].divisibility == 0:
-                    break
-            else:
-                raise Unsatisfiable(f"no free piece fits the stride gap {gap} at {at}")
-            placed.setdefault((rec[0], rec[1]), []).append((g, at))
-            rec[2] //= g
-            if rec[2] == 1:
-                free.remove(rec)
-            at, gap = at * g, gap // g
-
-    reach = 1
+    chain = _StrideChain(c)
     for e, s in sorted(c.concrete_modes(), key=lambda m: m[1]):
-        if s > reach:
-            fill(s // reach, reach)
-        reach = s * e
-    for d, p, e, var in free:
-        if reach % var.divisibility:
-            raise Unsatisfiable(f"stride {reach} is not a multiple of {var.divisibility}")
-        placed.setdefault((d, p), []).append((e, reach))
-        reach *= e
-    if reach != c.size():
-        raise Unsatisfiable(f"the strides span {reach}, the buffer holds {c.size()}")
-    trees = []
-    for d, dim in enumerate(c.splits):
-        runs = fuse_runs(r for p in range(len(dim)) for r in sorted(placed[(d, p)], key=lambda r: r[1])) or [(1, 0)]
-        trees.append(runs[0] if len(runs) == 1 else (tuple(e for e, _ in runs), tuple(s for _, s in runs)))
-    return Layout(tuple(s for s, _ in trees), tuple(d for _, d in trees))
+        if s > chain.reach:
+            chain.close_gap(s)
+        chain.reach = s * e
+    chain.extend()
+    if chain.reach != c.size():
+        raise Unsatisfiable(f"the strides span {chain.reach}, the buffer holds {c.size()}")
+    return chain.layout()
 
 
 # ----------------------------------------------------------------------------------------------- TMA
@@ -442,23 +464,27 @@ TmaCheck = record("TmaCheck", ["feasible", ("reason", ""), ("hint", None)],
                   "Bulk-tensor-engine feasibility of a buffer, why not, and the materialised hint.", module=__name__)
 
 
-def check_tma(c, element_bits, *, max_dims=5, align_bytes=16, max_box=256):
-    """Can a bulk tensor copy serve this buffer? Few enough pieces, every extent within the box cap,
-    a 16-byte contiguous innermost run; the hint materialises the free strides."""
-    pieces = sum(map(len, c.splits))
-    if pieces > max_dims:
-        return TmaCheck(False, f"{pieces} dims exceed limit {max_dims}")
-    if max(c.dims) > max_box:
-        return TmaCheck(False, f"extent exceeds box cap {max_box}")
+def _contiguous_run(c):
     run = 1
     for e, s in sorted(c.concrete_modes(), key=lambda m: m[1]):
         run *= e if s == run else 1
-    if run * element_bits // 8 < align_bytes:
-        return TmaCheck(False, f"innermost contiguous run is {run * element_bits // 8}B < {align_bytes}B")
+    return run
+
+
+def check_tma(c, element_bits, *, max_dims=5, align_bytes=16, max_box=256):
+    """Can a bulk tensor copy serve this buffer? Few enough pieces, every extent within the box cap,
+    a 16-byte contiguous innermost run; the hint materialises the free strides."""
+    pieces, run_bytes = sum(map(len, c.splits)), _contiguous_run(c) * element_bits // 8
+    for broken, reason in ((pieces > max_dims, f"{pieces} dims exceed limit {max_dims}"),
+                           (max(c.dims) > max_box, f"extent exceeds box cap {max_box}"),
+                           (run_bytes < align_bytes, f"innermost contiguous run is {run_bytes}B < {align_bytes}B")):
+        if broken:
+            return TmaCheck(False, reason)
     try:
-        return TmaCheck(True, "", materialize(c))
+        hint = materialize(c)
     except Unsatisfiable as e:
         return TmaCheck(False, str(e))
+    return TmaCheck(True, "", hint)
 
 
 # ------------------------------------------------------------------------------------------ buffers
@@ -521,8 +547,8 @@ def synthesize_buffer(buffer, dims, element_bits, copies):
             for sw, table in ((best, hit.copy_conflicts), (IDENTITY_SWIZZLE, hit.identity_conflicts)):
                 table[c.op_index] = int(phase_degrees(sw(rows), width).max(initial=1))
         _MEMO[key] = hit
-    return SmemLayout(buffer, hit.layout, hit.swizzle, hit.element_bits, dict(hit.copy_conflicts),
-                      dict(hit.identity_conflicts), hit.constraint, list(hit.copies))
+    return dataclasses.replace(hit, buffer=buffer, copy_conflicts=dict(hit.copy_conflicts),
+                               identity_conflicts=dict(hit.identity_conflicts), copies=list(hit.copies))
 
 
 def access_patterns(m, element_bits, copy):
