@@ -62,6 +62,18 @@ constexpr int kSmemBudget = 225 * 1024;
 // experiment (-DW4A16_SPLITA=1): prefill k-half TMEM A units; measured slower (gate/up T=8192 3.57 vs
 // 3.43 ms), see the Cfg comment
 constexpr bool kSplitAEnv = W4A16_SPLITA != 0;
+#ifndef W4A16_DECODE_ACC4
+#define W4A16_DECODE_ACC4 1
+#endif
+// Decode (offset-mode) tiles hold 2 A slots + 4 accumulator stages (2 x 128 + 4 x 64 TMEM columns)
+// rather than 3 + 2. With 2 accumulator stages the MMA of stage j + 2 waits for the epilogue of stage
+// j, and at every tile end the epilogue spends ~1100-1350 cycles (stores, next tile's setup) before
+// its next fold, against ~500 mid-tile: the following MMA stalled ~700 cycles per tile
+// (tools/trace_down.sh: DS-R1 down, 16-stage tiles, stage period ~935 vs ~870 for 56-stage gate|up).
+// Measured same box (tools/gpu_ab_acc4.sh, DS-R1 layer): T=1 68.7 -> 64.2 us, T=16 452 -> 416 us,
+// T=64 908 -> 867 us, T=256 1115 -> 1084 us; Mixtral T=16 172 -> 162 us; Qwen3 unchanged.
+// -DW4A16_DECODE_ACC4=0 restores 3 + 2.
+constexpr bool kDecodeAcc4Env = W4A16_DECODE_ACC4 != 0;
 
 struct GemmArgs {
   const uint8_t* wblocks;        // [E][NT][KT][parts * kPartBytes]
@@ -151,11 +163,13 @@ struct Cfg {
   static constexpr bool kDual = kDualEnv && !kOffset && !kPair && !kSplitA;
   static constexpr int kACols = (kSplitA ? 1 : kParts) * (kTileK / 2);  // fp16 pairs per 32-bit column
   // TMEM budget (512 columns): A ring + accumulator ring
-  // 3 A slots if two accumulator stages still fit, else 2; the gated prefill projection (56-stage
+  // Decode tiles: 2 A slots + 4 accumulator stages (kDecodeAcc4Env). Otherwise 3 A slots if two
+  // accumulator stages still fit, else 2; the gated prefill projection (56-stage
   // tiles) instead prefers 3 A slots (dequant / MMA overlap) over a second accumulator stage
   // (epilogue / next-tile overlap, once per long tile); the short k-pair tiles need two.
   // Split ring: two accumulator stages if 6 units still fit, then as many units as fit (<= 8).
-  static constexpr int kNumA_ = (kOffset || !(kGated || kNPer == 2)) ? ((3 * kACols + 2 * kAccCols <= 512) ? 3 : 2)
+  static constexpr int kNumA_ = (kOffset && kDecodeAcc4Env) ? 2
+                              : (kOffset || !(kGated || kNPer == 2)) ? ((3 * kACols + 2 * kAccCols <= 512) ? 3 : 2)
                                                                    : ((3 * kACols + kAccCols <= 512) ? 3 : 2);
   static constexpr int kNumAccS = (2 * kAccCols + 6 * kACols <= 512) ? 2 : 1;
   static constexpr int kNumAS = (512 - kNumAccS * kAccCols) / kACols > 8 ? 8 : (512 - kNumAccS * kAccCols) / kACols;
