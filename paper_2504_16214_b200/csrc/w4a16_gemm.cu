@@ -52,9 +52,9 @@ constexpr int kTileTab = 512;  // per-CTA tile table entries in smem (later tile
 // are 10-25 % faster with the scale applied in the dequant).
 constexpr int kDecodeMaxNTok = 16;
 #ifndef W4A16_KSPLIT
-#define W4A16_KSPLIT 1
+#define W4A16_KSPLIT 0
 #endif
-constexpr bool kKSplitEnv = W4A16_KSPLIT != 0;  // experiment: -DW4A16_KSPLIT=0
+constexpr bool kKSplitEnv = W4A16_KSPLIT != 0;  // experiment: -DW4A16_KSPLIT=1 (see Cfg::kKSplit)
 constexpr int kSmemBudget = 225 * 1024;
 #ifndef W4A16_SPLITA
 #define W4A16_SPLITA 0
@@ -62,18 +62,23 @@ constexpr int kSmemBudget = 225 * 1024;
 // experiment (-DW4A16_SPLITA=1): prefill k-half TMEM A units; measured slower (gate/up T=8192 3.57 vs
 // 3.43 ms), see the Cfg comment
 constexpr bool kSplitAEnv = W4A16_SPLITA != 0;
-#ifndef W4A16_DECODE_ACC4
-#define W4A16_DECODE_ACC4 1
+#ifndef W4A16_DECODE_NUMA
+#define W4A16_DECODE_NUMA 2
 #endif
-// Decode (offset-mode) tiles hold 2 A slots + 4 accumulator stages (2 x 128 + 4 x 64 TMEM columns)
-// rather than 3 + 2. With 2 accumulator stages the MMA of stage j + 2 waits for the epilogue of stage
-// j, and at every tile end the epilogue spends ~1100-1350 cycles (stores, next tile's setup) before
-// its next fold, against ~500 mid-tile: the following MMA stalled ~700 cycles per tile
-// (tools/trace_down.sh: DS-R1 down, 16-stage tiles, stage period ~935 vs ~870 for 56-stage gate|up).
-// Measured same box (tools/gpu_ab_acc4.sh, DS-R1 layer): T=1 68.7 -> 64.2 us, T=16 452 -> 416 us,
-// T=64 908 -> 867 us, T=256 1115 -> 1084 us; Mixtral T=16 172 -> 162 us; Qwen3 unchanged.
-// -DW4A16_DECODE_ACC4=0 restores 3 + 2.
-constexpr bool kDecodeAcc4Env = W4A16_DECODE_ACC4 != 0;
+#ifndef W4A16_DECODE_MAXACC
+#define W4A16_DECODE_MAXACC 8
+#endif
+// Decode (offset-mode) TMEM split: A slots (if two accumulator stages still fit) and the cap on
+// accumulator stages. With 3 A + 2 accumulator stages the MMA of stage j + 2 waited for the epilogue
+// of stage j, and at every tile end the epilogue spends ~1100-1350 cycles (stores, next tile's
+// setup) before its next fold, against ~500 mid-tile: the following MMA stalled ~700 cycles per tile
+// (tools/trace_down.sh: DS-R1 down, 16-stage tiles). 2 A + 4 accumulator stages, same box
+// (tools/gpu_ab_acc4.sh, DS-R1 layer): T=1 68.7 -> 64.2 us, T=16 452 -> 416 us, T=64 908 -> 867 us,
+// T=256 1115 -> 1084 us; Mixtral T=16 172 -> 162 us; Qwen3 unchanged. With one k-chain per part
+// (32-column accumulator stages) up to 8 stages fit beside 2 A slots; 3 A slots + 4 stages was
+// slower at every decode size (T=64 862 -> 910-920 us, tools/gpu_ab_knobs.sh).
+constexpr int kDecodeNumA = W4A16_DECODE_NUMA;
+constexpr int kDecodeMaxAcc = W4A16_DECODE_MAXACC;
 
 struct GemmArgs {
   const uint8_t* wblocks;        // [E][NT][KT][parts * kPartBytes]
@@ -135,9 +140,12 @@ struct Cfg {
   static constexpr int kXBytes = kGroupsPerStage * kXRows * kTileK * 2;  // X tile, 64-wide 128B-swizzle atoms
   // (C, S) fp32 per group/token, padded to one 8-byte slot per producer lane (see the sums copy)
   static constexpr int kSumBytes = kOffset ? (kGroupsPerStage * kNTok > 32 ? kGroupsPerStage * kNTok : 32) * 8 : 0;
-  // offset mode: each part's 128-k partial is split over kKSplit independent accumulators (k halves)
-  // so a stage issues kParts * kKSplit interleaved MMA chains -- a dependent chain of small-N MMAs is
-  // bound by the accumulate latency, not by the tensor pipe
+  // offset mode, experiment: each part's 128-k partial split over kKSplit = 2 independent
+  // accumulators (k halves), kParts * kKSplit interleaved MMA chains per stage. It helped with two
+  // accumulator stages; with the deeper ring (below) one chain per part is faster (DS-R1 layer
+  // T=64 868 -> 862 us, T=256 1.09-1.14 -> 1.06-1.08 ms, Mixtral T=16 162 -> 159 us;
+  // tools/gpu_ab_knobs.sh) -- tools/microbench/mma_stage.cu: a stage's 16 MMAs complete in ~250
+  // cycles streamed either way, so the chains were never the tensor pipe's limit
   static constexpr int kKSplit = (kOffset && kNTok == 16 && kKSplitEnv) ? 2 : 1;
   static constexpr int kChainLen = (kTileK / 16) / kKSplit;
   // one accumulator stage: offset mode = kKSplit partials per part; otherwise gate|up or one
@@ -163,18 +171,19 @@ struct Cfg {
   static constexpr bool kDual = kDualEnv && !kOffset && !kPair && !kSplitA;
   static constexpr int kACols = (kSplitA ? 1 : kParts) * (kTileK / 2);  // fp16 pairs per 32-bit column
   // TMEM budget (512 columns): A ring + accumulator ring
-  // Decode tiles: 2 A slots + 4 accumulator stages (kDecodeAcc4Env). Otherwise 3 A slots if two
+  // Decode tiles: kDecodeNumA A slots, up to kDecodeMaxAcc accumulator stages. Otherwise 3 A slots if two
   // accumulator stages still fit, else 2; the gated prefill projection (56-stage
   // tiles) instead prefers 3 A slots (dequant / MMA overlap) over a second accumulator stage
   // (epilogue / next-tile overlap, once per long tile); the short k-pair tiles need two.
   // Split ring: two accumulator stages if 6 units still fit, then as many units as fit (<= 8).
-  static constexpr int kNumA_ = (kOffset && kDecodeAcc4Env) ? 2
-                              : (kOffset || !(kGated || kNPer == 2)) ? ((3 * kACols + 2 * kAccCols <= 512) ? 3 : 2)
+  static constexpr int kNumA_ = kOffset ? ((kDecodeNumA * kACols + 2 * kAccCols <= 512) ? kDecodeNumA : 2)
+                              : !(kGated || kNPer == 2) ? ((3 * kACols + 2 * kAccCols <= 512) ? 3 : 2)
                                                                    : ((3 * kACols + kAccCols <= 512) ? 3 : 2);
   static constexpr int kNumAccS = (2 * kAccCols + 6 * kACols <= 512) ? 2 : 1;
   static constexpr int kNumAS = (512 - kNumAccS * kAccCols) / kACols > 8 ? 8 : (512 - kNumAccS * kAccCols) / kACols;
   static constexpr int kNumAccO = (512 - kNumA_ * kACols) / kAccCols;
-  static constexpr int kNumAcc = kSplitA ? kNumAccS : (kNumAccO > (kOffset ? 4 : 2) ? (kOffset ? 4 : 2) : kNumAccO);
+  static constexpr int kMaxAcc = kOffset ? kDecodeMaxAcc : 2;
+  static constexpr int kNumAcc = kSplitA ? kNumAccS : (kNumAccO > kMaxAcc ? kMaxAcc : kNumAccO);
   static constexpr int kNumA = kSplitA ? kNumAS : kNumA_;
   static constexpr int kStageBytes = kBlk + kXBytes + kSumBytes;
   // barriers, m-tile prefix, tile table, epilogue cross-warp reduction scratch (4 warps x 16 x float2)
@@ -908,6 +917,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             else mbar_arrive(&accempty[acc.i]);
             mbar_arrive(&empty[st.i]);
           }
+          if (tre) trace_at(tr, 22, egs - 1);
           acc.next(C::kNumAcc);
           st.next(C::kNS);
         }

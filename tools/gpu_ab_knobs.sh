@@ -1,4 +1,4 @@
-# A/B: decode TMEM split 3 A + 2 accumulator stages (v=0) vs 2 A + 4 (v=1)
+# A/B of compile-time knobs on the layer sweep: each line "NAME=VALUE ..." is one build
 sweep() {
   python tools/layer_sweep.py --model ds --tokens 1,16,64,256 --reps 30 2>&1 | grep '"T"' | python -c "
 import sys, json
@@ -8,12 +8,9 @@ import sys, json
 for l in sys.stdin: d=json.loads(l); print('  ', d['model'], 'T', d['T'], d['ms'], d['hbm_frac'])"
 }
 for rep in 1 2; do
-  for v in 0 1; do
-    if [ $v = 0 ]; then k="W4A16_DECODE_NUMA=3 W4A16_DECODE_MAXACC=2"; else k="X=1"; fi; env $k python -m paper_2504_16214_b200._build > /dev/null
-    echo "== $k rep $rep"
-    if [ $rep = 1 ] && [ $v = 1 ]; then
-      timeout 600 python -m pytest tests/test_gpu_moe.py tests/test_gpu_shapes.py -x -q -p no:cacheprovider 2>&1 | tail -2
-    fi
+  for cfg in "$@"; do
+    env $cfg python -m paper_2504_16214_b200._build > /dev/null
+    echo "== $cfg rep $rep"
     sweep
   done
 done

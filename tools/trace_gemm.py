@@ -38,7 +38,7 @@ nout = N // 2 if gated else N
 xs = ops.group_sums(x) if a.ntok <= 32 else None
 for _ in range(2):
     ops.grouped_gemm(x, w.blocks, E, nout, gated, counts, off, a.ntok, xsum=xs)
-buf = torch.full((22, 4096), -1, dtype=torch.int64, device=dev)
+buf = torch.full((24, 4096), -1, dtype=torch.int64, device=dev)
 _lib.call("w4a16_debug_trace_cta", a.cta)
 _lib.call("w4a16_debug_trace", buf.data_ptr())
 torch.cuda.synchronize()
