@@ -9,7 +9,18 @@
 
 namespace w4 {
 
-__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#ifndef W4A16_EARLY_PDL
+#define W4A16_EARLY_PDL 0
+#endif
+// After its own wait a kernel lets the next kernel in the stream launch (-DW4A16_EARLY_PDL=1):
+// without the explicit trigger the dependent launches only as this grid's blocks exit. Safe because
+// every kernel here waits (griddep_wait) before it reads or writes anything another kernel touches.
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#if W4A16_EARLY_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 
 inline bool pdl_enabled() {
   static const bool on = [] {

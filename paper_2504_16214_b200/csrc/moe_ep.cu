@@ -246,20 +246,27 @@ int w4a16_moe_forward_ep(w4a16_ep_comm* comm, const void* x, int64_t T, int64_t 
   if (T <= 0) return W4_OK;
   const int64_t Tg = T * comm->world;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
+  // the local layer's workspace first (its stream-K counters at offset 0 for every T)
+  const int nt = ep_ntok(T, comm->world, topk, local_experts);
+  const int64_t ga = w4a16_grouped_gemm_ws_bytes(Tg * topk, H, local_experts, I, 1, nt);
+  const int64_t gb = w4a16_grouped_gemm_ws_bytes(Tg * topk, I, local_experts, H, 0, nt);
+  void* inner = ws;
+  const int64_t inner_bytes =
+      align256(w4a16_moe_workspace_bytes(Tg, topk, local_experts, H, I)) + align256(ga > gb ? ga : gb);
+  ws += inner_bytes;
   void* x_all = ws; ws += align256(2 * Tg * H);
   int32_t* ids_all = reinterpret_cast<int32_t*>(ws); ws += align256(4 * Tg * topk);
   float* w_all = reinterpret_cast<float*>(ws); ws += align256(4 * Tg * topk);
   int32_t* ids_loc = reinterpret_cast<int32_t*>(ws); ws += align256(4 * Tg * topk);
   float* partial = reinterpret_cast<float*>(ws); ws += align256(4 * Tg * H);
-  float* reduced = reinterpret_cast<float*>(ws); ws += align256(4 * T * H);
-  const int64_t rest = workspace_bytes - (ws - static_cast<uint8_t*>(workspace));
+  float* reduced = reinterpret_cast<float*>(ws);
   int rc;
   if ((rc = w4a16_ep_dispatch(comm, x, topk_ids, topk_weights, T, H, topk, dtype, x_all, ids_all, w_all, stream)))
     return rc;
   if ((rc = w4a16_ep_localize(ids_all, Tg * topk, comm->rank * local_experts, local_experts, ids_loc, stream)))
     return rc;
-  if ((rc = w4a16_moe_forward_f32(x_all, Tg, H, I, local_experts, topk, ids_loc, w_all, w13, w2, dtype, partial,
-                                  ep_ntok(T, comm->world, topk, local_experts), ws, rest, stream)))
+  if ((rc = w4a16_moe_forward_f32(x_all, Tg, H, I, local_experts, topk, ids_loc, w_all, w13, w2, dtype, partial, nt,
+                                  inner, inner_bytes, stream)))
     return rc;
   return w4a16_ep_combine(comm, partial, T, H, dtype, reduced, y, stream);
 }

@@ -644,10 +644,14 @@ using namespace w4;
 
 namespace {
 inline int64_t align256(int64_t b) { return (b + 255) & ~int64_t(255); }
+// the GEMMs' workspace for the picked token tile or a forced decode (16-token) one, whichever is larger
 int64_t splitk_bytes(int64_t P, int64_t E, int64_t H, int64_t I) {
-  const int nt = w4a16_pick_ntok(P, E);
-  const int64_t a = w4a16_grouped_gemm_ws_bytes(P, H, E, I, 1, nt), b = w4a16_grouped_gemm_ws_bytes(P, I, E, H, 0, nt);
-  return a > b ? a : b;
+  int64_t m = 0;
+  for (const int nt : {w4a16_pick_ntok(P, E), 16}) {
+    const int64_t a = w4a16_grouped_gemm_ws_bytes(P, H, E, I, 1, nt), b = w4a16_grouped_gemm_ws_bytes(P, I, E, H, 0, nt);
+    m = std::max(m, std::max(a, b));
+  }
+  return m;
 }
 }  // namespace
 
@@ -874,8 +878,7 @@ int64_t w4a16_moe_workspace_bytes(int64_t T, int64_t topk, int64_t E, int64_t H,
 }  // extern "C"
 
 namespace {
-// ntok: the token tile (0 = w4a16_pick_ntok(T * topk, E)); the split-K workspace is whatever the caller's
-// workspace holds past the fixed buffers
+// ntok: the token tile (0 = w4a16_pick_ntok(T * topk, E))
 int moe_forward_impl(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, int64_t topk,
                      const int32_t* topk_ids, const float* topk_weights, const uint8_t* w13, const uint8_t* w2,
                      int dtype, void* y, bool f32_out, int ntok, void* workspace, int64_t workspace_bytes,
@@ -887,6 +890,11 @@ int moe_forward_impl(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, 
   const int64_t P = T * topk;
   const int64_t ld = w4a16_group_sums_ld(P);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
+  // the GEMMs' workspace first: its leading stream-K counters then sit at a fixed offset (0) for every
+  // T, so "zero once, left zero by every call" holds across calls of different sizes
+  void* kws = ws;
+  const int64_t kws_bytes = align256(splitk_bytes(P, E, H, I));
+  ws += kws_bytes;
   int32_t* counts = reinterpret_cast<int32_t*>(ws); ws += align256(4 * E);
   int32_t* offsets = reinterpret_cast<int32_t*>(ws); ws += align256(4 * (E + 1));
   int32_t* sorted = reinterpret_cast<int32_t*>(ws); ws += align256(4 * P);
@@ -896,9 +904,7 @@ int moe_forward_impl(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, 
   void* yp = ws; ws += align256(2 * P * H);
   float* xsum = reinterpret_cast<float*>(ws); ws += align256(8 * ld * (H / 128));
   float* hsum = reinterpret_cast<float*>(ws); ws += align256(8 * ld * (I / 128));
-  void* pws = ws; ws += align256(w4a16_moe_permute_ws_bytes(P, E));
-  void* kws = ws;
-  const int64_t kws_bytes = workspace_bytes - (ws - static_cast<uint8_t*>(workspace));
+  void* pws = ws;
   int rc;
   if ((rc = w4a16_moe_permute_ws(topk_ids, P, E, counts, offsets, sorted, pos, pws,
                                  w4a16_moe_permute_ws_bytes(P, E), stream)))

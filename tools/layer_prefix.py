@@ -29,7 +29,7 @@ def run(model, T):
     hbuf = torch.empty((P, I), dtype=torch.float16, device=dev)
     hs = torch.empty(ops.sums_shape(P, I), dtype=torch.float32, device=dev)
     yp = torch.empty((P, H), dtype=torch.float16, device=dev)
-    gws = [torch.empty(max(ops.gemm_ws_bytes(P, k_, E, n_, g_, nt), 1), dtype=torch.uint8, device=dev)
+    gws = [torch.zeros(max(ops.gemm_ws_bytes(P, k_, E, n_, g_, nt), 1), dtype=torch.uint8, device=dev)
            for k_, n_, g_ in ((H, I, True), (I, H, False))]
     small = P <= 64
     stages = ["route+permute", "gather", "gate_up", "down", "combine"]

@@ -37,12 +37,12 @@ def main():
     hs = torch.empty(ops.sums_shape(P, I), dtype=torch.float32, device=dev)
     for nt in (16, 32, 64, 128):
         dec = nt == 16
-        gu_ws = torch.empty(max(ops.gemm_ws_bytes(P, H, E, I, True, nt), 1), dtype=torch.uint8, device=dev)
+        gu_ws = torch.zeros(max(ops.gemm_ws_bytes(P, H, E, I, True, nt), 1), dtype=torch.uint8, device=dev)
         h = ops.grouped_gemm(xp, w13.blocks, E, I, True, c, o, nt, xsum=xs if dec else None, workspace=gu_ws,
                              osum=hs if dec else None)
         if dec:
             ops.group_sums(h, o[E:], out=hs)
-        dn_ws = torch.empty(max(ops.gemm_ws_bytes(P, I, E, H, False, nt), 1), dtype=torch.uint8, device=dev)
+        dn_ws = torch.zeros(max(ops.gemm_ws_bytes(P, I, E, H, False, nt), 1), dtype=torch.uint8, device=dev)
         y = ops.grouped_gemm(h, w2.blocks, E, H, False, c, o, nt, xsum=hs if dec else None, workspace=dn_ws)
         ops.grouped_gemm_gather(x, sp, k, w13.blocks, E, I, True, c, o, nt, xsum=ops.group_sums(x) if dec else None,
                                 rows=P)
@@ -54,7 +54,7 @@ def main():
     ids1 = torch.tensor([[1, 5]], dtype=torch.int32, device=dev)
     c1, o1, sp1, pp1 = ops.moe_permute(ids1, E)
     xp1, xs1 = ops.moe_gather_sums(x[:1], sp1, 2, 2, o1[E:])
-    sk = torch.empty(max(ops.gemm_ws_bytes(2, H, E, I, True, 16), 1), dtype=torch.uint8, device=dev)
+    sk = torch.zeros(max(ops.gemm_ws_bytes(2, H, E, I, True, 16), 1), dtype=torch.uint8, device=dev)
     ops.grouped_gemm(xp1, w13.blocks, E, I, True, c1, o1, 16, xsum=xs1, workspace=sk)
     loc = ops.ep_localize(ids, 4, 8)
     ops.dequant(w2.blocks[: w2.blocks.numel() // E], 1, H, I, 1, torch.float16)

@@ -21,6 +21,8 @@ ap.add_argument("--experts", type=int, default=224)
 ap.add_argument("--per-expert", type=int, default=2)
 ap.add_argument("--ntok", type=int, default=16)
 ap.add_argument("--cta", type=int, default=0, help="CTA whose timeline is recorded")
+ap.add_argument("--nk", default="", help="N,K override (e.g. 14336,4096 for the Llama-3-8B linear)")
+ap.add_argument("--dump", action="store_true", help="every stage's MMA-ready / epilogue-done time")
 ap.add_argument("--xscale", type=float, default=0.5, help="0 = all-zero activations (data-dependent power probe)")
 a = ap.parse_args()
 H, I = 7168, 2048
@@ -29,6 +31,9 @@ E = a.experts
 gd = torch.Generator(device=dev).manual_seed(1)
 gated = a.which == "gate_up"
 N, K = (2 * I, H) if gated else (H, I)
+if a.nk:
+    N, K = (int(v) for v in a.nk.split(","))
+    N = 2 * N if gated else N
 w = random_packed(E, N, K, gated, torch.float16, gd, dev)
 counts = torch.full((E,), a.per_expert, dtype=torch.int32, device=dev)
 off = torch.zeros(E + 1, dtype=torch.int32, device=dev)
@@ -36,13 +41,15 @@ off[1:] = torch.cumsum(counts, 0)
 x = (torch.randn((E * a.per_expert, K), device=dev) * a.xscale).half()
 nout = N // 2 if gated else N
 xs = ops.group_sums(x) if a.ntok <= 32 else None
+rows = E * a.per_expert
+ws = torch.zeros(max(ops.gemm_ws_bytes(rows, K, E, nout, gated, a.ntok), 1), dtype=torch.uint8, device=dev)
 for _ in range(2):
-    ops.grouped_gemm(x, w.blocks, E, nout, gated, counts, off, a.ntok, xsum=xs)
-buf = torch.full((24, 4096), -1, dtype=torch.int64, device=dev)
+    ops.grouped_gemm(x, w.blocks, E, nout, gated, counts, off, a.ntok, xsum=xs, workspace=ws)
+buf = torch.full((30, 4096), -1, dtype=torch.int64, device=dev)
 _lib.call("w4a16_debug_trace_cta", a.cta)
 _lib.call("w4a16_debug_trace", buf.data_ptr())
 torch.cuda.synchronize()
-ops.grouped_gemm(x, w.blocks, E, nout, gated, counts, off, a.ntok, xsum=xs)
+ops.grouped_gemm(x, w.blocks, E, nout, gated, counts, off, a.ntok, xsum=xs, workspace=ws)
 torch.cuda.synchronize()
 _lib.call("w4a16_debug_trace", None)
 t = buf.cpu().numpy()
@@ -51,7 +58,7 @@ t0 = t[t >= 0].min()
 t = np.where(t >= 0, t - t0, -1)
 lo, hi = n // 4, 3 * n // 4
 s = slice(lo, hi)
-print(f"{a.which}: stages traced {n}, steady window [{lo},{hi})")
+print(f"{a.which}: stages traced {n}, steady window [{lo},{hi}); CTA span (first to last event) {t.max()} cyc")
 per = np.diff(t[4][s] if (t[4] >= 0).sum() else t[1][s]).mean()
 print(f"  stage period (mma_ready diffs)          {per:8.1f} cyc")
 def m(x):
@@ -95,3 +102,28 @@ print(f"  tiles traced {len(ts)}")
 print("  first 12 stages (cycles rel.):")
 for i in range(lo, lo + 12):
     print("   ", i, " ".join(f"{EV[e][:10]}={t[e][i]}" for e in (0, 1, 2, 3, 4, 5, 7, 8)))
+
+if a.dump:
+    print("  stage: prod_empty_ok dq_full_ok mma_ready mma_issued epi_accfull epi_done (cycles from the first event)")
+    r = buf.cpu().numpy()[:10]
+    z = r[r >= 0].min()
+    r = np.where(r >= 0, r - z, -1)
+    for i in range(n):
+        print(f"  S{i:3d} {r[0][i]:8d} {r[1][i]:8d} {r[4][i]:8d} {r[5][i]:8d} {r[7][i]:8d} {r[8][i]:8d}")
+    print("  epilogue tile starts:", r[9][r[9] >= 0].tolist(), " last epilogue done:", int(r[8].max()))
+    rr = buf.cpu().numpy()[22:26]
+    rr = np.where(rr >= 0, rr - z, -1)
+    print("  stream-K piece: partial out (by item):", rr[1][rr[1] >= 0].tolist(), " flag known:", rr[2][rr[2] >= 0].tolist(), " exit barrier:", rr[3][rr[3] >= 0].tolist())
+    w26 = buf.cpu().numpy()[26][:16]
+    print("  warp arrivals at the exit barrier:", [int(v - z) if v >= 0 else -1 for v in w26])
+
+if a.dump:
+    g = buf.cpu().numpy()[28:30, :148]
+    ok = g[0] > 0
+    if ok.any():
+        t0 = g[0][ok].min()
+        ent, ex = (g[0][ok] - t0) / 1e3, (g[1][ok] - t0) / 1e3
+        order = np.argsort(-ex)
+        print(f"  CTA entry (us): min {ent.min():.2f} max {ent.max():.2f}; exit: min {ex.min():.2f} median "
+              f"{np.median(ex):.2f} max {ex.max():.2f}; latest CTAs: " +
+              ", ".join(f"{int(np.nonzero(ok)[0][j])}@{ex[j]:.2f}" for j in order[:6]))
