@@ -160,17 +160,11 @@ int w4a16_grouped_gemm(const void* x, int64_t rows, int64_t K, const uint8_t* wb
                        const float* xsum, void* out, int dtype, int ntok, cudaStream_t stream);
 int w4a16_pick_ntok(int64_t rows, int64_t num_experts);
 
-/* Same, with a caller workspace for decode mode (16-token offset-code tiles) when the (expert,
- * n-tile) tiles cannot fill the GPU evenly (e.g. one token touching 8 experts: 128 gate/up tiles for
- * 148 SMs). Stream-K (default): the whole waves of tiles run as usual and the stages of the remaining
- * tiles are cut into one contiguous range per SM; each piece writes an fp32 partial to ws and the
- * last piece of a tile to finish (an atomic counter in ws) sums the partials in piece order --
- * deterministic -- and runs the tile's epilogue. W4A16_STREAMK=0 (environment): split-K instead, the
- * k-groups split over CTAs and summed by a finalize kernel.
- * ws: zero-filled before its first use. Its first 1024 bytes are the stream-K tile counters, which
- * every launch leaves at zero; the rest is scratch. ws_bytes >= w4a16_grouped_gemm_ws_bytes(...) (0
- * when neither is planned); a smaller workspace disables both. osum (optional): also produce the
- * output's group sums (w4a16_group_sums
+/* Same, with a caller workspace that enables split-K in decode mode when the (expert, n-tile) tiles
+ * cannot fill the GPU (e.g. one token touching 8 experts): the k-groups of a tile are split over
+ * several CTAs writing fp32 partials to ws, then summed (and SiLU*up applied) by a finalize kernel.
+ * ws_bytes >= w4a16_grouped_gemm_ws_bytes(...) (0 when no split is planned); a smaller workspace
+ * just disables split-K. osum (optional): also produce the output's group sums (w4a16_group_sums
  * layout) -- the next GEMM's xsum; the decode gate/up epilogue computes them in place (gated, xsum
  * given, 16-token tiles, no split-K; otherwise a w4a16_group_sums pass follows the GEMM). out_rows
  * (optional): row i of the result is written to out row out_rows[i] (e.g. straight back into
@@ -194,10 +188,7 @@ int64_t w4a16_grouped_gemm_ws_bytes(int64_t rows, int64_t K, int64_t num_experts
                                     int ntok);
 
 /* ---- whole layer ------------------------------------------------------------------------------- */
-/* Workspace for w4a16_moe_forward with T tokens, top-k, E experts, hidden H, intermediate I. Zero-fill
- * it once after allocation: its first 1024 bytes are the GEMMs' stream-K tile counters (at offset 0
- * for every T, left zero by every call); the rest is scratch. The same holds for the expert-parallel
- * workspace (w4a16_moe_ep_workspace_bytes). */
+/* Workspace for w4a16_moe_forward with T tokens, top-k, E experts, hidden H, intermediate I. */
 int64_t w4a16_moe_workspace_bytes(int64_t T, int64_t topk, int64_t E, int64_t H, int64_t I);
 
 /* y = MoE(x) for precomputed routing: permute -> gather -> gate/up GEMM (+SiLU*up) -> down GEMM ->

@@ -246,7 +246,7 @@ int w4a16_moe_forward_ep(w4a16_ep_comm* comm, const void* x, int64_t T, int64_t 
   if (T <= 0) return W4_OK;
   const int64_t Tg = T * comm->world;
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  // the local layer's workspace first (its stream-K counters at offset 0 for every T)
+  // the local layer's workspace first
   const int nt = ep_ntok(T, comm->world, topk, local_experts);
   const int64_t ga = w4a16_grouped_gemm_ws_bytes(Tg * topk, H, local_experts, I, 1, nt);
   const int64_t gb = w4a16_grouped_gemm_ws_bytes(Tg * topk, I, local_experts, H, 0, nt);

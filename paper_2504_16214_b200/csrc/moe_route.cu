@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include "ptx.cuh"
@@ -505,9 +506,10 @@ __global__ void moe_gather_kernel(const uint4* __restrict__ x, int64_t hv, int t
                                   uint4* __restrict__ xp) {
   griddep_wait();  // PDL: inputs written by the previous kernel in the stream
   const int64_t p = blockIdx.x;
-  if (row_limit && p >= __ldg(row_limit)) return;
-  const int64_t t = __ldg(sorted_pairs + p) / topk;
-  const uint4* src = x + t * hv;
+  const int lim = row_limit ? __ldg(row_limit) : 0x7fffffff;
+  const int src_row = __ldg(sorted_pairs + p);  // (in flight with the limit's load)
+  if (p >= lim) return;
+  const uint4* src = x + static_cast<int64_t>(src_row / topk) * hv;
   uint4* dst = xp + p * hv;
   for (int64_t i = threadIdx.x; i < hv; i += blockDim.x) dst[i] = __ldg(src + i);
 }
@@ -537,16 +539,21 @@ __device__ __forceinline__ void vec_sums(const uint4& v, float& c, float& s) {
   }
 }
 
-// One CTA (128 threads) per row: thread vectors i = it*128 + tid; the 16 vectors of one group sit on
-// 16 consecutive lanes, reduced with xor shuffles. `src_rows` (gather) maps output row -> input row.
+// One CTA per row, sized to the row (sums_threads: up to 1024 threads, one 16-byte vector each), so
+// a row costs one dependent global round trip instead of one per 128 vectors (DS-R1 H=7168: 7 of
+// them); the 16 vectors of one group sit on 16 consecutive lanes, reduced with xor shuffles. The
+// row limit and the gather index are loaded together. `sorted_pairs` (gather) maps output row ->
+// input row.
 template <bool kBF16, bool kGather>
 __global__ void group_sums_kernel(const uint4* __restrict__ x, int64_t hv, int topk,
                                   const int32_t* __restrict__ sorted_pairs, const int32_t* __restrict__ row_limit,
                                   uint4* __restrict__ xp, int64_t ld, float2* __restrict__ xsum) {
   griddep_wait();  // PDL: inputs written by the previous kernel in the stream
   const int64_t p = blockIdx.x;
-  if (row_limit && p >= __ldg(row_limit)) return;
-  const uint4* src = kGather ? x + static_cast<int64_t>(__ldg(sorted_pairs + p) / topk) * hv : x + p * hv;
+  const int lim = row_limit ? __ldg(row_limit) : 0x7fffffff;
+  const int src_row = kGather ? __ldg(sorted_pairs + p) : 0;  // (in flight with the limit's load)
+  if (p >= lim) return;
+  const uint4* src = kGather ? x + static_cast<int64_t>(src_row / topk) * hv : x + p * hv;
   uint4* dst = kGather ? xp + p * hv : nullptr;
   const int lane = threadIdx.x & 31;
   for (int64_t base = 0; base < hv; base += blockDim.x) {
@@ -622,12 +629,23 @@ __global__ void moe_combine_kernel(const uint4* __restrict__ yp, int64_t hv, int
   __syncthreads();
   if (i >= hv) return;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int j = 0; j < topk; ++j) {
-    if (pos[j] < 0) continue;
-    float f[8];
-    unpack8<kBF16>(__ldg(yp + static_cast<int64_t>(pos[j]) * hv + i), f);
+  // up to 8 expert rows' loads in flight at once, then the fmas in slot order (same sum as one by one)
+  for (int j0 = 0; j0 < topk; j0 += 8) {
+    uint4 v[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = fmaf(wt[j], f[q], acc[q]);
+    for (int q = 0; q < 8; ++q) {
+      const int ps = j0 + q < topk ? pos[j0 + q] : -1;
+      v[q] = ps >= 0 ? __ldg(yp + static_cast<int64_t>(ps) * hv + i) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (j0 + q < topk && pos[j0 + q] >= 0) {
+        float f[8];
+        unpack8<kBF16>(v[q], f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = fmaf(wt[j0 + q], f[e], acc[e]);
+      }
+    }
   }
   if constexpr (kF32Out) {
     float4* o = static_cast<float4*>(y) + 2 * (t * hv + i);
@@ -644,6 +662,8 @@ using namespace w4;
 
 namespace {
 inline int64_t align256(int64_t b) { return (b + 255) & ~int64_t(255); }
+// threads per group_sums CTA: the row's 16-byte vectors rounded up to a warp, at most 1024
+inline int sums_threads(int64_t hv) { return static_cast<int>(std::min<int64_t>(1024, (hv + 31) / 32 * 32)); }
 // the GEMMs' workspace for the picked token tile or a forced decode (16-token) one, whichever is larger
 int64_t splitk_bytes(int64_t P, int64_t E, int64_t H, int64_t I) {
   int64_t m = 0;
@@ -804,10 +824,10 @@ int w4a16_moe_gather_sums(const void* x, int64_t H, int64_t topk, const int32_t*
   const int64_t ld = w4a16_group_sums_ld(rows);
   auto* xs = reinterpret_cast<float2*>(xsum);
   if (dtype == W4_DTYPE_BF16)
-    launch_pdl(group_sums_kernel<true, true>, rows, 128, 0, stream, static_cast<const uint4*>(x), H / 8, (int)topk,
+    launch_pdl(group_sums_kernel<true, true>, rows, sums_threads(H / 8), 0, stream, static_cast<const uint4*>(x), H / 8, (int)topk,
                                                             sorted_pairs, row_limit, static_cast<uint4*>(x_perm), ld, xs);
   else if (dtype == W4_DTYPE_F16)
-    launch_pdl(group_sums_kernel<false, true>, rows, 128, 0, stream, static_cast<const uint4*>(x), H / 8, (int)topk,
+    launch_pdl(group_sums_kernel<false, true>, rows, sums_threads(H / 8), 0, stream, static_cast<const uint4*>(x), H / 8, (int)topk,
                                                              sorted_pairs, row_limit, static_cast<uint4*>(x_perm), ld, xs);
   else
     return W4_ERR_DTYPE;
@@ -822,10 +842,10 @@ int w4a16_group_sums(const void* x, int64_t rows, int64_t K, const int32_t* row_
   const int64_t ld = w4a16_group_sums_ld(rows);
   auto* xs = reinterpret_cast<float2*>(xsum);
   if (dtype == W4_DTYPE_BF16)
-    launch_pdl(group_sums_kernel<true, false>, rows, 128, 0, stream, static_cast<const uint4*>(x), K / 8, 1, nullptr,
+    launch_pdl(group_sums_kernel<true, false>, rows, sums_threads(K / 8), 0, stream, static_cast<const uint4*>(x), K / 8, 1, nullptr,
                                                              row_limit, nullptr, ld, xs);
   else if (dtype == W4_DTYPE_F16)
-    launch_pdl(group_sums_kernel<false, false>, rows, 128, 0, stream, static_cast<const uint4*>(x), K / 8, 1, nullptr,
+    launch_pdl(group_sums_kernel<false, false>, rows, sums_threads(K / 8), 0, stream, static_cast<const uint4*>(x), K / 8, 1, nullptr,
                                                               row_limit, nullptr, ld, xs);
   else
     return W4_ERR_DTYPE;
@@ -890,9 +910,7 @@ int moe_forward_impl(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, 
   const int64_t P = T * topk;
   const int64_t ld = w4a16_group_sums_ld(P);
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  // the GEMMs' workspace first: its leading stream-K counters then sit at a fixed offset (0) for every
-  // T, so "zero once, left zero by every call" holds across calls of different sizes
-  void* kws = ws;
+  void* kws = ws;  // the GEMMs' (split-K) workspace first
   const int64_t kws_bytes = align256(splitk_bytes(P, E, H, I));
   ws += kws_bytes;
   int32_t* counts = reinterpret_cast<int32_t*>(ws); ws += align256(4 * E);

@@ -100,11 +100,6 @@ struct GemmArgs {
   const int32_t* gather_rows;
   int gather_div;
   int direct_rows;               // offset-mode tiles with <= this many real tokens store unstaged (<= kDirectRows)
-  // stream-K remainder (decode mode, see Sched): on/off, minimum stages per CTA range, the estimated
-  // per-piece cost in stages, tile counters (zero between launches) and the pieces' fp32 partials
-  int sk, sk_lmin, sk_fix, sk_min_stages, sk_min_waves;
-  int* sk_cnt;
-  float* sk_part;
 };
 
 // Numeric modes.
@@ -127,7 +122,6 @@ constexpr int kModeGateUp = 1;  // part 0 = gate rows, part 1 = up rows, same k-
 constexpr int kModeKPair = 2;   // parts = two consecutive k-groups of the same rows (down proj.)
 constexpr int kModeNPair = 3;   // parts = one k-group of two adjacent n-tiles sharing the X tile (prefill)
 constexpr int kEpiChunk = 4;    // offset-mode epilogue token granularity
-constexpr int kSkMaxPieces = 8;  // stream-K pieces per tile (L >= ceil(stages / (kSkMaxPieces - 1)))
 constexpr int kDirectRows = 4;  // max of GemmArgs::direct_rows (W4A16_DIRECT_ROWS overrides the default 4; 0 = off)
 
 // kPair: a CTA pair (cluster of 2 on one TPC) runs tcgen05.mma.cta_group::2 -- M = 256 weight rows
@@ -239,26 +233,6 @@ __device__ __forceinline__ void progress_at(int ev, uint32_t n) {
 
 struct TileInfo {
   int e, n_tile, m_start, m_rows, split;
-  int k0, k1;  // stages [k0, k1) of the tile (all of them, a split-K unit, or a stream-K piece)
-  int sk;      // stream-K tile index (-1: a whole tile or split-K unit)
-  int sk_q, sk_np, sk_slot0;  // this piece's index among the tile's sk_np pieces; partial slot of piece 0
-};
-
-// Work of one CTA. Whole tiles go round-robin (t = tile0 + i * tstride) -- all of them, or, in decode
-// mode when the last wave would leave SMs idle, only the `waves` full waves. The R < G remaining tiles
-// are then stream-K: their R * n_stages stages are cut into G contiguous ranges of L stages (CTA c
-// takes [c*L, (c+1)*L)), each range covering pieces of one or more tiles. A piece stores its fp32
-// partial; the last piece of a tile to finish (atomic counter) sums all of them in piece order
-// (deterministic) and runs the tile's epilogue. DS-R1 T=1: 128 gate/up tiles of 56 stages on 148
-// SMs -> 49 stages per SM instead of 56; 224 down tiles of 16 -> 16 + 9 instead of 32.
-struct Sched {
-  int n_sk;   // stream-K pieces of this CTA, processed FIRST: a piece's partial store / the tile's
-              // fix-up then overlaps the whole tiles that follow instead of ending the CTA's timeline
-              // (measured: ~3-5k cycles of cold code and L2 round trips at a CTA's very end)
-  int n_dp;   // whole tiles (or split-K units) of this CTA
-  int n_all;  // n_sk + n_dp
-  int F, L, R;  // first stream-K tile, stages per CTA range, stream-K tiles
-  int c;      // this CTA's index in the stream-K partition
 };
 
 // Static persistent schedule: tile t -> (expert, n-tile group, m-tile); m-tiles of one (expert, n-tile)
@@ -303,33 +277,16 @@ __device__ __forceinline__ void unpack_tile(uint2 p, TileInfo& ti, bool split_k)
   ti.split = split_k ? static_cast<int>(p.y >> 20) : 0;
 }
 
-// The CTA's i-th work item: its stream-K pieces in stage order (i < n_sk), then whole tiles
-// t = tile0 + d * tstride, d = i - n_sk (from the smem table when d < kTileTab, else searched).
+// The CTA's i-th tile (t = tile0 + i * tstride): from the smem table when i < kTileTab, else searched.
 template <int kNTok, int kNSplit, int kNPer = 1>
-__device__ __forceinline__ bool tile_at(int i, const Sched& sc, int n_stages, int tile0, int tstride, const uint2* tab,
-                                        const int* mt_off, const GemmArgs& a, uint32_t rank, TileInfo& ti) {
-  if (i >= sc.n_all) return false;
-  ti.sk = -1;
-  if (i >= sc.n_sk) {
-    const int d = i - sc.n_sk;
-    if (d < kTileTab) unpack_tile(tab[d], ti, a.splits > 1);
-    else get_tile<kNTok, kNSplit, kNPer>(tile0 + d * tstride, mt_off, a, rank, ti);
-    ti.k0 = ti.split * n_stages / a.splits;
-    ti.k1 = (ti.split + 1) * n_stages / a.splits;
+__device__ __forceinline__ bool tile_at(int i, int n_tiles, int tile0, int tstride, const uint2* tab, const int* mt_off,
+                                        const GemmArgs& a, uint32_t rank, TileInfo& ti) {
+  if (i >= n_tiles) return false;
+  if (i < kTileTab) {
+    unpack_tile(tab[i], ti, a.splits > 1);
     return true;
   }
-  const int g0 = sc.c * sc.L, end = sc.R * n_stages;  // this CTA's first stream-K stage; all of them
-  const int s = g0 / n_stages + i;
-  get_tile<kNTok, kNSplit, kNPer>(sc.F + s, mt_off, a, rank, ti);  // (no split-K under stream-K)
-  const int lo = max(g0, s * n_stages), hi = min(min(g0 + sc.L, end), (s + 1) * n_stages);
-  ti.k0 = lo - s * n_stages;
-  ti.k1 = hi - s * n_stages;
-  const int c0 = s * n_stages / sc.L, c1 = (min((s + 1) * n_stages, end) - 1) / sc.L;  // CTAs holding tile s
-  ti.sk = s;
-  ti.sk_q = sc.c - c0;
-  ti.sk_np = c1 - c0 + 1;
-  ti.sk_slot0 = s + c0;  // piece (tile s, CTA c) -> slot s + c: unique, the tile's pieces adjacent
-  return true;
+  return get_tile<kNTok, kNSplit, kNPer>(tile0 + i * tstride, mt_off, a, rank, ti);
 }
 
 // fast reciprocal division (exp overflow -> +inf -> 0, the limit): no IEEE slow-path branch, so the
@@ -376,9 +333,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   using C = Cfg<kNTok, kMode, kOffset, kPair>;
   constexpr bool kGated = C::kGated;
   const int n_stages = args.kt / C::kGroupsPerStage;  // stages per tile
-  // the work item's stages: a whole tile, a split-K unit or a stream-K piece
-  auto stage_beg = [&](const TileInfo& t) { return t.k0; };
-  auto stage_end = [&](const TileInfo& t) { return t.k1; };
+  // split-K: unit (tile, split) covers stages [stage_beg, stage_end) of the tile
+  auto stage_beg = [&](const TileInfo& t) { return t.split * n_stages / args.splits; };
+  auto stage_end = [&](const TileInfo& t) { return (t.split + 1) * n_stages / args.splits; };
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_x = smem;                                  // [NS][kXBytes]
@@ -393,10 +350,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   uint64_t* accempty = accfull + C::kNumAcc;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(accempty + C::kNumAcc);
   uint64_t* trbar = accempty + C::kNumAcc + 2;  // trace builds: per-stage MMA completion (8-deep ring)
-  Sched* sched_sm = reinterpret_cast<Sched*>(bars + 192);  // (the barriers use < 80 of the 256 slots)
-  int* sk_flag_sm = reinterpret_cast<int*>(bars + 200);    // epilogue: "this CTA finishes the stream-K tile"
   int* mt_off = reinterpret_cast<int*>(bars + 256);
   uint2* tile_tab = reinterpret_cast<uint2*>(mt_off + kMaxExperts + 2);  // 8-byte aligned (odd int count + 1)
+  int* n_tiles_sm = mt_off + kMaxExperts + 1;
   float2* red_sm = reinterpret_cast<float2*>(tile_tab + kTileTab);  // [4 warps][16 tokens]
   uint8_t* epi_sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(red_sm + 64) + 15) & ~uintptr_t(15));
 
@@ -451,33 +407,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     __syncwarp();
     // this CTA's tiles t = tile0 + i * tstride, the first kTileTab of them tabulated
     const int total = mt_off[E] * (args.nt / (C::kCG * C::kNPer)) * args.splits;
-    Sched sc{};
-    sc.n_dp = sc.n_all = tile0 < total ? (total - tile0 + tstride - 1) / tstride : 0;
-    if constexpr (kOffset && !kPair) {
-      if (args.sk && total > 0) {  // stream-K remainder when it shortens the critical path
-        const int waves = total / tstride, R = total - waves * tstride;
-        const int L = max(max((R * n_stages + tstride - 1) / tstride, min(n_stages, args.sk_lmin)),
-                          (n_stages + kSkMaxPieces - 2) / (kSkMaxPieces - 1));  // <= kSkMaxPieces per tile
-        // measured (tools/sk_probe.py, tools/gpu_ab_full.sh): a piece's epilogue end costs several
-        // stages (cold fix-up code, partial round trip), and with no whole wave (waves == 0) or short
-        // tiles the stream-K plan lost (Llama-3-8B M=1 16.4 -> 20.5 us, Qwen3 Zipf T=16 51 -> 56 us,
-        // DS-R1 T=1 down 20.5 -> 24 us); it won with long tiles behind >= 1 whole wave (DS-R1 T=16
-        // layer 406 -> 394 us, Mixtral T=1 72 -> 68 us)
-        if (R > 0 && waves >= args.sk_min_waves && n_stages >= args.sk_min_stages &&
-            5 * (L + args.sk_fix) <= 4 * n_stages) {
-          const int g0 = tile0 * L, end = R * n_stages;
-          sc.n_dp = waves;
-          sc.n_sk = g0 < end ? (min(g0 + L, end) - 1) / n_stages - g0 / n_stages + 1 : 0;
-          sc.n_all = sc.n_sk + waves;
-          sc.F = waves * tstride;
-          sc.L = L;
-          sc.R = R;
-          sc.c = tile0;
-        }
-      }
-    }
-    if (lane == 0) *sched_sm = sc;
-    for (int i = lane; i < min(sc.n_dp, kTileTab); i += 32) {
+    const int n_tiles = tile0 < total ? (total - tile0 + tstride - 1) / tstride : 0;
+    if (lane == 0) *n_tiles_sm = n_tiles;
+    for (int i = lane; i < min(n_tiles, kTileTab); i += 32) {
       TileInfo ti;
       get_tile<kNTok, C::kCG, C::kNPer>(tile0 + i * tstride, mt_off, args, rank, ti);
       tile_tab[i] = pack_tile(ti);
@@ -490,8 +422,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   else __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
-  const Sched sched = *sched_sm;
-  const int n_tiles = sched.n_all;
+  const int n_tiles = *n_tiles_sm;
   constexpr uint32_t kAcol0 = C::kNumAcc * C::kAccCols;  // first column of the TMEM A ring
   const uint32_t w_u32 = smem_u32(smem_w);
 
@@ -504,7 +435,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     if (!kOffset && lane == 1 && tr && !kPair && !C::kDual) {  // MMA completion times (trace event 15)
       uint32_t n = 0;
       TileInfo ti;
-      for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, sched, n_stages, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it)
+      for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it)
         for (int j = stage_beg(ti); j < stage_end(ti); ++j, ++n) {
           mbar_wait(&trbar[n & 7], (n >> 3) & 1);
           trace_at(tr, 15, n);
@@ -521,7 +452,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       Ring st;
       uint32_t pgs = 0;
       TileInfo ti;
-      for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, sched, n_stages, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
+      for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
         // per (expert, n-tile): kt k-groups of (gated ? 2 : 1) parts, stage j = bytes [j*kBlk, (j+1)*kBlk)
         const uint8_t* wsrc = args.wblocks + (static_cast<int64_t>(ti.e) * args.nt + ti.n_tile) *
                                                  static_cast<int64_t>(args.kt) * (kGated ? 2 : 1) * kPartBytes;
@@ -604,7 +535,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       Ring st, ar, acc;
       uint32_t gs = 0;
       TileInfo ti;
-      for (int it = 0; tile_at<kNTok, 1, C::kNPer>(it, sched, n_stages, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
+      for (int it = 0; tile_at<kNTok, 1, C::kNPer>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
         const uint32_t n_mma = min(kNTok, (ti.m_rows + 15) / 16 * 16);
         const uint32_t idesc = (idesc_full & ~(0x3Fu << 17)) | ((n_mma >> 3) << 17);
         const int jb = stage_beg(ti), je = stage_end(ti);
@@ -647,7 +578,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       Ring st, ar, acc;
       uint32_t gs = 0;
       TileInfo ti;
-      for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, sched, n_stages, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
+      for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
         // MMA N sized to the tile's real tokens (multiple of 16 per CTA of the group): an expert's last,
         // partial m-tile costs tensor time in proportion to its rows, not to kNTok
         const uint32_t n_mma = min(kNTok, (ti.m_rows + 16 * C::kCG - 1) / (16 * C::kCG) * (16 * C::kCG));
@@ -757,7 +688,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     uint32_t gs = 0;
     TileInfo ti;
-    for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, sched, n_stages, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
+    for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
       for (int j = stage_beg(ti); j < stage_end(ti); ++j, ++gs) {
         if (!C::kSplitA && (gs & 1u) != my_par) {
           st.next(C::kNS);
@@ -863,7 +794,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     uint32_t egs = 0;
     const bool tre = lane == 0 && quad == 0;
     TileInfo ti;
-    for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, sched, n_stages, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
+    for (int it = 0; tile_at<kNTok, C::kCG, C::kNPer>(it, n_tiles, tile0, tstride, tile_tab, mt_off, args, rank, ti); ++it) {
       if (tre) trace_at(tr, 9, egs);
       uint16_t* ocol = out + ti.n_tile * kTileRows + row;
       // output row of the tile's token m (identity, or scattered through args.out_rows)
@@ -993,55 +924,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           if (tre) trace_at(tr, 22, egs - 1);
           acc.next(C::kNumAcc);
           st.next(C::kNS);
-        }
-        if (ti.sk >= 0 && ti.sk_np > 1) {
-          // stream-K piece: publish the fp32 partial; the tile's last piece to arrive sums all of them
-          // in piece order (the same sum whichever CTA is last) and runs the tile's epilogue below
-          constexpr int kSlot = kOuts * kNTok * kTileRows;  // floats per piece: [out][token][row]
-          float* const slots = args.sk_part + static_cast<int64_t>(ti.sk_slot0) * kSlot;
-          float* const mine = slots + ti.sk_q * kSlot;
-#pragma unroll
-          for (int m = 0; m < kNTok; ++m) {
-            if (m < m_rows) {  // warp-uniform
-#pragma unroll
-              for (int o = 0; o < kOuts; ++o) __stcg(mine + (o * kNTok + m) * kTileRows + row, a[o][m]);
-            }
-          }
-          if (tre) trace_at(tr, 23, it);
-          // publish: the barrier orders the 128 threads' stores before thread 0's release fence and
-          // counter increment (fence.acq_rel + relaxed atomic; a per-thread fence.sc cost ~1.5k cycles)
-          named_bar_sync(1, 128);
-          if (warp == kEpiWarp0 && lane == 0) {
-            int old;
-            asm volatile("fence.acq_rel.gpu;\n\tatom.relaxed.gpu.global.add.s32 %0, [%1], 1;\n\tfence.acq_rel.gpu;"
-                         : "=r"(old) : "l"(args.sk_cnt + ti.sk) : "memory");
-            const bool last = old == ti.sk_np - 1;
-            if (last) asm volatile("st.relaxed.gpu.global.s32 [%0], 0;" ::"l"(args.sk_cnt + ti.sk) : "memory");
-            *sk_flag_sm = last ? 1 : 0;  // (all pieces in: the counter is zero again for the next launch)
-          }
-          named_bar_sync(1, 128);
-          if (tre) trace_at(tr, 24, it);
-          if (*sk_flag_sm == 0) continue;  // (rewritten only after the next piece's first barrier)
-#pragma unroll
-          for (int m = 0; m < kNTok; ++m) {
-            if (m < m_rows) {
-#pragma unroll
-              for (int o = 0; o < kOuts; ++o) {
-                // all pieces' loads in flight at once (<= kSkMaxPieces per tile, see the host plan), then
-                // the sum in piece order
-                const float* src = slots + (o * kNTok + m) * kTileRows + row;
-                float v[kSkMaxPieces];
-#pragma unroll
-                for (int q = 0; q < kSkMaxPieces; ++q)
-                  v[q] = (q < ti.sk_np && q != ti.sk_q) ? __ldcg(src + q * kSlot) : a[o][m];
-                float t = v[0];
-#pragma unroll
-                for (int q = 1; q < kSkMaxPieces; ++q)
-                  if (q < ti.sk_np) t += v[q];
-                a[o][m] = t;
-              }
-            }
-          }
         }
         if (args.splits > 1) {  // split-K: fp32 partials, summed (and activated) by splitk_finalize
           float* pbase = args.part + (static_cast<int64_t>(ti.split) * args.rows + ti.m_start) * args.part_ld +
@@ -1214,7 +1096,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     __syncthreads();
   }
   if (threadIdx.x == 0) progress_at(3, 1000000);  // CTA reached the exit barrier
-  if (threadIdx.x == 0) trace_at(tr, 25, 0);
 #ifdef W4A16_TRACE
   if (threadIdx.x == 0 && g_w4_trace) {  // every CTA: %globaltimer (ns) at entry (row 28) and exit (row 29)
     unsigned long long t1;
@@ -1500,24 +1381,6 @@ bool prefill_pairs_enabled() {
   return on;
 }
 
-// Stream-K remainder for decode launches (W4A16_STREAMK=0 disables: split-K as planned instead);
-// W4A16_SK_LMIN / _FIX / _MIN_STAGES / _MIN_WAVES tune the minimum stages per CTA range, the
-// per-piece cost estimate (stages), the shortest tile (stages) and the fewest whole waves before
-// the remainder that the kernel cuts (see Sched).
-int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
-bool streamk_enabled() { return env_int("W4A16_STREAMK", 1) != 0; }  // read per call: tests switch it
-
-// Decode-GEMM workspace: [0, kSkCntBytes) stream-K tile counters -- zero before the first launch,
-// left zero by every launch -- then the fp32 partials (split-K units or stream-K pieces).
-constexpr int64_t kSkCntBytes = 1024;
-constexpr int kSkMaxGrid = kSkCntBytes / 4;  // counters exist for R < grid tiles
-int64_t sk_part_bytes(int grid, int outs) {  // <= 2 * grid pieces (slot s + c, s < R < grid, c < grid)
-  return 2LL * grid * outs * kDecodeMaxNTok * kTileRows * 4;
-}
-
 // Experiment knob: W4A16_PAIR=1 runs the decode kernel on CTA pairs.
 bool pairs_enabled() {
   static const bool on = [] {
@@ -1573,7 +1436,9 @@ GemmPlan plan_gemm(int64_t rows, int64_t K, int64_t num_experts, int64_t n_out, 
   const int n_stages = kt / (pl.mode == kModeKPair ? 2 : 1);
   pl.splits = (pl.offset && rows < (1 << 20)) ? choose_splits(rows, num_experts, nt, n_stages, sm_count()) : 1;
   // experiment: W4A16_SPLITS_GU / W4A16_SPLITS_DN force the decode split-K factor of gate/up / down launches
-  const int force = env_int(gated ? "W4A16_SPLITS_GU" : "W4A16_SPLITS_DN", 0);  // (read per call: tests set it)
+  static const int force_gu = getenv("W4A16_SPLITS_GU") ? atoi(getenv("W4A16_SPLITS_GU")) : 0;
+  static const int force_dn = getenv("W4A16_SPLITS_DN") ? atoi(getenv("W4A16_SPLITS_DN")) : 0;
+  const int force = gated ? force_gu : force_dn;
   if (pl.offset && rows < (1 << 20) && force > 0) pl.splits = std::min(force, n_stages);
   return pl;
 }
@@ -1620,11 +1485,7 @@ int64_t w4a16_grouped_gemm_ws_bytes(int64_t rows, int64_t K, int64_t num_experts
                                     int ntok) {
   if (rows <= 0 || K % kTileK || n_out % kTileRows || num_experts <= 0) return 0;
   const GemmPlan pl = plan_gemm(rows, K, num_experts, n_out, gated, true, ntok);
-  const int grid = sm_count();
-  if (pl.splits > 1) return kSkCntBytes + static_cast<int64_t>(pl.splits) * rows * (gated ? 2 : 1) * n_out * 4;
-  if (pl.offset && pl.ntok <= kDecodeMaxNTok && streamk_enabled() && grid <= kSkMaxGrid)
-    return kSkCntBytes + sk_part_bytes(grid, (gated || pl.mode == kModeNPair) ? 2 : 1);
-  return 0;
+  return pl.splits > 1 ? static_cast<int64_t>(pl.splits) * rows * (gated ? 2 : 1) * n_out * 4 : 0;
 }
 
 static int grouped_gemm_impl(const void* x, int64_t x_rows, const int32_t* gather_rows, int gather_div,
@@ -1641,16 +1502,8 @@ static int grouped_gemm_impl(const void* x, int64_t x_rows, const int32_t* gathe
   if (rows <= 0) return W4_OK;
   if (ntok != 0 && ntok != 16 && ntok != 32 && ntok != 64 && ntok != 128) return W4_ERR_ARG;
   GemmPlan pl = plan_gemm(rows, K, num_experts, n_out, gated, xsum != nullptr, ntok);
-  const int grid = sm_count();
-  const int outs = (gated || pl.mode == kModeNPair) ? 2 : 1;
-  const int64_t need =
-      pl.splits > 1 ? kSkCntBytes + static_cast<int64_t>(pl.splits) * rows * (gated ? 2 : 1) * n_out * 4 : 0;
+  const int64_t need = pl.splits > 1 ? static_cast<int64_t>(pl.splits) * rows * (gated ? 2 : 1) * n_out * 4 : 0;
   if (pl.splits > 1 && (!ws || ws_bytes < need)) pl.splits = 1;  // no / too small workspace: no split-K
-  // stream-K remainder (decode launches without a split-K plan; the kernel decides from the real tile
-  // count whether to cut the last wave -- Sched). Split-K stays for the few-tile launches it was
-  // planned for (Llama-3-8B M=1, Mixtral T=1 down), where stream-K measured slower.
-  const bool sk = pl.offset && pl.splits == 1 && pl.ntok <= kDecodeMaxNTok && streamk_enabled() &&
-                  grid <= kSkMaxGrid && ws && ws_bytes >= kSkCntBytes + sk_part_bytes(grid, outs);
   GemmArgs a;
   a.wblocks = wblocks;
   a.expert_counts = expert_counts;
@@ -1673,15 +1526,8 @@ static int grouped_gemm_impl(const void* x, int64_t x_rows, const int32_t* gathe
     return v < 0 ? 0 : (v > kDirectRows ? kDirectRows : v);
   }();
   a.direct_rows = direct_rows;
-  a.part = ws ? reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + kSkCntBytes) : nullptr;
+  a.part = static_cast<float*>(ws);
   a.part_ld = (gated ? 2 : 1) * n_out;
-  a.sk = sk ? 1 : 0;
-  a.sk_lmin = env_int("W4A16_SK_LMIN", 4);
-  a.sk_fix = env_int("W4A16_SK_FIX", 8);
-  a.sk_min_stages = env_int("W4A16_SK_MIN_STAGES", 32);
-  a.sk_min_waves = env_int("W4A16_SK_MIN_WAVES", 1);
-  a.sk_cnt = static_cast<int*>(ws);
-  a.sk_part = a.part;
   // the decode gate/up epilogue writes the output's group sums itself; otherwise a sums pass follows
   const bool fused_osum = osum != nullptr && gated && pl.offset && pl.ntok <= 16 && pl.splits == 1;
   a.osum = fused_osum ? reinterpret_cast<float2*>(osum) : nullptr;
@@ -1689,8 +1535,8 @@ static int grouped_gemm_impl(const void* x, int64_t x_rows, const int32_t* gathe
   if (out_rows && osum) return W4_ERR_ARG;  // sums of a scattered output are not supported
   // CTA pairs (cta_group::2) measured slower at decode token counts (an M=256 x N=16 MMA with 8-row B
   // halves executes ~4x slower than two M=128 ones): opt-in only (W4A16_PAIR=1)
-  const bool pair = !gather_rows && !sk && pl.splits == 1 && a.nt % 2 == 0 &&
-                    (pl.offset ? pairs_enabled() : prefill_pairs_enabled());
+  const bool pair = !gather_rows && pl.splits == 1 && a.nt % 2 == 0 && (pl.offset ? pairs_enabled() : prefill_pairs_enabled());
+  const int grid = sm_count();
   const bool bf = dtype == W4_DTYPE_BF16;
   int rc;
   if (gather_rows) {  // fused gather: gate/up projection only

@@ -53,9 +53,7 @@ class _Workspace:
         self.buf: dict[tuple, torch.Tensor] = {}
         self.per_stream = per_stream
 
-    def get(self, name: str, shape, dtype, device, zero: bool = False) -> torch.Tensor:
-        """``zero``: a new buffer is zero-filled (the decode GEMM workspace, whose stream-K counters
-        must start at zero; every launch leaves them zero)."""
+    def get(self, name: str, shape, dtype, device) -> torch.Tensor:
         n = 1
         for s in shape:
             n *= s
@@ -63,7 +61,7 @@ class _Workspace:
         key = (name, dtype, str(dev), torch.cuda.current_stream(dev).cuda_stream if self.per_stream else 0)
         t = self.buf.get(key)
         if t is None or t.numel() < n:
-            t = (torch.zeros if zero else torch.empty)(max(n, 1), dtype=dtype, device=dev)
+            t = torch.empty(max(n, 1), dtype=dtype, device=dev)
             self.buf[key] = t
         return t[:n].view(*shape)
 
@@ -233,7 +231,7 @@ def moe_w4a16(x: torch.Tensor, weights, topk_weights: torch.Tensor, topk_ids: to
     def splitk_ws(K: int, n_out: int, gated: bool):
         # one buffer per GEMM: a captured graph keeps _ws's buffers alive, so neither may be reallocated
         b = ops.gemm_ws_bytes(P, K, E, n_out, gated, nt) if decode else 0
-        return _ws.get("splitk_gu" if gated else "splitk_dn", (b,), torch.uint8, dev, True) if b else None
+        return _ws.get("splitk_gu" if gated else "splitk_dn", (b,), torch.uint8, dev) if b else None
 
     hs = _ws.get("hs", ops.sums_shape(P, I), torch.float32, dev) if decode else None
     gu_ws = splitk_ws(H, I, True)
@@ -473,5 +471,5 @@ def w4a16_linear(x: torch.Tensor, w, ntok: int = 0) -> torch.Tensor:
     decode = nt <= _DECODE_MAX_NTOK
     xs = ops.group_sums(x) if decode else None
     wsb = ops.gemm_ws_bytes(M, K, 1, w.n_rows, False, nt) if decode else 0
-    ws = _ws.get("linear_splitk", (wsb,), torch.uint8, dev, True) if wsb else None
+    ws = _ws.get("linear_splitk", (wsb,), torch.uint8, dev) if wsb else None
     return ops.grouped_gemm(x, w.blocks, 1, w.n_rows, False, counts, offsets, nt, xsum=xs, workspace=ws)

@@ -284,10 +284,7 @@ def grouped_gemm(x: torch.Tensor, blocks: torch.Tensor, num_experts: int, n_out:
                  out_rows: torch.Tensor | None = None) -> torch.Tensor:
     """out[off_e + m] = act(x[off_e + m] @ W_e^T) (gated: silu(gate) * up), per expert. ``xsum``
     (group_sums / moe_gather_sums of x) selects the decode kernel for 16/32-token tiles; a
-    ``workspace`` of gemm_ws_bytes(...) bytes -- zero-filled before its first use: its leading stream-K
-    tile counters must start at zero, and every launch leaves them zero -- lets a decode launch whose
-    last wave of tiles would leave SMs idle cut those tiles' stages over all SMs (stream-K) or, with
-    W4A16_STREAMK=0, split K (split-K units + a finalize kernel); ``osum`` (shape
+    ``workspace`` of gemm_ws_bytes(...) bytes enables split-K when few tiles exist; ``osum`` (shape
     sums_shape(rows, n_out)) receives the output's group sums (the next GEMM's xsum); ``out_rows``
     (int32 [rows]) scatters result row i to out row out_rows[i]."""
     _need_cuda(x, blocks, expert_counts, expert_offsets)

@@ -204,7 +204,7 @@ def _gemm_case(dt, gated, counts, K, N, ntok, seed=0, sums=False, splitk=False):
     if splitk:
         wsb = _ops().gemm_ws_bytes(rows, K, E, N, gated, ntok)
         assert wsb > 0, "expected a split-K plan"
-        ws = torch.zeros(wsb, dtype=torch.uint8, device="cuda")  # (stream-K counters start at zero)
+        ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
     out = _ops().grouped_gemm(xd, w.blocks, E, N, gated, torch.from_numpy(cnt).cuda(),
                               torch.from_numpy(off).cuda(), ntok, xsum=xs, workspace=ws)
     torch.cuda.synchronize()
@@ -248,119 +248,18 @@ def test_grouped_gemm_odd_ntiles_decode(N, ntok, dt):
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=ATOL)
 
 
-@pytest.fixture(params=["streamk", "splitk"])
-def sched(request, monkeypatch):
-    """Decode schedule for few tiles (the library reads these per call): stream-K pieces (split-K
-    planning off, the kernel's thresholds relaxed so even these small launches take it) or split-K
-    units + finalize kernel (W4A16_STREAMK=0)."""
-    monkeypatch.setenv("W4A16_STREAMK", "1" if request.param == "streamk" else "0")
-    if request.param == "streamk":
-        monkeypatch.setenv("W4A16_SPLITS_GU", "1")
-        monkeypatch.setenv("W4A16_SPLITS_DN", "1")
-    monkeypatch.setenv("W4A16_SK_FIX", "0")
-    monkeypatch.setenv("W4A16_SK_MIN_STAGES", "0")
-    monkeypatch.setenv("W4A16_SK_MIN_WAVES", "0")
-    return request.param
-
-
 @pytest.mark.parametrize("gated,K,N", [(True, 2048, 1024), (False, 4096, 512), (False, 1920, 256)])
 @pytest.mark.parametrize("dt", ["f16", "bf16"])
-def test_grouped_gemm_splitk(gated, K, N, dt, sched):
-    """Few tiles (1-2 experts, a few tokens): the decode GEMM cuts K over CTAs -- stream-K pieces
-    summed by each tile's last piece, or split-K units and a finalize kernel (gated and n-pair block
-    modes; K/128 = 15 is odd)."""
+def test_grouped_gemm_splitk(gated, K, N, dt):
+    """Few tiles (1-2 experts, a few tokens): the decode GEMM splits K over CTAs into fp32 partials
+    and a finalize kernel (gated and n-pair block modes; K/128 = 15 is odd)."""
     got, want = _gemm_case(dt, gated, [2, 0, 3] if gated else [1, 2], K=K, N=N, ntok=16, seed=8, sums=True,
                            splitk=True)
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=(2 if dt == "bf16" else 1) * ATOL)
 
 
-# Stream-K cases: (gated, K, N, per-expert rows, W4A16_SK_LMIN). Tiles: gated -> one per 128 output
-# columns (gate|up parts of one stage), K/128 stages; down (even N/128) -> n-pair tiles of 256 columns.
-_SK_CASES = [
-    (True, 1024, 256, [1, 2, 1], 4),      # 6 tiles of 8 stages: 2 pieces per tile
-    (True, 2048, 256, [1, 0, 3], 4),      # 16 stages: 4 pieces per tile
-    (True, 2048, 256, [2, 1], 3),         # L = 3: pieces of 1-3 stages, ragged boundaries
-    (False, 2048, 512, [2, 1, 0, 4], 4),  # n-pair down tiles (16 stages, two n-tiles per stage)
-    (False, 1920, 256, [1, 2], 4),        # odd K/128 = 15: 15-stage n-pair tiles, ragged pieces
-    (True, 1024, 256, [1] * 75, 4),       # 150 tiles: one whole-tile wave, then 2 stream-K tiles
-]
-
-
-@pytest.mark.parametrize("case", range(len(_SK_CASES)))
-@pytest.mark.parametrize("dt", ["f16", "bf16"])
-def test_grouped_gemm_streamk(case, dt, monkeypatch):
-    """Stream-K remainder: pieces publish fp32 partials, each tile's last piece sums them in piece
-    order. Checked against the oracle; a second launch on the same workspace is bit-identical (the
-    tile counters were left at zero) and the partial slots were really used."""
-    gated, K, N, counts, lmin = _SK_CASES[case]
-    monkeypatch.setenv("W4A16_STREAMK", "1")
-    monkeypatch.setenv("W4A16_SK_LMIN", str(lmin))
-    monkeypatch.setenv("W4A16_SPLITS_GU", "1")  # no split-K plan: these few-tile launches would get one
-    monkeypatch.setenv("W4A16_SPLITS_DN", "1")
-    monkeypatch.setenv("W4A16_SK_FIX", "0")  # take the stream-K plan whenever it shortens the path
-    monkeypatch.setenv("W4A16_SK_MIN_STAGES", "0")
-    monkeypatch.setenv("W4A16_SK_MIN_WAVES", "0")
-    rng = np.random.default_rng(100 + case)
-    E = len(counts)
-    rows = int(sum(counts))
-    q, z, s = O.synth_awq_expert_weights(rng, E, 2 * N if gated else N, K, dt)
-    w = _packed(q, z, s, dt, gated)
-    x = O.round_act(rng.standard_normal((rows, K)).astype(np.float32) * 0.5, dt)
-    cnt = np.asarray(counts, np.int32)
-    off = np.zeros(E + 1, np.int32)
-    np.cumsum(cnt, out=off[1:])
-    ops = _ops()
-    xd = _to_dev_act(x, dt)
-    xs = ops.group_sums(xd)
-    wsb = ops.gemm_ws_bytes(rows, K, E, N, gated, 16)
-    ws = torch.zeros(wsb, dtype=torch.uint8, device="cuda")
-    args = (xd, w.blocks, E, N, gated, torch.from_numpy(cnt).cuda(), torch.from_numpy(off).cuda(), 16)
-    out1 = ops.grouped_gemm(*args, xsum=xs, workspace=ws).clone()
-    out2 = ops.grouped_gemm(*args, xsum=xs, workspace=ws)
-    torch.cuda.synchronize()
-    assert torch.equal(out1, out2)
-    assert not ws[:1024].any(), "stream-K tile counters not back at zero"
-    assert ws[1024:].any(), "no stream-K partial was written (schedule not taken)"
-    want = O.grouped_gemm(x, O.dequant(q, z, s, dt), cnt, off, dt, gated)
-    np.testing.assert_allclose(_from_dev_act(out1, dt), want, rtol=RTOL, atol=(2 if dt == "bf16" else 1) * ATOL)
-
-
-def test_grouped_gemm_streamk_graph(monkeypatch):
-    """A captured stream-K launch replays bit-identically (counters reset inside every replay)."""
-    monkeypatch.setenv("W4A16_STREAMK", "1")
-    monkeypatch.setenv("W4A16_SPLITS_GU", "1")
-    monkeypatch.setenv("W4A16_SK_FIX", "0")
-    monkeypatch.setenv("W4A16_SK_MIN_STAGES", "0")
-    monkeypatch.setenv("W4A16_SK_MIN_WAVES", "0")
-    gated, K, N, counts, _ = _SK_CASES[1]
-    rng = np.random.default_rng(7)
-    E, rows = len(counts), int(sum(counts))
-    q, z, s = O.synth_awq_expert_weights(rng, E, 2 * N, K, "f16")
-    w = _packed(q, z, s, "f16", True)
-    xd = _to_dev_act(O.round_act(rng.standard_normal((rows, K)).astype(np.float32) * 0.5, "f16"), "f16")
-    cnt = torch.tensor(counts, dtype=torch.int32).cuda()
-    off = torch.tensor(np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)).cuda()
-    ops = _ops()
-    xs = ops.group_sums(xd)
-    ws = torch.zeros(ops.gemm_ws_bytes(rows, K, E, N, True, 16), dtype=torch.uint8, device="cuda")
-    out = torch.empty((rows, N), dtype=torch.float16, device="cuda")
-    eager = ops.grouped_gemm(xd, w.blocks, E, N, True, cnt, off, 16, xsum=xs, workspace=ws).clone()
-    side = torch.cuda.Stream()
-    side.wait_stream(torch.cuda.current_stream())
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(side), torch.cuda.graph(g, stream=side):
-        ops.grouped_gemm(xd, w.blocks, E, N, True, cnt, off, 16, xsum=xs, workspace=ws, out=out)
-    torch.cuda.current_stream().wait_stream(side)
-    for _ in range(3):
-        out.zero_()
-        g.replay()
-        torch.cuda.synchronize()
-        assert torch.equal(out, eager)
-    assert not ws[:1024].any()
-
-
 @pytest.mark.parametrize("splitk", [False, True])
-def test_gate_up_output_sums(splitk, sched):
+def test_gate_up_output_sums(splitk):
     """The gated GEMM also emits its output's (C, S) group sums (fused in the decode epilogue, or a
     sums pass after split-K): equal to group_sums of the output."""
     rng = np.random.default_rng(31)
@@ -523,7 +422,7 @@ def test_ep_local_order(world, el):
 
 
 @pytest.mark.parametrize("ntok,splitk", [(16, False), (16, True), (64, False)])
-def test_grouped_gemm_out_rows(ntok, splitk, sched):
+def test_grouped_gemm_out_rows(ntok, splitk):
     """out_rows scatters result rows (the EP down GEMM writes arrival order directly): equals the
     plain output permuted."""
     rng = np.random.default_rng(41)
@@ -571,7 +470,7 @@ def test_c_abi_moe_forward(T):
     idd, wd = torch.from_numpy(ids).cuda(), torch.from_numpy(wts).cuda()
     y = torch.empty_like(xd)
     wsb = lib.w4a16_moe_workspace_bytes(T, k, E, H, I)
-    ws = torch.zeros(wsb, dtype=torch.uint8, device="cuda")  # zero once (stream-K counters), reused below
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
     rc = lib.w4a16_moe_forward(xd.data_ptr(), T, H, I, E, k, idd.data_ptr(), wd.data_ptr(), w.w13.blocks.data_ptr(),
                                w.w2.blocks.data_ptr(), 0, y.data_ptr(), ws.data_ptr(), wsb,
                                torch.cuda.current_stream().cuda_stream)

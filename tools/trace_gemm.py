@@ -111,9 +111,6 @@ if a.dump:
     for i in range(n):
         print(f"  S{i:3d} {r[0][i]:8d} {r[1][i]:8d} {r[4][i]:8d} {r[5][i]:8d} {r[7][i]:8d} {r[8][i]:8d}")
     print("  epilogue tile starts:", r[9][r[9] >= 0].tolist(), " last epilogue done:", int(r[8].max()))
-    rr = buf.cpu().numpy()[22:26]
-    rr = np.where(rr >= 0, rr - z, -1)
-    print("  stream-K piece: partial out (by item):", rr[1][rr[1] >= 0].tolist(), " flag known:", rr[2][rr[2] >= 0].tolist(), " exit barrier:", rr[3][rr[3] >= 0].tolist())
     w26 = buf.cpu().numpy()[26][:16]
     print("  warp arrivals at the exit barrier:", [int(v - z) if v >= 0 else -1 for v in w26])
 
