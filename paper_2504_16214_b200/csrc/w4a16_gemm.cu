@@ -278,6 +278,8 @@ __device__ __forceinline__ void unpack_tile(uint2 p, TileInfo& ti, bool split_k)
 }
 
 // The CTA's i-th tile (t = tile0 + i * tstride): from the smem table when i < kTileTab, else searched.
+// (An out-of-line search for the rare i >= kTileTab made the kernel 200 instructions smaller but
+// 1-2 % slower at decode sizes -- the call's stack frame; measured with tools/gpu_ab_libs.sh.)
 template <int kNTok, int kNSplit, int kNPer = 1>
 __device__ __forceinline__ bool tile_at(int i, int n_tiles, int tile0, int tstride, const uint2* tab, const int* mt_off,
                                         const GemmArgs& a, uint32_t rank, TileInfo& ti) {
@@ -987,17 +989,18 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               // (C, S) = (sum_r c_r h_r, sum_r h_r), c_r the decode offset of k = r (Dq::offset_bits).
               const float cr = act_bits_to_float<kBF16>(Dq<kBF16>::offset_bits(row & 7));
               const uint32_t ew = warp - kEpiWarp0;
+              // a rolled loop over the real tokens: one copy of the shuffle tree instead of kNTok
+              // (ptxas wraps every shuffle under a data-dependent branch in divergence handling:
+              // ~1000 of the kernel's ~4600 SASS instructions, all of it cold tile-end code)
+#pragma unroll 1
+              for (int m = 0; m < m_rows; ++m) {
+                float sc = cr * hv[m], ss = hv[m];
 #pragma unroll
-              for (int m = 0; m < kNTok; ++m) {
-                if (m < m_rows) {  // warp-uniform
-                  float sc = cr * hv[m], ss = hv[m];
-#pragma unroll
-                  for (int o = 16; o; o >>= 1) {
-                    sc += __shfl_xor_sync(0xffffffffu, sc, o);
-                    ss += __shfl_xor_sync(0xffffffffu, ss, o);
-                  }
-                  if (lane == 0) red_sm[ew * 16 + m] = make_float2(sc, ss);
+                for (int o = 16; o; o >>= 1) {
+                  sc += __shfl_xor_sync(0xffffffffu, sc, o);
+                  ss += __shfl_xor_sync(0xffffffffu, ss, o);
                 }
+                if (lane == 0) red_sm[ew * 16 + m] = make_float2(sc, ss);
               }
               named_bar_sync(1, 128);  // the 4 epilogue warps
               if (ew == 0 && static_cast<int>(lane) < m_rows) {
