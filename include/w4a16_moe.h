@@ -159,6 +159,10 @@ int w4a16_grouped_gemm(const void* x, int64_t rows, int64_t K, const uint8_t* wb
                        int64_t n_out, int gated, const int32_t* expert_counts, const int32_t* expert_offsets,
                        const float* xsum, void* out, int dtype, int ntok, cudaStream_t stream);
 int w4a16_pick_ntok(int64_t rows, int64_t num_experts);
+/* Largest token tile that runs in offset-code (decode) mode when xsum is given: 16 (default) or 32
+ * (environment W4A16_DECODE_MAX_NTOK=32; 0 turns the mode off). Larger tiles apply the scale in the
+ * dequant (prefill mode). */
+int w4a16_decode_max_ntok(void);
 
 /* Same, with a caller workspace that enables split-K in decode mode when the (expert, n-tile) tiles
  * cannot fill the GPU (e.g. one token touching 8 experts): the k-groups of a tile are split over

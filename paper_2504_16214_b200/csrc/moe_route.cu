@@ -928,7 +928,7 @@ int moe_forward_impl(const void* x, int64_t T, int64_t H, int64_t I, int64_t E, 
                                  w4a16_moe_permute_ws_bytes(P, E), stream)))
     return rc;
   const int nt = ntok > 0 ? ntok : w4a16_pick_ntok(P, E);
-  const bool decode = nt <= 16;  // offset-code GEMMs (16-token tiles) need the per-group activation sums
+  const bool decode = nt <= w4a16_decode_max_ntok();  // offset-code GEMMs need the per-group activation sums
   if (decode) {
     if ((rc = w4a16_moe_gather_sums(x, H, topk, sorted, P, offsets + E, xp, dtype, xsum, stream))) return rc;
   } else if ((rc = w4a16_moe_gather(x, H, topk, sorted, P, offsets + E, xp, stream))) {

@@ -47,10 +47,10 @@ constexpr int kDequantGroup = 4;
 constexpr int kEpiWarp0 = 10;
 constexpr int kMaxExperts = 1024;
 constexpr int kTileTab = 512;  // per-CTA tile table entries in smem (later tiles are searched on the fly)
-// Largest token tile run in offset-code (decode) mode: its epilogue costs 3 FFMA per (row, real token,
-// k-group), which beats the dequant's per-weight scale only at <= 16 tokens (measured: 32-token tiles
-// are 10-25 % faster with the scale applied in the dequant).
-constexpr int kDecodeMaxNTok = 16;
+// Largest token tile compiled in offset-code (decode) mode. Its epilogue costs 3 FFMA per (row, real
+// token, k-group), against the dequant's per-weight scale in prefill mode; the largest tile actually
+// run in offset mode is decode_max_ntok() (W4A16_DECODE_MAX_NTOK, default below).
+constexpr int kDecodeMaxNTok = 32;
 #ifndef W4A16_KSPLIT
 #define W4A16_KSPLIT 0
 #endif
@@ -1321,6 +1321,7 @@ int dispatch_ntok(int ntok, bool offset, bool pair, const GemmArgs& a, const voi
                   int grid, cudaStream_t st) {
   if (offset && pair && ntok == 16) return launch_gemm<16, kMode, kBF16, true, true>(a, x, rows, K, grid, st);
   if (offset && ntok == 16) return launch_gemm<16, kMode, kBF16, true, false>(a, x, rows, K, grid, st);
+  if (offset && ntok == 32) return launch_gemm<32, kMode, kBF16, true, false>(a, x, rows, K, grid, st);
   if (pair) {
     if (ntok == 64) return launch_gemm<64, kMode, kBF16, false, true>(a, x, rows, K, grid, st);
     if (ntok == 128) return launch_gemm<128, kMode, kBF16, false, true>(a, x, rows, K, grid, st);
@@ -1339,6 +1340,7 @@ template <bool kBF16>
 int dispatch_gather(int ntok, bool offset, const GemmArgs& a, const void* x, int64_t rows, int64_t K, int grid,
                     cudaStream_t st) {
   if (offset && ntok == 16) return launch_gemm<16, kModeGateUp, kBF16, true, false, true>(a, x, rows, K, grid, st);
+  if (offset && ntok == 32) return launch_gemm<32, kModeGateUp, kBF16, true, false, true>(a, x, rows, K, grid, st);
   switch (ntok) {
     case 16: return launch_gemm<16, kModeGateUp, kBF16, false, false, true>(a, x, rows, K, grid, st);
     case 32: return launch_gemm<32, kModeGateUp, kBF16, false, false, true>(a, x, rows, K, grid, st);
@@ -1427,7 +1429,7 @@ GemmPlan plan_gemm(int64_t rows, int64_t K, int64_t num_experts, int64_t n_out, 
   GemmPlan pl;
   pl.ntok = ntok > 0 ? ntok : w4a16_pick_ntok(rows, num_experts);
   const int kt = static_cast<int>(K / kTileK), nt = static_cast<int>(n_out / kTileRows);
-  pl.offset = has_xsum && pl.ntok <= kDecodeMaxNTok;
+  pl.offset = has_xsum && pl.ntok <= w4a16_decode_max_ntok();
   // k-pair (two k-groups per 17 KB stage) for decode tiles; at 128 tokens the X tile dominates a stage
   // (64 KB for a k-pair -> only 2 smem stages), so 128-token tiles use one group per stage
   pl.mode = gated ? kModeGateUp : ((kt % 2 == 0 && pl.ntok <= 64) ? kModeKPair : kModePlain);
@@ -1435,7 +1437,7 @@ GemmPlan plan_gemm(int64_t rows, int64_t K, int64_t num_experts, int64_t n_out, 
   if (!gated && !pl.offset && pl.ntok >= 32 && pl.ntok >= npair_min_ntok() && nt % 2 == 0) pl.mode = kModeNPair;
   // decode down projection: n-pair stages too (one k-group of two n-tiles on one X tile): tiles of
   // K/128 stages instead of K/256 k-pair stages, half the X bytes per stage
-  if (!gated && pl.offset && pl.ntok == 16 && nt % 2 == 0 && decode_npair_enabled()) pl.mode = kModeNPair;
+  if (!gated && pl.offset && nt % 2 == 0 && decode_npair_enabled()) pl.mode = kModeNPair;
   const int n_stages = kt / (pl.mode == kModeKPair ? 2 : 1);
   pl.splits = (pl.offset && rows < (1 << 20)) ? choose_splits(rows, num_experts, nt, n_stages, sm_count()) : 1;
   // experiment: W4A16_SPLITS_GU / W4A16_SPLITS_DN force the decode split-K factor of gate/up / down launches
@@ -1466,6 +1468,11 @@ int w4a16_debug_stamp(void* buf, cudaStream_t stream) {
 }
 
 int w4a16_tile_rows(void) { return kTileRows; }
+int w4a16_decode_max_ntok(void) {
+  const char* e = getenv("W4A16_DECODE_MAX_NTOK");  // (read per call: the A/B knob)
+  const int v = e ? atoi(e) : 16;
+  return v >= 32 ? 32 : (v >= 16 ? 16 : 0);
+}
 int w4a16_tile_k(void) { return kTileK; }
 int w4a16_part_bytes(void) { return kPartBytes; }
 
@@ -1552,7 +1559,10 @@ static int grouped_gemm_impl(const void* x, int64_t x_rows, const int32_t* gathe
   else if (pl.mode == kModeKPair)
     rc = bf ? dispatch_ntok<kModeKPair, true>(pl.ntok, pl.offset, pair, a, x, x_rows, K, grid, stream)
             : dispatch_ntok<kModeKPair, false>(pl.ntok, pl.offset, pair, a, x, x_rows, K, grid, stream);
-  else if (pl.mode == kModeNPair && pl.offset)  // decode n-pair: 16-token tiles, no CTA pairs
+  else if (pl.mode == kModeNPair && pl.offset && pl.ntok == 32)  // decode n-pair, no CTA pairs
+    rc = bf ? launch_gemm<32, kModeNPair, true, true, false>(a, x, x_rows, K, grid, stream)
+            : launch_gemm<32, kModeNPair, false, true, false>(a, x, x_rows, K, grid, stream);
+  else if (pl.mode == kModeNPair && pl.offset)
     rc = bf ? launch_gemm<16, kModeNPair, true, true, false>(a, x, x_rows, K, grid, stream)
             : launch_gemm<16, kModeNPair, false, true, false>(a, x, x_rows, K, grid, stream);
   else if (pl.mode == kModeNPair)

@@ -103,7 +103,6 @@ _FUSED_GATHER = os.environ.get("W4A16_FUSED_GATHER", "0") not in ("", "0")
 # forces it on / off; unset: by rows per expert (see moe_w4a16)
 _FUSED_OSUM = None if os.environ.get("W4A16_FUSED_OSUM", "") == "" else os.environ["W4A16_FUSED_OSUM"] != "0"
 # largest token tile that runs the offset-code (decode) GEMM; larger tiles dequantise with the scale
-_DECODE_MAX_NTOK = int(__import__("os").environ.get("W4A16_DECODE_MAX_NTOK", "16"))
 
 
 class KernelTimer:
@@ -212,7 +211,7 @@ def moe_w4a16(x: torch.Tensor, weights, topk_weights: torch.Tensor, topk_ids: to
             counts, offsets, sorted_pairs, pair_pos = ops.moe_permute(
                 topk_ids, E, _ws.get("perm_ws", (max(ops.permute_ws_bytes(P, E), 1),), torch.uint8, dev))
     nt = ntok or ops.pick_ntok(P, E)
-    decode = nt <= _DECODE_MAX_NTOK  # offset-code GEMMs: per-group activation sums ride along with X and h
+    decode = nt <= ops.decode_max_ntok()  # offset-code GEMMs: per-group activation sums ride along with X and h
     if _FUSED_GATHER:  # the gate/up producer gathers x's rows itself (TMA gather4); decode sums over x
         xp = None
         if decode:
@@ -468,7 +467,7 @@ def w4a16_linear(x: torch.Tensor, w, ntok: int = 0) -> torch.Tensor:
     counts, offsets = _LINEAR_ROUTING[key]
     nt = ntok or ops.pick_ntok(M, 1)
     x = x.contiguous()
-    decode = nt <= _DECODE_MAX_NTOK
+    decode = nt <= ops.decode_max_ntok()
     xs = ops.group_sums(x) if decode else None
     wsb = ops.gemm_ws_bytes(M, K, 1, w.n_rows, False, nt) if decode else 0
     ws = _ws.get("linear_splitk", (wsb,), torch.uint8, dev) if wsb else None

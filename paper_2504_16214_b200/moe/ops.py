@@ -319,6 +319,11 @@ def grouped_gemm_gather(x: torch.Tensor, gather_rows: torch.Tensor, gather_div: 
     return out
 
 
+def decode_max_ntok() -> int:
+    """Largest token tile the grouped GEMM runs in offset-code (decode) mode (W4A16_DECODE_MAX_NTOK)."""
+    return int(_lib.load().w4a16_decode_max_ntok())
+
+
 def gemm_ws_bytes(rows: int, K: int, num_experts: int, n_out: int, gated: bool, ntok: int = 0) -> int:
     """Split-K workspace bytes the decode-mode grouped GEMM would use (0: no split planned)."""
     return int(_lib.load().w4a16_grouped_gemm_ws_bytes(rows, K, num_experts, n_out, int(gated), ntok))

@@ -258,6 +258,17 @@ def test_grouped_gemm_splitk(gated, K, N, dt):
     np.testing.assert_allclose(got, want, rtol=RTOL, atol=(2 if dt == "bf16" else 1) * ATOL)
 
 
+@pytest.mark.parametrize("gated,K,N", [(True, 1024, 256), (False, 2048, 512), (False, 1024, 384)])
+@pytest.mark.parametrize("dt", ["f16", "bf16"])
+def test_grouped_gemm_offset_32(gated, K, N, dt, monkeypatch):
+    """W4A16_DECODE_MAX_NTOK=32 (read per call): 32-token tiles in offset-code mode -- gate/up,
+    n-pair down and (odd n-tile count) k-pair down kernels -- against the oracle."""
+    monkeypatch.setenv("W4A16_DECODE_MAX_NTOK", "32")
+    assert _ops().decode_max_ntok() == 32
+    got, want = _gemm_case(dt, gated, [20, 0, 32, 7, 45], K=K, N=N, ntok=32, seed=12, sums=True)
+    np.testing.assert_allclose(got, want, rtol=RTOL, atol=(2 if dt == "bf16" else 1) * ATOL)
+
+
 @pytest.mark.parametrize("splitk", [False, True])
 def test_gate_up_output_sums(splitk):
     """The gated GEMM also emits its output's (C, S) group sums (fused in the decode epilogue, or a

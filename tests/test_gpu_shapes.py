@@ -95,7 +95,7 @@ def _layer_case(E, k, H, I, T, dt, n_check, seed, zipf=False, outliers=False, gr
     w2 = [_expert_awq(2 * seed + 1, e, H, I, dt) for e in pick]
     st = lambda ws, i: np.stack([w[i] for w in ws])  # noqa: E731
     from paper_2504_16214_b200.moe import ops
-    decode = ops.pick_ntok(T * k, E) <= 16  # offset-code GEMMs: unrounded (q - z) * s
+    decode = ops.pick_ntok(T * k, E) <= ops.decode_max_ntok()  # offset-code GEMMs: unrounded (q - z) * s
     want, scale = O.moe_forward_expertwise(x, st(w13, 0), st(w13, 1), st(w13, 2), st(w2, 0), st(w2, 1), st(w2, 2),
                                            ids_loc, w_masked, dt, with_scale=True, exact_dequant=decode)
     return got, want, scale, pick
