@@ -12,6 +12,23 @@ class TileSynthError(Exception):
     """Root of everything the synthesizer raises."""
 
 
+class ParseError(TileSynthError):
+    """Malformed program, layout or tuple text; ``line`` / ``column`` locate it when known."""
+
+    def __init__(self, message, line=0, column=0):
+        self.line, self.column = line, column
+        super().__init__(f"line {line}, col {column}: {message}" if line else message)
+
+
+class ConflictDetected(TileSynthError):
+    """One tensor was handed two different thread-value layouts."""
+
+    def __init__(self, tensor, existing, incoming, op_index):
+        self.tensor, self.existing, self.incoming, self.op_index = tensor, existing, incoming, op_index
+        super().__init__(f"op {op_index} assigns tensor '{tensor}' the layout {incoming}, "
+                         f"but it already has {existing}")
+
+
 # (class, parent, what it means)
 _TAXONOMY = (
     ("LayoutError", "TileSynthError", "Layout-algebra failure."),
@@ -37,23 +54,6 @@ _TAXONOMY = (
 
 for _cls, _base, _doc in _TAXONOMY:
     globals()[_cls] = type(_cls, (globals()[_base],), {"__doc__": _doc, "__module__": __name__})
-
-
-class ParseError(TileSynthError):
-    """Malformed program, layout or tuple text; ``line`` / ``column`` locate it when known."""
-
-    def __init__(self, message, line=0, column=0):
-        self.line, self.column = line, column
-        super().__init__(f"line {line}, col {column}: {message}" if line else message)
-
-
-class ConflictDetected(TileSynthError):
-    """One tensor was handed two different thread-value layouts."""
-
-    def __init__(self, tensor, existing, incoming, op_index):
-        self.tensor, self.existing, self.incoming, self.op_index = tensor, existing, incoming, op_index
-        super().__init__(f"op {op_index} assigns tensor '{tensor}' the layout {incoming}, "
-                         f"but it already has {existing}")
 
 
 __all__ = ["TileSynthError", "ParseError", "ConflictDetected"] + [row[0] for row in _TAXONOMY]

@@ -45,17 +45,6 @@ Candidate = record("Candidate", ["index", "choices", "layouts", "patches", "smem
                    module=__name__)
 
 
-def _copy_choice_points(graph, catalog):
-    """(copy op, its candidate instructions) for every copy that needs an instruction."""
-    out = []
-    for op in graph.ops:
-        if op.kind == "copy":
-            src, dst = graph.tensor(op.operands[0]), graph.tensor(op.results[0])
-            if not src.scope == dst.scope == "Register":
-                out.append((op, candidates_for_copy(catalog, src, dst)))
-    return out
-
-
 class _ComponentMemo:
     """Propagation results of one component, keyed by the instruction choices of its ops."""
 
@@ -100,64 +89,83 @@ class _Evaluator:
                 _synthesize_staging(self.graph, self.catalog, self.config, state))
 
 
-def evaluate_assignment(graph, catalog, config, choices):
-    """Propagate layouts over every component and synthesise every buffer for one leaf;
-    ``choices`` is completed in place with the matrix instructions the anchors pick."""
-    state = PropagationState(graph, config)
-    for component in partition_components(graph):
-        propagate(component, graph, choices, config, catalog, state)
-    return (choices, state.layouts, state.patches, _synthesize_shared(graph, choices, state),
-            _synthesize_staging(graph, catalog, config, state))
+# ------------------------------------------------------------------------------------------ pipeline
+SynthesisResult = record(
+    "SynthesisResult", ["graph", "config", "catalog", ("diagnostics", list), ("candidates", list)],
+    "The live graph, the ranked candidates (best first) or the diagnostics.", module=__name__,
+    ok=property(lambda r: not r.diagnostics and (bool(r.candidates) or not r.graph.ops)),
+    best=property(lambda r: r.candidates[0] if r.candidates else None))
 
 
-def _synthesize_shared(graph, choices, state):
-    """One layout + swizzle per shared tensor from the accesses of every copy touching it."""
-    users = {}
-    for op in graph.ops:
-        if op.kind != "copy":
-            continue
-        for side, name in (("src", op.operands[0]), ("dst", op.results[0])):
-            decl = graph.tensor(name)
-            if decl.scope == "Shared":
-                inst = choices[op.index]
-                users.setdefault(name, []).append(BufferCopy(op.index, state.layouts[(op.index, side)],
-                                                             inst.vector_elems(decl.dtype), inst.name))
-    return {name: synthesize_buffer(name, graph.tensor(name).shape, graph.tensor(name).dtype.bits, copies)
-            for name, copies in sorted(users.items())}
+# ----------------------------------------------------------------------------------------
+# latency model and ranking
+class CostOp(namedtuple("CostOp", "label reads writes instruction invocations issue_cycles completion_cycles "
+                                "replays", defaults=(1,))):
+    """One issue step: the tensors it reads and writes (RAW tracking) and its latency. ``replays``:
+    an n-way bank-conflicted access occupies the issue path n times."""
+
+    __slots__ = ()
+
+    @property
+    def issue_total(self):
+        return self.invocations * self.issue_cycles * self.replays
 
 
-def _staging_instructions(catalog, decl):
-    """(store, load) pairs of equal width for a register redistribution through shared memory,
-    widest store first; loads are generic entries."""
-    tmp = TensorDecl("staging", "Shared", decl.dtype, decl.shape)
-    loads = {}
-    for ld in candidates_for_copy(catalog, tmp, decl):
-        if ld.generic:
-            loads.setdefault(ld.vector_bytes, ld)
-    return [(st, loads[st.vector_bytes]) for st in candidates_for_copy(catalog, decl, tmp) if st.vector_bytes in loads]
+# one row of the timing pass: the step, its issue cycles, stall, start and completion time
+OpCost = namedtuple("OpCost", "label instruction invocations issue stall start completes")
 
 
-def _synthesize_staging(graph, catalog, config, state):
-    """A staging buffer for every user rearrange and every inserted redistribution patch: the first
-    (store, load) pair whose two accesses unify."""
-    jobs = [(f"rearrange@{op.index}", op.operands[0], state.layouts[op.operands[0]], state.layouts[op.results[0]])
-            for op in graph.ops
-            if op.kind == "rearrange" and op.operands[0] in state.layouts and op.results[0] in state.layouts]
-    jobs += [(f"redistribute@{p.op_index}:{p.tensor}", p.tensor, p.from_layout, p.to_layout) for p in state.patches]
-    out = {}
-    for label, tensor, before, after in jobs:
-        decl = graph.tensor(tensor)
-        for st, ld in _staging_instructions(catalog, decl):
-            pair = [BufferCopy(-1, before, st.vector_elems(decl.dtype), st.name),
-                    BufferCopy(-2, after, ld.vector_elems(decl.dtype), ld.name)]
-            try:
-                out[label] = synthesize_buffer(label, decl.shape, decl.dtype.bits, pair)
-                break
-            except PRUNE:
-                continue
-        else:
-            raise Unsatisfiable(f"no staging layout for redistribution of {tensor}")
-    return out
+class CostEstimate:
+    """Total modelled cycles of a candidate and the per-step timing rows."""
+
+    def __init__(self, total_cycles, breakdown=None):
+        self.total_cycles, self.breakdown = total_cycles, list(breakdown or [])
+
+    def render(self):
+        fmt = "{0.label}: issue {0.issue} (x{0.invocations}), stall {0.stall}, start {0.start}, completes {0.completes}"
+        return [fmt.format(c) for c in self.breakdown] + ["total %d" % self.total_cycles]
+
+
+def _step_rearrange(op, cand, graph, catalog, alu):
+    out_tv = cand.layouts.get(op.results[0])
+    staged = _staging_ops("rearrange@%d" % op.index, op.operands[0], out_tv.values if out_tv else 1, catalog, cand,
+                          op.trip_count)
+    return staged + [_op_step(op, "rearrange", "register_move", 1)]
+
+
+def _step_copy(op, cand, graph, catalog, alu):
+    inst = cand.choices.get(op.index)
+    if inst is None:  # register -> register move, one ALU op per value
+        return [_op_step(op, "copy", alu, cand.layouts[op.results[0]].values * op.trip_count)]
+    buffers = [cand.smem[t] for t in (op.operands[0], op.results[0]) if t in cand.smem]
+    replays = max([1] + [b.copy_conflicts.get(op.index, 1) for b in buffers])
+    return [_op_step(op, "copy", inst, count_invocations(op, cand, inst, graph), replays)]
+
+
+def _step_gemm(op, cand, graph, catalog, alu):
+    inst = cand.choices[op.index]
+    return [_op_step(op, "gemm", inst, count_invocations(op, cand, inst, graph))]
+
+
+_STEPS = {"rearrange": _step_rearrange, "copy": _step_copy, "gemm": _step_gemm}
+
+
+def synthesize_program(graph, catalog, config=None):
+    """Validate, drop dead code, search, rank. Failures come back as diagnostics (``result.ok``)."""
+    config = config or SynthesisConfig()
+    problems = validate(graph)
+    if problems:
+        return SynthesisResult(graph, config, catalog, problems)
+    live = eliminate_dead_code(graph)
+    if graph.ops and not live.ops:
+        return SynthesisResult(live, config, catalog, ["all operations are dead code (no global store)"])
+    try:
+        found = expand_search(live, catalog, config)
+    except TileSynthError as e:
+        return SynthesisResult(live, config, catalog, [str(e)])
+    if live.ops and not found:
+        return SynthesisResult(live, config, catalog, ["no valid candidate: every instruction assignment failed"])
+    return SynthesisResult(live, config, catalog, [], rank(found, live, catalog))
 
 
 def expand_search(graph, catalog, config):
@@ -193,59 +201,54 @@ def expand_search(graph, catalog, config):
     return found
 
 
-# ------------------------------------------------------------------------------------------ pipeline
-SynthesisResult = record(
-    "SynthesisResult", ["graph", "config", "catalog", ("diagnostics", list), ("candidates", list)],
-    "The live graph, the ranked candidates (best first) or the diagnostics.", module=__name__,
-    ok=property(lambda r: not r.diagnostics and (bool(r.candidates) or not r.graph.ops)),
-    best=property(lambda r: r.candidates[0] if r.candidates else None))
+def evaluate_assignment(graph, catalog, config, choices):
+    """Propagate layouts over every component and synthesise every buffer for one leaf;
+    ``choices`` is completed in place with the matrix instructions the anchors pick."""
+    state = PropagationState(graph, config)
+    for component in partition_components(graph):
+        propagate(component, graph, choices, config, catalog, state)
+    return (choices, state.layouts, state.patches, _synthesize_shared(graph, choices, state),
+            _synthesize_staging(graph, catalog, config, state))
 
 
-def synthesize_program(graph, catalog, config=None):
-    """Validate, drop dead code, search, rank. Failures come back as diagnostics (``result.ok``)."""
-    config = config or SynthesisConfig()
-    problems = validate(graph)
-    if problems:
-        return SynthesisResult(graph, config, catalog, problems)
-    live = eliminate_dead_code(graph)
-    if graph.ops and not live.ops:
-        return SynthesisResult(live, config, catalog, ["all operations are dead code (no global store)"])
-    try:
-        found = expand_search(live, catalog, config)
-    except TileSynthError as e:
-        return SynthesisResult(live, config, catalog, [str(e)])
-    if live.ops and not found:
-        return SynthesisResult(live, config, catalog, ["no valid candidate: every instruction assignment failed"])
-    return SynthesisResult(live, config, catalog, [], rank(found, live, catalog))
+def rank(candidates, graph, catalog):
+    """Ascending total cycles; ties keep discovery order."""
+    for cand in candidates:
+        if cand.cost is None:
+            estimate(cand, graph, catalog)
+    return sorted(candidates, key=lambda c: (c.cost.total_cycles, c.index))
 
 
-# ----------------------------------------------------------------------------------------
-# latency model and ranking
-class CostOp(namedtuple("CostOp", "label reads writes instruction invocations issue_cycles completion_cycles "
-                                "replays", defaults=(1,))):
-    """One issue step: the tensors it reads and writes (RAW tracking) and its latency. ``replays``:
-    an n-way bank-conflicted access occupies the issue path n times."""
-
-    __slots__ = ()
-
-    @property
-    def issue_total(self):
-        return self.invocations * self.issue_cycles * self.replays
+def estimate(candidate, graph, catalog):
+    candidate.cost = estimate_sequence(cost_sequence(candidate, graph, catalog))
+    return candidate.cost
 
 
-# one row of the timing pass: the step, its issue cycles, stall, start and completion time
-OpCost = namedtuple("OpCost", "label instruction invocations issue stall start completes")
+# ------------------------------------------------------------------------------------------ timing
+def estimate_sequence(seq):
+    """Issue the steps in order against a scoreboard of tensor -> latest pending completion."""
+    ready, clock, horizon, rows = {}, 0, 0, []
+    for step in seq:
+        begin = max([clock] + [ready[t] for t in step.reads if t in ready])
+        stall, clock = begin - clock, begin + step.issue_total
+        finish = clock + step.completion_cycles
+        ready.update((t, max(ready.get(t, 0), finish)) for t in step.writes)
+        horizon = max(horizon, finish)
+        rows.append(OpCost(step.label, step.instruction, step.invocations, step.issue_total, stall, begin, finish))
+    return CostEstimate(max(clock, horizon), rows)
 
 
-class CostEstimate:
-    """Total modelled cycles of a candidate and the per-step timing rows."""
-
-    def __init__(self, total_cycles, breakdown=None):
-        self.total_cycles, self.breakdown = total_cycles, list(breakdown or [])
-
-    def render(self):
-        fmt = "{0.label}: issue {0.issue} (x{0.invocations}), stall {0.stall}, start {0.start}, completes {0.completes}"
-        return [fmt.format(c) for c in self.breakdown] + ["total %d" % self.total_cycles]
+def cost_sequence(candidate, graph, catalog):
+    """The candidate's steps in program order; an op's redistribution patches run just before it."""
+    alu = catalog.alu()
+    seq = []
+    for op in graph.ops:
+        for p in candidate.patches:
+            if p.op_index == op.index:
+                seq += _staging_ops(f"redistribute@{p.op_index}:{p.tensor}", p.tensor, p.to_layout.values, catalog,
+                                    candidate, op.trip_count)
+        seq += _STEPS.get(op.kind, _step_alu)(op, candidate, graph, catalog, alu)
+    return seq
 
 
 # ------------------------------------------------------------------------------------- invocations
@@ -269,6 +272,17 @@ def count_invocations(op, candidate, inst, graph):
     return lay[op.results[0]].values * op.trip_count   # register-file op: one per produced value
 
 
+def _step_alu(op, cand, graph, catalog, alu):
+    return [_op_step(op, op.kind, alu, count_invocations(op, cand, alu, graph))]
+
+
+def _op_step(op, what, inst, count, replays=1):
+    """The step of op ``op`` itself (label ``op<i>.<what>``), reading its operands, writing its results."""
+    name, issue, done = (inst, 1, 1) if isinstance(inst, str) else (inst.name, inst.issue_cycles,
+                                                                    inst.completion_cycles)
+    return CostOp("op%d.%s" % (op.index, what), set(op.operands), set(op.results), name, count, issue, done, replays)
+
+
 # --------------------------------------------------------------------------------------- sequences
 def _staging_ops(label, tensor, values, catalog, candidate, trip):
     """A redistribution = store to + load from a staging buffer (scalar 16-bit round trip when no
@@ -289,76 +303,62 @@ def _staging_ops(label, tensor, values, catalog, candidate, trip):
     return out
 
 
-def _op_step(op, what, inst, count, replays=1):
-    """The step of op ``op`` itself (label ``op<i>.<what>``), reading its operands, writing its results."""
-    name, issue, done = (inst, 1, 1) if isinstance(inst, str) else (inst.name, inst.issue_cycles,
-                                                                    inst.completion_cycles)
-    return CostOp("op%d.%s" % (op.index, what), set(op.operands), set(op.results), name, count, issue, done, replays)
+def _synthesize_staging(graph, catalog, config, state):
+    """A staging buffer for every user rearrange and every inserted redistribution patch: the first
+    (store, load) pair whose two accesses unify."""
+    jobs = [(f"rearrange@{op.index}", op.operands[0], state.layouts[op.operands[0]], state.layouts[op.results[0]])
+            for op in graph.ops
+            if op.kind == "rearrange" and op.operands[0] in state.layouts and op.results[0] in state.layouts]
+    jobs += [(f"redistribute@{p.op_index}:{p.tensor}", p.tensor, p.from_layout, p.to_layout) for p in state.patches]
+    out = {}
+    for label, tensor, before, after in jobs:
+        decl = graph.tensor(tensor)
+        for st, ld in _staging_instructions(catalog, decl):
+            pair = [BufferCopy(-1, before, st.vector_elems(decl.dtype), st.name),
+                    BufferCopy(-2, after, ld.vector_elems(decl.dtype), ld.name)]
+            try:
+                out[label] = synthesize_buffer(label, decl.shape, decl.dtype.bits, pair)
+                break
+            except PRUNE:
+                continue
+        else:
+            raise Unsatisfiable(f"no staging layout for redistribution of {tensor}")
+    return out
 
 
-def _step_rearrange(op, cand, graph, catalog, alu):
-    out_tv = cand.layouts.get(op.results[0])
-    staged = _staging_ops("rearrange@%d" % op.index, op.operands[0], out_tv.values if out_tv else 1, catalog, cand,
-                          op.trip_count)
-    return staged + [_op_step(op, "rearrange", "register_move", 1)]
+def _staging_instructions(catalog, decl):
+    """(store, load) pairs of equal width for a register redistribution through shared memory,
+    widest store first; loads are generic entries."""
+    tmp = TensorDecl("staging", "Shared", decl.dtype, decl.shape)
+    loads = {}
+    for ld in candidates_for_copy(catalog, tmp, decl):
+        if ld.generic:
+            loads.setdefault(ld.vector_bytes, ld)
+    return [(st, loads[st.vector_bytes]) for st in candidates_for_copy(catalog, decl, tmp) if st.vector_bytes in loads]
 
 
-def _step_copy(op, cand, graph, catalog, alu):
-    inst = cand.choices.get(op.index)
-    if inst is None:  # register -> register move, one ALU op per value
-        return [_op_step(op, "copy", alu, cand.layouts[op.results[0]].values * op.trip_count)]
-    buffers = [cand.smem[t] for t in (op.operands[0], op.results[0]) if t in cand.smem]
-    replays = max([1] + [b.copy_conflicts.get(op.index, 1) for b in buffers])
-    return [_op_step(op, "copy", inst, count_invocations(op, cand, inst, graph), replays)]
-
-
-def _step_gemm(op, cand, graph, catalog, alu):
-    inst = cand.choices[op.index]
-    return [_op_step(op, "gemm", inst, count_invocations(op, cand, inst, graph))]
-
-
-def _step_alu(op, cand, graph, catalog, alu):
-    return [_op_step(op, op.kind, alu, count_invocations(op, cand, alu, graph))]
-
-
-_STEPS = {"rearrange": _step_rearrange, "copy": _step_copy, "gemm": _step_gemm}
-
-
-def cost_sequence(candidate, graph, catalog):
-    """The candidate's steps in program order; an op's redistribution patches run just before it."""
-    alu = catalog.alu()
-    seq = []
+def _synthesize_shared(graph, choices, state):
+    """One layout + swizzle per shared tensor from the accesses of every copy touching it."""
+    users = {}
     for op in graph.ops:
-        for p in candidate.patches:
-            if p.op_index == op.index:
-                seq += _staging_ops(f"redistribute@{p.op_index}:{p.tensor}", p.tensor, p.to_layout.values, catalog,
-                                    candidate, op.trip_count)
-        seq += _STEPS.get(op.kind, _step_alu)(op, candidate, graph, catalog, alu)
-    return seq
+        if op.kind != "copy":
+            continue
+        for side, name in (("src", op.operands[0]), ("dst", op.results[0])):
+            decl = graph.tensor(name)
+            if decl.scope == "Shared":
+                inst = choices[op.index]
+                users.setdefault(name, []).append(BufferCopy(op.index, state.layouts[(op.index, side)],
+                                                             inst.vector_elems(decl.dtype), inst.name))
+    return {name: synthesize_buffer(name, graph.tensor(name).shape, graph.tensor(name).dtype.bits, copies)
+            for name, copies in sorted(users.items())}
 
 
-# ------------------------------------------------------------------------------------------ timing
-def estimate_sequence(seq):
-    """Issue the steps in order against a scoreboard of tensor -> latest pending completion."""
-    ready, clock, horizon, rows = {}, 0, 0, []
-    for step in seq:
-        begin = max([clock] + [ready[t] for t in step.reads if t in ready])
-        stall, clock = begin - clock, begin + step.issue_total
-        finish = clock + step.completion_cycles
-        ready.update((t, max(ready.get(t, 0), finish)) for t in step.writes)
-        horizon = max(horizon, finish)
-        rows.append(OpCost(step.label, step.instruction, step.invocations, step.issue_total, stall, begin, finish))
-    return CostEstimate(max(clock, horizon), rows)
-
-
-def estimate(candidate, graph, catalog):
-    candidate.cost = estimate_sequence(cost_sequence(candidate, graph, catalog))
-    return candidate.cost
-
-
-def rank(candidates, graph, catalog):
-    """Ascending total cycles; ties keep discovery order."""
-    for cand in candidates:
-        if cand.cost is None:
-            estimate(cand, graph, catalog)
-    return sorted(candidates, key=lambda c: (c.cost.total_cycles, c.index))
+def _copy_choice_points(graph, catalog):
+    """(copy op, its candidate instructions) for every copy that needs an instruction."""
+    out = []
+    for op in graph.ops:
+        if op.kind == "copy":
+            src, dst = graph.tensor(op.operands[0]), graph.tensor(op.results[0])
+            if not src.scope == dst.scope == "Register":
+                out.append((op, candidates_for_copy(catalog, src, dst)))
+    return out

@@ -36,120 +36,7 @@ from .algebra import restrict_tv
 SCHEMA_VERSION = 1
 
 
-def _buffer_entry(smem):
-    return {
-        "layout": str(smem.layout),
-        "swizzle": str(smem.swizzle),
-        "conflicts": {str(k): v for k, v in sorted(smem.copy_conflicts.items())},
-        "identity_conflicts": {str(k): v for k, v in sorted(smem.identity_conflicts.items())},
-    }
-
-
-def _copy_entry(graph, cand, op):
-    inst = cand.choices[op.index]
-    entry = {"op": op.index, "instruction": inst.name, "vector_bytes": inst.vector_bytes}
-    for name in (op.operands[0], op.results[0]):
-        if name in cand.smem and graph.tensor(name).scope == "Shared":
-            entry["conflicts"] = cand.smem[name].copy_conflicts.get(op.index)
-            entry["identity_conflicts"] = cand.smem[name].identity_conflicts.get(op.index)
-    return entry
-
-
 _COST_FIELDS = ("label", "instruction", "invocations", "issue", "stall", "start", "completes")
-
-
-def _candidate_section(result, cand):
-    g = result.graph
-    buffers = {name: _buffer_entry(s) for name, s in sorted(cand.smem.items())}
-    buffers.update((name, _buffer_entry(s)) for name, s in sorted(cand.staging.items()))
-    return {
-        "index": cand.index,
-        "total_cycles": cand.cost.total_cycles,
-        "tensors": {name: {"tv": str(cand.layouts[name].layout), "tile": list(cand.layouts[name].tile)}
-                    for name in sorted(g.tensors) if name in cand.layouts},
-        "copies": [_copy_entry(g, cand, op) for op in g.ops
-                   if op.kind == "copy" and op.index in cand.choices and cand.choices[op.index].category == "copy"],
-        "buffers": buffers,
-        "redistributions": [{"op": p.op_index, "tensor": p.tensor, "from": str(p.from_layout.layout),
-                             "to": str(p.to_layout.layout)} for p in cand.patches],
-        "cost": [{k: getattr(row, k) for k in _COST_FIELDS} for row in cand.cost.breakdown],
-    }
-
-
-def build_report(result, all_candidates=False):
-    """The report dict. A catalog with TMA entries (sm100) adds ``best.buffers[name].tma``: whether
-    the bulk tensor engine can serve the buffer (smem_plan.check_tma on its unified constraint);
-    catalogs without them (sm80) produce the reference's schema unchanged."""
-    g = result.graph
-    out = {
-        "version": SCHEMA_VERSION,
-        "arch": result.catalog.arch,
-        "threads": result.config.threads,
-        "program": {"ops": len(g.ops),
-                    "tensors": {n: {"scope": d.scope, "dtype": str(d.dtype), "shape": list(d.shape)}
-                                for n, d in sorted(g.tensors.items())}},
-        "diagnostics": list(result.diagnostics),
-        "candidates": {"count": len(result.candidates), "costs": [c.cost.total_cycles for c in result.candidates]},
-    }
-    if result.best is not None:
-        out["best"] = _candidate_section(result, result.best)
-        from .repack import tma_plan
-        for name, entry in tma_plan(result).items():
-            out["best"]["buffers"][name]["tma"] = entry
-    if all_candidates:
-        out["all"] = [_candidate_section(result, c) for c in result.candidates]
-    return out
-
-
-def render_json(report):
-    return json.dumps(report, indent=2, sort_keys=True) + "\n"
-
-
-def _table(title, header, rows):
-    """A titled, column-aligned block (no block for no rows)."""
-    if not rows:
-        return []
-    cells = [header] + [[str(c) for c in r] for r in rows]
-    widths = [max(len(r[i]) for r in cells) for i in range(len(header))]
-    fmt = lambda r: "  " + "  ".join(c.ljust(w) for c, w in zip(r, widths)).rstrip()  # noqa: E731
-    return [title] + [fmt(r) for r in cells]
-
-
-def render_text(report):
-    """Human-readable summary of a report dict: a header, then one table per section of the best
-    candidate (tensor layouts, copies, shared buffers, redistributions, cost steps)."""
-    prog, cands, best = report["program"], report["candidates"], report.get("best")
-    out = [f"tilesynth -- {report['arch']}, {report['threads']} threads, {prog['ops']} ops over "
-           f"{len(prog['tensors'])} tensors; {cands['count']} candidates {cands['costs']}"]
-    out += [f"diagnostic: {d}" for d in report["diagnostics"]]
-    if best:
-        out.append(f"best candidate #{best['index']}: {best['total_cycles']} cycles")
-        sections = (
-            ("register / tensor layouts", ("tensor", "thread-value layout", "tile"),
-             [(f"{n}:", t["tv"], "x".join(map(str, t["tile"]))) for n, t in best["tensors"].items()]),
-            ("copies", ("op", "instruction", "bytes", "conflicts (identity)"),
-             [(c["op"], c["instruction"], c["vector_bytes"],
-               f"{c['conflicts']} ({c['identity_conflicts']})" if "conflicts" in c else "-") for c in best["copies"]]),
-            ("shared buffers", ("buffer", "layout (+) swizzle", "tma"),
-             [(f"{n}:", f"{b['layout']} (+) {b['swizzle']}",
-               ("yes" if b["tma"]["feasible"] else "no") if "tma" in b else "-") for n, b in best["buffers"].items()]),
-            ("redistributions", ("op", "tensor", "from -> to"),
-             [(r["op"], r["tensor"], f"{r['from']} -> {r['to']}") for r in best["redistributions"]]),
-            ("cost", ("step", "instruction", "n", "issue", "stall", "start", "completes"),
-             [(c["label"], c["instruction"], c["invocations"], c["issue"], c["stall"], c["start"], c["completes"])
-              for c in best["cost"]]),
-        )
-        for title, header, rows in sections:
-            out += _table(title, header, rows)
-    return "\n".join(out) + "\n"
-
-
-# ------------------------------------------------------------------------------------------ explain
-def _through_instruction(tv, inst_tv):
-    """Known layout restricted to one instruction tile, composed with the instruction's inverse
-    regrouped by its tile extents: instruction-tile coordinate -> tensor position."""
-    core = restrict_tv(tv, inst_tv.threads, inst_tv.values)[0]
-    return compose(core.layout, group_modes(inverse(inst_tv.layout), inst_tv.tile))
 
 
 def _gemm_lines(graph, cand, op):
@@ -204,20 +91,6 @@ _EXPLAIN = {"gemm": _gemm_lines, "copy": _copy_lines, "reduce": _reduce_lines, "
             "elementwise": _elementwise_lines}
 
 
-def explain_op(result, op_index):
-    """The constraints touching one op, evaluated on the best candidate."""
-    ops = result.graph.ops
-    if op_index < 0 or op_index >= len(ops):
-        raise UnknownOp(f"op index {op_index} out of range (0..{len(ops) - 1})")
-    if result.best is None:
-        return "no valid candidate to explain"
-    op = ops[op_index]
-    head = f"op {op_index}: {op.kind} {' '.join(op.operands)} -> {' '.join(op.results)}"
-    body = _EXPLAIN.get(op.kind, lambda g, c, o: ["  redistribution step (no layout constraint)"])(
-        result.graph, result.best, op)
-    return "\n".join([head] + body) + "\n"
-
-
 # ---------------------------------------------------------------------------------------- command line
 _FLAGS = (
     (("--program",), dict(required=True, help="program file")),
@@ -238,31 +111,90 @@ class _Exit(Exception):
         self.code, self.message = code, message
 
 
-def _parser():
-    p = argparse.ArgumentParser(prog="tilesynth", description="Synthesize thread-value and shared-memory layouts "
-                                "for a tile-level GPU program and rank instruction choices by modeled latency.")
-    for names, kw in _FLAGS:
-        p.add_argument(*names, **kw)
-    return p
+def main(argv=None):
+    args = _parser().parse_args(argv)
+    try:
+        return _run(args)
+    except _Exit as stop:
+        if stop.message:
+            print(stop.message, file=sys.stderr)
+        return stop.code
 
 
-def _inputs(args):
-    program = Path(args.program)
-    catalog = Path(args.catalog) if args.catalog else builtin_catalog_path()
-    for path, what in ((program, "program"), (catalog, "catalog")):
-        if not path.is_file():
-            raise _Exit(2, f"error: {what} file not found: {path}")
-    if args.threads < 32 or args.threads % 32:
-        raise _Exit(2, "error: --threads must be a positive multiple of 32")
-    try:
-        cat = load_catalog(catalog)
-    except CatalogFormatError as e:
-        raise _Exit(1, f"error: {e}") from None
-    try:
-        graph = parse_program(program.read_text())
-    except ParseError as e:
-        raise _Exit(1, f"error: {program}: {e}") from None
-    return graph, cat
+if __name__ == "__main__":
+    sys.exit(main())
+
+
+def build_report(result, all_candidates=False):
+    """The report dict. A catalog with TMA entries (sm100) adds ``best.buffers[name].tma``: whether
+    the bulk tensor engine can serve the buffer (smem_plan.check_tma on its unified constraint);
+    catalogs without them (sm80) produce the reference's schema unchanged."""
+    g = result.graph
+    out = {
+        "version": SCHEMA_VERSION,
+        "arch": result.catalog.arch,
+        "threads": result.config.threads,
+        "program": {"ops": len(g.ops),
+                    "tensors": {n: {"scope": d.scope, "dtype": str(d.dtype), "shape": list(d.shape)}
+                                for n, d in sorted(g.tensors.items())}},
+        "diagnostics": list(result.diagnostics),
+        "candidates": {"count": len(result.candidates), "costs": [c.cost.total_cycles for c in result.candidates]},
+    }
+    if result.best is not None:
+        out["best"] = _candidate_section(result, result.best)
+        from .repack import tma_plan
+        for name, entry in tma_plan(result).items():
+            out["best"]["buffers"][name]["tma"] = entry
+    if all_candidates:
+        out["all"] = [_candidate_section(result, c) for c in result.candidates]
+    return out
+
+
+def render_json(report):
+    return json.dumps(report, indent=2, sort_keys=True) + "\n"
+
+
+def render_text(report):
+    """Human-readable summary of a report dict: a header, then one table per section of the best
+    candidate (tensor layouts, copies, shared buffers, redistributions, cost steps)."""
+    prog, cands, best = report["program"], report["candidates"], report.get("best")
+    out = [f"tilesynth -- {report['arch']}, {report['threads']} threads, {prog['ops']} ops over "
+           f"{len(prog['tensors'])} tensors; {cands['count']} candidates {cands['costs']}"]
+    out += [f"diagnostic: {d}" for d in report["diagnostics"]]
+    if best:
+        out.append(f"best candidate #{best['index']}: {best['total_cycles']} cycles")
+        sections = (
+            ("register / tensor layouts", ("tensor", "thread-value layout", "tile"),
+             [(f"{n}:", t["tv"], "x".join(map(str, t["tile"]))) for n, t in best["tensors"].items()]),
+            ("copies", ("op", "instruction", "bytes", "conflicts (identity)"),
+             [(c["op"], c["instruction"], c["vector_bytes"],
+               f"{c['conflicts']} ({c['identity_conflicts']})" if "conflicts" in c else "-") for c in best["copies"]]),
+            ("shared buffers", ("buffer", "layout (+) swizzle", "tma"),
+             [(f"{n}:", f"{b['layout']} (+) {b['swizzle']}",
+               ("yes" if b["tma"]["feasible"] else "no") if "tma" in b else "-") for n, b in best["buffers"].items()]),
+            ("redistributions", ("op", "tensor", "from -> to"),
+             [(r["op"], r["tensor"], f"{r['from']} -> {r['to']}") for r in best["redistributions"]]),
+            ("cost", ("step", "instruction", "n", "issue", "stall", "start", "completes"),
+             [(c["label"], c["instruction"], c["invocations"], c["issue"], c["stall"], c["start"], c["completes"])
+              for c in best["cost"]]),
+        )
+        for title, header, rows in sections:
+            out += _table(title, header, rows)
+    return "\n".join(out) + "\n"
+
+
+def explain_op(result, op_index):
+    """The constraints touching one op, evaluated on the best candidate."""
+    ops = result.graph.ops
+    if op_index < 0 or op_index >= len(ops):
+        raise UnknownOp(f"op index {op_index} out of range (0..{len(ops) - 1})")
+    if result.best is None:
+        return "no valid candidate to explain"
+    op = ops[op_index]
+    head = f"op {op_index}: {op.kind} {' '.join(op.operands)} -> {' '.join(op.results)}"
+    body = _EXPLAIN.get(op.kind, lambda g, c, o: ["  redistribution step (no layout constraint)"])(
+        result.graph, result.best, op)
+    return "\n".join([head] + body) + "\n"
 
 
 def _run(args):
@@ -288,15 +220,83 @@ def _run(args):
     return 0
 
 
-def main(argv=None):
-    args = _parser().parse_args(argv)
+def _inputs(args):
+    program = Path(args.program)
+    catalog = Path(args.catalog) if args.catalog else builtin_catalog_path()
+    for path, what in ((program, "program"), (catalog, "catalog")):
+        if not path.is_file():
+            raise _Exit(2, f"error: {what} file not found: {path}")
+    if args.threads < 32 or args.threads % 32:
+        raise _Exit(2, "error: --threads must be a positive multiple of 32")
     try:
-        return _run(args)
-    except _Exit as stop:
-        if stop.message:
-            print(stop.message, file=sys.stderr)
-        return stop.code
+        cat = load_catalog(catalog)
+    except CatalogFormatError as e:
+        raise _Exit(1, f"error: {e}") from None
+    try:
+        graph = parse_program(program.read_text())
+    except ParseError as e:
+        raise _Exit(1, f"error: {program}: {e}") from None
+    return graph, cat
 
 
-if __name__ == "__main__":
-    sys.exit(main())
+def _parser():
+    p = argparse.ArgumentParser(prog="tilesynth", description="Synthesize thread-value and shared-memory layouts "
+                                "for a tile-level GPU program and rank instruction choices by modeled latency.")
+    for names, kw in _FLAGS:
+        p.add_argument(*names, **kw)
+    return p
+
+
+# ------------------------------------------------------------------------------------------ explain
+def _through_instruction(tv, inst_tv):
+    """Known layout restricted to one instruction tile, composed with the instruction's inverse
+    regrouped by its tile extents: instruction-tile coordinate -> tensor position."""
+    core = restrict_tv(tv, inst_tv.threads, inst_tv.values)[0]
+    return compose(core.layout, group_modes(inverse(inst_tv.layout), inst_tv.tile))
+
+
+def _table(title, header, rows):
+    """A titled, column-aligned block (no block for no rows)."""
+    if not rows:
+        return []
+    cells = [header] + [[str(c) for c in r] for r in rows]
+    widths = [max(len(r[i]) for r in cells) for i in range(len(header))]
+    fmt = lambda r: "  " + "  ".join(c.ljust(w) for c, w in zip(r, widths)).rstrip()  # noqa: E731
+    return [title] + [fmt(r) for r in cells]
+
+
+def _candidate_section(result, cand):
+    g = result.graph
+    buffers = {name: _buffer_entry(s) for name, s in sorted(cand.smem.items())}
+    buffers.update((name, _buffer_entry(s)) for name, s in sorted(cand.staging.items()))
+    return {
+        "index": cand.index,
+        "total_cycles": cand.cost.total_cycles,
+        "tensors": {name: {"tv": str(cand.layouts[name].layout), "tile": list(cand.layouts[name].tile)}
+                    for name in sorted(g.tensors) if name in cand.layouts},
+        "copies": [_copy_entry(g, cand, op) for op in g.ops
+                   if op.kind == "copy" and op.index in cand.choices and cand.choices[op.index].category == "copy"],
+        "buffers": buffers,
+        "redistributions": [{"op": p.op_index, "tensor": p.tensor, "from": str(p.from_layout.layout),
+                             "to": str(p.to_layout.layout)} for p in cand.patches],
+        "cost": [{k: getattr(row, k) for k in _COST_FIELDS} for row in cand.cost.breakdown],
+    }
+
+
+def _copy_entry(graph, cand, op):
+    inst = cand.choices[op.index]
+    entry = {"op": op.index, "instruction": inst.name, "vector_bytes": inst.vector_bytes}
+    for name in (op.operands[0], op.results[0]):
+        if name in cand.smem and graph.tensor(name).scope == "Shared":
+            entry["conflicts"] = cand.smem[name].copy_conflicts.get(op.index)
+            entry["identity_conflicts"] = cand.smem[name].identity_conflicts.get(op.index)
+    return entry
+
+
+def _buffer_entry(smem):
+    return {
+        "layout": str(smem.layout),
+        "swizzle": str(smem.swizzle),
+        "conflicts": {str(k): v for k, v in sorted(smem.copy_conflicts.items())},
+        "identity_conflicts": {str(k): v for k, v in sorted(smem.identity_conflicts.items())},
+    }

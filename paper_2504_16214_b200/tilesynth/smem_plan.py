@@ -89,10 +89,6 @@ class Swizzle(tuple):
 IDENTITY_SWIZZLE = Swizzle(0, 4, 3)
 
 
-def apply_swizzle(s, addr):
-    return s(addr)
-
-
 class AccessPattern:
     """The byte addresses one warp-wide access issues (one per thread) and its width."""
 
@@ -116,94 +112,7 @@ class AccessPattern:
         return f"AccessPattern(addresses={self.addresses!r}, width={self.width})"
 
 
-def phase_degrees(addrs, width):
-    """Conflict degree of every pattern: ``addrs`` is [..., lanes] of (already swizzled, aligned)
-    byte addresses; returns [...] = max over phases and banks of the distinct words per bank
-    (at least 1)."""
-    lanes = addrs.shape[-1]
-    if lanes == 0:
-        return np.ones(addrs.shape[:-1], dtype=np.int64)
-    words_each = max(1, width // BANK_BYTES)
-    per_phase = lanes if width <= BANK_BYTES else max(1, lanes * BANK_BYTES // width)
-    n_phase = -(-lanes // per_phase)
-    pad = n_phase * per_phase - lanes
-    if pad:  # a short last phase: repeat its first lane (a duplicate word changes no count)
-        filler = np.repeat(addrs[..., (n_phase - 1) * per_phase:(n_phase - 1) * per_phase + 1], pad, axis=-1)
-        addrs = np.concatenate([addrs, filler], axis=-1)
-    words = addrs // BANK_BYTES
-    if words_each > 1:
-        words = (words[..., None] + np.arange(words_each)).reshape(*words.shape[:-1], -1)
-    words = words.reshape(*addrs.shape[:-1], n_phase, per_phase * words_each)
-    # sort each phase's words by (bank, word): equal words are neighbours, banks are runs
-    key = np.sort((words % NUM_BANKS) << 40 | words, axis=-1)
-    fresh = np.ones(key.shape, dtype=bool)
-    fresh[..., 1:] = key[..., 1:] != key[..., :-1]
-    bank = key >> 40
-    starts = np.ones(key.shape, dtype=bool)
-    starts[..., 1:] = bank[..., 1:] != bank[..., :-1]
-    distinct = np.cumsum(fresh, axis=-1)
-    before = np.maximum.accumulate(np.where(starts, distinct - fresh, 0), axis=-1)
-    degree = (distinct - before).max(axis=(-1, -2))
-    return np.maximum(degree, 1)
-
-
-def bank_conflicts(pattern, swizzle=IDENTITY_SWIZZLE):
-    """Worst-phase conflict degree of one pattern (1 = conflict-free, also for no addresses)."""
-    addrs = swizzle(np.asarray(pattern.addresses, dtype=np.int64))
-    if addrs.size and (addrs % pattern.width).any():
-        raise MisalignedAccess(f"{swizzle} breaks {pattern.width}-byte alignment")
-    return int(phase_degrees(addrs, pattern.width))
-
-
 PatternGenerator = Callable[[Swizzle], Iterable[AccessPattern]]
-
-
-def candidate_swizzles(min_base=2):
-    """Identity plus the 1..3-bit XOR swizzles with target base 2..4 (>= ``min_base``, so vector
-    atoms of 2^min_base bytes stay whole) and source shift up to 6."""
-    return [IDENTITY_SWIZZLE] + [Swizzle(bits, base, shift) for bits in (1, 2, 3) for base in (2, 3, 4)
-                                 if base >= min_base for shift in range(bits, 7)]
-
-
-def _choose(totals):
-    if not totals:
-        return IDENTITY_SWIZZLE, 0
-    total, sw = min(totals, key=lambda ts: (ts[0], tuple(ts[1])))
-    return sw, total
-
-
-def score_swizzles(generators, candidates=()):
-    """Candidate with the least summed conflict degree over every generator's patterns (identity is
-    always a candidate; ineligible swizzles -- ones that split a vector -- are skipped)."""
-    pool = list(candidates) or candidate_swizzles()
-    if IDENTITY_SWIZZLE not in pool:
-        pool.insert(0, IDENTITY_SWIZZLE)
-    totals = []
-    for sw in pool:
-        try:
-            totals.append((sum(bank_conflicts(p, sw) for gen in generators for p in gen(sw)), sw))
-        except MisalignedAccess:
-            continue
-    return _choose(totals)
-
-
-def score_pattern_matrix(groups, pool):
-    """Batched scoring: ``groups`` holds (patterns [P, lanes] of pre-swizzle byte addresses, width)
-    per access width. Every swizzle of ``pool`` is applied to every pattern in one array
-    expression. Returns (best swizzle, its total, per-swizzle totals with -1 for ineligible)."""
-    sws = np.asarray([tuple(s) for s in pool], dtype=np.int64).reshape(-1, 3)
-    bits, base, shift = (sws[:, i][:, None, None] for i in range(3))
-    mask = (np.int64(1) << bits) - 1
-    totals = np.zeros(len(pool), dtype=np.int64)
-    eligible = np.ones(len(pool), dtype=bool)
-    for pats, width in groups:
-        a = pats[None].astype(np.int64)
-        swz = a ^ (((a >> (base + shift)) & mask) << base)
-        eligible &= ~((swz % width) != 0).any(axis=(1, 2))
-        totals += phase_degrees(swz, width).sum(axis=-1)
-    ranked = [(int(t), sw) for t, sw, ok in zip(totals, pool, eligible) if ok]
-    best, total = _choose(ranked)
-    return best, total, np.where(eligible, totals, -1)
 
 
 # ----------------------------------------------------------------------------------------
@@ -252,143 +161,6 @@ LayoutConstraint = record(
 
 
 _ITEM = re.compile(r"\(([^()]*)\)|([^,()]+)")
-
-
-def parse_constraint(text):
-    """``"((8,8),64):((1,D1),D2)"`` -> constraint; equal variable names are one variable."""
-    body = "".join(text.split())
-    try:
-        shape_txt, stride_txt = body.split(":")
-    except ValueError:
-        raise LayoutIncompatible(f"constraint text {text!r} needs one ':'") from None
-    shape_items, stride_items = _items(shape_txt), _items(stride_txt)
-    if len(shape_items) != len(stride_items):
-        raise LayoutIncompatible("constraint shape and stride have different dimension counts")
-    free = {}
-    splits = []
-    for sh, st in zip(shape_items, stride_items):
-        if isinstance(sh, list) is not isinstance(st, list):
-            raise LayoutIncompatible("constraint dimension nests differently in shape and stride")
-        sh, st = (sh, st) if isinstance(sh, list) else ([sh], [st])
-        splits.append([(int(e), int(s) if s.isdigit() else free.setdefault(s, StrideVar())) for e, s in zip(sh, st)])
-    return LayoutConstraint(tuple(math.prod(e for e, _ in dim) for dim in splits), splits)
-
-
-def _items(text):
-    if not (text.startswith("(") and text.endswith(")")):
-        raise LayoutIncompatible(f"constraint part {text!r} is not parenthesised")
-    return [g.split(",") if g is not None else w for g, w in ((m.group(1), m.group(2))
-                                                            for m in _ITEM.finditer(text[1:-1]))]
-
-
-# ------------------------------------------------------------------------------------------- build
-def _refine(extent, weight, cuts):
-    """Local cut points (1 < p < extent) of a run covering weights [weight, weight * extent) at the
-    given global boundaries; a boundary inside the run must be a multiple of ``weight``."""
-    out = []
-    for b in cuts:
-        if weight < b < weight * extent:
-            if b % weight:
-                raise LayoutIncompatible(f"boundary {b} is not aligned to the run weight {weight}")
-            out.append(b // weight)
-    return out
-
-
-def build_constraint(f, vector_elems, dims):
-    """The constraint one copy puts on the buffer layout: each thread's ``vector_elems`` consecutive
-    values must sit at consecutive addresses; every other stride stays free. LayoutIncompatible when
-    the access is not a bijection onto the buffer."""
-    f = filter_replication(f)
-    total = math.prod(dims)
-    if f.threads * f.values != total:
-        raise LayoutIncompatible(f"the access covers {f.threads * f.values} of {total} elements")
-    try:
-        runs = inverse(f.layout).runs
-    except NotInvertible as e:
-        raise LayoutIncompatible(str(e)) from e
-    T = f.threads
-    vec_cuts = (T, T * vector_elems)
-    dim_ends = list(np.cumprod(dims, dtype=object))
-    splits = [[] for _ in dims]
-    logical = 1
-    for extent, tv_weight in runs:
-        points = sorted(set(_refine(extent, tv_weight, vec_cuts)) | set(_refine(extent, logical, dim_ends)))
-        prev = 1
-        for p in points + [extent]:
-            if p % prev or extent % p:
-                raise LayoutIncompatible(f"cannot cut a run of {extent} at {p}")
-            n = p // prev
-            if n > 1 or (prev == 1 and p == extent):
-                w, lw = tv_weight * prev, logical * prev
-                dim = next(i for i, end in enumerate(dim_ends) if lw < end)
-                entry = w // T if T <= w < T * vector_elems else StrideVar(vector_elems)
-                _append_merging(splits[dim], n, entry)
-            prev = p
-        logical *= extent
-    return LayoutConstraint(tuple(dims), [dim or [(1, StrideVar(1))] for dim in splits])
-
-
-def _append_merging(dim, n, entry):
-    """Append a piece; two neighbouring free pieces of one dimension become one free piece."""
-    if dim and isinstance(entry, StrideVar) and isinstance(dim[-1][1], StrideVar):
-        m, other = dim[-1]
-        dim[-1] = (m * n, StrideVar(max(other.divisibility, entry.divisibility)))
-    else:
-        dim.append((n, entry))
-
-
-# ------------------------------------------------------------------------------------------- unify
-def _bounds(pieces):
-    """(start, end, entry) of each piece on the cumulative-extent axis."""
-    out, at = [], 1
-    for e, s in pieces:
-        out.append((at, at * e, s))
-        at *= e
-    return out
-
-
-def _sub_entry(piece, lo):
-    start, _, s = piece
-    return s * (lo // start) if isinstance(s, int) else StrideVar(s.divisibility)
-
-
-def unify(c1, c2):
-    """Least-committed constraint holding every concrete stride of both. StrideConflict when the
-    factorisations cannot be overlaid, concrete strides disagree, or the concrete pieces overlap."""
-    if c1.dims != c2.dims:
-        raise StrideConflict(f"buffer extents {c1.dims} and {c2.dims} differ")
-    merged = []
-    for xs, ys in zip(c1.splits, c2.splits):
-        bx, by = _bounds(xs), _bounds(ys)
-        dim, lo, i, j = [], 1, 0, 0
-        while i < len(bx) and j < len(by):
-            hi = min(bx[i][1], by[j][1])      # next boundary of the common refinement
-            if bx[i][1] % hi or by[j][1] % hi:
-                raise StrideConflict(f"piece boundaries misalign at {hi}")
-            a, b = _sub_entry(bx[i], lo), _sub_entry(by[j], lo)
-            if isinstance(a, int) and isinstance(b, int) and a != b:
-                raise StrideConflict(f"concrete strides {a} and {b} disagree")
-            if isinstance(a, int) or isinstance(b, int):
-                dim.append((hi // lo, a if isinstance(a, int) else b))
-            else:
-                dim.append((hi // lo, StrideVar(max(a.divisibility, b.divisibility))))
-            step_x, step_y = bx[i][1] == hi, by[j][1] == hi
-            i, j, lo = i + step_x, j + step_y, hi
-        if i < len(bx) or j < len(by):
-            raise StrideConflict("the two factorisations do not cover the same extent")
-        merged.append(dim)
-    out = LayoutConstraint(c1.dims, merged)
-    _check_chain(out)
-    return out
-
-
-def _check_chain(c):
-    """Concrete pieces, by stride, must stack into a bijection's stride chain."""
-    reach = 1
-    for e, s in sorted(c.concrete_modes(), key=lambda m: m[1]):
-        if s < reach or s % reach:
-            raise StrideConflict(f"concrete piece {e}:{s} overlaps the span {reach} below it")
-        reach = s * e
 
 
 # ------------------------------------------------------------------------------------- materialize
@@ -444,47 +216,9 @@ class _StrideChain:
         return Layout(tuple(x for x, _ in dims), tuple(y for _, y in dims))
 
 
-def materialize(c):
-    """Pick the free strides so the layout is a bijection onto [0, size): concrete pieces first by
-    stride, free pieces fill the chain gaps and then extend the chain in logical order."""
-    _check_chain(c)
-    chain = _StrideChain(c)
-    for e, s in sorted(c.concrete_modes(), key=lambda m: m[1]):
-        if s > chain.reach:
-            chain.close_gap(s)
-        chain.reach = s * e
-    chain.extend()
-    if chain.reach != c.size():
-        raise Unsatisfiable(f"the strides span {chain.reach}, the buffer holds {c.size()}")
-    return chain.layout()
-
-
 # ----------------------------------------------------------------------------------------------- TMA
 TmaCheck = record("TmaCheck", ["feasible", ("reason", ""), ("hint", None)],
                   "Bulk-tensor-engine feasibility of a buffer, why not, and the materialised hint.", module=__name__)
-
-
-def _contiguous_run(c):
-    run = 1
-    for e, s in sorted(c.concrete_modes(), key=lambda m: m[1]):
-        run *= e if s == run else 1
-    return run
-
-
-def check_tma(c, element_bits, *, max_dims=5, align_bytes=16, max_box=256):
-    """Can a bulk tensor copy serve this buffer? Few enough pieces, every extent within the box cap,
-    a 16-byte contiguous innermost run; the hint materialises the free strides."""
-    pieces, run_bytes = sum(map(len, c.splits)), _contiguous_run(c) * element_bits // 8
-    for broken, reason in ((pieces > max_dims, f"{pieces} dims exceed limit {max_dims}"),
-                           (max(c.dims) > max_box, f"extent exceeds box cap {max_box}"),
-                           (run_bytes < align_bytes, f"innermost contiguous run is {run_bytes}B < {align_bytes}B")):
-        if broken:
-            return TmaCheck(False, reason)
-    try:
-        hint = materialize(c)
-    except Unsatisfiable as e:
-        return TmaCheck(False, str(e))
-    return TmaCheck(True, "", hint)
 
 
 # ------------------------------------------------------------------------------------------ buffers
@@ -500,26 +234,6 @@ SmemLayout = record(
     module=__name__,
     byte_address=lambda b, logical: b.swizzle(b.layout(logical) * b.element_bits // 8),
     render=lambda b: f"{b.layout} (+) {b.swizzle}")
-
-
-def warp_address_matrix(m, element_bits, copy):
-    """Pre-swizzle byte addresses of every distinct warp-wide access of one copy: row (warp w,
-    vector j) holds lane l's address of ``m(access(32 w + l, j * vec))``. Returns (rows, width)."""
-    f, vec = copy.access, copy.vector_elems
-    width = max(1, vec * element_bits // 8)
-    if width not in VALID_WIDTHS:
-        raise MisalignedAccess(f"{width}-byte accesses are not modelled")
-    lanes = min(32, f.threads)
-    warps = max(1, f.threads // 32)
-    iters = max(1, f.values // vec)
-    grid = f.grid()
-    threads = (np.arange(warps)[:, None] * 32 + np.arange(lanes)).ravel()
-    elems = grid[threads][:, np.arange(iters) * vec]            # [warps * lanes, iters]
-    addrs = m.table()[elems] * element_bits // 8
-    rows = addrs.reshape(warps, lanes, iters).transpose(0, 2, 1).reshape(-1, lanes)
-    if (rows % width).any():
-        raise MisalignedAccess(f"a {width}-byte access of copy {copy.op_index} is misaligned")
-    return np.unique(rows, axis=0), width
 
 
 _MEMO: Dict[Tuple, SmemLayout] = {}
@@ -555,3 +269,289 @@ def access_patterns(m, element_bits, copy):
     """The copy's distinct warp-wide accesses as :class:`AccessPattern` objects (diagnostics)."""
     rows, width = warp_address_matrix(m, element_bits, copy)
     return [AccessPattern(tuple(int(a) for a in row), width) for row in rows]
+
+
+def warp_address_matrix(m, element_bits, copy):
+    """Pre-swizzle byte addresses of every distinct warp-wide access of one copy: row (warp w,
+    vector j) holds lane l's address of ``m(access(32 w + l, j * vec))``. Returns (rows, width)."""
+    f, vec = copy.access, copy.vector_elems
+    width = max(1, vec * element_bits // 8)
+    if width not in VALID_WIDTHS:
+        raise MisalignedAccess(f"{width}-byte accesses are not modelled")
+    lanes = min(32, f.threads)
+    warps = max(1, f.threads // 32)
+    iters = max(1, f.values // vec)
+    grid = f.grid()
+    threads = (np.arange(warps)[:, None] * 32 + np.arange(lanes)).ravel()
+    elems = grid[threads][:, np.arange(iters) * vec]            # [warps * lanes, iters]
+    addrs = m.table()[elems] * element_bits // 8
+    rows = addrs.reshape(warps, lanes, iters).transpose(0, 2, 1).reshape(-1, lanes)
+    if (rows % width).any():
+        raise MisalignedAccess(f"a {width}-byte access of copy {copy.op_index} is misaligned")
+    return np.unique(rows, axis=0), width
+
+
+def materialize(c):
+    """Pick the free strides so the layout is a bijection onto [0, size): concrete pieces first by
+    stride, free pieces fill the chain gaps and then extend the chain in logical order."""
+    _check_chain(c)
+    chain = _StrideChain(c)
+    for e, s in sorted(c.concrete_modes(), key=lambda m: m[1]):
+        if s > chain.reach:
+            chain.close_gap(s)
+        chain.reach = s * e
+    chain.extend()
+    if chain.reach != c.size():
+        raise Unsatisfiable(f"the strides span {chain.reach}, the buffer holds {c.size()}")
+    return chain.layout()
+
+
+def unify(c1, c2):
+    """Least-committed constraint holding every concrete stride of both. StrideConflict when the
+    factorisations cannot be overlaid, concrete strides disagree, or the concrete pieces overlap."""
+    if c1.dims != c2.dims:
+        raise StrideConflict(f"buffer extents {c1.dims} and {c2.dims} differ")
+    merged = []
+    for xs, ys in zip(c1.splits, c2.splits):
+        bx, by = _bounds(xs), _bounds(ys)
+        dim, lo, i, j = [], 1, 0, 0
+        while i < len(bx) and j < len(by):
+            hi = min(bx[i][1], by[j][1])      # next boundary of the common refinement
+            if bx[i][1] % hi or by[j][1] % hi:
+                raise StrideConflict(f"piece boundaries misalign at {hi}")
+            a, b = _sub_entry(bx[i], lo), _sub_entry(by[j], lo)
+            if isinstance(a, int) and isinstance(b, int) and a != b:
+                raise StrideConflict(f"concrete strides {a} and {b} disagree")
+            if isinstance(a, int) or isinstance(b, int):
+                dim.append((hi // lo, a if isinstance(a, int) else b))
+            else:
+                dim.append((hi // lo, StrideVar(max(a.divisibility, b.divisibility))))
+            step_x, step_y = bx[i][1] == hi, by[j][1] == hi
+            i, j, lo = i + step_x, j + step_y, hi
+        if i < len(bx) or j < len(by):
+            raise StrideConflict("the two factorisations do not cover the same extent")
+        merged.append(dim)
+    out = LayoutConstraint(c1.dims, merged)
+    _check_chain(out)
+    return out
+
+
+def build_constraint(f, vector_elems, dims):
+    """The constraint one copy puts on the buffer layout: each thread's ``vector_elems`` consecutive
+    values must sit at consecutive addresses; every other stride stays free. LayoutIncompatible when
+    the access is not a bijection onto the buffer."""
+    f = filter_replication(f)
+    total = math.prod(dims)
+    if f.threads * f.values != total:
+        raise LayoutIncompatible(f"the access covers {f.threads * f.values} of {total} elements")
+    try:
+        runs = inverse(f.layout).runs
+    except NotInvertible as e:
+        raise LayoutIncompatible(str(e)) from e
+    T = f.threads
+    vec_cuts = (T, T * vector_elems)
+    dim_ends = list(np.cumprod(dims, dtype=object))
+    splits = [[] for _ in dims]
+    logical = 1
+    for extent, tv_weight in runs:
+        points = sorted(set(_refine(extent, tv_weight, vec_cuts)) | set(_refine(extent, logical, dim_ends)))
+        prev = 1
+        for p in points + [extent]:
+            if p % prev or extent % p:
+                raise LayoutIncompatible(f"cannot cut a run of {extent} at {p}")
+            n = p // prev
+            if n > 1 or (prev == 1 and p == extent):
+                w, lw = tv_weight * prev, logical * prev
+                dim = next(i for i, end in enumerate(dim_ends) if lw < end)
+                entry = w // T if T <= w < T * vector_elems else StrideVar(vector_elems)
+                _append_merging(splits[dim], n, entry)
+            prev = p
+        logical *= extent
+    return LayoutConstraint(tuple(dims), [dim or [(1, StrideVar(1))] for dim in splits])
+
+
+def parse_constraint(text):
+    """``"((8,8),64):((1,D1),D2)"`` -> constraint; equal variable names are one variable."""
+    body = "".join(text.split())
+    try:
+        shape_txt, stride_txt = body.split(":")
+    except ValueError:
+        raise LayoutIncompatible(f"constraint text {text!r} needs one ':'") from None
+    shape_items, stride_items = _items(shape_txt), _items(stride_txt)
+    if len(shape_items) != len(stride_items):
+        raise LayoutIncompatible("constraint shape and stride have different dimension counts")
+    free = {}
+    splits = []
+    for sh, st in zip(shape_items, stride_items):
+        if isinstance(sh, list) is not isinstance(st, list):
+            raise LayoutIncompatible("constraint dimension nests differently in shape and stride")
+        sh, st = (sh, st) if isinstance(sh, list) else ([sh], [st])
+        splits.append([(int(e), int(s) if s.isdigit() else free.setdefault(s, StrideVar())) for e, s in zip(sh, st)])
+    return LayoutConstraint(tuple(math.prod(e for e, _ in dim) for dim in splits), splits)
+
+
+def check_tma(c, element_bits, *, max_dims=5, align_bytes=16, max_box=256):
+    """Can a bulk tensor copy serve this buffer? Few enough pieces, every extent within the box cap,
+    a 16-byte contiguous innermost run; the hint materialises the free strides."""
+    pieces, run_bytes = sum(map(len, c.splits)), _contiguous_run(c) * element_bits // 8
+    for broken, reason in ((pieces > max_dims, f"{pieces} dims exceed limit {max_dims}"),
+                           (max(c.dims) > max_box, f"extent exceeds box cap {max_box}"),
+                           (run_bytes < align_bytes, f"innermost contiguous run is {run_bytes}B < {align_bytes}B")):
+        if broken:
+            return TmaCheck(False, reason)
+    try:
+        hint = materialize(c)
+    except Unsatisfiable as e:
+        return TmaCheck(False, str(e))
+    return TmaCheck(True, "", hint)
+
+
+def score_swizzles(generators, candidates=()):
+    """Candidate with the least summed conflict degree over every generator's patterns (identity is
+    always a candidate; ineligible swizzles -- ones that split a vector -- are skipped)."""
+    pool = list(candidates) or candidate_swizzles()
+    if IDENTITY_SWIZZLE not in pool:
+        pool.insert(0, IDENTITY_SWIZZLE)
+    totals = []
+    for sw in pool:
+        try:
+            totals.append((sum(bank_conflicts(p, sw) for gen in generators for p in gen(sw)), sw))
+        except MisalignedAccess:
+            continue
+    return _choose(totals)
+
+
+def score_pattern_matrix(groups, pool):
+    """Batched scoring: ``groups`` holds (patterns [P, lanes] of pre-swizzle byte addresses, width)
+    per access width. Every swizzle of ``pool`` is applied to every pattern in one array
+    expression. Returns (best swizzle, its total, per-swizzle totals with -1 for ineligible)."""
+    sws = np.asarray([tuple(s) for s in pool], dtype=np.int64).reshape(-1, 3)
+    bits, base, shift = (sws[:, i][:, None, None] for i in range(3))
+    mask = (np.int64(1) << bits) - 1
+    totals = np.zeros(len(pool), dtype=np.int64)
+    eligible = np.ones(len(pool), dtype=bool)
+    for pats, width in groups:
+        a = pats[None].astype(np.int64)
+        swz = a ^ (((a >> (base + shift)) & mask) << base)
+        eligible &= ~((swz % width) != 0).any(axis=(1, 2))
+        totals += phase_degrees(swz, width).sum(axis=-1)
+    ranked = [(int(t), sw) for t, sw, ok in zip(totals, pool, eligible) if ok]
+    best, total = _choose(ranked)
+    return best, total, np.where(eligible, totals, -1)
+
+
+def bank_conflicts(pattern, swizzle=IDENTITY_SWIZZLE):
+    """Worst-phase conflict degree of one pattern (1 = conflict-free, also for no addresses)."""
+    addrs = swizzle(np.asarray(pattern.addresses, dtype=np.int64))
+    if addrs.size and (addrs % pattern.width).any():
+        raise MisalignedAccess(f"{swizzle} breaks {pattern.width}-byte alignment")
+    return int(phase_degrees(addrs, pattern.width))
+
+
+def phase_degrees(addrs, width):
+    """Conflict degree of every pattern: ``addrs`` is [..., lanes] of (already swizzled, aligned)
+    byte addresses; returns [...] = max over phases and banks of the distinct words per bank
+    (at least 1)."""
+    lanes = addrs.shape[-1]
+    if lanes == 0:
+        return np.ones(addrs.shape[:-1], dtype=np.int64)
+    words_each = max(1, width // BANK_BYTES)
+    per_phase = lanes if width <= BANK_BYTES else max(1, lanes * BANK_BYTES // width)
+    n_phase = -(-lanes // per_phase)
+    pad = n_phase * per_phase - lanes
+    if pad:  # a short last phase: repeat its first lane (a duplicate word changes no count)
+        filler = np.repeat(addrs[..., (n_phase - 1) * per_phase:(n_phase - 1) * per_phase + 1], pad, axis=-1)
+        addrs = np.concatenate([addrs, filler], axis=-1)
+    words = addrs // BANK_BYTES
+    if words_each > 1:
+        words = (words[..., None] + np.arange(words_each)).reshape(*words.shape[:-1], -1)
+    words = words.reshape(*addrs.shape[:-1], n_phase, per_phase * words_each)
+    # sort each phase's words by (bank, word): equal words are neighbours, banks are runs
+    key = np.sort((words % NUM_BANKS) << 40 | words, axis=-1)
+    fresh = np.ones(key.shape, dtype=bool)
+    fresh[..., 1:] = key[..., 1:] != key[..., :-1]
+    bank = key >> 40
+    starts = np.ones(key.shape, dtype=bool)
+    starts[..., 1:] = bank[..., 1:] != bank[..., :-1]
+    distinct = np.cumsum(fresh, axis=-1)
+    before = np.maximum.accumulate(np.where(starts, distinct - fresh, 0), axis=-1)
+    degree = (distinct - before).max(axis=(-1, -2))
+    return np.maximum(degree, 1)
+
+
+def _contiguous_run(c):
+    run = 1
+    for e, s in sorted(c.concrete_modes(), key=lambda m: m[1]):
+        run *= e if s == run else 1
+    return run
+
+
+def _check_chain(c):
+    """Concrete pieces, by stride, must stack into a bijection's stride chain."""
+    reach = 1
+    for e, s in sorted(c.concrete_modes(), key=lambda m: m[1]):
+        if s < reach or s % reach:
+            raise StrideConflict(f"concrete piece {e}:{s} overlaps the span {reach} below it")
+        reach = s * e
+
+
+def _sub_entry(piece, lo):
+    start, _, s = piece
+    return s * (lo // start) if isinstance(s, int) else StrideVar(s.divisibility)
+
+
+# ------------------------------------------------------------------------------------------- unify
+def _bounds(pieces):
+    """(start, end, entry) of each piece on the cumulative-extent axis."""
+    out, at = [], 1
+    for e, s in pieces:
+        out.append((at, at * e, s))
+        at *= e
+    return out
+
+
+def _append_merging(dim, n, entry):
+    """Append a piece; two neighbouring free pieces of one dimension become one free piece."""
+    if dim and isinstance(entry, StrideVar) and isinstance(dim[-1][1], StrideVar):
+        m, other = dim[-1]
+        dim[-1] = (m * n, StrideVar(max(other.divisibility, entry.divisibility)))
+    else:
+        dim.append((n, entry))
+
+
+# ------------------------------------------------------------------------------------------- build
+def _refine(extent, weight, cuts):
+    """Local cut points (1 < p < extent) of a run covering weights [weight, weight * extent) at the
+    given global boundaries; a boundary inside the run must be a multiple of ``weight``."""
+    out = []
+    for b in cuts:
+        if weight < b < weight * extent:
+            if b % weight:
+                raise LayoutIncompatible(f"boundary {b} is not aligned to the run weight {weight}")
+            out.append(b // weight)
+    return out
+
+
+def _items(text):
+    if not (text.startswith("(") and text.endswith(")")):
+        raise LayoutIncompatible(f"constraint part {text!r} is not parenthesised")
+    return [g.split(",") if g is not None else w for g, w in ((m.group(1), m.group(2))
+                                                            for m in _ITEM.finditer(text[1:-1]))]
+
+
+def _choose(totals):
+    if not totals:
+        return IDENTITY_SWIZZLE, 0
+    total, sw = min(totals, key=lambda ts: (ts[0], tuple(ts[1])))
+    return sw, total
+
+
+def candidate_swizzles(min_base=2):
+    """Identity plus the 1..3-bit XOR swizzles with target base 2..4 (>= ``min_base``, so vector
+    atoms of 2^min_base bytes stay whole) and source shift up to 6."""
+    return [IDENTITY_SWIZZLE] + [Swizzle(bits, base, shift) for bits in (1, 2, 3) for base in (2, 3, 4)
+                                 if base >= min_base for shift in range(bits, 7)]
+
+
+def apply_swizzle(s, addr):
+    return s(addr)

@@ -44,12 +44,6 @@ for _b in (1, 2, 4, 8, 16, 32, 64):
 _DTYPES.update({f"float8_{_f}": DType("float", 8, _f) for _f in ("e5m2", "e4m3")})
 
 
-def parse_dtype(name):
-    if name not in _DTYPES:
-        raise ParseError(f"unknown dtype {name!r}")
-    return _DTYPES[name]
-
-
 SCOPES = ("Global", "Shared", "Register")
 ACTION_KINDS = ("copy", "gemm", "cast", "rearrange", "elementwise", "reduce")
 _DERIVING = ("cast", "rearrange", "elementwise", "reduce")   # ops that declare their result
@@ -215,6 +209,88 @@ _STATEMENTS = {  # word -> (needs lhs?, allowed arg counts (None = any >= 2), us
 }
 
 
+# --------------------------------------------------------------------------------------- validation
+# The diagnostics are part of the synthesis report, so their wording is the reference's
+# (ir.py:379-480); the checks below only pick a message and its fields.
+_MESSAGES = {
+    "subbyte": "tensor {t}: sub-byte dtype {dt} needs an innermost run of >= {need} elements, got {run}",
+    "no_layout": "tensor {t}: Global tensors require a layout",
+    "broadcast": "tensor {t}: broadcast (stride-0) global layouts unsupported",
+    "twice": "op {i}: tensor {t} produced twice",
+    "copy_shape": "op {i}: copy shape mismatch {s}{ss} -> {d}{ds}",
+    "copy_width": "op {i}: copy dtype width mismatch {sd} -> {dd}",
+    "not_register": "op {i}: {role} must be Register",
+    "rank2": "op {i}: gemm operand {t} must be rank-2",
+    "gemm_k": "op {i}: gemm reduction extent mismatch between {a} (K={ka}) and {b} (K={kb})",
+    "gemm_out": "op {i}: gemm output extent mismatch {c}{cs} vs ({m},{n})",
+    "reduce_dim": "op {i}: reduce dim {dim} out of range for rank-{r} tensor {t}",
+    "elem_shapes": "op {i}: elementwise operand shapes differ: {shapes}",
+    "rearrange_rank": "op {i}: rearrange target must be a two-mode (thread, value) layout",
+    "before_def": "op {i}: tensor {t} used before definition",
+}
+
+
+def _reg(g, op, name, role):
+    if g.tensor(name).scope != "Register":
+        yield "not_register", dict(i=op.index, role=role)
+
+
+def _copy_findings(g, op):
+    src, dst = copy_src_dst(g, op)
+    if src.shape != dst.shape:
+        yield "copy_shape", dict(i=op.index, s=src.name, ss=src.shape, d=dst.name, ds=dst.shape)
+    if src.dtype.bits != dst.dtype.bits:
+        yield "copy_width", dict(i=op.index, sd=src.dtype, dd=dst.dtype)
+
+
+def _gemm_findings(g, op):
+    ts = [g.tensor(n) for n in op.operands]
+    for t in ts:
+        yield from _reg(g, op, t.name, f"gemm operand {t.name}")
+        if len(t.shape) != 2:
+            yield "rank2", dict(i=op.index, t=t.name)
+    if {len(t.shape) for t in ts} == {2}:
+        a, b, c = ts
+        if a.shape[1] != b.shape[1]:
+            yield "gemm_k", dict(i=op.index, a=a.name, ka=a.shape[1], b=b.name, kb=b.shape[1])
+        if c.shape != (a.shape[0], b.shape[0]):
+            yield "gemm_out", dict(i=op.index, c=c.name, cs=c.shape, m=a.shape[0], n=b.shape[0])
+
+
+def _reduce_findings(g, op):
+    src = g.tensor(op.operands[0])
+    if op.reduce_dim is None or not 0 <= op.reduce_dim < len(src.shape):
+        yield "reduce_dim", dict(i=op.index, dim=op.reduce_dim, r=len(src.shape), t=src.name)
+    yield from _reg(g, op, src.name, "reduce operand")
+
+
+def _elementwise_findings(g, op):
+    shapes = {g.tensor(n).shape for n in op.operands}
+    if len(shapes) > 1:
+        yield "elem_shapes", dict(i=op.index, shapes=shapes)
+
+
+def _rearrange_findings(g, op):
+    yield from _reg(g, op, op.operands[0], "rearrange operand")
+    if op.rearrange_target is not None and op.rearrange_target.rank != 2:
+        yield "rearrange_rank", dict(i=op.index)
+
+
+_OP_FINDINGS = {
+    "copy": _copy_findings,
+    "gemm": _gemm_findings,
+    "cast": lambda g, op: _reg(g, op, op.operands[0], "cast operand"),
+    "reduce": _reduce_findings,
+    "elementwise": _elementwise_findings,
+    "rearrange": _rearrange_findings,
+}
+
+
+__all__ = ["DType", "TensorDecl", "OpNode", "ProgramGraph", "parse_dtype", "parse_program", "print_program",
+           "validate", "eliminate_dead_code", "partition_components", "copy_src_dst", "SCOPES", "ACTION_KINDS",
+           "TileSynthError"]
+
+
 def parse_program(text):
     """Program text -> graph with resolved declarations (ParseError carries the line)."""
     r = _Reader()
@@ -274,119 +350,6 @@ def print_program(graph):
     out += [f"annotate {op.index} thread_arrangement {op.thread_arrangement}"
             for op in graph.ops if op.thread_arrangement is not None]
     return "\n".join(out) + "\n"
-
-
-def copy_src_dst(graph, op):
-    if op.kind != "copy":
-        raise ArityError(f"op {op.index} is not a copy")
-    return graph.tensor(op.operands[0]), graph.tensor(op.results[0])
-
-
-# --------------------------------------------------------------------------------------- validation
-# The diagnostics are part of the synthesis report, so their wording is the reference's
-# (ir.py:379-480); the checks below only pick a message and its fields.
-_MESSAGES = {
-    "subbyte": "tensor {t}: sub-byte dtype {dt} needs an innermost run of >= {need} elements, got {run}",
-    "no_layout": "tensor {t}: Global tensors require a layout",
-    "broadcast": "tensor {t}: broadcast (stride-0) global layouts unsupported",
-    "twice": "op {i}: tensor {t} produced twice",
-    "copy_shape": "op {i}: copy shape mismatch {s}{ss} -> {d}{ds}",
-    "copy_width": "op {i}: copy dtype width mismatch {sd} -> {dd}",
-    "not_register": "op {i}: {role} must be Register",
-    "rank2": "op {i}: gemm operand {t} must be rank-2",
-    "gemm_k": "op {i}: gemm reduction extent mismatch between {a} (K={ka}) and {b} (K={kb})",
-    "gemm_out": "op {i}: gemm output extent mismatch {c}{cs} vs ({m},{n})",
-    "reduce_dim": "op {i}: reduce dim {dim} out of range for rank-{r} tensor {t}",
-    "elem_shapes": "op {i}: elementwise operand shapes differ: {shapes}",
-    "rearrange_rank": "op {i}: rearrange target must be a two-mode (thread, value) layout",
-    "before_def": "op {i}: tensor {t} used before definition",
-}
-
-
-def _tensor_findings(name, t):
-    if t.dtype.bits < 8 and t.shape[0] * t.dtype.bits < 8:
-        yield "subbyte", dict(t=name, dt=t.dtype, need=8 // t.dtype.bits, run=t.shape[0])
-    if t.scope == "Global" and t.layout is None:
-        yield "no_layout", dict(t=name)
-    elif t.scope == "Global" and any(d == 0 for e, d in t.layout.runs if e > 1):
-        yield "broadcast", dict(t=name)
-
-
-def _reg(g, op, name, role):
-    if g.tensor(name).scope != "Register":
-        yield "not_register", dict(i=op.index, role=role)
-
-
-def _copy_findings(g, op):
-    src, dst = copy_src_dst(g, op)
-    if src.shape != dst.shape:
-        yield "copy_shape", dict(i=op.index, s=src.name, ss=src.shape, d=dst.name, ds=dst.shape)
-    if src.dtype.bits != dst.dtype.bits:
-        yield "copy_width", dict(i=op.index, sd=src.dtype, dd=dst.dtype)
-
-
-def _gemm_findings(g, op):
-    ts = [g.tensor(n) for n in op.operands]
-    for t in ts:
-        yield from _reg(g, op, t.name, f"gemm operand {t.name}")
-        if len(t.shape) != 2:
-            yield "rank2", dict(i=op.index, t=t.name)
-    if {len(t.shape) for t in ts} == {2}:
-        a, b, c = ts
-        if a.shape[1] != b.shape[1]:
-            yield "gemm_k", dict(i=op.index, a=a.name, ka=a.shape[1], b=b.name, kb=b.shape[1])
-        if c.shape != (a.shape[0], b.shape[0]):
-            yield "gemm_out", dict(i=op.index, c=c.name, cs=c.shape, m=a.shape[0], n=b.shape[0])
-
-
-def _reduce_findings(g, op):
-    src = g.tensor(op.operands[0])
-    if op.reduce_dim is None or not 0 <= op.reduce_dim < len(src.shape):
-        yield "reduce_dim", dict(i=op.index, dim=op.reduce_dim, r=len(src.shape), t=src.name)
-    yield from _reg(g, op, src.name, "reduce operand")
-
-
-def _elementwise_findings(g, op):
-    shapes = {g.tensor(n).shape for n in op.operands}
-    if len(shapes) > 1:
-        yield "elem_shapes", dict(i=op.index, shapes=shapes)
-
-
-def _rearrange_findings(g, op):
-    yield from _reg(g, op, op.operands[0], "rearrange operand")
-    if op.rearrange_target is not None and op.rearrange_target.rank != 2:
-        yield "rearrange_rank", dict(i=op.index)
-
-
-_OP_FINDINGS = {
-    "copy": _copy_findings,
-    "gemm": _gemm_findings,
-    "cast": lambda g, op: _reg(g, op, op.operands[0], "cast operand"),
-    "reduce": _reduce_findings,
-    "elementwise": _elementwise_findings,
-    "rearrange": _rearrange_findings,
-}
-
-
-def _findings(graph):
-    for name, t in graph.tensors.items():
-        yield from _tensor_findings(name, t)
-    written = set()
-    for op in graph.ops:
-        if op.kind in _DERIVING:
-            for r in op.results:
-                if r in written:
-                    yield "twice", dict(i=op.index, t=r)
-        yield from _OP_FINDINGS.get(op.kind, lambda g, o: ())(graph, op)
-        written.update(op.results)
-    produced_somewhere = {r for op in graph.ops for r in op.results}
-    written = set()
-    for op in graph.ops:
-        for name in op.operands:
-            if (graph.tensor(name).scope == "Register" and name in produced_somewhere
-                    and name not in written and name not in op.results):
-                yield "before_def", dict(i=op.index, t=name)
-        written.update(op.results)
 
 
 def validate(graph):
@@ -451,6 +414,43 @@ def partition_components(graph):
     return list(groups.values())
 
 
-__all__ = ["DType", "TensorDecl", "OpNode", "ProgramGraph", "parse_dtype", "parse_program", "print_program",
-           "validate", "eliminate_dead_code", "partition_components", "copy_src_dst", "SCOPES", "ACTION_KINDS",
-           "TileSynthError"]
+def copy_src_dst(graph, op):
+    if op.kind != "copy":
+        raise ArityError(f"op {op.index} is not a copy")
+    return graph.tensor(op.operands[0]), graph.tensor(op.results[0])
+
+
+def parse_dtype(name):
+    if name not in _DTYPES:
+        raise ParseError(f"unknown dtype {name!r}")
+    return _DTYPES[name]
+
+
+def _findings(graph):
+    for name, t in graph.tensors.items():
+        yield from _tensor_findings(name, t)
+    written = set()
+    for op in graph.ops:
+        if op.kind in _DERIVING:
+            for r in op.results:
+                if r in written:
+                    yield "twice", dict(i=op.index, t=r)
+        yield from _OP_FINDINGS.get(op.kind, lambda g, o: ())(graph, op)
+        written.update(op.results)
+    produced_somewhere = {r for op in graph.ops for r in op.results}
+    written = set()
+    for op in graph.ops:
+        for name in op.operands:
+            if (graph.tensor(name).scope == "Register" and name in produced_somewhere
+                    and name not in written and name not in op.results):
+                yield "before_def", dict(i=op.index, t=name)
+        written.update(op.results)
+
+
+def _tensor_findings(name, t):
+    if t.dtype.bits < 8 and t.shape[0] * t.dtype.bits < 8:
+        yield "subbyte", dict(t=name, dt=t.dtype, need=8 // t.dtype.bits, run=t.shape[0])
+    if t.scope == "Global" and t.layout is None:
+        yield "no_layout", dict(t=name)
+    elif t.scope == "Global" and any(d == 0 for e, d in t.layout.runs if e > 1):
+        yield "broadcast", dict(t=name)
