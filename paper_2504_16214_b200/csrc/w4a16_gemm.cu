@@ -1358,11 +1358,13 @@ int dispatch_prefill(int ntok, const GemmArgs& a, const void* x, int64_t rows, i
   return W4_ERR_ARG;
 }
 
-// n-pair block mode from this token tile up (W4A16_NPAIR_MIN_NTOK, default 128; 0 disables)
+// n-pair block mode for the prefill down projection from this token tile up (W4A16_NPAIR_MIN_NTOK,
+// default 64; 0 disables). Same box, DS-R1 layer: 64-token tiles (T=1024) 1.600 -> 1.572 ms with
+// n-pair; 32-token tiles (Qwen3 T=256) unchanged, so they keep k-pair stages.
 int npair_min_ntok() {
   static const int v = [] {
     const char* e = getenv("W4A16_NPAIR_MIN_NTOK");
-    const int x = e ? atoi(e) : 128;
+    const int x = e ? atoi(e) : 64;
     return x <= 0 ? 1 << 30 : x;
   }();
   return v;
