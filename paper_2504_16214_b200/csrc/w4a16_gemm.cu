@@ -1479,15 +1479,43 @@ int w4a16_tile_k(void) { return kTileK; }
 int w4a16_part_bytes(void) { return kPartBytes; }
 
 int w4a16_pick_ntok(int64_t rows, int64_t num_experts) {
-  // Token tile = smallest of 16/32/64/128 that holds a typical expert's rows in ONE m-tile (weights
-  // are streamed once per m-tile): mean + 2.5 sigma of the per-expert count under uniform routing.
-  const double mu = num_experts > 0 ? static_cast<double>(rows) / static_cast<double>(num_experts)
-                                    : static_cast<double>(rows);
-  const double est = mu + 2.5 * sqrt(mu);
-  if (est <= 16.0) return 16;
-  if (est <= 32.0) return 32;
-  if (est <= 64.0) return 64;
-  return 128;
+  // Token tile = the one minimising (relative cost of one m-tile) x (expected m-tiles per touched
+  // expert), with an expert's row count ~ Binomial(rows, 1/E) (normal approximation; exact for one
+  // expert). The relative m-tile costs are measured whole-layer times with one m-tile per expert
+  // (Mixtral T=8: 137.5 / 188.7 / 190.6 / 192.9 us for 16 / 32 / 64 / 128-token tiles) -- the
+  // 16-token tile runs in offset-code mode. Measured (tools/ntok_probe.py): the rule it replaced
+  // (mean + 2.5 sigma rows in ONE m-tile) picked 32 at Mixtral T=48 (16: 204 -> 177 us) and 128 at
+  // Mixtral T=192 (64: 231 -> 218 us), and agrees with this one everywhere else measured.
+  static const double kCost[4] = {1.0, 1.37, 1.39, 1.45};
+  const int kTiles[4] = {16, 32, 64, 128};
+  if (num_experts <= 1) {
+    // one dense matrix: its tiles are full, where the offset-code epilogue's per-token fold costs
+    // more than the costs above assume (measured: M=16 in 16-token offset tiles 14.3 -> 17.0 us,
+    // N=K=1024 8.2 -> 10.2 us) -- the smallest tile holding mean + 2.5 sigma rows, as before
+    const double est = static_cast<double>(rows) + 2.5 * sqrt(static_cast<double>(rows));
+    return est <= 16.0 ? 16 : est <= 32.0 ? 32 : est <= 64.0 ? 64 : 128;
+  }
+  const double E = static_cast<double>(num_experts);
+  const double mu = static_cast<double>(rows) / E;
+  const double sd = E > 1.0 ? sqrt(mu * (1.0 - 1.0 / E)) : 0.0;
+  double best = 1e300;
+  int pick = 16;
+  for (int i = 0; i < 4; ++i) {
+    const double n = kTiles[i];
+    double m;  // expected m-tiles of a touched expert: 1 + sum_k P(rows > k n)
+    if (sd == 0.0) {
+      m = std::max(1.0, ceil(mu / n));
+    } else {
+      m = 1.0;
+      for (double t = n; t < mu + 8.0 * sd + n; t += n) m += 0.5 * erfc((t + 0.5 - mu) / (sqrt(2.0) * sd));
+    }
+    const double cost = kCost[i] * m;
+    if (cost < best - 1e-12) {
+      best = cost;
+      pick = kTiles[i];
+    }
+  }
+  return pick;
 }
 
 int64_t w4a16_group_sums_ld(int64_t rows) { return (rows + 1) & ~int64_t(1); }

@@ -49,3 +49,25 @@ def test_ops_refuse_cpu_tensors():
     from paper_2504_16214_b200.moe import _lib, ops
     with pytest.raises(_lib.W4A16Error):
         ops.moe_permute(torch.zeros(8, dtype=torch.int32), 4)
+
+
+def test_token_tile_choice():
+    """w4a16_pick_ntok at the points tools/ntok_probe.py measured (whole-layer time per tile size):
+    the expected-m-tiles cost model picks the measured-fastest tile for each MoE case; one dense
+    matrix keeps the mean + 2.5 sigma rule (its full 16-token offset tiles measured slower)."""
+    from paper_2504_16214_b200.moe import _lib
+    lib = _lib.load()
+    picks = {  # (rows = T * k, experts) -> measured-best tile
+        (96, 8): 16,      # Mixtral T=48
+        (384, 8): 64,     # Mixtral T=192
+        (128, 8): 32,     # Mixtral T=64 (32 and 64 measured equal)
+        (2048, 128): 32,  # Qwen3 T=256
+        (1536, 128): 16,  # Qwen3 T=192
+        (4096, 256): 32,  # DS-R1 T=512
+        (512, 256): 16,   # DS-R1 T=64
+        (65536, 256): 128,
+        (16, 1): 32,      # dense M=16
+        (1, 1): 16,
+    }
+    for (rows, e), want in picks.items():
+        assert lib.w4a16_pick_ntok(rows, e) == want, (rows, e)
