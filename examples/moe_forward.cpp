@@ -2,7 +2,8 @@
 // -> packed blocks (w4a16_repack_awq) -> top-k routing (w4a16_route_topk) -> the whole layer
 // (w4a16_moe_forward), checked against a plain CPU restatement of the same arithmetic -- dequant
 // fp16((q - z) * s), SwiGLU with h rounded to fp16, each expert's down output rounded to fp16, the
-// fp32 weighted combine (the conventions of oracle/moe_oracle.py).
+// fp32 weighted combine (the conventions of oracle/moe_oracle.py). Then the same layer through the
+// expert-parallel entry (w4a16_moe_forward_ep) on a one-rank NCCL communicator, bit for bit.
 //
 //   make -C examples   (or see tests/test_c_example.py)   ./examples/moe_forward  -> exit 0 when it matches
 #include <cuda_fp16.h>
@@ -178,5 +179,30 @@ int main() {
   }
   std::printf("moe_forward: T=%d E=%d k=%d H=%d I=%d  routing mismatches %d  max |diff| %.3g  outside tol %d\n", T,
               E, TOPK, H, I, route_mismatch, max_err, bad);
-  return (route_mismatch == 0 && bad == 0) ? 0 : 1;
+  int ep_diff = 0;
+  if (w4a16_ep_available()) {
+    // the expert-parallel entry on a one-rank communicator: all-gather, localize, local experts, fp32
+    // partial combine, reduce-scatter and the one rounding -- bit-identical to the single-GPU layer
+    unsigned char id[128];
+    W4(w4a16_ep_unique_id(id));
+    w4a16_ep_comm* comm = nullptr;
+    W4(w4a16_ep_comm_init(id, 0, 1, &comm));
+    const int64_t ep_bytes = w4a16_moe_ep_workspace_bytes(T, 1, TOPK, E, H, I);
+    void* ep_ws = nullptr;
+    CK(cudaMalloc(&ep_ws, ep_bytes));
+    CK(cudaMemset(ep_ws, 0, ep_bytes));
+    __half* d_y_ep = nullptr;
+    CK(cudaMalloc(&d_y_ep, sizeof(__half) * T * H));
+    W4(w4a16_moe_forward_ep(comm, d_x, T, H, I, E, TOPK, d_ids, d_wts, d_w13, d_w2, W4_DTYPE_F16, d_y_ep, ep_ws,
+                            ep_bytes, 0));
+    CK(cudaDeviceSynchronize());
+    std::vector<__half> y_ep(size_t(T) * H);
+    CK(cudaMemcpy(y_ep.data(), d_y_ep, y_ep.size() * sizeof(__half), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < y.size(); ++i) ep_diff += __half_as_ushort(y_ep[i]) != __half_as_ushort(y[i]);
+    W4(w4a16_ep_comm_destroy(comm));
+    std::printf("moe_forward_ep (1 rank): %d elements differ from moe_forward\n", ep_diff);
+  } else {
+    std::printf("moe_forward_ep: NCCL not available, skipped\n");
+  }
+  return (route_mismatch == 0 && bad == 0 && ep_diff == 0) ? 0 : 1;
 }
