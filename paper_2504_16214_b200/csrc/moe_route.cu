@@ -74,6 +74,7 @@ template <int kPer>
 __global__ void route_topk_kernel(const float* __restrict__ logits, int T, int E, int k, int scoring, int renorm,
                                   int32_t* __restrict__ ids, float* __restrict__ wts) {
   griddep_wait();  // PDL: inputs written by the previous kernel in the stream
+  griddep_launch_dependents();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (warp >= T) return;
   route_token<kPer>(logits, warp, E, k, scoring, renorm, ids, wts, threadIdx.x & 31);
@@ -92,6 +93,7 @@ __global__ void route_grouped_topk_kernel(const float* __restrict__ logits, int 
                                           int scoring, int renorm, const float* __restrict__ bias, float scale,
                                           int32_t* __restrict__ ids, float* __restrict__ wts) {
   griddep_wait();  // PDL: inputs written by the previous kernel in the stream
+  griddep_launch_dependents();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= T) return;
@@ -276,6 +278,7 @@ __global__ void __launch_bounds__(kPermThreads, 1)
                        int32_t* __restrict__ offsets, int32_t* __restrict__ sorted_pairs,
                        int32_t* __restrict__ pair_pos) {
   griddep_wait();  // PDL: inputs written by the previous kernel in the stream
+  griddep_launch_dependents();
   permute_block(ids, P, E, counts, offsets, sorted_pairs, pair_pos);
 }
 
@@ -289,6 +292,7 @@ __global__ void __launch_bounds__(kPermThreads, 1)
                          int32_t* __restrict__ offsets, int32_t* __restrict__ sorted_pairs,
                          int32_t* __restrict__ pair_pos) {
   griddep_wait();  // PDL: inputs written by the previous kernel in the stream
+  griddep_launch_dependents();
   const int warp = threadIdx.x >> 5;
   for (int t = warp; t < T; t += kPermWarps) route_token<kPer>(logits, t, E, k, scoring, renorm, ids, wts, threadIdx.x & 31);
   __syncthreads();
@@ -304,6 +308,7 @@ constexpr int kChunk = 2048;
 __global__ void __launch_bounds__(512) permute_hist_kernel(const int32_t* __restrict__ ids, int P, int E,
                                                            int32_t* __restrict__ ws) {
   griddep_wait();  // PDL: inputs written by the previous kernel in the stream
+  griddep_launch_dependents();
   extern __shared__ int hist[];
   for (int e = threadIdx.x; e < E; e += blockDim.x) hist[e] = 0;
   __syncthreads();
@@ -321,6 +326,7 @@ __global__ void __launch_bounds__(1024) permute_scan_kernel(int nb, int E, int32
                                                             int32_t* __restrict__ counts,
                                                             int32_t* __restrict__ offsets) {
   griddep_wait();  // PDL: inputs written by the previous kernel in the stream
+  griddep_launch_dependents();
   __shared__ int wsum[32];
   const int e = threadIdx.x, lane = e & 31, warp = e >> 5;
   int total = 0;
@@ -363,6 +369,7 @@ __global__ void __launch_bounds__(kPermThreads, 1)
     permute_scatter_kernel(const int32_t* __restrict__ ids, int P, int E, const int32_t* __restrict__ ws,
                            int32_t* __restrict__ sorted_pairs, int32_t* __restrict__ pair_pos) {
   griddep_wait();  // PDL: inputs written by the previous kernel in the stream
+  griddep_launch_dependents();
   extern __shared__ int sm[];
   int* base = sm;                    // [E]
   int* wcnt = base + E;              // [kPermWarps][E]
@@ -505,6 +512,7 @@ __global__ void moe_gather_kernel(const uint4* __restrict__ x, int64_t hv, int t
                                   const int32_t* __restrict__ sorted_pairs, const int32_t* __restrict__ row_limit,
                                   uint4* __restrict__ xp) {
   griddep_wait();  // PDL: inputs written by the previous kernel in the stream
+  griddep_launch_dependents();
   const int64_t p = blockIdx.x;
   const int lim = row_limit ? __ldg(row_limit) : 0x7fffffff;
   const int src_row = __ldg(sorted_pairs + p);  // (in flight with the limit's load)
@@ -549,6 +557,7 @@ __global__ void group_sums_kernel(const uint4* __restrict__ x, int64_t hv, int t
                                   const int32_t* __restrict__ sorted_pairs, const int32_t* __restrict__ row_limit,
                                   uint4* __restrict__ xp, int64_t ld, float2* __restrict__ xsum) {
   griddep_wait();  // PDL: inputs written by the previous kernel in the stream
+  griddep_launch_dependents();
   const int64_t p = blockIdx.x;
   const int lim = row_limit ? __ldg(row_limit) : 0x7fffffff;
   const int src_row = kGather ? __ldg(sorted_pairs + p) : 0;  // (in flight with the limit's load)
@@ -617,6 +626,7 @@ __global__ void moe_combine_kernel(const uint4* __restrict__ yp, int64_t hv, int
                                    const int32_t* __restrict__ pair_pos, const float* __restrict__ wts,
                                    void* __restrict__ y) {
   griddep_wait();  // PDL: inputs written by the previous kernel in the stream
+  griddep_launch_dependents();
   const int64_t t = blockIdx.x;
   const int64_t i = static_cast<int64_t>(blockIdx.y) * blockDim.x + threadIdx.x;
   constexpr int kMaxK = 32;
