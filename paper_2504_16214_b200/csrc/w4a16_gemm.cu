@@ -30,6 +30,11 @@
 
 namespace w4 {
 
+#ifndef W4A16_GEMM_TAIL_TRIGGER
+// experiment: PDL trigger this many stages before a CTA's last (0 = off). Measured with 4: no gain
+// (DS-R1 T=1 58.9 -> 59.3 us, Qwen3 Zipf T=16 45.1 -> 46.8 us, the rest within noise)
+#define W4A16_GEMM_TAIL_TRIGGER 0
+#endif
 // Experiment (-DW4A16_DUAL=1): a 15th warp as the second MMA issuer of the prefill kernel (see kDual).
 #ifndef W4A16_DUAL
 #define W4A16_DUAL 0
@@ -474,6 +479,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           mbar_wait(&empty[st.i], st.ph ^ 1);
           if (lane == 0) {
             trace_at(tr, 0, pgs++);
+#if W4A16_GEMM_TAIL_TRIGGER
+            // experiment: let the next kernel launch once this CTA's producer is within its last few
+            // stages (the CTA exits ~NS stages later), hiding the dependent's launch latency
+            if (it == n_tiles - 1 && j == max(stage_beg(ti), stage_end(ti) - W4A16_GEMM_TAIL_TRIGGER))
+              asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
             mbar_arrive_expect_tx(&full[st.i], C::kBlk + C::kXBytes);
             if constexpr (C::kNPer == 2) {  // k-group j of n-tiles n_tile and n_tile + 1 (blocks kt apart)
               bulk_g2s_hint(smem_w + st.i * C::kBlk, wsrc + static_cast<int64_t>(j) * kPartBytes, kPartBytes,
