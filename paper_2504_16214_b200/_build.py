@@ -24,7 +24,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", f"-I{INCLUDE}", f"-I{CSRC}"]
 if os.environ.get("W4A16_TRACE"):  # debug build: per-stage clock64 timeline (w4a16_debug_trace)
     FLAGS.append("-DW4A16_TRACE")
-for knob in ("W4A16_SPLITA", "W4A16_WAIT", "W4A16_DUAL", "W4A16_DECODE_NUMA", "W4A16_DECODE_MAXACC", "W4A16_EARLY_PDL", "W4A16_SMALL_TRIGGER", "W4A16_GEMM_TAIL_TRIGGER"):  # experiments (see w4a16_gemm.cu)
+for knob in ("W4A16_SPLITA", "W4A16_WAIT", "W4A16_DUAL", "W4A16_DECODE_NUMA", "W4A16_DECODE_MAXACC", "W4A16_EARLY_PDL", "W4A16_SMALL_TRIGGER", "W4A16_GEMM_TAIL_TRIGGER", "W4A16_SP_NUMA", "W4A16_SP_MAXACC", "W4A16_SP_MAXNTOK"):  # experiments (see w4a16_gemm.cu)
     if os.environ.get(knob):
         FLAGS.append(f"-D{knob}=" + os.environ[knob])
 if os.environ.get("W4A16_KSPLIT"):  # experiment: k-split accumulators of the 16-token decode tile

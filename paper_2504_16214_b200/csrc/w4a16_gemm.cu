@@ -83,6 +83,24 @@ constexpr bool kSplitAEnv = W4A16_SPLITA != 0;
 // (32-column accumulator stages) up to 8 stages fit beside 2 A slots; 3 A slots + 4 stages was
 // slower at every decode size (T=64 862 -> 910-920 us, tools/gpu_ab_knobs.sh).
 constexpr int kDecodeNumA = W4A16_DECODE_NUMA;
+// Prefill-mode (scale-in-dequant) tiles of up to W4A16_SP_MAXNTOK tokens: W4A16_SP_NUMA A slots and
+// up to W4A16_SP_MAXACC accumulator stages (the general rule -- 3 A slots beside 1-2 accumulator
+// stages -- stalled the MMA on each short tile's epilogue). 2 A + 2-4 accumulator stages, same box:
+// Qwen3 T=256 108 -> 102 us, its Zipf case 108 -> 103 us, Mixtral T=64 205 -> 188 us, T=128 209 ->
+// 198 us, DS-R1 T=512 1.44 -> 1.33 ms, T=1024 1.57 -> 1.52 ms (tools/gpu_ab_sp.sh); 128-token tiles
+// keep the general rule (their accumulator is 256 columns). W4A16_SP_NUMA=0 restores the general rule.
+#ifndef W4A16_SP_NUMA
+#define W4A16_SP_NUMA 2
+#endif
+#ifndef W4A16_SP_MAXACC
+#define W4A16_SP_MAXACC 4
+#endif
+#ifndef W4A16_SP_MAXNTOK
+#define W4A16_SP_MAXNTOK 64
+#endif
+constexpr int kSmallPrefillNumA = W4A16_SP_NUMA;
+constexpr int kSmallPrefillMaxNTok = W4A16_SP_MAXNTOK;
+constexpr int kSmallPrefillMaxAcc = W4A16_SP_MAXACC;
 constexpr int kDecodeMaxAcc = W4A16_DECODE_MAXACC;
 
 struct GemmArgs {
@@ -182,12 +200,13 @@ struct Cfg {
   // (epilogue / next-tile overlap, once per long tile); the short k-pair tiles need two.
   // Split ring: two accumulator stages if 6 units still fit, then as many units as fit (<= 8).
   static constexpr int kNumA_ = kOffset ? ((kDecodeNumA * kACols + 2 * kAccCols <= 512) ? kDecodeNumA : 2)
+                              : (kNTok <= kSmallPrefillMaxNTok && kSmallPrefillNumA > 0) ? kSmallPrefillNumA
                               : !(kGated || kNPer == 2) ? ((3 * kACols + 2 * kAccCols <= 512) ? 3 : 2)
                                                                    : ((3 * kACols + kAccCols <= 512) ? 3 : 2);
   static constexpr int kNumAccS = (2 * kAccCols + 6 * kACols <= 512) ? 2 : 1;
   static constexpr int kNumAS = (512 - kNumAccS * kAccCols) / kACols > 8 ? 8 : (512 - kNumAccS * kAccCols) / kACols;
   static constexpr int kNumAccO = (512 - kNumA_ * kACols) / kAccCols;
-  static constexpr int kMaxAcc = kOffset ? kDecodeMaxAcc : 2;
+  static constexpr int kMaxAcc = kOffset ? kDecodeMaxAcc : (kNTok <= kSmallPrefillMaxNTok ? kSmallPrefillMaxAcc : 2);
   static constexpr int kNumAcc = kSplitA ? kNumAccS : (kNumAccO > kMaxAcc ? kMaxAcc : kNumAccO);
   static constexpr int kNumA = kSplitA ? kNumAS : kNumA_;
   static constexpr int kStageBytes = kBlk + kXBytes + kSumBytes;
