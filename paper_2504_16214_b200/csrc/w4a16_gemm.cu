@@ -1466,7 +1466,12 @@ GemmPlan plan_gemm(int64_t rows, int64_t K, int64_t num_experts, int64_t n_out, 
   // (64 KB for a k-pair -> only 2 smem stages), so 128-token tiles use one group per stage
   pl.mode = gated ? kModeGateUp : ((kt % 2 == 0 && pl.ntok <= 64) ? kModeKPair : kModePlain);
   // prefill down projection: two n-tiles per stage share the X tile (halves the X smem traffic)
-  if (!gated && !pl.offset && pl.ntok >= 32 && pl.ntok >= npair_min_ntok() && nt % 2 == 0) pl.mode = kModeNPair;
+  // (not for 128-token tiles of short K: their single 256-column accumulator stalls the MMA on
+  // every few-stage tile's epilogue -- Qwen3 down, K/128 = 6: T=8192 layer 0.740 -> 0.725 ms in plain
+  // stages with two accumulator stages; DS-R1 / Mixtral / Llama, K/128 >= 16, keep n-pair)
+  if (!gated && !pl.offset && pl.ntok >= 32 && pl.ntok >= npair_min_ntok() && nt % 2 == 0 &&
+      (pl.ntok < 128 || kt >= 12))
+    pl.mode = kModeNPair;
   // decode down projection: n-pair stages too (one k-group of two n-tiles on one X tile): tiles of
   // K/128 stages instead of K/256 k-pair stages, half the X bytes per stage
   if (!gated && pl.offset && nt % 2 == 0 && decode_npair_enabled()) pl.mode = kModeNPair;
