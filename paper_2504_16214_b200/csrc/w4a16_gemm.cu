@@ -1473,8 +1473,13 @@ GemmPlan plan_gemm(int64_t rows, int64_t K, int64_t num_experts, int64_t n_out, 
       (pl.ntok < 128 || kt >= 12))
     pl.mode = kModeNPair;
   // decode down projection: n-pair stages too (one k-group of two n-tiles on one X tile): tiles of
-  // K/128 stages instead of K/256 k-pair stages, half the X bytes per stage
-  if (!gated && pl.offset && nt % 2 == 0 && decode_npair_enabled()) pl.mode = kModeNPair;
+  // K/128 stages instead of K/256 k-pair stages, half the X bytes per stage -- unless even an upper
+  // estimate of the n-pair tiles leaves SMs idle, where k-pair's twice as many tiles cover more of
+  // them (same box: Qwen3 T=1 30.7 -> 28.7 us, Mixtral T=1 59.5 -> 58.4 us, T=16 154 -> 150 us;
+  // DS-R1, with >= 148 n-pair tiles from T=1 on, measured better with n-pair)
+  if (!gated && pl.offset && nt % 2 == 0 && decode_npair_enabled() &&
+      std::min<int64_t>(num_experts, rows) * (nt / 2) >= sm_count())
+    pl.mode = kModeNPair;
   const int n_stages = kt / (pl.mode == kModeKPair ? 2 : 1);
   pl.splits = (pl.offset && rows < (1 << 20)) ? choose_splits(rows, num_experts, nt, n_stages, sm_count()) : 1;
   // experiment: W4A16_SPLITS_GU / W4A16_SPLITS_DN force the decode split-K factor of gate/up / down launches
