@@ -62,6 +62,10 @@ enum { W4_SCORE_SOFTMAX = 0, W4_SCORE_SIGMOID = 1 };
 /* Bytes of the packed block format for [num_experts][n_rows][K] (== AWQ bytes; -1 if misaligned). */
 int64_t w4a16_packed_bytes(int64_t num_experts, int64_t n_rows, int64_t K);
 int w4a16_tile_rows(void); /* 128 */
+/* The launch plan w4a16_grouped_gemm_ws would use (host only, no GPU needed): token tile, block mode
+ * (0 plain, 1 gate|up, 2 k-pair, 3 n-pair), offset-code decode mode or not, split-K factor. */
+int w4a16_gemm_plan(int64_t rows, int64_t K, int64_t num_experts, int64_t n_out, int gated, int has_xsum, int ntok,
+                    int* out_ntok, int* out_mode, int* out_offset, int* out_splits);
 int w4a16_tile_k(void);    /* 128 */
 int w4a16_part_bytes(void);
 

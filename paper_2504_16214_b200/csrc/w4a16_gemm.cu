@@ -1510,6 +1510,19 @@ int w4a16_debug_stamp(void* buf, cudaStream_t stream) {
 }
 
 int w4a16_tile_rows(void) { return kTileRows; }
+
+/* The launch plan w4a16_grouped_gemm_ws would use (no GPU needed): token tile, block mode (0 plain,
+ * 1 gate|up, 2 k-pair, 3 n-pair), decode (offset-code) or not, split-K factor. */
+int w4a16_gemm_plan(int64_t rows, int64_t K, int64_t num_experts, int64_t n_out, int gated, int has_xsum, int ntok,
+                    int* out_ntok, int* out_mode, int* out_offset, int* out_splits) {
+  if (rows <= 0 || K <= 0 || K % kTileK || n_out <= 0 || n_out % kTileRows || num_experts <= 0) return W4_ERR_SHAPE;
+  const GemmPlan pl = plan_gemm(rows, K, num_experts, n_out, gated, has_xsum != 0, ntok);
+  if (out_ntok) *out_ntok = pl.ntok;
+  if (out_mode) *out_mode = pl.mode;
+  if (out_offset) *out_offset = pl.offset ? 1 : 0;
+  if (out_splits) *out_splits = pl.splits;
+  return W4_OK;
+}
 int w4a16_decode_max_ntok(void) {
   const char* e = getenv("W4A16_DECODE_MAX_NTOK");  // (read per call: the A/B knob)
   const int v = e ? atoi(e) : 16;

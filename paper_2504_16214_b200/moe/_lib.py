@@ -59,6 +59,7 @@ SIGNATURES = {
                                        _p, _i64, _p]),
     "w4a16_grouped_gemm_ws_bytes": (_i64, [_i64, _i64, _i64, _i64, _i, _i]),
     "w4a16_decode_max_ntok": (_i, []),
+    "w4a16_gemm_plan": (_i, [_i64, _i64, _i64, _i64, _i, _i, _i, _p, _p, _p, _p]),
     "w4a16_moe_workspace_bytes": (_i64, [_i64, _i64, _i64, _i64, _i64]),
     "w4a16_moe_forward": (_i, [_p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, _i, _p, _p, _i64, _p]),
     "w4a16_moe_combine_f32": (_i, [_p, _i64, _i64, _i64, _p, _p, _i, _p, _p]),

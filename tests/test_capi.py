@@ -71,3 +71,31 @@ def test_token_tile_choice():
     }
     for (rows, e), want in picks.items():
         assert lib.w4a16_pick_ntok(rows, e) == want, (rows, e)
+
+
+def test_gemm_plan_rules():
+    """The planner's block-mode rules (w4a16_gemm_plan, no GPU): decode down projections use n-pair
+    stages unless an upper estimate of the n-pair tiles leaves SMs idle (k-pair then); 128-token
+    prefill down projections of short K use plain stages; 64-token ones n-pair (sm_count() is 148
+    when no GPU is visible, as on a B200)."""
+    import ctypes
+    from paper_2504_16214_b200.moe import _lib
+    lib = _lib.load()
+    f = lib.w4a16_gemm_plan
+    f.restype = ctypes.c_int
+    f.argtypes = [ctypes.c_int64] * 4 + [ctypes.c_int] * 3 + [ctypes.POINTER(ctypes.c_int)] * 4
+
+    def plan(rows, K, E, N, gated, xsum, ntok=0):
+        o = [ctypes.c_int() for _ in range(4)]
+        assert f(rows, K, E, N, gated, xsum, ntok, *[ctypes.byref(v) for v in o]) == 0
+        return tuple(v.value for v in o)  # (ntok, mode, offset, splits)
+
+    PLAIN, GATEUP, KPAIR, NPAIR = 0, 1, 2, 3
+    assert plan(512, 2048, 256, 7168, 0, 1)[:3] == (16, NPAIR, 1)   # DS-R1 T=64 down: decode n-pair
+    assert plan(8, 2048, 256, 7168, 0, 1)[1] == NPAIR               # DS-R1 T=1 down: 224 n-pair tiles
+    assert plan(8, 768, 128, 2048, 0, 1)[1] == KPAIR                # Qwen3 T=1 down: 64 n-pair tiles < 148
+    assert plan(2, 14336, 8, 4096, 0, 1)[1] == KPAIR                # Mixtral T=1 down
+    assert plan(512, 7168, 256, 2048, 1, 1)[:3] == (16, GATEUP, 1)  # DS-R1 T=64 gate/up
+    assert plan(65536, 2048, 256, 7168, 0, 0)[:3] == (128, NPAIR, 0)  # DS-R1 prefill down (K/128 = 16)
+    assert plan(65536, 768, 128, 2048, 0, 0)[:3] == (128, PLAIN, 0)   # Qwen3 prefill down (K/128 = 6)
+    assert plan(8192, 2048, 256, 7168, 0, 0)[:2] == (64, NPAIR)       # DS-R1 T=1024 down: 64-token n-pair
